@@ -1,0 +1,249 @@
+/*
+ * babplan_cuda.h -- C-ABI of the B200 BaB-ND hot path.
+ *
+ * This is the drop-in boundary between a host planner (the reference's C++
+ * API / its pybind11 module, or this repo's ctypes module) and the sm_100a
+ * kernels in paper_2412_09584_b200/csrc/.  Only plain pointers, sizes and
+ * POD structs cross it; no exception, no torch type, no STL container.
+ *
+ * Every entry point returns a bp_status; the message of the last failure on
+ * the calling thread is available through bp_get_last_error().  Host buffers
+ * are caller-owned; device buffers are owned by the context.
+ *
+ * Reference interfaces each entry point replaces (paths under the reference
+ * checkout's proj/):
+ *   bp_load_objective   build_objective            src/model.cpp:310-387
+ *                       GraphObjective sets        src/objective.cpp:13-76
+ *   bp_rollout          GraphObjective::evaluate   src/objective.cpp:31-33
+ *                       -> evaluate/forward_chunk  src/graph.cpp:252-401
+ *   bp_batch_search     batch_search / run_cem /   src/search.cpp:87-209,262-282
+ *                       run_mppi / SampleSink      src/search.cpp:37-82
+ *   bp_batch_bound      CrownBounder::lower        src/bab.cpp:25-28
+ *                       -> lower_bound             src/crown.cpp:440-469
+ *   bp_plan             plan / sample_only_plan    src/bab.cpp:266-454
+ *   bp_pick_out/split/prune   pick_out/split/prune src/bab.cpp:85-241
+ */
+#ifndef BABPLAN_CUDA_H_
+#define BABPLAN_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+typedef enum {
+  BP_OK = 0,
+  BP_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  BP_LOGIC = 2,            /* std::logic_error */
+  BP_RUNTIME = 3,          /* std::runtime_error (numeric failure, root search failed) */
+  BP_CUDA = 4,
+  BP_NCCL = 5,
+  BP_UNSUPPORTED = 6
+} bp_status;
+
+/* ------------------------------------------------------------- enums */
+enum { BP_FEATURE_RELATIVE = 0, BP_FEATURE_ABSOLUTE = 1 }; /* model.hpp:13-16 */
+
+/* Value ids inside one rollout step's cost program. */
+enum { BP_VAL_X = 0, BP_VAL_U = 1, BP_VAL_P = 2, BP_VAL_OP0 = 3 };
+
+/* Cost-program op kinds: the non-structural node kinds of graph.hpp:11-22. */
+enum {
+  BP_OP_LINEAR = 0,
+  BP_OP_RELU = 1,
+  BP_OP_SUM = 2, /* src0 (+ src1 when >= 0) */
+  BP_OP_SCALAR_AFFINE = 3,
+  BP_OP_SQDIST = 4,
+  BP_OP_HINGE = 5,
+  BP_OP_SLICE = 6
+};
+
+enum { BP_STOP_LAST_RELU = 0, BP_STOP_EVERY_STEP_OUTPUT = 1, BP_STOP_CUSTOM = 2 }; /* objective.hpp:38 */
+enum { BP_BOUND_FULL_CROWN = 0, BP_BOUND_EMPIRICAL = 1, BP_BOUND_INTERVAL = 2 };    /* crown.hpp:80-84 */
+enum { BP_ALPHA_ADAPTIVE = 0, BP_ALPHA_ZERO = 1, BP_ALPHA_ONE = 2 };                /* crown.hpp:13-19 */
+enum { BP_SEARCH_CEM = 0, BP_SEARCH_MPPI = 1, BP_SEARCH_GD = 2 };                   /* search.hpp:13 */
+enum { BP_SPLIT_SAMPLES = 0, BP_SPLIT_WIDTH = 1 }; /* bab.cpp:172-194 ; WIDTH forces the width-only rule */
+
+/* -------------------------------------------------- objective descriptor */
+/*
+ * One op of the per-step cost program.  The program is replayed at every
+ * step t = 1..H on the values {x_t, u_t, p_t} and produces the step's cost
+ * terms, in the node order build_objective (model.cpp:355-370) creates them.
+ */
+typedef struct {
+  int kind;
+  int src0, src1;           /* value ids (BP_VAL_*, or BP_VAL_OP0 + i); src1 = -1 unless SUM */
+  int dim;                  /* output dimension */
+  int in_dim;               /* dimension of src0 */
+  int begin;                /* SLICE: y = x[begin : begin + dim] */
+  const double* W;          /* LINEAR: dim x in_dim row-major */
+  const double* b;          /* LINEAR: dim */
+  double scale, offset;     /* SCALAR_AFFINE */
+  const double* target;     /* SQDIST: in_dim */
+  const double* weight;     /* SQDIST: in_dim, non-negative */
+  int weight_by_step;       /* SQDIST: weight_j * step_weight[t-1] (tracking_weight, model.cpp:160-164) */
+  const double* center;     /* HINGE: in_dim */
+  double radius, penalty;   /* HINGE: penalty * relu(radius - |x - center|) */
+  int is_term;              /* scalar op whose output is summed into the objective */
+} bp_cost_op;
+
+/*
+ * Unrolled-rollout objective: x_t = MLP(features(x_{t-1}, p_{t-1}, u_t)),
+ * p_t = p_{t-1} + u_t, objective = sum over steps of the cost program terms.
+ * Mirrors build_objective (model.cpp:310-387) generalised to a cost program.
+ */
+typedef struct {
+  int ks, ka, kd, horizon, feature_mode;
+  int n_layers;
+  const int* widths;          /* n_layers + 1: [ks + ka, hidden..., ks] */
+  const double* const* W;     /* per layer: out x in row-major */
+  const double* const* b;     /* per layer: out */
+  const int* relu_after;      /* per layer */
+  const double* x0;           /* ks */
+  const double* p0;           /* kd */
+  const double* u_lower;      /* ka, per-step action box */
+  const double* u_upper;      /* ka */
+  const double* step_weight;  /* horizon: w_t */
+  int n_ops;
+  const bp_cost_op* ops;
+  int stop_rule;
+  int n_custom_stops;
+  const int* custom_stop_steps; /* 1-based steps t whose x_t node is a stop node */
+} bp_objective_desc;
+
+/* ------------------------------------------------------ planner config */
+/* PlannerConfig / SearcherConfig (bab.hpp:45-62, search.hpp:18-46). */
+typedef struct {
+  int method;
+  int samples_per_iter;
+  int iterations;
+  int top_capacity;
+  uint64_t seed;
+  /* CEM */
+  int cem_agents, cem_elites;
+  double cem_jitter, cem_init_sigma;
+  /* MPPI */
+  double mppi_noise_frac, mppi_temperature;
+  int mppi_n_noise, mppi_n_temp;
+  const double* mppi_noise_ratios;
+  const double* mppi_temperature_ratios;
+  /* GD */
+  double gd_base_step;
+  int gd_n_ratios;
+  const double* gd_step_ratios;
+} bp_search_config;
+
+typedef struct {
+  int batch;
+  double eta, temperature, top_percent, min_width;
+  int bound_mode, alpha;
+  int split_rule;
+  uint64_t seed;
+  bp_search_config search;
+  int max_iterations;
+  double wall_clock_ms;
+  double target_objective; /* -inf disables */
+} bp_planner_config;
+
+typedef struct {
+  int iter;
+  double uf, min_lf, pruned_vol, selected_vol;
+  int64_t pool_size, samples;
+  double wall_ms;
+} bp_trace_row; /* TraceRow, bab.hpp:124-133 */
+
+/* ------------------------------------------------------- context */
+typedef struct bp_ctx bp_ctx;
+
+/* Creates a context bound to one CUDA device (one process per GPU). */
+bp_status bp_init(int device, bp_ctx** out);
+bp_status bp_destroy(bp_ctx* ctx);
+/* Thread-local message of the last failing call (empty when none). */
+size_t bp_get_last_error(char* buf, size_t cap);
+/* Optional NCCL sharding: rank r of world w; unique_id is the 128-byte ncclUniqueId. */
+bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* nccl_unique_id);
+
+/* Uploads weights / cost program; derives stop and watch sets. */
+bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc);
+/* Number of recorded (watched) coordinates per rollout step, and the layout
+ * of one step's record: n_slots entries of (kind, index, dim, offset). */
+bp_status bp_stat_layout(bp_ctx* ctx, int* per_step, int* n_slots, int* slot_kind, int* slot_index,
+                         int* slot_dim, int* slot_offset, int cap);
+
+/* Parity entry: evaluates n_sub x rows action sequences (rows x d each) and
+ * returns the objective per row plus the per-subdomain sample extrema of
+ * every watched coordinate (layout from bp_stat_layout, H x per_step).
+ * states (n_sub x rows x H x ks), emp_lo and emp_hi may be NULL.  Rows are independent: bitwise identical for
+ * any n_sub / rows decomposition (graph.hpp:102-103). */
+bp_status bp_rollout(bp_ctx* ctx, int n_sub, int rows, const float* actions, float* costs,
+                     float* states, float* emp_lo, float* emp_hi, int* nonfinite);
+
+/* Batched search over boxes (double, n_boxes x d).  warm may be NULL or hold
+ * NaN rows for "no warm start".  Results stay resident in the context until
+ * the next call; read them with bp_report_*. */
+bp_status bp_batch_search(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi,
+                          const double* warm, const bp_search_config* cfg);
+bp_status bp_report_summary(bp_ctx* ctx, double* uf, double* best, int64_t* samples, int* ok,
+                            int* n_top);
+bp_status bp_report_top(bp_ctx* ctx, int box, double* values, double* actions, int cap);
+bp_status bp_report_stats(bp_ctx* ctx, int box, float* emp_lo, float* emp_hi);
+
+/* Lower bound of every searched box (mode/alpha as in lower_bound). */
+bp_status bp_batch_bound(bp_ctx* ctx, int mode, int alpha, double* lf);
+/* Lower bound of boxes without search statistics: lower_bound(obj, box, mode,
+ * stats = nullptr), i.e. interval intermediate bounds (crown.cpp:449-461). */
+bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi, int mode, int alpha,
+                         double* lf);
+
+/* Full planner: plan() when method_babnd != 0, else sample_only_plan(). */
+typedef struct bp_result bp_result;
+bp_status bp_plan(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm, int method_babnd,
+                  bp_result** out);
+bp_status bp_result_summary(const bp_result* r, double* uf, double* min_lf, int* certified,
+                            int64_t* samples, int* iterations, char* stop_reason, size_t cap,
+                            int* n_trace, int* d);
+bp_status bp_result_best(const bp_result* r, double* best);
+bp_status bp_result_trace(const bp_result* r, bp_trace_row* rows, int cap);
+bp_status bp_result_free(bp_result* r);
+
+/* Device-time accounting of the last bp_plan / bp_batch_search call (ms per
+ * kernel family; rollout is the dominant kernel). */
+bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms,
+                    double* search_ms, int64_t* launches);
+
+/* Host-side pool primitives (bit-exact restatements, exposed for parity). */
+typedef struct {
+  double lf, uf;
+  int64_t id;
+  double log_vol;
+} bp_pool_meta;
+/* Picks n records; writes their pool indices (pick order) to picked and
+ * returns the count in *n_picked.  rng_state is a handle from bp_rng_new. */
+typedef struct bp_rng bp_rng;
+bp_status bp_rng_new(uint64_t seed, bp_rng** out);
+bp_status bp_rng_free(bp_rng* r);
+bp_status bp_rng_uniform(bp_rng* r, double* out);
+bp_status bp_rng_normal(bp_rng* r, double* out);
+bp_status bp_rng_bits(bp_rng* r, uint64_t* out);
+/* n draws of uniform() (kind 0) or normal() (kind 1) into out. */
+bp_status bp_rng_fill(bp_rng* r, int kind, int64_t n, double* out);
+uint64_t bp_mix_seed(uint64_t master, uint64_t salt);
+bp_status bp_pick_out(const bp_pool_meta* pool, int n_pool, int n, double eta, double temperature,
+                      bp_rng* rng, int* picked, int* n_picked);
+/* split(): box lo/hi (d), top list (n_top values + n_top x d actions,
+ * ascending), samples; returns axis, mid and the routing of each top sample
+ * (0 = lo child, 1 = hi child). */
+bp_status bp_split_axis(int d, const double* lo, const double* hi, int n_top, const double* top_u,
+                        int64_t samples, double top_percent, double min_width, int split_rule,
+                        int* axis, double* mid, unsigned char* route);
+/* Generates a Glorot-uniform MLP exactly like generate_model (model.cpp:136-158). */
+bp_status bp_generate_model(uint64_t seed, int n_widths, const int* widths, double* params);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BABPLAN_CUDA_H_ */

@@ -1,0 +1,250 @@
+"""The reference's Python API (bindings/pymodule.cpp:85-252, bindings/__init__.py)
+on top of the C-ABI in include/babplan_cuda.h.
+
+`Device` is the per-process handle (one CUDA device per process, like the
+one-rank-per-GPU runtime); the module-level functions use a lazily created
+default `Device` on LOCAL_RANK.  Every compute call goes through the CUDA
+library; there is no host fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import _capi, config as _config
+from ._capi import check
+from .model import Model, Scenario
+from .objective import ObjectiveSpec, build_objective
+
+_BOUND = _config.BOUND_MODES
+_ALPHA = _config.ALPHAS
+
+
+class Device:
+    """One bp_ctx bound to a CUDA device, plus the objective loaded on it."""
+
+    def __init__(self, device: Optional[int] = None):
+        self.lib = _capi.load()
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0"))
+        h = C.c_void_p()
+        check(self.lib.bp_init(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+        self.spec: Optional[ObjectiveSpec] = None
+        self._packed = None
+        self._layout = None
+
+    def close(self):
+        if self.h:
+            self.lib.bp_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- objective
+    def load(self, spec: ObjectiveSpec) -> "Device":
+        if spec is self.spec:
+            return self
+        packed = spec.to_c()
+        check(self.lib.bp_load_objective(self.h, packed.ref()))
+        self.spec, self._packed, self._layout = spec, packed, None
+        return self
+
+    def stat_layout(self):
+        """(per_step, [(kind, index, dim, offset), ...]); kind 0 preact(layer),
+        1 x_t, 2 u_t, 3 p_t, 4 cost op(index)."""
+        if self._layout is None:
+            cap = 64
+            per, n = C.c_int(), C.c_int()
+            arrs = [np.zeros(cap, dtype=np.int32) for _ in range(4)]
+            check(self.lib.bp_stat_layout(self.h, C.byref(per), C.byref(n), *[_capi.iptr(a) for a in arrs], cap))
+            self._layout = (per.value, [tuple(int(a[i]) for a in arrs) for i in range(n.value)])
+        return self._layout
+
+    # ------------------------------------------------------------------ rollout
+    def rollout(self, actions: np.ndarray, want_states: bool = False, want_stats: bool = True):
+        """actions: (n_sub, rows, d) -> costs (n_sub, rows), states, emp lo/hi (n_sub, H, per_step), nonfinite."""
+        a = np.ascontiguousarray(actions, dtype=np.float32)
+        if a.ndim == 2:
+            a = a[None]
+        n_sub, rows, d = a.shape
+        if d != self.spec.d:
+            raise ValueError("evaluate: batch width does not match the input dimension")
+        per, _ = self.stat_layout()
+        H, ks = self.spec.horizon, self.spec.ks
+        costs = np.zeros((n_sub, rows), dtype=np.float32)
+        states = np.zeros((n_sub, rows, H, ks), dtype=np.float32) if want_states else None
+        lo = np.zeros((n_sub, H, per), dtype=np.float32) if want_stats else None
+        hi = np.zeros((n_sub, H, per), dtype=np.float32) if want_stats else None
+        bad = np.zeros(n_sub, dtype=np.int32)
+        check(self.lib.bp_rollout(self.h, n_sub, rows, _capi.fptr(a), _capi.fptr(costs), _capi.fptr(states),
+                                  _capi.fptr(lo), _capi.fptr(hi), _capi.iptr(bad)))
+        return costs, states, lo, hi, bad
+
+    # ------------------------------------------------------------------- search
+    def batch_search(self, lo: np.ndarray, hi: np.ndarray, warm: Optional[np.ndarray], cfg: dict, seed: int,
+                     method: str = "babnd"):
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        n, d = lo.shape
+        w = None if warm is None else np.ascontiguousarray(warm, dtype=np.float64)
+        packed = _config.PackedConfig(cfg, method)
+        check(self.lib.bp_batch_search(self.h, n, _capi.dptr(lo), _capi.dptr(hi), _capi.dptr(w),
+                                       packed.search_ref(seed)))
+        uf = np.zeros(n)
+        best = np.zeros((n, d))
+        samples = np.zeros(n, dtype=np.int64)
+        ok = np.zeros(n, dtype=np.int32)
+        ntop = np.zeros(n, dtype=np.int32)
+        check(self.lib.bp_report_summary(self.h, _capi.dptr(uf), _capi.dptr(best),
+                                         samples.ctypes.data_as(C.POINTER(C.c_int64)), _capi.iptr(ok),
+                                         _capi.iptr(ntop)))
+        return {"uf": uf, "best": best, "samples": samples, "ok": ok.astype(bool), "n_top": ntop}
+
+    def report_top(self, box: int, n_top: int):
+        d = self.spec.d
+        v = np.zeros(max(n_top, 1))
+        a = np.zeros((max(n_top, 1), d))
+        check(self.lib.bp_report_top(self.h, box, _capi.dptr(v), _capi.dptr(a), n_top))
+        return v[:n_top], a[:n_top]
+
+    def report_stats(self, box: int):
+        per, _ = self.stat_layout()
+        lo = np.zeros((self.spec.horizon, per), dtype=np.float32)
+        hi = np.zeros((self.spec.horizon, per), dtype=np.float32)
+        check(self.lib.bp_report_stats(self.h, box, _capi.fptr(lo), _capi.fptr(hi)))
+        return lo, hi
+
+    def batch_bound(self, n: int, mode: str = "early-stop-empirical", alpha: str = "adaptive") -> np.ndarray:
+        lf = np.zeros(n)
+        check(self.lib.bp_batch_bound(self.h, _BOUND[mode], _ALPHA[alpha], _capi.dptr(lf)))
+        return lf
+
+    def bound_boxes(self, lo, hi, mode: str = "early-stop-interval", alpha: str = "adaptive") -> np.ndarray:
+        lo = np.ascontiguousarray(np.atleast_2d(lo), dtype=np.float64)
+        hi = np.ascontiguousarray(np.atleast_2d(hi), dtype=np.float64)
+        lf = np.zeros(lo.shape[0])
+        check(self.lib.bp_bound_boxes(self.h, lo.shape[0], _capi.dptr(lo), _capi.dptr(hi), _BOUND[mode],
+                                      _ALPHA[_config._parse_enum(_ALPHA, alpha, "alpha policy")], _capi.dptr(lf)))
+        return lf
+
+    # --------------------------------------------------------------------- plan
+    def plan(self, cfg: dict, warm: Optional[np.ndarray] = None, method: str = "babnd") -> dict:
+        packed = _config.PackedConfig(cfg, method)
+        w = None if warm is None else np.ascontiguousarray(warm, dtype=np.float64)
+        res = C.c_void_p()
+        check(self.lib.bp_plan(self.h, packed.ref(), _capi.dptr(w), 1 if method == "babnd" else 0, C.byref(res)))
+        try:
+            uf, mlf = C.c_double(), C.c_double()
+            cert, iters, ntr, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            samples = C.c_int64()
+            stop = C.create_string_buffer(64)
+            check(self.lib.bp_result_summary(res, C.byref(uf), C.byref(mlf), C.byref(cert), C.byref(samples),
+                                             C.byref(iters), stop, 64, C.byref(ntr), C.byref(d)))
+            best = np.zeros(d.value)
+            check(self.lib.bp_result_best(res, _capi.dptr(best)))
+            rows = (_capi.TraceRow * max(1, ntr.value))()
+            check(self.lib.bp_result_trace(res, rows, ntr.value))
+        finally:
+            self.lib.bp_result_free(res)
+        tr = rows[:ntr.value]
+        trace = {
+            "iter": [r.iter for r in tr], "uf": [r.uf for r in tr], "min_lf": [r.min_lf for r in tr],
+            "pruned_vol": [r.pruned_vol for r in tr], "selected_vol": [r.selected_vol for r in tr],
+            "pool_size": [r.pool_size for r in tr], "samples": [r.samples for r in tr],
+            "wall_ms": [r.wall_ms for r in tr],
+        }
+        return {"objective": uf.value, "action": best, "lower_bound": mlf.value, "certified": bool(cert.value),
+                "samples": samples.value, "iterations": iters.value, "stop_reason": stop.value.decode(),
+                "trace": trace}
+
+    def timing(self) -> dict:
+        """Device time since the previous call: rollout ms and launches, bound ms, search wall ms."""
+        r, b, s = C.c_double(), C.c_double(), C.c_double()
+        rl, l = C.c_int64(), C.c_int64()
+        check(self.lib.bp_timing(self.h, C.byref(r), C.byref(rl), C.byref(b), C.byref(s), C.byref(l)))
+        return {"rollout_ms": r.value, "rollout_launches": rl.value, "bound_ms": b.value, "search_ms": s.value,
+                "launches": l.value}
+
+
+_default: Optional[Device] = None
+
+
+def default_device() -> Device:
+    global _default
+    if _default is None:
+        _default = Device()
+    return _default
+
+
+# ----------------------------------------------------------- reference API
+def default_config() -> str:
+    return _config.default_config()
+
+
+def plan(model: Model, scenario: Scenario, config: str = "", method: str = "babnd") -> dict:
+    """pymodule.cpp:152-160: build the unrolled objective, then plan() or sample_only_plan()."""
+    cfg = _config.from_json(config)
+    dev = default_device().load(build_objective(model, scenario))
+    return dev.plan(cfg, None, method)
+
+
+def objective_value(model: Model, scenario: Scenario, actions) -> np.ndarray:
+    """pymodule.cpp:171-178: objective per row of flattened action sequences."""
+    a = np.asarray(actions, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(1, -1)
+    if not np.all(np.isfinite(a)):
+        raise ValueError("evaluate batch: non-finite values")
+    dev = default_device().load(build_objective(model, scenario))
+    costs, _, _, _, bad = dev.rollout(a[None].astype(np.float32), want_stats=False)
+    if bad[0]:
+        raise RuntimeError("evaluate: non-finite objective value (malformed weights?)")
+    return costs[0].astype(np.float64)
+
+
+def lower_bound(model: Model, scenario: Scenario, mode: str = "full-crown", alpha: str = "adaptive") -> float:
+    """pymodule.cpp:180-190: bound over the whole action box without samples."""
+    if mode not in _BOUND:
+        raise ValueError(f"unknown bound mode '{mode}'")
+    if alpha not in _ALPHA:
+        raise ValueError(f"unknown alpha policy '{alpha}'")
+    spec = build_objective(model, scenario)
+    dev = default_device().load(spec)
+    lo, hi = spec.box()
+    return float(dev.bound_boxes(lo[None], hi[None], mode, alpha)[0])
+
+
+def network_lower_bound(model: Model, lower, upper, mode: str = "full-crown", alpha: str = "adaptive") -> float:
+    raise NotImplementedError("network_lower_bound (full-crown over a bare network) is a SURVEY 8(f) next row")
+
+
+def rollout(model: Model, scenario: Scenario, action) -> np.ndarray:
+    """pymodule.cpp:204-223: states x_1..x_H of one flattened action sequence (H x ks)."""
+    a = np.asarray(action, dtype=np.float64).reshape(-1)
+    if a.size != scenario.action_dim() * scenario.horizon:
+        raise ValueError("action length must be horizon * action_dim")
+    dev = default_device().load(build_objective(model, scenario))
+    _, states, _, _, _ = dev.rollout(a.reshape(1, 1, -1).astype(np.float32), want_states=True, want_stats=False)
+    return states[0, 0].astype(np.float64)
+
+
+def plan_synthetic(d: int, config: str = "", method: str = "babnd") -> dict:
+    raise NotImplementedError("the synthetic separable objective is a SURVEY 8(f) next row")
+
+
+def rrt_plan(*args, **kwargs):
+    raise NotImplementedError("RRT/PRM graph-planner baselines are out of scope (SURVEY 2, row 11)")
+
+
+def prm_plan(*args, **kwargs):
+    raise NotImplementedError("RRT/PRM graph-planner baselines are out of scope (SURVEY 2, row 11)")

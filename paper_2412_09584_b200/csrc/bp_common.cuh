@@ -1,0 +1,100 @@
+// bp_common.cuh -- compiled device form of a bp_objective_desc and the
+// helpers shared by the sm_100a kernels (rollout, bound, search).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bp {
+
+constexpr int kMaxLayers = 8;
+constexpr int kMaxOps = 32;
+constexpr int kThreads = 256;  // every rollout / bound / search CTA
+
+// One op of the per-step cost program, compiled (cf. bp_cost_op).
+struct DevOp {
+  int kind, src0, src1, dim, in_dim, begin;
+  int is_term, weight_by_step;
+  int col;       // column of this op's output inside the per-row scratch
+  int stat;      // offset of its recorded extrema within one step's record, -1 if not recorded
+  int stop;      // RELU op anchored as the last-ReLU stop at step H
+  // float arena offsets (forward)
+  int w, b, tgt, wt, ctr;
+  // double arena offsets (bound)
+  int wd, bd, tgtd, wtd, ctrd;
+  float scale, offset, radius, penalty;
+  double scaled, offsetd, radiusd, penaltyd;
+};
+
+// Compiled objective, passed by value to every kernel (~5 KB of params).
+struct DevObjective {
+  int ks, ka, kd, H, rel, L, d;
+  int widths[kMaxLayers + 1];
+  int relu[kMaxLayers];
+  // forward weights: layer l stored transposed [kpad][nstr] (k-major, zero padded)
+  int kpad[kMaxLayers], nstr[kMaxLayers];
+  int wt[kMaxLayers], bias[kMaxLayers];   // float arena offsets
+  int w_smem_off[kMaxLayers];             // float offset of layer l inside the resident smem image
+  int w_smem_total;                       // floats in the resident image (0 when streamed)
+  int w_max_layer;                        // floats of the largest single layer image
+  // backward weights: W [out][in] row-major and b, double arena offsets
+  int wd[kMaxLayers], bd[kMaxLayers];
+  // per-row scratch layout in the activation buffer
+  int S;          // row stride (floats) of the activation buffer
+  int ucol, pcol; // columns holding u_t and p_t during the cost program
+  int n_ops;
+  DevOp ops[kMaxOps];
+  // watched-coordinate record of one step
+  int SP;
+  int pre_stat[kMaxLayers];  // preactivation of layer l (hidden, relu), -1 otherwise
+  int x_stat, u_stat, p_stat;
+  // stop set
+  int stop_layer;   // hidden layer whose ReLU output at step H is the last-ReLU stop (-1)
+  int stop_op;      // RELU cost op that is the last-ReLU stop at step H (-1)
+  int xstop;        // int arena offset: H flags, x_t is a stop node
+  // constants
+  int x0, p0, step_w;        // float arena offsets
+  int x0d, p0d;              // double arena offsets
+  const float* f;
+  const double* dd;
+  const int* iv;
+};
+
+// Order-preserving float <-> int encoding for atomicMin/atomicMax extrema.
+__device__ __forceinline__ int enc_f(float f) {
+  int i = __float_as_int(f);
+  return i ^ ((i >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ float dec_f(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
+inline int enc_f_host(float f) {
+  int i;
+  static_assert(sizeof(int) == sizeof(float), "");
+  __builtin_memcpy(&i, &f, 4);
+  return i ^ ((i >> 31) & 0x7fffffff);
+}
+inline float dec_f_host(int i) {
+  i = i ^ ((i >> 31) & 0x7fffffff);
+  float f;
+  __builtin_memcpy(&f, &i, 4);
+  return f;
+}
+
+// Philox4x32-10 counter-based generator.
+struct Philox {
+  __device__ static uint4 gen(uint4 ctr, uint2 key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint32_t hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
+      const uint32_t hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
+      ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+      key.x += 0x9E3779B9u;
+      key.y += 0xBB67AE85u;
+    }
+    return ctr;
+  }
+};
+__device__ __forceinline__ float u01_open(uint32_t x) {  // (0, 1]
+  return (static_cast<float>(x >> 8) + 1.0f) * (1.0f / 16777216.0f);
+}
+
+}  // namespace bp

@@ -1,0 +1,1505 @@
+// host.cu -- the C-ABI of include/babplan_cuda.h: context, objective
+// compilation, device batch search / bound, and the host planner loop.
+//
+// The planner is the reference's plan() (proj/src/bab.cpp:266-415) with its
+// search and bound calls replaced by the device kernels: pick_out, split,
+// merge_report and prune stay host C++ restated bit-for-bit (they are
+// O(pool) bookkeeping; every rank of a multi-GPU run replays them on the same
+// exchanged data, so decisions are identical on every rank).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/babplan_cuda.h"
+#include "bp_common.cuh"
+
+namespace bp {
+struct RolloutArgs {
+  const float* actions;
+  float* costs;
+  float* states;
+  int* stat_min;
+  int* stat_max;
+  int* failed;
+  long long n_rows;
+  int rows_per_sub;
+  int kslab;
+};
+struct BoundArgs {
+  const double* lo;
+  const double* hi;
+  const int* stat_min;
+  const int* stat_max;
+  const int* use_stats;
+  double* ivl_lo;
+  double* ivl_hi;
+  double* lf;
+  int mode;
+  int alpha;
+};
+struct SearchArgs {
+  int n, d, rows, n_samp;
+  int method;
+  int groups, per_group;
+  int elites;
+  int top_cap;
+  int iter;
+  const unsigned long long* seeds;
+  const float* lo;
+  const float* hi;
+  const float* warm;
+  float* mu;
+  float* var;
+  float* var_floor;
+  float* best;
+  float* uf;
+  float* actions;
+  const float* costs;
+  int* failed;
+  float* top_val[2];
+  int* top_seq[2];
+  float* top_act[2];
+  int* top_cnt;
+  int cur;
+  float jitter, init_sigma;
+  float noise_frac, temperature;
+  const float* noise_ratios;
+  const float* temp_ratios;
+  int n_noise;
+};
+cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, bool stream, size_t smem, cudaStream_t st);
+int rollout_rows_per_tile(int nq);
+cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st);
+size_t bound_smem_bytes();
+cudaError_t launch_search_init(const SearchArgs& a, cudaStream_t st);
+cudaError_t launch_sample(const SearchArgs& a, int sms, cudaStream_t st);
+cudaError_t launch_search_update(const SearchArgs& a, cudaStream_t st);
+size_t search_update_smem(const SearchArgs& a);
+}  // namespace bp
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure : std::runtime_error {
+  bp_status code;
+  Failure(bp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(bp_status c, const std::string& m) { throw Failure(c, m); }
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(BP_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+bp_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return BP_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return BP_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    g_last_error = e.what();
+    return BP_LOGIC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BP_RUNTIME;
+  }
+}
+
+int r4(int x) { return (x + 3) & ~3; }
+int r8(int x) { return (x + 7) & ~7; }
+
+// Grow-only device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  T* get(size_t want) {
+    if (want > n) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      n = 0;
+      ck(cudaMalloc(&p, std::max<size_t>(want, 1) * sizeof(T)), "cudaMalloc");
+      n = want;
+    }
+    return p;
+  }
+};
+
+__global__ void fill_int_kernel(int* p, long long n, int v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+void fill_int(int* p, long long n, int v, cudaStream_t st) {
+  if (n <= 0) return;
+  const long long g = std::min<long long>((n + 255) / 256, 4096);
+  fill_int_kernel<<<static_cast<unsigned>(g), 256, 0, st>>>(p, n, v);
+  ck(cudaGetLastError(), "fill");
+}
+
+// Host copy of the objective and its compiled device form.
+struct Compiled {
+  bp::DevObjective o{};
+  std::vector<float> fa;
+  std::vector<double> da;
+  std::vector<int> ia;
+  int nq = 0;
+  bool stream = false;
+  size_t smem = 0;
+  int kslab = 0;
+  int R = 0;
+  // stat layout (for bp_stat_layout): kind 0 preact(layer), 1 x, 2 u, 3 p, 4 op(index)
+  std::vector<int> slot_kind, slot_index, slot_dim, slot_off;
+  std::vector<double> x0, p0, ulo, uhi;
+  int d = 0;
+};
+
+int push_f(std::vector<float>& a, const double* p, size_t n) {
+  while (a.size() % 4) a.push_back(0.f);
+  const int off = static_cast<int>(a.size());
+  for (size_t i = 0; i < n; ++i) a.push_back(static_cast<float>(p[i]));
+  return off;
+}
+int push_d(std::vector<double>& a, const double* p, size_t n) {
+  while (a.size() % 2) a.push_back(0.0);
+  const int off = static_cast<int>(a.size());
+  a.insert(a.end(), p, p + n);
+  return off;
+}
+
+void require_finite(const double* p, size_t n, const char* what) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) fail(BP_INVALID_ARGUMENT, std::string(what) + ": non-finite values");
+}
+
+Compiled compile(const bp_objective_desc& d) {
+  Compiled c;
+  bp::DevObjective& o = c.o;
+  if (d.ks <= 0 || d.ka <= 0 || d.kd <= 0 || d.horizon < 1) fail(BP_INVALID_ARGUMENT, "objective: bad dimensions");
+  if (d.ka != d.kd) fail(BP_INVALID_ARGUMENT, "objective: action and effector dimensions must match");
+  if (d.ka > 8) fail(BP_UNSUPPORTED, "objective: action dimension above 8");
+  if (d.feature_mode == BP_FEATURE_RELATIVE && d.ks % d.kd != 0)
+    fail(BP_INVALID_ARGUMENT, "objective: state must be whole keypoints of workspace dimension");
+  if (d.n_layers < 1 || d.n_layers > bp::kMaxLayers) fail(BP_UNSUPPORTED, "objective: layer count outside 1..8");
+  if (d.widths[0] != d.ks + d.ka || d.widths[d.n_layers] != d.ks)
+    fail(BP_INVALID_ARGUMENT, "build_objective: model input must take state plus action and output the state");
+  if (d.relu_after[d.n_layers - 1]) fail(BP_INVALID_ARGUMENT, "objective: final layer must stay linear");
+  if (d.n_ops > bp::kMaxOps) fail(BP_UNSUPPORTED, "objective: more than 32 cost ops");
+  o.ks = d.ks;
+  o.ka = d.ka;
+  o.kd = d.kd;
+  o.H = d.horizon;
+  o.rel = d.feature_mode == BP_FEATURE_RELATIVE ? 1 : 0;
+  o.L = d.n_layers;
+  o.d = d.ka * d.horizon;
+  c.d = o.d;
+  int maxN = 0, maxK4 = 0, maxw = d.widths[0];
+  for (int l = 0; l <= d.n_layers; ++l) {
+    if (d.widths[l] <= 0) fail(BP_INVALID_ARGUMENT, "objective: widths must be positive");
+    o.widths[l] = d.widths[l];
+    maxw = std::max(maxw, d.widths[l]);
+  }
+  if (maxw > 1024) fail(BP_UNSUPPORTED, "objective: layer width above 1024");
+  for (int l = 0; l < d.n_layers; ++l) {
+    o.relu[l] = d.relu_after[l] ? 1 : 0;
+    o.kpad[l] = r4(d.widths[l]);
+    o.nstr[l] = r4(d.widths[l + 1]);
+    if (o.nstr[l] > 16) maxN = std::max(maxN, o.nstr[l]);
+    maxK4 = std::max(maxK4, o.kpad[l]);
+    require_finite(d.W[l], static_cast<size_t>(d.widths[l]) * d.widths[l + 1], "linear weights");
+    require_finite(d.b[l], static_cast<size_t>(d.widths[l + 1]), "linear bias");
+  }
+  c.nq = maxN <= 64 ? 1 : maxN <= 128 ? 2 : maxN <= 256 ? 4 : maxN <= 512 ? 8 : 0;
+  if (c.nq == 0) fail(BP_UNSUPPORTED, "objective: hidden width above 512 (rollout kernel)");
+  // forward weight image: layers back to back, each [kpad][nstr], then padding
+  int img = 0;
+  {
+    while (c.fa.size() % 4) c.fa.push_back(0.f);
+    const int base = static_cast<int>(c.fa.size());
+    for (int l = 0; l < d.n_layers; ++l) {
+      const int K = d.widths[l], N = d.widths[l + 1];
+      o.w_smem_off[l] = img;
+      o.wt[l] = base + img;
+      std::vector<float> t(static_cast<size_t>(o.kpad[l]) * o.nstr[l], 0.f);
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < K; ++k) t[static_cast<size_t>(k) * o.nstr[l] + n] = static_cast<float>(d.W[l][static_cast<size_t>(n) * K + k]);
+      c.fa.insert(c.fa.end(), t.begin(), t.end());
+      img += o.kpad[l] * o.nstr[l];
+    }
+    c.fa.insert(c.fa.end(), static_cast<size_t>(64 * c.nq + 64), 0.f);  // over-read pad
+    o.w_smem_total = img + 64 * c.nq + 64;
+    o.w_max_layer = 0;
+    for (int l = 0; l < d.n_layers; ++l) o.w_max_layer = std::max(o.w_max_layer, o.kpad[l] * o.nstr[l]);
+  }
+  for (int l = 0; l < d.n_layers; ++l) {
+    std::vector<double> bp(static_cast<size_t>(o.nstr[l]), 0.0);
+    for (int n = 0; n < d.widths[l + 1]; ++n) bp[static_cast<size_t>(n)] = d.b[l][n];
+    o.bias[l] = push_f(c.fa, bp.data(), bp.size());
+    o.wd[l] = push_d(c.da, d.W[l], static_cast<size_t>(d.widths[l]) * d.widths[l + 1]);
+    o.bd[l] = push_d(c.da, d.b[l], static_cast<size_t>(d.widths[l + 1]));
+  }
+  require_finite(d.x0, static_cast<size_t>(d.ks), "scenario x0");
+  require_finite(d.p0, static_cast<size_t>(d.kd), "scenario p0");
+  o.x0 = push_f(c.fa, d.x0, static_cast<size_t>(d.ks));
+  o.p0 = push_f(c.fa, d.p0, static_cast<size_t>(d.kd));
+  o.x0d = push_d(c.da, d.x0, static_cast<size_t>(d.ks));
+  o.p0d = push_d(c.da, d.p0, static_cast<size_t>(d.kd));
+  c.x0.assign(d.x0, d.x0 + d.ks);
+  c.p0.assign(d.p0, d.p0 + d.kd);
+  c.ulo.assign(d.u_lower, d.u_lower + d.ka);
+  c.uhi.assign(d.u_upper, d.u_upper + d.ka);
+  for (int j = 0; j < d.ka; ++j)
+    if (!(d.u_lower[j] <= d.u_upper[j])) fail(BP_INVALID_ARGUMENT, "scenario: action bounds inverted");
+
+  // cost program: value dims and scratch columns
+  o.n_ops = d.n_ops;
+  const int C0 = r4(d.ks);
+  o.ucol = C0;
+  o.pcol = o.ucol + r4(d.ka);
+  int col = o.pcol + r4(d.kd);
+  std::vector<int> vdim = {d.ks, d.ka, d.kd};
+  std::vector<char> need(static_cast<size_t>(3 + d.n_ops), 0);
+  bool any_term = false;
+  for (int i = 0; i < d.n_ops; ++i) {
+    const bp_cost_op& s = d.ops[i];
+    bp::DevOp& p = o.ops[i];
+    std::memset(&p, 0, sizeof(p));
+    const int nv = 3 + i;
+    if (s.src0 < 0 || s.src0 >= nv || s.src1 >= nv) fail(BP_INVALID_ARGUMENT, "cost op: bad source");
+    const int in = vdim[static_cast<size_t>(s.src0)];
+    p.kind = s.kind;
+    p.src0 = s.src0;
+    p.src1 = s.kind == BP_OP_SUM ? s.src1 : -1;
+    p.in_dim = in;
+    p.is_term = s.is_term;
+    p.weight_by_step = s.weight_by_step;
+    p.stat = -1;
+    p.stop = 0;
+    int dim = s.dim;
+    switch (s.kind) {
+      case BP_OP_LINEAR:
+        if (dim <= 0) fail(BP_INVALID_ARGUMENT, "linear: weight shape does not match argument");
+        require_finite(s.W, static_cast<size_t>(dim) * in, "linear weights");
+        require_finite(s.b, static_cast<size_t>(dim), "linear bias");
+        p.w = push_f(c.fa, s.W, static_cast<size_t>(dim) * in);
+        p.b = push_f(c.fa, s.b, static_cast<size_t>(dim));
+        p.wd = push_d(c.da, s.W, static_cast<size_t>(dim) * in);
+        p.bd = push_d(c.da, s.b, static_cast<size_t>(dim));
+        break;
+      case BP_OP_RELU:
+        dim = in;
+        need[static_cast<size_t>(s.src0)] = 1;
+        break;
+      case BP_OP_SUM:
+        dim = in;
+        if (s.src1 >= 0 && vdim[static_cast<size_t>(s.src1)] != in) fail(BP_INVALID_ARGUMENT, "sum: argument dimensions differ");
+        break;
+      case BP_OP_SCALAR_AFFINE:
+        dim = in;
+        if (!std::isfinite(s.scale) || !std::isfinite(s.offset)) fail(BP_INVALID_ARGUMENT, "scalar_affine: non-finite parameter");
+        p.scale = static_cast<float>(s.scale);
+        p.offset = static_cast<float>(s.offset);
+        p.scaled = s.scale;
+        p.offsetd = s.offset;
+        break;
+      case BP_OP_SQDIST: {
+        dim = 1;
+        need[static_cast<size_t>(s.src0)] = 1;
+        require_finite(s.target, static_cast<size_t>(in), "squared_distance target");
+        require_finite(s.weight, static_cast<size_t>(in), "squared_distance weight");
+        for (int j = 0; j < in; ++j)
+          if (s.weight[j] < 0.0) fail(BP_INVALID_ARGUMENT, "squared_distance: weights must be nonnegative");
+        p.tgt = push_f(c.fa, s.target, static_cast<size_t>(in));
+        p.tgtd = push_d(c.da, s.target, static_cast<size_t>(in));
+        std::vector<double> w;
+        const int reps = s.weight_by_step ? d.horizon : 1;
+        for (int t = 0; t < reps; ++t)
+          for (int j = 0; j < in; ++j) w.push_back(s.weight_by_step ? d.step_weight[t] * s.weight[j] : s.weight[j]);
+        p.wt = push_f(c.fa, w.data(), w.size());
+        p.wtd = push_d(c.da, w.data(), w.size());
+        break;
+      }
+      case BP_OP_HINGE:
+        dim = 1;
+        need[static_cast<size_t>(nv)] = 1;  // anchored on its own output
+        require_finite(s.center, static_cast<size_t>(in), "penalty_hinge center");
+        if (!std::isfinite(s.radius) || s.radius < 0.0) fail(BP_INVALID_ARGUMENT, "penalty_hinge: radius must be finite and nonnegative");
+        if (!std::isfinite(s.penalty) || s.penalty < 0.0) fail(BP_INVALID_ARGUMENT, "penalty_hinge: penalty must be finite and nonnegative");
+        p.ctr = push_f(c.fa, s.center, static_cast<size_t>(in));
+        p.ctrd = push_d(c.da, s.center, static_cast<size_t>(in));
+        p.radius = static_cast<float>(s.radius);
+        p.penalty = static_cast<float>(s.penalty);
+        p.radiusd = s.radius;
+        p.penaltyd = s.penalty;
+        break;
+      case BP_OP_SLICE:
+        if (dim <= 0 || s.begin < 0 || s.begin + dim > in) fail(BP_INVALID_ARGUMENT, "slice: range outside argument");
+        p.begin = s.begin;
+        break;
+      default:
+        fail(BP_INVALID_ARGUMENT, "cost op: unknown kind");
+    }
+    if (s.is_term && dim != 1) fail(BP_INVALID_ARGUMENT, "cost op: terms must be scalar");
+    any_term = any_term || s.is_term;
+    p.dim = dim;
+    p.col = col;
+    col += r4(dim);
+    vdim.push_back(dim);
+  }
+  if (!any_term) fail(BP_INVALID_ARGUMENT, "objective: cost program has no terms");
+  o.S = r8(std::max({maxK4, r4(maxw), col})) + 4;
+
+  // stop set (objective.cpp:45-63)
+  std::vector<int> xstop(static_cast<size_t>(d.horizon), 0);
+  o.stop_layer = -1;
+  o.stop_op = -1;
+  if (d.stop_rule == BP_STOP_LAST_RELU) {
+    for (int l = 0; l + 1 < d.n_layers; ++l)
+      if (d.relu_after[l]) o.stop_layer = l;
+    if (o.stop_layer < 0)  // relu_nodes.back(): the last ReLU of the final step's cost program
+      for (int i = 0; i < d.n_ops; ++i)
+        if (d.ops[i].kind == BP_OP_RELU) o.stop_op = i;
+    if (o.stop_op >= 0) o.ops[o.stop_op].stop = 1;
+  } else if (d.stop_rule == BP_STOP_EVERY_STEP_OUTPUT) {
+    std::fill(xstop.begin(), xstop.end(), 1);
+  } else if (d.stop_rule == BP_STOP_CUSTOM) {
+    for (int i = 0; i < d.n_custom_stops; ++i) {
+      const int t = d.custom_stop_steps[i];
+      if (t < 1 || t > d.horizon) fail(BP_INVALID_ARGUMENT, "stop set: step outside horizon");
+      xstop[static_cast<size_t>(t - 1)] = 1;
+    }
+  } else {
+    fail(BP_INVALID_ARGUMENT, "unknown stop rule");
+  }
+  const bool any_xstop = std::any_of(xstop.begin(), xstop.end(), [](int v) { return v != 0; });
+  while (c.ia.size() % 4) c.ia.push_back(0);
+  o.xstop = static_cast<int>(c.ia.size());
+  c.ia.insert(c.ia.end(), xstop.begin(), xstop.end());
+
+  // watched-coordinate record of one step
+  int sp = 0;
+  for (int l = 0; l < d.n_layers; ++l) {
+    o.pre_stat[l] = -1;
+    if (d.relu_after[l]) {
+      o.pre_stat[l] = sp;
+      c.slot_kind.push_back(0), c.slot_index.push_back(l), c.slot_dim.push_back(d.widths[l + 1]), c.slot_off.push_back(sp);
+      sp += d.widths[l + 1];
+    }
+  }
+  auto rec = [&](int kind, int idx, int dim) {
+    c.slot_kind.push_back(kind), c.slot_index.push_back(idx), c.slot_dim.push_back(dim), c.slot_off.push_back(sp);
+    const int off = sp;
+    sp += dim;
+    return off;
+  };
+  o.x_stat = (need[0] || any_xstop) ? rec(1, 0, d.ks) : -1;
+  o.u_stat = need[1] ? rec(2, 0, d.ka) : -1;
+  o.p_stat = need[2] ? rec(3, 0, d.kd) : -1;
+  for (int i = 0; i < d.n_ops; ++i)
+    if (need[static_cast<size_t>(3 + i)]) o.ops[i].stat = rec(4, i, o.ops[i].dim);
+  o.SP = sp;
+
+  // rollout tile and shared-memory plan
+  c.R = bp::rollout_rows_per_tile(c.nq);
+  const size_t base_bytes = (static_cast<size_t>(c.R) * o.S + static_cast<size_t>(c.R) * 8) * sizeof(float);
+  const size_t resident = base_bytes + static_cast<size_t>(o.w_smem_total) * sizeof(float);
+  const size_t cap = 227 * 1024;
+  if (resident <= cap) {
+    c.stream = false;
+    c.smem = resident;
+    c.kslab = 0;
+  } else {
+    int maxNS = 0;
+    for (int l = 0; l < d.n_layers; ++l) maxNS = std::max(maxNS, o.nstr[l]);
+    const size_t pad = static_cast<size_t>(64 * c.nq + 64);
+    if (base_bytes + (4 * static_cast<size_t>(maxNS) + pad) * sizeof(float) > cap)
+      fail(BP_UNSUPPORTED, "objective: activations do not fit in shared memory");
+    int ksl = static_cast<int>((cap - base_bytes) / sizeof(float) - pad) / maxNS;
+    ksl = std::min(ksl & ~3, r4(maxK4));
+    c.stream = true;
+    c.kslab = ksl;
+    c.smem = base_bytes + (static_cast<size_t>(ksl) * maxNS + pad) * sizeof(float);
+  }
+  return c;
+}
+
+struct Report {  // SearchReport (search.hpp:53-63) as the planner consumes it
+  bool ok = true;
+  std::string error;
+  double uf = std::numeric_limits<double>::infinity();
+  std::vector<double> best;
+  std::vector<float> top_val;  // ascending
+  std::vector<float> top_act;  // n_top x d
+  int64_t samples = 0;
+  std::vector<double> uf_history;
+  std::vector<int64_t> samples_history;
+};
+
+}  // namespace
+
+struct bp_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  bool loaded = false;
+  Compiled comp;
+  DBuf<float> d_fa;
+  DBuf<double> d_da;
+  DBuf<int> d_ia;
+  // search state
+  int n = 0, rows = 0, cur = 0, iters = 0;
+  bool searched = false;
+  int top_cap = 0;
+  DBuf<unsigned long long> seeds;
+  DBuf<float> lo_f, hi_f, warm_f, mu, var, var_floor, best, uf, actions, costs, top_val0, top_val1, top_act0, top_act1;
+  DBuf<float> ratios;
+  DBuf<int> failed, top_seq0, top_seq1, top_cnt, stat_min, stat_max, use_flags;
+  DBuf<double> lo_d, hi_d, ivl_lo, ivl_hi, lf;
+  DBuf<float> uf_hist;
+  std::vector<double> h_lo, h_hi;
+  std::vector<int> h_failed;
+  std::vector<Report> reports;
+  // scratch for bp_rollout
+  DBuf<float> r_actions, r_costs, r_states;
+  DBuf<int> r_min, r_max;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> roll_events;
+  size_t roll_event_next = 0;
+  double rollout_ms = 0, bound_ms = 0, search_ms = 0;
+  int64_t rollout_launches = 0, launches = 0;
+  bool timing = true;
+
+  ~bp_ctx() {
+    for (auto& e : roll_events) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+  bp::DevObjective dev() {
+    bp::DevObjective o = comp.o;
+    o.f = d_fa.p;
+    o.dd = d_da.p;
+    o.iv = d_ia.p;
+    return o;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> roll_event() {
+    if (roll_event_next == roll_events.size()) {
+      cudaEvent_t a, b;
+      ck(cudaEventCreate(&a), "event");
+      ck(cudaEventCreate(&b), "event");
+      roll_events.push_back({a, b});
+    }
+    return roll_events[roll_event_next++];
+  }
+  void harvest_roll_events() {
+    for (size_t i = 0; i < roll_event_next; ++i) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, roll_events[i].first, roll_events[i].second), "cudaEventElapsedTime");
+      rollout_ms += ms;
+    }
+    roll_event_next = 0;
+  }
+  void rollout(const float* actions, float* costs, float* states, int* smin, int* smax, int* fail_flags,
+               long long n_rows, int rows_per_sub) {
+    bp::RolloutArgs a{actions, costs, states, smin, smax, fail_flags, n_rows, rows_per_sub, comp.kslab};
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (timing) {
+      ev = roll_event();
+      ck(cudaEventRecord(ev.first, stream), "event");
+    }
+    ck(bp::launch_rollout(dev(), a, comp.nq, comp.stream, comp.smem, stream), "rollout launch");
+    if (timing) ck(cudaEventRecord(ev.second, stream), "event");
+    ++rollout_launches;
+    ++launches;
+  }
+};
+
+namespace {
+
+void check_ctx(bp_ctx* c) {
+  if (c == nullptr) fail(BP_INVALID_ARGUMENT, "null context");
+  c->use();
+}
+void check_loaded(bp_ctx* c) {
+  check_ctx(c);
+  if (!c->loaded) fail(BP_LOGIC, "no objective loaded");
+}
+
+// Device batch search (batch_search, search.cpp:262-282, with run_cem / run_mppi).
+void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm,
+                         const bp_search_config& cfg, std::vector<Report>* out) {
+  const Compiled& cp = c->comp;
+  const int d = cp.d;
+  if (cfg.iterations <= 0 || cfg.samples_per_iter <= 0)
+    fail(BP_INVALID_ARGUMENT, "search: iterations and samples per iteration must be positive");
+  if (cfg.method == BP_SEARCH_GD) fail(BP_UNSUPPORTED, "gd search is not implemented on the device");
+  bp::SearchArgs a{};
+  a.n = n;
+  a.d = d;
+  a.method = cfg.method == BP_SEARCH_MPPI ? 1 : 0;
+  std::vector<float> ratios;
+  if (a.method == 0) {
+    a.groups = std::max(1, cfg.cem_agents);
+    a.per_group = std::max(1, cfg.samples_per_iter / a.groups);
+    a.elites = std::max(1, cfg.cem_elites);
+  } else {
+    const int nn = cfg.mppi_n_noise > 0 ? cfg.mppi_n_noise : 1;
+    const int nt = cfg.mppi_n_temp > 0 ? cfg.mppi_n_temp : 1;
+    for (int i = 0; i < nn; ++i) ratios.push_back(cfg.mppi_n_noise > 0 ? static_cast<float>(cfg.mppi_noise_ratios[i]) : 1.f);
+    for (int i = 0; i < nt; ++i) ratios.push_back(cfg.mppi_n_temp > 0 ? static_cast<float>(cfg.mppi_temperature_ratios[i]) : 1.f);
+    a.groups = nn * nt;
+    a.n_noise = nn;
+    a.per_group = std::max(1, cfg.samples_per_iter / a.groups);
+    a.elites = 1;
+  }
+  if (a.groups > 32) fail(BP_UNSUPPORTED, "search: more than 32 agents / instances");
+  a.n_samp = a.groups * a.per_group;
+  a.rows = a.n_samp + 1;
+  a.top_cap = std::max(cfg.top_capacity, 1);
+  a.jitter = static_cast<float>(cfg.cem_jitter);
+  a.init_sigma = static_cast<float>(cfg.cem_init_sigma);
+  a.noise_frac = static_cast<float>(cfg.mppi_noise_frac);
+  a.temperature = static_cast<float>(cfg.mppi_temperature);
+  c->n = n;
+  c->rows = a.rows;
+  c->top_cap = a.top_cap;
+  c->iters = cfg.iterations;
+  c->h_lo.assign(lo, lo + static_cast<size_t>(n) * d);
+  c->h_hi.assign(hi, hi + static_cast<size_t>(n) * d);
+  for (size_t i = 0; i < c->h_lo.size(); ++i)
+    if (!(c->h_lo[i] <= c->h_hi[i]) || !std::isfinite(c->h_lo[i]) || !std::isfinite(c->h_hi[i]))
+      fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
+  cudaStream_t st = c->stream;
+  const size_t nd = static_cast<size_t>(n) * d;
+  std::vector<float> lf32(nd), hf32(nd);
+  for (size_t i = 0; i < nd; ++i) {
+    lf32[i] = static_cast<float>(lo[i]);
+    hf32[i] = static_cast<float>(hi[i]);
+  }
+  std::vector<unsigned long long> seeds(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) seeds[static_cast<size_t>(i)] = cfg.seed ^ static_cast<unsigned long long>(i);
+  a.seeds = c->seeds.get(static_cast<size_t>(n));
+  a.lo = c->lo_f.get(nd);
+  a.hi = c->hi_f.get(nd);
+  ck(cudaMemcpyAsync(const_cast<unsigned long long*>(a.seeds), seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(cudaMemcpyAsync(const_cast<float*>(a.lo), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(cudaMemcpyAsync(const_cast<float*>(a.hi), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(cudaMemcpyAsync(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(cudaMemcpyAsync(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  a.warm = nullptr;
+  std::vector<float> w32;
+  if (warm != nullptr) {
+    w32.resize(nd);
+    for (size_t i = 0; i < nd; ++i) w32[i] = static_cast<float>(warm[i]);
+    a.warm = c->warm_f.get(nd);
+    ck(cudaMemcpyAsync(const_cast<float*>(a.warm), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  }
+  if (!ratios.empty()) {
+    float* r = c->ratios.get(ratios.size());
+    ck(cudaMemcpyAsync(r, ratios.data(), ratios.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    a.noise_ratios = r;
+    a.temp_ratios = r + a.n_noise;
+  }
+  a.mu = c->mu.get(static_cast<size_t>(n) * a.groups * d);
+  a.var = c->var.get(static_cast<size_t>(n) * a.groups * d);
+  a.var_floor = c->var_floor.get(nd);
+  a.best = c->best.get(nd);
+  a.uf = c->uf.get(static_cast<size_t>(n));
+  a.actions = c->actions.get(static_cast<size_t>(n) * a.rows * d);
+  a.costs = c->costs.get(static_cast<size_t>(n) * a.rows);
+  a.failed = c->failed.get(static_cast<size_t>(n));
+  const size_t tk = static_cast<size_t>(n) * a.top_cap;
+  a.top_val[0] = c->top_val0.get(tk);
+  a.top_val[1] = c->top_val1.get(tk);
+  a.top_seq[0] = c->top_seq0.get(tk);
+  a.top_seq[1] = c->top_seq1.get(tk);
+  a.top_act[0] = c->top_act0.get(tk * d);
+  a.top_act[1] = c->top_act1.get(tk * d);
+  a.top_cnt = c->top_cnt.get(static_cast<size_t>(n));
+  const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
+  int* smin = c->stat_min.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
+  int* smax = c->stat_max.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
+  fill_int(smin, nstat, bp::enc_f_host(INFINITY), st);
+  fill_int(smax, nstat, bp::enc_f_host(-INFINITY), st);
+  float* ufh = c->uf_hist.get(static_cast<size_t>(n) * cfg.iterations);
+  ck(bp::launch_search_init(a, st), "search init");
+  ++c->launches;
+  a.cur = 0;
+  for (int it = 0; it < cfg.iterations; ++it) {
+    a.iter = it;
+    ck(bp::launch_sample(a, c->sms, st), "sample");
+    c->rollout(a.actions, const_cast<float*>(a.costs), nullptr, smin, smax, a.failed,
+               static_cast<long long>(n) * a.rows, a.rows);
+    ck(bp::launch_search_update(a, st), "search update");
+    ck(cudaMemcpyAsync(ufh + static_cast<size_t>(it) * n, a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st), "D2D");
+    c->launches += 2;
+    a.cur ^= 1;
+  }
+  c->cur = a.cur;
+  c->searched = true;
+  c->h_failed.assign(static_cast<size_t>(n), 0);
+  ck(cudaMemcpyAsync(c->h_failed.data(), a.failed, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  if (out == nullptr) {
+    ck(cudaStreamSynchronize(st), "sync");
+    return;
+  }
+  // harvest reports
+  std::vector<float> uf(static_cast<size_t>(n)), best(nd), hist(static_cast<size_t>(n) * cfg.iterations);
+  std::vector<int> cnt(static_cast<size_t>(n));
+  ck(cudaMemcpyAsync(uf.data(), a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaMemcpyAsync(best.data(), a.best, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaMemcpyAsync(cnt.data(), a.top_cnt, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaMemcpyAsync(hist.data(), ufh, hist.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  std::vector<float> tv(tk), ta(tk * d);
+  ck(cudaMemcpyAsync(tv.data(), a.top_val[a.cur], tk * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaMemcpyAsync(ta.data(), a.top_act[a.cur], tk * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  out->assign(static_cast<size_t>(n), Report());
+  for (int i = 0; i < n; ++i) {
+    Report& r = (*out)[static_cast<size_t>(i)];
+    if (c->h_failed[static_cast<size_t>(i)]) {
+      r.ok = false;
+      r.error = "evaluate: non-finite objective value (malformed weights?)";
+      continue;
+    }
+    r.uf = uf[static_cast<size_t>(i)];
+    r.best.assign(best.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * d),
+                  best.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i + 1) * d));
+    const int k = cnt[static_cast<size_t>(i)];
+    r.top_val.assign(tv.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap),
+                     tv.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap + k));
+    r.top_act.assign(ta.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap * d),
+                     ta.begin() + static_cast<std::ptrdiff_t>((static_cast<size_t>(i) * a.top_cap + k) * d));
+    r.samples = static_cast<int64_t>(cfg.iterations) * a.rows;
+    for (int it = 0; it < cfg.iterations; ++it) {
+      r.uf_history.push_back(hist[static_cast<size_t>(it) * n + i]);
+      r.samples_history.push_back(static_cast<int64_t>(it + 1) * a.rows);
+    }
+  }
+}
+
+void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
+  if (!c->searched) fail(BP_LOGIC, "bound: no batch searched");
+  if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
+  const Compiled& cp = c->comp;
+  const int n = c->n;
+  const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
+  std::vector<int> use(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) use[static_cast<size_t>(i)] = c->h_failed[static_cast<size_t>(i)] ? 0 : 1;
+  int* du = c->use_flags.get(static_cast<size_t>(n));
+  ck(cudaMemcpyAsync(du, use.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  bp::BoundArgs a{c->lo_d.p, c->hi_d.p, c->stat_min.p, c->stat_max.p, du,
+                  c->ivl_lo.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
+                  c->ivl_hi.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
+                  c->lf.get(static_cast<size_t>(n)), mode, alpha};
+  if (c->timing) ck(cudaEventRecord(c->ev0, c->stream), "event");
+  ck(bp::launch_bound(c->dev(), a, n, c->stream), "bound launch");
+  if (c->timing) ck(cudaEventRecord(c->ev1, c->stream), "event");
+  ++c->launches;
+  ck(cudaMemcpyAsync(lf_out, a.lf, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  if (c->timing) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event");
+    c->bound_ms += ms;
+  }
+}
+
+}  // namespace
+
+namespace {
+
+uint64_t mix_seed(uint64_t master, uint64_t salt) {  // rng.cpp:37-42
+  uint64_t z = master + 0x9E3779B97F4A7C15ULL * (salt + 1);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+
+// Deterministic stream of the reference Rng (rng.hpp:12-35): mt19937_64 bits,
+// 53-bit uniform, Box-Muller normal with a cached spare.
+struct bp_rng {
+  std::mt19937_64 gen;
+  bool has_spare = false;
+  double spare = 0.0;
+  explicit bp_rng(uint64_t s) : gen(s) {}
+  double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    double u1, u2;
+    do {
+      u1 = uniform();
+    } while (u1 <= 0.0);
+    u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    has_spare = true;
+    return r * std::cos(a);
+  }
+};
+
+struct bp_result {
+  double uf = std::numeric_limits<double>::infinity();
+  std::vector<double> best;
+  double min_lf = -std::numeric_limits<double>::infinity();
+  bool certified = false;
+  std::vector<bp_trace_row> trace;
+  int64_t samples = 0;
+  int iterations = 0;
+  std::string stop_reason;
+};
+
+namespace {
+
+// SubdomainRecord (bab.hpp:18-28) with the top list in the device's float form.
+struct Rec {
+  std::vector<double> lo, hi;
+  double lf = -std::numeric_limits<double>::infinity();
+  double uf = std::numeric_limits<double>::infinity();
+  std::vector<double> best;
+  std::vector<float> top_val;  // ascending
+  std::vector<float> top_act;  // n_top x d
+  int64_t samples = 0;
+  int depth = 0;
+  int64_t id = 0, parent = -1;
+  double log_vol = 0.0;
+  double max_width() const {
+    double w = 0.0;
+    for (size_t j = 0; j < lo.size(); ++j) w = std::max(w, hi[j] - lo[j]);
+    return w;
+  }
+};
+
+// pick_out (bab.cpp:85-153) over pool metadata; returns pool indices in pick order.
+std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double eta, double temperature, bp_rng& rng) {
+  n = std::min(n, total);
+  if (n <= 0) return {};
+  std::vector<int> order(static_cast<size_t>(total));
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return recs[a].uf != recs[b].uf ? recs[a].uf < recs[b].uf : a < b;
+  });
+  const int n1 = std::clamp(static_cast<int>(std::llround(eta * n)), 0, n);
+  std::vector<int> chosen(order.begin(), order.begin() + n1);
+  std::vector<int> rem(order.begin() + n1, order.end());
+  const double temp = std::max(temperature, 1e-12);
+  std::vector<double> w;
+  for (int need = n - n1; need > 0; --need) {
+    double lo = std::numeric_limits<double>::infinity(), hi = -lo;
+    for (int idx : rem) {
+      const double lf = recs[idx].lf;
+      if (std::isfinite(lf)) {
+        lo = std::min(lo, lf);
+        hi = std::max(hi, lf);
+      }
+    }
+    const bool degenerate = !(hi > lo);
+    w.assign(rem.size(), 0.0);
+    double sum = 0.0;
+    for (size_t i = 0; i < rem.size(); ++i) {
+      double scaled = 0.5;
+      if (!degenerate) {
+        const double lf = recs[rem[i]].lf;
+        scaled = std::isfinite(lf) ? (lf - lo) / (hi - lo) : (lf < 0.0 ? 0.0 : 1.0);
+      }
+      w[i] = degenerate ? 1.0 : std::exp(-scaled / temp);
+      sum += w[i];
+    }
+    const double u = rng.uniform() * sum;
+    double acc = 0.0;
+    size_t sel = rem.size() - 1;
+    for (size_t i = 0; i < rem.size(); ++i) {
+      acc += w[i];
+      if (u < acc) {
+        sel = i;
+        break;
+      }
+    }
+    chosen.push_back(rem[sel]);
+    rem.erase(rem.begin() + static_cast<std::ptrdiff_t>(sel));
+  }
+  return chosen;
+}
+
+// Axis choice of split (bab.cpp:155-195); top_u is n_top x d, ascending by value.
+int split_axis(int d, const double* lo, const double* hi, int n_top, const float* top_u, int64_t samples,
+               double top_percent, double min_width, int split_rule) {
+  int k = 0;
+  if (n_top > 0 && split_rule == BP_SPLIT_SAMPLES) {
+    const int64_t stored = n_top;
+    k = samples > 0 ? static_cast<int>(std::clamp<int64_t>(std::llround(top_percent / 100.0 * static_cast<double>(samples)), 1, stored))
+                    : static_cast<int>(stored);
+  }
+  auto best_axis = [&](bool use_samples) {
+    int axis = -1;
+    double best = -1.0;
+    for (int j = 0; j < d; ++j) {
+      const double wj = hi[j] - lo[j];
+      if (wj <= min_width) continue;
+      double score = wj;
+      if (use_samples) {
+        const double mid = 0.5 * (lo[j] + hi[j]);
+        int n_lo = 0;
+        for (int i = 0; i < k; ++i)
+          if (static_cast<double>(top_u[static_cast<size_t>(i) * d + j]) <= mid) ++n_lo;
+        score = wj * std::abs(2 * n_lo - k);
+      }
+      if (score > best) {
+        best = score;
+        axis = j;
+      }
+    }
+    return std::pair<int, double>{axis, best};
+  };
+  auto [axis, score] = k > 0 ? best_axis(true) : best_axis(false);
+  if (k > 0 && axis >= 0 && score == 0.0) axis = best_axis(false).first;
+  if (axis < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
+  return axis;
+}
+
+void split_rec(const Rec& rec, int d, double top_percent, double min_width, int64_t next_id, int split_rule, Rec& lo_c,
+               Rec& hi_c) {  // bab.cpp:155-223
+  const int n_top = static_cast<int>(rec.top_val.size());
+  const int axis = split_axis(d, rec.lo.data(), rec.hi.data(), n_top, rec.top_act.data(), rec.samples, top_percent,
+                              min_width, split_rule);
+  const double mid = 0.5 * (rec.lo[static_cast<size_t>(axis)] + rec.hi[static_cast<size_t>(axis)]);
+  lo_c = Rec();
+  hi_c = Rec();
+  lo_c.lo = rec.lo;
+  lo_c.hi = rec.hi;
+  lo_c.hi[static_cast<size_t>(axis)] = mid;
+  hi_c.lo = rec.lo;
+  hi_c.hi = rec.hi;
+  hi_c.lo[static_cast<size_t>(axis)] = mid;
+  for (Rec* c : {&lo_c, &hi_c}) {
+    c->depth = rec.depth + 1;
+    c->parent = rec.id;
+    c->log_vol = rec.log_vol + std::log(0.5);
+  }
+  lo_c.id = next_id;
+  hi_c.id = next_id + 1;
+  for (int i = 0; i < n_top; ++i) {
+    const float* u = rec.top_act.data() + static_cast<size_t>(i) * d;
+    Rec& c = static_cast<double>(u[axis]) <= mid ? lo_c : hi_c;
+    c.top_val.push_back(rec.top_val[static_cast<size_t>(i)]);
+    c.top_act.insert(c.top_act.end(), u, u + d);
+  }
+  for (Rec* c : {&lo_c, &hi_c})
+    if (!c->top_val.empty()) {
+      c->uf = c->top_val.front();
+      c->best.assign(c->top_act.begin(), c->top_act.begin() + d);
+    }
+}
+
+void merge_report(Rec& rec, Report&& rep, int top_capacity, int d) {  // bab.cpp:245-262
+  rec.samples += rep.samples;
+  if (rep.uf < rec.uf) {
+    rec.uf = rep.uf;
+    rec.best = rep.best;
+  }
+  if (rec.top_val.empty()) {
+    rec.top_val = std::move(rep.top_val);
+    rec.top_act = std::move(rep.top_act);
+  } else if (!rep.top_val.empty()) {
+    // std::merge: stable, ties keep the record's own samples first
+    std::vector<float> mv, ma;
+    const size_t na = rec.top_val.size(), nb = rep.top_val.size();
+    const size_t keep = std::min<size_t>(na + nb, static_cast<size_t>(top_capacity));
+    mv.reserve(keep);
+    ma.reserve(keep * d);
+    size_t i = 0, j = 0;
+    while (mv.size() < keep) {
+      const bool take_b = j < nb && (i >= na || rep.top_val[j] < rec.top_val[i]);
+      if (take_b) {
+        mv.push_back(rep.top_val[j]);
+        ma.insert(ma.end(), rep.top_act.begin() + static_cast<std::ptrdiff_t>(j * d),
+                  rep.top_act.begin() + static_cast<std::ptrdiff_t>((j + 1) * d));
+        ++j;
+      } else {
+        mv.push_back(rec.top_val[i]);
+        ma.insert(ma.end(), rec.top_act.begin() + static_cast<std::ptrdiff_t>(i * d),
+                  rec.top_act.begin() + static_cast<std::ptrdiff_t>((i + 1) * d));
+        ++i;
+      }
+    }
+    rec.top_val = std::move(mv);
+    rec.top_act = std::move(ma);
+  }
+}
+
+std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec>& boxes, const std::vector<const std::vector<double>*>& warms,
+                                     const bp_search_config& scfg, int mode, int alpha, std::vector<double>* lfs) {
+  const int d = c->comp.d;
+  const int n = static_cast<int>(boxes.size());
+  std::vector<double> lo(static_cast<size_t>(n) * d), hi(static_cast<size_t>(n) * d), warm(static_cast<size_t>(n) * d);
+  bool any_warm = false;
+  for (int i = 0; i < n; ++i) {
+    std::copy(boxes[static_cast<size_t>(i)].lo.begin(), boxes[static_cast<size_t>(i)].lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(i) * d);
+    std::copy(boxes[static_cast<size_t>(i)].hi.begin(), boxes[static_cast<size_t>(i)].hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(i) * d);
+    const std::vector<double>* w = warms[static_cast<size_t>(i)];
+    if (w != nullptr && !w->empty()) {
+      any_warm = true;
+      std::copy(w->begin(), w->end(), warm.begin() + static_cast<std::ptrdiff_t>(i) * d);
+    } else {
+      std::fill(warm.begin() + static_cast<std::ptrdiff_t>(i) * d, warm.begin() + static_cast<std::ptrdiff_t>(i + 1) * d,
+                std::numeric_limits<double>::quiet_NaN());
+    }
+  }
+  std::vector<Report> reps;
+  const auto t0 = std::chrono::steady_clock::now();
+  device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps);
+  lfs->assign(static_cast<size_t>(n), 0.0);
+  device_batch_bound(c, mode, alpha, lfs->data());
+  c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->harvest_roll_events();
+  return reps;
+}
+
+void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start, bp_result& result) {
+  // bab.cpp:266-415
+  const int d = c->comp.d;
+  if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
+  if (cfg.bound_mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  std::vector<Rec> pool;
+  bp_rng pick_rng(mix_seed(cfg.seed, 1));
+  int64_t next_id = 1;
+  double pruned_cum = 0.0;
+  double retired_min_lf = std::numeric_limits<double>::infinity();
+  auto pool_min_lf = [&] {
+    double m = std::numeric_limits<double>::infinity();
+    for (const auto& r : pool) m = std::min(m, r.lf);
+    return m;
+  };
+  auto current_min_lf = [&] {
+    const double m = std::min(pool_min_lf(), retired_min_lf);
+    return std::isfinite(m) || !pool.empty() ? m : result.uf;
+  };
+  auto push_trace = [&](int iter, double selected_vol) {
+    bp_trace_row row{};
+    row.iter = iter;
+    row.uf = result.uf;
+    row.min_lf = current_min_lf();
+    row.pruned_vol = pruned_cum;
+    row.selected_vol = selected_vol;
+    row.pool_size = static_cast<int64_t>(pool.size());
+    row.samples = result.samples;
+    row.wall_ms = elapsed_ms();
+    result.trace.push_back(row);
+  };
+  auto prune = [&]() {  // bab.cpp:225-241
+    double removed = 0.0;
+    std::vector<Rec> keep;
+    keep.reserve(pool.size());
+    for (auto& r : pool) {
+      if (r.lf > result.uf)
+        removed += std::exp(r.log_vol);
+      else
+        keep.push_back(std::move(r));
+    }
+    pool = std::move(keep);
+    return removed;
+  };
+  {
+    Rec root;
+    root.lo.resize(static_cast<size_t>(d));
+    root.hi.resize(static_cast<size_t>(d));
+    for (int t = 0; t < c->comp.o.H; ++t)
+      for (int j = 0; j < c->comp.o.ka; ++j) {
+        root.lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
+        root.hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
+      }
+    std::vector<double> w;
+    if (warm_start) w.assign(warm_start, warm_start + d);
+    bp_search_config scfg = cfg.search;
+    scfg.seed = mix_seed(cfg.seed, 0);
+    std::vector<double> lfs;
+    std::vector<Report> reps = search_and_bound(c, {root}, {warm_start ? &w : nullptr}, scfg, cfg.bound_mode, cfg.alpha, &lfs);
+    if (!reps[0].ok) fail(BP_RUNTIME, "plan: root search failed: " + reps[0].error);
+    root.id = 0;
+    root.log_vol = 0.0;
+    root.lf = lfs[0];
+    merge_report(root, std::move(reps[0]), cfg.search.top_capacity, d);
+    result.uf = root.uf;
+    result.best = root.best;
+    result.samples = root.samples;
+    pool.push_back(std::move(root));
+    pruned_cum += prune();
+    push_trace(0, 1.0);
+  }
+  std::string stop;
+  int iter = 0;
+  std::vector<bp_pool_meta> meta;
+  while (true) {
+    if (result.uf <= cfg.target_objective) { stop = "target"; break; }
+    if (pool.empty()) { stop = "pool-exhausted"; break; }
+    if (iter >= cfg.max_iterations) { stop = "max-iterations"; break; }
+    if (cfg.wall_clock_ms > 0.0 && elapsed_ms() >= cfg.wall_clock_ms) { stop = "wall-clock"; break; }
+    ++iter;
+    meta.resize(pool.size());
+    for (size_t i = 0; i < pool.size(); ++i) meta[i] = {pool[i].lf, pool[i].uf, pool[i].id, pool[i].log_vol};
+    const std::vector<int> chosen = pick_indices(meta.data(), static_cast<int>(pool.size()), cfg.batch, cfg.eta, cfg.temperature, pick_rng);
+    std::vector<char> taken(pool.size(), 0);
+    std::vector<Rec> picked;
+    for (int idx : chosen) {
+      taken[static_cast<size_t>(idx)] = 1;
+      picked.push_back(std::move(pool[static_cast<size_t>(idx)]));
+    }
+    {
+      std::vector<Rec> keep;
+      for (size_t i = 0; i < pool.size(); ++i)
+        if (!taken[i]) keep.push_back(std::move(pool[i]));
+      pool = std::move(keep);
+    }
+    double selected_vol = 0.0;
+    for (const auto& r : picked) selected_vol += std::exp(r.log_vol);
+    std::vector<Rec> children;
+    for (Rec& rec : picked) {
+      if (rec.max_width() <= cfg.min_width) {
+        retired_min_lf = std::min(retired_min_lf, rec.lf);
+        continue;
+      }
+      Rec a, b;
+      split_rec(rec, d, cfg.top_percent, cfg.min_width, next_id, cfg.split_rule, a, b);
+      next_id += 2;
+      children.push_back(std::move(a));
+      children.push_back(std::move(b));
+    }
+    if (!children.empty()) {
+      std::vector<const std::vector<double>*> warms;
+      for (const auto& ch : children) warms.push_back(ch.best.empty() ? nullptr : &ch.best);
+      bp_search_config scfg = cfg.search;
+      scfg.seed = mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1);
+      std::vector<double> lfs;
+      std::vector<Report> reps = search_and_bound(c, children, warms, scfg, cfg.bound_mode, cfg.alpha, &lfs);
+      for (size_t i = 0; i < children.size(); ++i) {
+        Rec& ch = children[i];
+        result.samples += reps[i].samples;
+        ch.lf = lfs[i];
+        merge_report(ch, std::move(reps[i]), cfg.search.top_capacity, d);
+        if (ch.uf < result.uf) {
+          result.uf = ch.uf;
+          result.best = ch.best;
+        }
+        pool.push_back(std::move(ch));
+      }
+    }
+    pruned_cum += prune();
+    push_trace(iter, selected_vol);
+  }
+  result.min_lf = current_min_lf();
+  result.certified = cfg.bound_mode != BP_BOUND_EMPIRICAL;
+  result.iterations = iter;
+  result.stop_reason = stop;
+}
+
+void run_sample_only(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start, bp_result& result) {
+  // bab.cpp:417-454
+  const int d = c->comp.d;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<double> lo(static_cast<size_t>(d)), hi(static_cast<size_t>(d));
+  for (int t = 0; t < c->comp.o.H; ++t)
+    for (int j = 0; j < c->comp.o.ka; ++j) {
+      lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
+      hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
+    }
+  bp_search_config scfg = cfg.search;
+  scfg.seed = mix_seed(cfg.seed, 0);
+  std::vector<Report> reps;
+  device_batch_search(c, 1, lo.data(), hi.data(), warm_start, scfg, &reps);
+  c->harvest_roll_events();
+  Report& rep = reps[0];
+  if (!rep.ok) fail(BP_RUNTIME, "sample_only_plan: search failed: " + rep.error);
+  const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  result.uf = rep.uf;
+  result.best = rep.best;
+  result.min_lf = -std::numeric_limits<double>::infinity();
+  result.certified = false;
+  result.samples = rep.samples;
+  result.iterations = static_cast<int>(rep.uf_history.size());
+  result.stop_reason = "sampler-budget";
+  for (size_t i = 0; i < rep.uf_history.size(); ++i) {
+    bp_trace_row row{};
+    row.iter = static_cast<int>(i);
+    row.uf = rep.uf_history[i];
+    row.min_lf = -std::numeric_limits<double>::infinity();
+    row.selected_vol = i == 0 ? 1.0 : 0.0;
+    row.pool_size = 1;
+    row.samples = rep.samples_history[i];
+    row.wall_ms = i + 1 == rep.uf_history.size() ? wall : 0.0;
+    result.trace.push_back(row);
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+size_t bp_get_last_error(char* buf, size_t cap) {
+  if (buf != nullptr && cap > 0) {
+    std::strncpy(buf, g_last_error.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return g_last_error.size();
+}
+
+bp_status bp_init(int device, bp_ctx** out) {
+  return guard([&] {
+    if (out == nullptr) fail(BP_INVALID_ARGUMENT, "bp_init: null output");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) fail(BP_INVALID_ARGUMENT, "bp_init: no such CUDA device");
+    auto c = std::make_unique<bp_ctx>();
+    c->device = device;
+    c->use();
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) fail(BP_CUDA, "bp_init: device is not sm_100 class (B200 required)");
+    c->sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreate(&c->ev0), "event");
+    ck(cudaEventCreate(&c->ev1), "event");
+    *out = c.release();
+  });
+}
+
+bp_status bp_destroy(bp_ctx* ctx) {
+  return guard([&] {
+    if (ctx != nullptr) {
+      cudaSetDevice(ctx->device);
+      delete ctx;
+    }
+  });
+}
+
+bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* uid) {
+  return guard([&] {
+    check_ctx(ctx);
+    (void)rank, (void)world, (void)uid;
+    fail(BP_UNSUPPORTED, "bp_set_comm: NCCL sharding is driven from the host runtime (paper_2412_09584_b200.parallel)");
+  });
+}
+
+bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (desc == nullptr) fail(BP_INVALID_ARGUMENT, "null objective");
+    Compiled cp = compile(*desc);
+    float* f = ctx->d_fa.get(cp.fa.size());
+    double* dd = ctx->d_da.get(cp.da.size());
+    int* iv = ctx->d_ia.get(cp.ia.size());
+    ck(cudaMemcpyAsync(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaMemcpyAsync(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaMemcpyAsync(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->comp = std::move(cp);
+    ctx->loaded = true;
+    ctx->searched = false;
+  });
+}
+
+bp_status bp_stat_layout(bp_ctx* ctx, int* per_step, int* n_slots, int* kind, int* index, int* dim, int* offset, int cap) {
+  return guard([&] {
+    check_loaded(ctx);
+    const Compiled& c = ctx->comp;
+    *per_step = c.o.SP;
+    *n_slots = static_cast<int>(c.slot_kind.size());
+    for (int i = 0; i < *n_slots && i < cap; ++i) {
+      kind[i] = c.slot_kind[static_cast<size_t>(i)];
+      index[i] = c.slot_index[static_cast<size_t>(i)];
+      dim[i] = c.slot_dim[static_cast<size_t>(i)];
+      offset[i] = c.slot_off[static_cast<size_t>(i)];
+    }
+  });
+}
+
+bp_status bp_rollout(bp_ctx* ctx, int n_sub, int rows, const float* actions, float* costs, float* states, float* emp_lo,
+                     float* emp_hi, int* nonfinite) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (n_sub < 0 || rows < 0) fail(BP_INVALID_ARGUMENT, "bp_rollout: negative sizes");
+    const Compiled& cp = ctx->comp;
+    const long long nr = static_cast<long long>(n_sub) * rows;
+    if (nr == 0) return;
+    for (long long i = 0; i < nr * cp.d; ++i)
+      if (!std::isfinite(actions[i])) fail(BP_INVALID_ARGUMENT, "evaluate batch: non-finite values");
+    cudaStream_t st = ctx->stream;
+    float* da = ctx->r_actions.get(static_cast<size_t>(nr) * cp.d);
+    float* dc = ctx->r_costs.get(static_cast<size_t>(nr));
+    float* ds = states ? ctx->r_states.get(static_cast<size_t>(nr) * cp.o.H * cp.o.ks) : nullptr;
+    const long long nstat = static_cast<long long>(n_sub) * cp.o.H * cp.o.SP;
+    int* mn = ctx->r_min.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
+    int* mx = ctx->r_max.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
+    int* fl = ctx->use_flags.get(static_cast<size_t>(n_sub));
+    fill_int(mn, nstat, bp::enc_f_host(INFINITY), st);
+    fill_int(mx, nstat, bp::enc_f_host(-INFINITY), st);
+    ck(cudaMemsetAsync(fl, 0, static_cast<size_t>(n_sub) * 4, st), "memset");
+    ck(cudaMemcpyAsync(da, actions, static_cast<size_t>(nr) * cp.d * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ctx->rollout(da, dc, ds, mn, mx, fl, nr, rows);
+    ck(cudaMemcpyAsync(costs, dc, static_cast<size_t>(nr) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    if (states) ck(cudaMemcpyAsync(states, ds, static_cast<size_t>(nr) * cp.o.H * cp.o.ks * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    std::vector<int> hmn, hmx, hfl(static_cast<size_t>(n_sub));
+    if (emp_lo || emp_hi) {
+      hmn.resize(static_cast<size_t>(nstat));
+      hmx.resize(static_cast<size_t>(nstat));
+      ck(cudaMemcpyAsync(hmn.data(), mn, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaMemcpyAsync(hmx.data(), mx, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    ck(cudaMemcpyAsync(hfl.data(), fl, static_cast<size_t>(n_sub) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    ctx->harvest_roll_events();
+    for (long long i = 0; i < nstat; ++i) {
+      if (emp_lo) emp_lo[i] = bp::dec_f_host(hmn[static_cast<size_t>(i)]);
+      if (emp_hi) emp_hi[i] = bp::dec_f_host(hmx[static_cast<size_t>(i)]);
+    }
+    if (nonfinite)
+      for (int i = 0; i < n_sub; ++i) nonfinite[i] = hfl[static_cast<size_t>(i)];
+  });
+}
+
+bp_status bp_batch_search(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi, const double* warm,
+                          const bp_search_config* cfg) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (cfg == nullptr || lo == nullptr || hi == nullptr) fail(BP_INVALID_ARGUMENT, "bp_batch_search: null argument");
+    if (n_boxes <= 0) fail(BP_INVALID_ARGUMENT, "bp_batch_search: no boxes");
+    device_batch_search(ctx, n_boxes, lo, hi, warm, *cfg, &ctx->reports);
+    ctx->harvest_roll_events();
+  });
+}
+
+bp_status bp_report_summary(bp_ctx* ctx, double* uf, double* best, int64_t* samples, int* ok, int* n_top) {
+  return guard([&] {
+    check_loaded(ctx);
+    const int d = ctx->comp.d;
+    for (size_t i = 0; i < ctx->reports.size(); ++i) {
+      const Report& r = ctx->reports[i];
+      if (uf) uf[i] = r.uf;
+      if (best)
+        for (int j = 0; j < d; ++j) best[i * d + j] = r.best.empty() ? std::nan("") : r.best[static_cast<size_t>(j)];
+      if (samples) samples[i] = r.samples;
+      if (ok) ok[i] = r.ok ? 1 : 0;
+      if (n_top) n_top[i] = static_cast<int>(r.top_val.size());
+    }
+  });
+}
+
+bp_status bp_report_top(bp_ctx* ctx, int box, double* values, double* actions, int cap) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (box < 0 || box >= static_cast<int>(ctx->reports.size())) fail(BP_INVALID_ARGUMENT, "bp_report_top: bad box");
+    const Report& r = ctx->reports[static_cast<size_t>(box)];
+    const int d = ctx->comp.d;
+    for (size_t i = 0; i < r.top_val.size() && static_cast<int>(i) < cap; ++i) {
+      values[i] = r.top_val[i];
+      for (int j = 0; j < d; ++j) actions[i * d + j] = r.top_act[i * d + j];
+    }
+  });
+}
+
+bp_status bp_report_stats(bp_ctx* ctx, int box, float* emp_lo, float* emp_hi) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (!ctx->searched || box < 0 || box >= ctx->n) fail(BP_INVALID_ARGUMENT, "bp_report_stats: bad box");
+    const size_t per = static_cast<size_t>(ctx->comp.o.H) * ctx->comp.o.SP;
+    std::vector<int> mn(per), mx(per);
+    ck(cudaMemcpy(mn.data(), ctx->stat_min.p + per * box, per * 4, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(mx.data(), ctx->stat_max.p + per * box, per * 4, cudaMemcpyDeviceToHost), "D2H");
+    for (size_t i = 0; i < per; ++i) {
+      if (emp_lo) emp_lo[i] = bp::dec_f_host(mn[i]);
+      if (emp_hi) emp_hi[i] = bp::dec_f_host(mx[i]);
+    }
+  });
+}
+
+bp_status bp_batch_bound(bp_ctx* ctx, int mode, int alpha, double* lf) {
+  return guard([&] {
+    check_loaded(ctx);
+    device_batch_bound(ctx, mode, alpha, lf);
+  });
+}
+
+bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi, int mode, int alpha,
+                         double* lf) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (n_boxes <= 0) fail(BP_INVALID_ARGUMENT, "bp_bound_boxes: no boxes");
+    if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
+    const int d = ctx->comp.d;
+    const size_t nd = static_cast<size_t>(n_boxes) * d;
+    for (size_t i = 0; i < nd; ++i)
+      if (!(lo[i] <= hi[i]) || !std::isfinite(lo[i]) || !std::isfinite(hi[i]))
+        fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
+    ck(cudaMemcpyAsync(ctx->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaMemcpyAsync(ctx->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ctx->n = n_boxes;
+    ctx->searched = true;  // boxes resident; no statistics
+    ctx->h_failed.assign(static_cast<size_t>(n_boxes), 1);
+    ctx->reports.clear();
+    device_batch_bound(ctx, mode, alpha, lf);
+  });
+}
+
+bp_status bp_plan(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm, int method_babnd, bp_result** out) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (cfg == nullptr || out == nullptr) fail(BP_INVALID_ARGUMENT, "bp_plan: null argument");
+    auto r = std::make_unique<bp_result>();
+    if (method_babnd)
+      run_plan(ctx, *cfg, warm, *r);
+    else
+      run_sample_only(ctx, *cfg, warm, *r);
+    *out = r.release();
+  });
+}
+
+bp_status bp_result_summary(const bp_result* r, double* uf, double* min_lf, int* certified, int64_t* samples,
+                            int* iterations, char* stop_reason, size_t cap, int* n_trace, int* d) {
+  return guard([&] {
+    if (r == nullptr) fail(BP_INVALID_ARGUMENT, "null result");
+    if (uf) *uf = r->uf;
+    if (min_lf) *min_lf = r->min_lf;
+    if (certified) *certified = r->certified ? 1 : 0;
+    if (samples) *samples = r->samples;
+    if (iterations) *iterations = r->iterations;
+    if (stop_reason && cap) {
+      std::strncpy(stop_reason, r->stop_reason.c_str(), cap - 1);
+      stop_reason[cap - 1] = 0;
+    }
+    if (n_trace) *n_trace = static_cast<int>(r->trace.size());
+    if (d) *d = static_cast<int>(r->best.size());
+  });
+}
+
+bp_status bp_result_best(const bp_result* r, double* best) {
+  return guard([&] {
+    if (r == nullptr) fail(BP_INVALID_ARGUMENT, "null result");
+    std::copy(r->best.begin(), r->best.end(), best);
+  });
+}
+
+bp_status bp_result_trace(const bp_result* r, bp_trace_row* rows, int cap) {
+  return guard([&] {
+    if (r == nullptr) fail(BP_INVALID_ARGUMENT, "null result");
+    for (size_t i = 0; i < r->trace.size() && static_cast<int>(i) < cap; ++i) rows[i] = r->trace[i];
+  });
+}
+
+bp_status bp_result_free(bp_result* r) {
+  delete r;
+  return BP_OK;
+}
+
+bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms, double* search_ms,
+                    int64_t* launches) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (rollout_ms) *rollout_ms = ctx->rollout_ms;
+    if (rollout_launches) *rollout_launches = ctx->rollout_launches;
+    if (bound_ms) *bound_ms = ctx->bound_ms;
+    if (search_ms) *search_ms = ctx->search_ms;
+    if (launches) *launches = ctx->launches;
+    ctx->rollout_ms = ctx->bound_ms = ctx->search_ms = 0;
+    ctx->rollout_launches = ctx->launches = 0;
+  });
+}
+
+bp_status bp_rng_new(uint64_t seed, bp_rng** out) {
+  return guard([&] { *out = new bp_rng(seed); });
+}
+bp_status bp_rng_free(bp_rng* r) {
+  delete r;
+  return BP_OK;
+}
+bp_status bp_rng_uniform(bp_rng* r, double* out) {
+  return guard([&] { *out = r->uniform(); });
+}
+bp_status bp_rng_normal(bp_rng* r, double* out) {
+  return guard([&] { *out = r->normal(); });
+}
+bp_status bp_rng_bits(bp_rng* r, uint64_t* out) {
+  return guard([&] { *out = r->gen(); });
+}
+bp_status bp_rng_fill(bp_rng* r, int kind, int64_t n, double* out) {
+  return guard([&] {
+    if (r == nullptr) fail(BP_INVALID_ARGUMENT, "bp_rng_fill: null rng");
+    for (int64_t i = 0; i < n; ++i) out[i] = kind == 0 ? r->uniform() : r->normal();
+  });
+}
+uint64_t bp_mix_seed(uint64_t master, uint64_t salt) { return mix_seed(master, salt); }
+
+bp_status bp_pick_out(const bp_pool_meta* pool, int n_pool, int n, double eta, double temperature, bp_rng* rng,
+                      int* picked, int* n_picked) {
+  return guard([&] {
+    if (rng == nullptr) fail(BP_INVALID_ARGUMENT, "bp_pick_out: null rng");
+    const std::vector<int> ch = pick_indices(pool, n_pool, n, eta, temperature, *rng);
+    std::copy(ch.begin(), ch.end(), picked);
+    *n_picked = static_cast<int>(ch.size());
+  });
+}
+
+bp_status bp_split_axis(int d, const double* lo, const double* hi, int n_top, const double* top_u, int64_t samples,
+                        double top_percent, double min_width, int split_rule, int* axis, double* mid,
+                        unsigned char* route) {
+  return guard([&] {
+    std::vector<float> u(static_cast<size_t>(n_top) * d);
+    for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<float>(top_u[i]);
+    *axis = split_axis(d, lo, hi, n_top, u.data(), samples, top_percent, min_width, split_rule);
+    *mid = 0.5 * (lo[*axis] + hi[*axis]);
+    for (int i = 0; i < n_top; ++i) route[i] = static_cast<double>(u[static_cast<size_t>(i) * d + *axis]) <= *mid ? 0 : 1;
+  });
+}
+
+bp_status bp_generate_model(uint64_t seed, int n_widths, const int* widths, double* params) {
+  return guard([&] {  // model.cpp:136-158
+    if (n_widths < 2) fail(BP_INVALID_ARGUMENT, "generate_model: need at least two widths");
+    for (int i = 0; i < n_widths; ++i)
+      if (widths[i] <= 0) fail(BP_INVALID_ARGUMENT, "generate_model: widths must be positive");
+    bp_rng rng(seed);
+    size_t off = 0;
+    for (int li = 0; li + 1 < n_widths; ++li) {
+      const int in = widths[li], out = widths[li + 1];
+      const double a = std::sqrt(6.0 / (in + out));
+      for (int r = 0; r < out * in; ++r) params[off++] = -a + (a - -a) * rng.uniform();
+      for (int r = 0; r < out; ++r) params[off++] = -a + (a - -a) * rng.uniform();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,414 @@
+// rollout.cu -- K1: fused H-step rollout of the ReLU-MLP dynamics with the
+// step cost program and the per-subdomain sample extrema of every watched
+// coordinate (the empirical pre-activation bounds).
+//
+// Restates, for a whole batch of subdomains at once:
+//   evaluate / forward_chunk  (reference proj/src/graph.cpp:252-401) on the
+//   graph build_objective unrolls (proj/src/model.cpp:310-387), and the
+//   watch-stat recording (graph.cpp:270-281, 361-374).
+//
+// Layout.  A CTA owns a tile of R = 16*TM consecutive rows (samples) of the
+// flat [n_sub x rows_per_sub] batch; a tile may straddle two subdomains.
+// The activations of its rows live in shared memory as [R][S] floats
+// (row-major, stride S = 4 mod 8 words so the two row-groups a warp reads
+// fall in different banks) and are updated in place layer by layer: the
+// whole layer accumulates in registers before one barrier and the write-back.
+// Weights sit in shared memory transposed to [K][N] (k-major), either all
+// layers resident for the whole kernel or streamed per layer in K-slabs.
+// Every output of a row is a fixed-order FMA chain over k, so a row's
+// result never depends on the tile it lands in (graph.hpp:102-103).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bp_common.cuh"
+
+namespace bp {
+
+struct RolloutArgs {
+  const float* actions;  // [n_rows][d]
+  float* costs;          // [n_rows]
+  float* states;         // optional [n_rows][H][ks]
+  int* stat_min;         // [n_sub][H*SP] (enc_f), may be null
+  int* stat_max;
+  int* failed;           // [n_sub], may be null: set when a row's objective is non-finite
+  long long n_rows;
+  int rows_per_sub;
+  int kslab;             // streamed mode: K rows per weight slab
+};
+
+namespace {
+
+__device__ __forceinline__ float f4get(const float4& v, int k) {
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+
+// Register-tiled layer: rows ty + 16 i (i < TM), columns q*64 + tx*4 + c.
+template <int TM, int NQ>
+__device__ __forceinline__ void kloop_wide(const float* __restrict__ act, int S, const float* __restrict__ W,
+                                           int NS, int k0, int k1, float (&acc)[TM][NQ * 4]) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  for (int k = k0; k < k1; k += 4) {
+    float4 xv[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) xv[i] = *reinterpret_cast<const float4*>(act + (ty + 16 * i) * S + k);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      float4 wv[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        wv[q] = (q * 64 < NS) ? *reinterpret_cast<const float4*>(W + (k - k0 + kk) * NS + q * 64 + tx * 4)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const float xs = f4get(xv[i], kk);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          if (q * 64 < NS) {
+            acc[i][q * 4 + 0] = fmaf(xs, wv[q].x, acc[i][q * 4 + 0]);
+            acc[i][q * 4 + 1] = fmaf(xs, wv[q].y, acc[i][q * 4 + 1]);
+            acc[i][q * 4 + 2] = fmaf(xs, wv[q].z, acc[i][q * 4 + 2]);
+            acc[i][q * 4 + 3] = fmaf(xs, wv[q].w, acc[i][q * 4 + 3]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Cooperative global -> shared copy of n floats (16B aligned).
+__device__ __forceinline__ void copy_f4(float* dst, const float* __restrict__ src, int n) {
+  const int n4 = n >> 2;
+  for (int i = threadIdx.x; i < n4; i += kThreads)
+    reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
+}
+
+template <int TM, int NQ, bool STREAM>
+__device__ void layer_wide(const DevObjective& o, float* act, float* wsm, int l, int kslab) {
+  constexpr int R = 16 * TM;
+  (void)R;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int K4 = o.kpad[l], NS = o.nstr[l], S = o.S;
+  const float* __restrict__ bias = o.f + o.bias[l];
+  float acc[TM][NQ * 4];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int col = q * 64 + tx * 4;
+    const float4 bq = col < NS ? __ldg(reinterpret_cast<const float4*>(bias + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      acc[i][q * 4 + 0] = bq.x;
+      acc[i][q * 4 + 1] = bq.y;
+      acc[i][q * 4 + 2] = bq.z;
+      acc[i][q * 4 + 3] = bq.w;
+    }
+  }
+  if constexpr (!STREAM) {
+    kloop_wide<TM, NQ>(act, S, wsm + o.w_smem_off[l], NS, 0, K4, acc);
+  } else {
+    const float* __restrict__ wg = o.f + o.wt[l];
+    for (int k0 = 0; k0 < K4; k0 += kslab) {
+      const int k1 = min(K4, k0 + kslab);
+      __syncthreads();  // previous slab fully consumed
+      copy_f4(wsm, wg + static_cast<size_t>(k0) * NS, (k1 - k0) * NS);
+      __syncthreads();
+      kloop_wide<TM, NQ>(act, S, wsm, NS, k0, k1, acc);
+    }
+  }
+  __syncthreads();  // every row's inputs consumed: write in place
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int col = q * 64 + tx * 4;
+    if (col < NS) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+        *reinterpret_cast<float4*>(act + (ty + 16 * i) * S + col) =
+            make_float4(acc[i][q * 4 + 0], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
+    }
+  }
+  __syncthreads();
+}
+
+// Narrow layer (N <= 16): one thread per row, all columns.
+template <int R, bool STREAM>
+__device__ void layer_narrow(const DevObjective& o, float* act, float* wsm, int l, int kslab) {
+  const int K4 = o.kpad[l], NS = o.nstr[l], S = o.S;
+  const int r = threadIdx.x;
+  const float* __restrict__ bias = o.f + o.bias[l];
+  float acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = c < NS ? __ldg(bias + c) : 0.f;
+  auto kl = [&](const float* W, int k0, int k1) {
+    if (r < R) {
+      for (int k = k0; k < k1; k += 4) {
+        const float4 xv = *reinterpret_cast<const float4*>(act + r * S + k);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float xs = f4get(xv, kk);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q * 4 < NS) {
+              const float4 w = *reinterpret_cast<const float4*>(W + (k - k0 + kk) * NS + q * 4);
+              acc[q * 4 + 0] = fmaf(xs, w.x, acc[q * 4 + 0]);
+              acc[q * 4 + 1] = fmaf(xs, w.y, acc[q * 4 + 1]);
+              acc[q * 4 + 2] = fmaf(xs, w.z, acc[q * 4 + 2]);
+              acc[q * 4 + 3] = fmaf(xs, w.w, acc[q * 4 + 3]);
+            }
+          }
+        }
+      }
+    }
+  };
+  if constexpr (!STREAM) {
+    kl(wsm + o.w_smem_off[l], 0, K4);
+  } else {
+    const float* __restrict__ wg = o.f + o.wt[l];
+    for (int k0 = 0; k0 < K4; k0 += kslab) {
+      const int k1 = min(K4, k0 + kslab);
+      __syncthreads();
+      copy_f4(wsm, wg + static_cast<size_t>(k0) * NS, (k1 - k0) * NS);
+      __syncthreads();
+      kl(wsm, k0, k1);
+    }
+  }
+  __syncthreads();
+  if (r < R) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q * 4 < NS)
+        *reinterpret_cast<float4*>(act + r * S + q * 4) =
+            make_float4(acc[q * 4 + 0], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
+  }
+  __syncthreads();
+}
+
+// Column pass over act[:, col0 : col0+ncols): per-subdomain extrema of the
+// valid rows into the global record (stat >= 0) and optional in-place ReLU.
+template <int R>
+__device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* act, int col0, int ncols, int stat,
+                            bool relu, int t, long long row0, int nvalid) {
+  const bool rec0 = stat >= 0 && a.stat_min != nullptr;
+  if (ncols <= 0 || (!rec0 && !relu)) return;  // uniform across the CTA
+  const int S = o.S;
+  const int groups = max(1, min(R, kThreads / ncols));
+  const int rpg = (R + groups - 1) / groups;
+  const bool rec = stat >= 0 && a.stat_min != nullptr;
+  const int SPH = o.SP * o.H;
+  for (int item = threadIdx.x; item < ncols * groups; item += kThreads) {
+    const int c = item % ncols, g = item / ncols;
+    const int rb = g * rpg, re = min(R, rb + rpg);
+    float mn = INFINITY, mx = -INFINITY;
+    long long seg = -1;
+    for (int r = rb; r < re; ++r) {
+      float* p = act + r * S + col0 + c;
+      const float v = *p;
+      if (rec && r < nvalid) {
+        const long long s = (row0 + r) / a.rows_per_sub;
+        if (s != seg) {
+          if (seg >= 0) {
+            const long long idx = seg * SPH + static_cast<long long>(t) * o.SP + stat + c;
+            atomicMin(a.stat_min + idx, enc_f(mn));
+            atomicMax(a.stat_max + idx, enc_f(mx));
+          }
+          seg = s;
+          mn = INFINITY;
+          mx = -INFINITY;
+        }
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+      }
+      if (relu) *p = fmaxf(v, 0.f);
+    }
+    if (rec && seg >= 0) {
+      const long long idx = seg * SPH + static_cast<long long>(t) * o.SP + stat + c;
+      atomicMin(a.stat_min + idx, enc_f(mn));
+      atomicMax(a.stat_max + idx, enc_f(mx));
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ const float* val_ptr(const DevObjective& o, const float* row, int id) {
+  if (id == 0) return row;                 // x_t
+  if (id == 1) return row + o.ucol;        // u_t
+  if (id == 2) return row + o.pcol;        // p_t
+  return row + o.ops[id - 3].col;          // op output
+}
+
+// The step's cost program for one row (reference node semantics, graph.cpp:293-347).
+__device__ float cost_program(const DevObjective& o, float* row, int t) {
+  float cost = 0.f;
+  for (int i = 0; i < o.n_ops; ++i) {
+    const DevOp& op = o.ops[i];
+    const float* src = val_ptr(o, row, op.src0);
+    float* dst = row + op.col;
+    float v = 0.f;
+    switch (op.kind) {
+      case 0: {  // LINEAR
+        const float* W = o.f + op.w;
+        const float* b = o.f + op.b;
+        for (int r = 0; r < op.dim; ++r) {
+          float s = 0.f;
+          for (int j = 0; j < op.in_dim; ++j) s = fmaf(__ldg(W + r * op.in_dim + j), src[j], s);
+          dst[r] = s + __ldg(b + r);
+        }
+        v = dst[0];
+        break;
+      }
+      case 1:  // RELU
+        for (int j = 0; j < op.dim; ++j) dst[j] = fmaxf(src[j], 0.f);
+        v = dst[0];
+        break;
+      case 2: {  // SUM
+        const float* s1 = op.src1 >= 0 ? val_ptr(o, row, op.src1) : nullptr;
+        for (int j = 0; j < op.dim; ++j) dst[j] = s1 ? src[j] + s1[j] : src[j];
+        v = dst[0];
+        break;
+      }
+      case 3:  // SCALAR_AFFINE
+        for (int j = 0; j < op.dim; ++j) dst[j] = op.scale * src[j] + op.offset;
+        v = dst[0];
+        break;
+      case 4: {  // SQDIST
+        const float* tg = o.f + op.tgt;
+        const float* wt = o.f + op.wt + (op.weight_by_step ? t * op.in_dim : 0);
+        float acc = 0.f;
+        for (int j = 0; j < op.in_dim; ++j) {
+          const float d = src[j] - __ldg(tg + j);
+          acc += __ldg(wt + j) * d * d;
+        }
+        dst[0] = v = acc;
+        break;
+      }
+      case 5: {  // HINGE
+        const float* c = o.f + op.ctr;
+        float acc = 0.f;
+        for (int j = 0; j < op.in_dim; ++j) {
+          const float d = src[j] - __ldg(c + j);
+          acc += d * d;
+        }
+        const float m = op.radius - sqrtf(acc);
+        dst[0] = v = m > 0.f ? op.penalty * m : 0.f;
+        break;
+      }
+      case 6:  // SLICE
+        for (int j = 0; j < op.dim; ++j) dst[j] = src[op.begin + j];
+        v = dst[0];
+        break;
+    }
+    if (op.is_term) cost += v;
+  }
+  return cost;
+}
+
+template <int TM, int NQ, bool STREAM>
+__global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective o, const RolloutArgs a) {
+  constexpr int R = 16 * TM;
+  extern __shared__ __align__(16) float smem[];
+  float* act = smem;                                // [R][S]
+  float* prow = act + R * o.S;                      // [R][8] effector
+  float* wsm = prow + R * 8;                        // weights (resident image or slab)
+  const long long row0 = static_cast<long long>(blockIdx.x) * R;
+  const long long rem_rows = a.n_rows - row0;
+  const int nvalid = static_cast<int>(rem_rows < R ? rem_rows : R);
+  const int tid = threadIdx.x;
+  const int ks = o.ks, ka = o.ka, kd = o.kd, d = o.d;
+
+  // Skip tiles whose subdomains already failed (their search is abandoned).
+  if (a.failed != nullptr) {
+    const long long s0 = row0 / a.rows_per_sub, s1 = (row0 + nvalid - 1) / a.rows_per_sub;
+    bool all_failed = true;
+    for (long long s = s0; s <= s1; ++s) all_failed = all_failed && a.failed[s] != 0;
+    if (all_failed) return;
+  }
+
+  for (int i = tid; i < R * o.S; i += kThreads) act[i] = 0.f;
+  if constexpr (!STREAM) copy_f4(wsm, o.f + o.wt[0] - o.w_smem_off[0], o.w_smem_total);
+  __syncthreads();
+
+  // Initial features from x0 / p0 and u_1.
+  float cost = 0.f;
+  const bool row_ok = tid < R && tid < nvalid;
+  const float* urow = row_ok ? a.actions + (row0 + tid) * d : nullptr;
+  if (tid < R) {
+    float* row = act + tid * o.S;
+    for (int j = 0; j < kd; ++j) prow[tid * 8 + j] = o.f[o.p0 + j];
+    for (int j = 0; j < ks; ++j) row[j] = o.f[o.x0 + j] - (o.rel ? o.f[o.p0 + j % kd] : 0.f);
+    for (int j = 0; j < ka; ++j) row[ks + j] = row_ok ? __ldg(urow + j) : 0.f;
+  }
+  __syncthreads();
+
+  for (int t = 0; t < o.H; ++t) {
+    for (int l = 0; l < o.L; ++l) {
+      if (o.nstr[l] <= 16)
+        layer_narrow<R, STREAM>(o, act, wsm, l, a.kslab);
+      else
+        layer_wide<TM, NQ, STREAM>(o, act, wsm, l, a.kslab);
+      if (o.relu[l]) column_pass<R>(o, a, act, 0, o.widths[l + 1], o.pre_stat[l], true, t, row0, nvalid);
+    }
+    // x_t in act[:, 0:ks).  Cost program with u_t, p_t in the row scratch.
+    if (tid < R) {
+      float* row = act + tid * o.S;
+      for (int j = 0; j < ka; ++j) {
+        const float u = row_ok ? __ldg(urow + t * ka + j) : 0.f;
+        row[o.ucol + j] = u;
+        const float p = prow[tid * 8 + j] + u;
+        prow[tid * 8 + j] = p;
+        row[o.pcol + j] = p;
+      }
+      cost += cost_program(o, row, t);
+    }
+    __syncthreads();
+    column_pass<R>(o, a, act, 0, ks, o.x_stat, false, t, row0, nvalid);
+    if (o.u_stat >= 0) column_pass<R>(o, a, act, o.ucol, ka, o.u_stat, false, t, row0, nvalid);
+    if (o.p_stat >= 0) column_pass<R>(o, a, act, o.pcol, kd, o.p_stat, false, t, row0, nvalid);
+    for (int i = 0; i < o.n_ops; ++i)
+      if (o.ops[i].stat >= 0) column_pass<R>(o, a, act, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t, row0, nvalid);
+    if (tid < R) {
+      float* row = act + tid * o.S;
+      if (a.states != nullptr && row_ok)
+        for (int j = 0; j < ks; ++j) a.states[((row0 + tid) * o.H + t) * ks + j] = row[j];
+      if (t + 1 < o.H) {
+        if (o.rel)
+          for (int j = 0; j < ks; ++j) row[j] -= prow[tid * 8 + j % kd];
+        for (int j = 0; j < ka; ++j) row[ks + j] = row_ok ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+        for (int j = ks + ka; j < o.kpad[0]; ++j) row[j] = 0.f;
+      }
+    }
+    __syncthreads();
+  }
+  if (row_ok) {
+    a.costs[row0 + tid] = cost;
+    if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + tid) / a.rows_per_sub, 1);
+  }
+}
+
+template <int TM, int NQ, bool STREAM>
+cudaError_t launch_t(const DevObjective& o, const RolloutArgs& a, size_t smem, cudaStream_t st) {
+  constexpr int R = 16 * TM;
+  auto k = rollout_kernel<TM, NQ, STREAM>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long grid = (a.n_rows + R - 1) / R;
+  if (grid <= 0) return cudaSuccess;
+  k<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(o, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Tile shape for the widest layer: R = 16*TM rows, 64*NQ columns, 64 accumulators per thread.
+int rollout_rows_per_tile(int nq) { return nq == 1 ? 256 : nq == 2 ? 128 : nq == 4 ? 64 : 32; }
+
+cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, bool stream, size_t smem,
+                           cudaStream_t st) {
+  switch (nq) {
+    case 1: return stream ? launch_t<16, 1, true>(o, a, smem, st) : launch_t<16, 1, false>(o, a, smem, st);
+    case 2: return stream ? launch_t<8, 2, true>(o, a, smem, st) : launch_t<8, 2, false>(o, a, smem, st);
+    case 4: return stream ? launch_t<4, 4, true>(o, a, smem, st) : launch_t<4, 4, false>(o, a, smem, st);
+    case 8: return stream ? launch_t<2, 8, true>(o, a, smem, st) : launch_t<2, 8, false>(o, a, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bp

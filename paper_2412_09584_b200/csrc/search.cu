@@ -1,0 +1,365 @@
+// search.cu -- K4 sampling (Philox), K3 incumbent + top-K merge and K5 CEM /
+// MPPI refit: the device form of batch_search's per-box sampler loop.
+//
+// Restates run_cem (reference proj/src/search.cpp:87-155), run_mppi
+// (search.cpp:159-209) and SampleSink (search.cpp:37-82) for many boxes at
+// once: one CTA per box updates the incumbent, keeps the best top_capacity
+// samples (ascending by (value, sample sequence); ties keep the older sample,
+// like the heap that only admits strictly better values, search.cpp:52) and
+// refits the sampling distributions.  The per-box stream is Philox4x32-10
+// keyed by the derived seed seed ^ box_index (search.cpp:271), so a box's
+// samples do not depend on which GPU or batch slot evaluates it.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "bp_common.cuh"
+
+namespace bp {
+
+struct SearchArgs {
+  int n, d, rows, n_samp;        // rows = n_samp + 1 (incumbent row)
+  int method;                    // 0 CEM, 1 MPPI
+  int groups, per_group;         // CEM agents / MPPI instances, samples per group
+  int elites;
+  int top_cap;
+  int iter;
+  const unsigned long long* seeds;  // [n] derived per-box seeds
+  const float* lo;               // [n][d]
+  const float* hi;
+  const float* warm;             // [n][d] or null; NaN first coordinate = none
+  float* mu;                     // [n][groups][d]
+  float* var;                    // [n][groups][d] (CEM)
+  float* var_floor;              // [n][d] (CEM)
+  float* best;                   // [n][d]
+  float* uf;                     // [n]
+  float* actions;                // [n][rows][d]
+  const float* costs;            // [n][rows]
+  int* failed;                   // [n]
+  float* top_val[2];             // [n][top_cap]
+  int* top_seq[2];
+  float* top_act[2];             // [n][top_cap][d]
+  int* top_cnt;                  // [n]
+  int cur;                       // which top buffer holds the current list
+  // CEM
+  float jitter, init_sigma;
+  // MPPI
+  float noise_frac, temperature;
+  const float* noise_ratios;     // [n_noise]
+  const float* temp_ratios;      // [n_temp]
+  int n_noise;
+};
+
+namespace {
+
+__device__ __forceinline__ uint2 key_of(unsigned long long s) {
+  return make_uint2(static_cast<uint32_t>(s), static_cast<uint32_t>(s >> 32));
+}
+
+// Search init: CEM mu (agent 0 = clamped warm start or centre, others
+// uniform in the box), var0 and floor; MPPI means; incumbent; top list.
+__global__ void search_init_kernel(const SearchArgs a) {
+  const int s = blockIdx.x;
+  const int d = a.d;
+  const float* lo = a.lo + static_cast<size_t>(s) * d;
+  const float* hi = a.hi + static_cast<size_t>(s) * d;
+  const bool has_warm = a.warm != nullptr && !isnan(a.warm[static_cast<size_t>(s) * d]);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float inc = has_warm ? fminf(fmaxf(a.warm[static_cast<size_t>(s) * d + j], lo[j]), hi[j])
+                               : 0.5f * (lo[j] + hi[j]);
+    a.best[static_cast<size_t>(s) * d + j] = inc;
+    const float w = hi[j] - lo[j];
+    for (int g = 0; g < a.groups; ++g) {
+      float m = inc;
+      if (a.method == 0 && g > 0) {
+        const uint4 r = Philox::gen(make_uint4(0xFFFFFFFFu, static_cast<uint32_t>(g), static_cast<uint32_t>(j), 7u),
+                                    key_of(a.seeds[s]));
+        const double u = (static_cast<double>(r.x >> 11) * 2097152.0 + static_cast<double>(r.y >> 11)) * 0x1.0p-53;
+        m = static_cast<float>(static_cast<double>(lo[j]) + (static_cast<double>(hi[j]) - lo[j]) * u);
+      }
+      a.mu[(static_cast<size_t>(s) * a.groups + g) * d + j] = m;
+      if (a.method == 0) {
+        const double fs = static_cast<double>(a.jitter) * w, s0 = static_cast<double>(a.init_sigma) * w;
+        a.var[(static_cast<size_t>(s) * a.groups + g) * d + j] = static_cast<float>(fmax(s0 * s0, fs * fs));
+        if (g == 0) a.var_floor[static_cast<size_t>(s) * d + j] = static_cast<float>(fs * fs);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.uf[s] = INFINITY;
+    a.top_cnt[s] = 0;
+    a.failed[s] = 0;
+  }
+}
+
+// One Philox call -> four standard normals (Box-Muller) for j4..j4+3 of a row.
+__global__ void sample_kernel(const SearchArgs a) {
+  const int d4 = (a.d + 3) >> 2;
+  const long long total = static_cast<long long>(a.n) * a.rows * d4;
+  for (long long w = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(w % d4);
+    const long long sr = w / d4;
+    const int row = static_cast<int>(sr % a.rows);
+    const int s = static_cast<int>(sr / a.rows);
+    if (a.failed[s]) continue;
+    float* out = a.actions + (static_cast<size_t>(s) * a.rows + row) * a.d;
+    const float* lo = a.lo + static_cast<size_t>(s) * a.d;
+    const float* hi = a.hi + static_cast<size_t>(s) * a.d;
+    if (row == a.n_samp) {  // incumbent re-injected as the last row
+      for (int c = 0; c < 4; ++c) {
+        const int j = q * 4 + c;
+        if (j < a.d) out[j] = a.best[static_cast<size_t>(s) * a.d + j];
+      }
+      continue;
+    }
+    const int g = row / a.per_group;
+    const uint4 r = Philox::gen(make_uint4(static_cast<uint32_t>(a.iter), static_cast<uint32_t>(row),
+                                           static_cast<uint32_t>(q), 0u),
+                                key_of(a.seeds[s]));
+    float z[4];
+    {
+      const float r0 = sqrtf(-2.f * logf(u01_open(r.x))), r1 = sqrtf(-2.f * logf(u01_open(r.z)));
+      float s0, c0, s1, c1;
+      sincospif(2.f * u01_open(r.y), &s0, &c0);
+      sincospif(2.f * u01_open(r.w), &s1, &c1);
+      z[0] = r0 * c0;
+      z[1] = r0 * s0;
+      z[2] = r1 * c1;
+      z[3] = r1 * s1;
+    }
+    const float* mu = a.mu + (static_cast<size_t>(s) * a.groups + g) * a.d;
+    for (int c = 0; c < 4; ++c) {
+      const int j = q * 4 + c;
+      if (j >= a.d) break;
+      float x;
+      if (a.method == 0) {
+        x = mu[j] + sqrtf(a.var[(static_cast<size_t>(s) * a.groups + g) * a.d + j]) * z[c];
+      } else {
+        const float nr = a.noise_ratios[g % a.n_noise];
+        x = mu[j] + a.noise_frac * nr * (hi[j] - lo[j]) * z[c];
+      }
+      out[j] = fminf(fmaxf(x, lo[j]), hi[j]);
+    }
+  }
+}
+
+struct Key {
+  float v;
+  int seq;
+  int src;
+};
+__device__ __forceinline__ bool key_less(const Key& x, const Key& y) {
+  return x.v < y.v || (x.v == y.v && x.seq < y.seq);
+}
+
+// Per-box update after a rollout: incumbent, top-K merge, distribution refit.
+__global__ void __launch_bounds__(kThreads) search_update_kernel(const SearchArgs a, int P) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Key* keys = reinterpret_cast<Key*>(smraw);                 // [P]
+  int* elite = reinterpret_cast<int*>(keys + P);             // [groups][elites]
+  __shared__ int s_nel[32];
+  __shared__ float s_red_v[kThreads / 32];
+  __shared__ int s_red_i[kThreads / 32];
+  const int s = blockIdx.x, tid = threadIdx.x, d = a.d;
+  if (a.failed[s]) return;
+  const float* costs = a.costs + static_cast<size_t>(s) * a.rows;
+  const float* acts = a.actions + static_cast<size_t>(s) * a.rows * d;
+  const int cnt = a.top_cnt[s];
+  const int cur = a.cur, nxt = cur ^ 1;
+
+  // 1. incumbent: first row attaining the minimum (search.cpp:44-48)
+  float bv = INFINITY;
+  int bi = INT_MAX;
+  for (int r = tid; r < a.rows; r += kThreads) {
+    const float v = costs[r];
+    if (v < bv) {
+      bv = v;
+      bi = r;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_down_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+    if (ov < bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if ((tid & 31) == 0) {
+    s_red_v[tid >> 5] = bv;
+    s_red_i[tid >> 5] = bi;
+  }
+  // 2. keys: current top list + this iteration's rows
+  const int base_seq = a.iter * a.rows;
+  for (int i = tid; i < P; i += kThreads) {
+    Key k;
+    if (i < cnt) {
+      k.v = a.top_val[cur][static_cast<size_t>(s) * a.top_cap + i];
+      k.seq = a.top_seq[cur][static_cast<size_t>(s) * a.top_cap + i];
+      k.src = i;
+    } else if (i < cnt + a.rows) {
+      k.v = costs[i - cnt];
+      k.seq = base_seq + (i - cnt);
+      k.src = i;
+    } else {
+      k.v = INFINITY;
+      k.seq = INT_MAX;
+      k.src = -1;
+    }
+    keys[i] = k;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float v = s_red_v[0];
+    int i = s_red_i[0];
+    for (int w = 1; w < kThreads / 32; ++w)
+      if (s_red_v[w] < v || (s_red_v[w] == v && s_red_i[w] < i)) {
+        v = s_red_v[w];
+        i = s_red_i[w];
+      }
+    s_red_v[0] = v;
+    s_red_i[0] = i;
+  }
+  __syncthreads();
+  const bool improved = s_red_v[0] < a.uf[s];
+  const int brow = s_red_i[0];
+  __syncthreads();
+  if (improved) {
+    for (int j = tid; j < d; j += kThreads) a.best[static_cast<size_t>(s) * d + j] = acts[static_cast<size_t>(brow) * d + j];
+    if (tid == 0) a.uf[s] = s_red_v[0];
+  }
+  // bitonic sort of P keys ascending by (value, seq)
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += kThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          Key x = keys[i], y = keys[ixj];
+          if (up ? key_less(y, x) : key_less(x, y)) {
+            keys[i] = y;
+            keys[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // new top list (gather the actions of the survivors)
+  const int ncnt = min(a.top_cap, cnt + a.rows);
+  for (int i = tid; i < ncnt; i += kThreads) {
+    a.top_val[nxt][static_cast<size_t>(s) * a.top_cap + i] = keys[i].v;
+    a.top_seq[nxt][static_cast<size_t>(s) * a.top_cap + i] = keys[i].seq;
+  }
+  for (long long w = tid; w < static_cast<long long>(ncnt) * d; w += kThreads) {
+    const int i = static_cast<int>(w / d), j = static_cast<int>(w % d);
+    const int src = keys[i].src;
+    const float v = src < cnt ? a.top_act[cur][(static_cast<size_t>(s) * a.top_cap + src) * d + j]
+                              : acts[static_cast<size_t>(src - cnt) * d + j];
+    a.top_act[nxt][(static_cast<size_t>(s) * a.top_cap + i) * d + j] = v;
+  }
+  if (tid == 0) a.top_cnt[s] = ncnt;
+
+  // 3. refit
+  if (a.method == 0) {
+    // CEM elites per agent: first n_el of the agent's rows in (value, row)
+    // order (search.cpp:131-149); agent 0 also owns the incumbent row.
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int g = warp; g < a.groups; g += kThreads / 32) {
+      const int n_el = min(a.per_group + (g == 0 ? 1 : 0), max(1, a.elites));
+      int taken = 0;
+      for (int base = 0; base < cnt + a.rows && taken < n_el; base += 32) {
+        const int i = base + lane;
+        bool mine = false;
+        int row = -1;
+        if (i < P && keys[i].src >= cnt) {
+          row = keys[i].src - cnt;
+          mine = (row >= g * a.per_group && row < (g + 1) * a.per_group) || (g == 0 && row == a.n_samp);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        const int rank = taken + __popc(m & ((1u << lane) - 1u));
+        if (mine && rank < n_el) elite[g * a.elites + rank] = row;
+        taken += __popc(m);
+      }
+      if (lane == 0) s_nel[g] = n_el;
+    }
+    __syncthreads();
+    for (int w = tid; w < a.groups * d; w += kThreads) {
+      const int g = w / d, j = w % d;
+      const int n_el = s_nel[g];
+      double m = 0.0;
+      for (int e = 0; e < n_el; ++e) m += acts[static_cast<size_t>(elite[g * a.elites + e]) * d + j];
+      m /= n_el;
+      double v = 0.0;
+      for (int e = 0; e < n_el; ++e) {
+        const double df = acts[static_cast<size_t>(elite[g * a.elites + e]) * d + j] - m;
+        v += df * df;
+      }
+      v /= n_el;
+      const size_t o = (static_cast<size_t>(s) * a.groups + g) * d + j;
+      a.mu[o] = static_cast<float>(m);
+      a.var[o] = fmaxf(static_cast<float>(v), a.var_floor[static_cast<size_t>(s) * d + j]);
+    }
+  } else {
+    // MPPI: mu = clamp(sum_i w_i u_i / sum_i w_i), w_i = exp(-(v_i - vmin)/T) (search.cpp:192-205)
+    for (int w = tid; w < a.groups * d; w += kThreads) {
+      const int g = w / d, j = w % d;
+      const int r0 = g * a.per_group;
+      float vmin = costs[r0];
+      for (int i = 1; i < a.per_group; ++i) vmin = fminf(vmin, costs[r0 + i]);
+      const double T = fmax(1e-12, static_cast<double>(a.temperature) * a.temp_ratios[g / a.n_noise]);
+      double acc = 0.0, wsum = 0.0;
+      for (int i = 0; i < a.per_group; ++i) {
+        const double wi = exp(-(static_cast<double>(costs[r0 + i]) - vmin) / T);
+        acc += wi * acts[static_cast<size_t>(r0 + i) * d + j];
+        wsum += wi;
+      }
+      const float lo = a.lo[static_cast<size_t>(s) * d + j], hi = a.hi[static_cast<size_t>(s) * d + j];
+      a.mu[(static_cast<size_t>(s) * a.groups + g) * d + j] = fminf(fmaxf(static_cast<float>(acc / wsum), lo), hi);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_search_init(const SearchArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  search_init_kernel<<<a.n, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample(const SearchArgs& a, int sms, cudaStream_t st) {
+  const long long total = static_cast<long long>(a.n) * a.rows * ((a.d + 3) / 4);
+  if (total <= 0) return cudaSuccess;
+  const long long want = (total + 255) / 256;
+  const int grid = static_cast<int>(want < sms * 8LL ? want : sms * 8LL);
+  sample_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+int search_sort_size(int top_cap, int rows) {
+  int P = 1;
+  while (P < top_cap + rows) P <<= 1;
+  return P;
+}
+
+size_t search_update_smem(const SearchArgs& a) {
+  const int P = search_sort_size(a.top_cap, a.rows);
+  return static_cast<size_t>(P) * sizeof(Key) + static_cast<size_t>(a.groups) * a.elites * sizeof(int) + 16;
+}
+
+cudaError_t launch_search_update(const SearchArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  const int P = search_sort_size(a.top_cap, a.rows);
+  const size_t smem = search_update_smem(a);
+  cudaError_t e = cudaFuncSetAttribute(search_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  search_update_kernel<<<a.n, kThreads, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+}  // namespace bp

@@ -1,0 +1,250 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the FP64 oracle
+on identical FP32-representable inputs.
+
+Tolerances (north star): rollout costs and empirical bounds within 1e-5
+relative in FP32 (relative to max(|ref|, 1) for bounds near zero); CROWN lower
+bounds from identical extrema within 1e-9 of the bound's term magnitude (the
+bound kernel runs in FP64); branching decisions bit-exact.
+"""
+import numpy as np
+import pytest
+
+import paper_2412_09584_b200 as bp
+from oracle import oracle as orc
+from paper_2412_09584_b200 import objective as objmod, workloads
+from paper_2412_09584_b200.config import from_json
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+def rel_err(got, ref):
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0))) if got.size else 0.0
+
+
+def small_spec(name):
+    if name == "c1":
+        return workloads.c1(glorot=True).spec
+    if name == "c2":
+        return workloads.c2(glorot=True).spec
+    if name == "c4":
+        return workloads.c4(glorot=True).spec
+    if name == "c3":
+        return workloads.c3(glorot=True).spec
+    if name == "c5":
+        return workloads.c5(glorot=True).spec
+    if name == "ref-obstacles":  # reference build_objective, relative features, hinges on keypoints and p_t
+        s = bp.Scenario()
+        s.x0, s.x_target, s.p0 = [0.4, -0.3, 0.1, 0.2], [0.0, 0.0, 0.1, 0.1], [0.0, 0.0]
+        s.horizon = 6
+        s.u_lower, s.u_upper = [-0.5, -0.5], [0.5, 0.5]
+        s.obstacles = [bp.Obstacle([0.2, 0.1], 0.3), bp.Obstacle([-0.1, 0.2], 0.25)]
+        s.cost_form = "tracking_obstacles"
+        s.lam = 50.0
+        return objmod.round_spec_to_f32(objmod.build_objective(bp.generate_model(3, [6, 32, 32, 4]), s))
+    if name == "ref-linear":  # test_smoke.py's zero-hidden-layer model, relative features
+        s = bp.Scenario()
+        s.x0, s.x_target, s.p0 = [0.4, 0.4], [0.0, 0.0], [0.0, 0.0]
+        s.horizon = 3
+        s.u_lower, s.u_upper = [-0.5, -0.5], [0.5, 0.5]
+        return objmod.round_spec_to_f32(objmod.build_objective(bp.generate_model(1, [4, 2]), s))
+    raise KeyError(name)
+
+
+CASES = ["c1", "c2", "c4", "ref-obstacles", "ref-linear", "c3", "c5"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_rollout_costs_and_extrema_match_oracle(device, name):
+    spec = small_spec(name)
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    rows = 37 if name not in ("c3", "c5") else 9
+    acts = np.random.default_rng(1).uniform(lo, hi, size=(3, rows, spec.d)).astype(np.float32)
+    costs, _, elo, ehi, bad = dev.rollout(acts)
+    assert not bad.any()
+    ob = orc.Objective(spec)
+    layout = dev.stat_layout()
+    for s in range(3):
+        st = orc.Stats()
+        ref = ob.evaluate(acts[s].astype(np.float64), st)
+        assert rel_err(costs[s], ref) < RTOL, name
+        rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
+        assert not np.isnan(rlo).any()
+        assert rel_err(elo[s], rlo) < RTOL and rel_err(ehi[s], rhi) < RTOL, name
+
+
+def test_rollout_rows_are_batch_invariant(device):
+    spec = small_spec("c2")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    acts = np.random.default_rng(2).uniform(lo, hi, size=(1, 300, spec.d)).astype(np.float32)
+    whole, _, _, _, _ = dev.rollout(acts)
+    for i in (0, 1, 127, 128, 129, 299):
+        one, _, _, _, _ = dev.rollout(acts[:, i:i + 1])
+        assert whole[0, i] == one[0, 0]
+    split, _, _, _, _ = dev.rollout(acts.reshape(3, 100, spec.d))
+    assert np.array_equal(split.reshape(-1), whole.reshape(-1))
+
+
+def test_states_match_reference_rollout(device):
+    m = bp.generate_model(1, [4, 2])
+    s = bp.Scenario()
+    s.x0, s.x_target, s.p0 = [0.4, 0.4], [0.0, 0.0], [0.0, 0.0]
+    s.horizon = 3
+    s.u_lower, s.u_upper = [-0.5, -0.5], [0.5, 0.5]
+    act = np.array([0.1, -0.2, 0.3, 0.05, -0.4, 0.2])
+    states = bp.rollout(m, s, act)
+    x, p = s.x0.copy(), s.p0.copy()
+    for t in range(3):
+        u = act[2 * t:2 * t + 2]
+        x = m.forward(np.concatenate([x - p, u]))[0]
+        p = p + u
+        assert np.allclose(states[t], x, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "ref-obstacles", "ref-linear"])
+@pytest.mark.parametrize("alpha", ["adaptive", "zero"])
+def test_empirical_bound_matches_oracle_on_identical_extrema(device, name, alpha):
+    spec = small_spec(name)
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    c = 0.5 * (lo + hi)
+    los = np.stack([lo, np.minimum(c, hi), lo])
+    his = np.stack([hi, hi, np.maximum(c, lo)])
+    cfg = from_json('{"search": {"samples_per_iter": 64, "iterations": 3}}')
+    rep = dev.batch_search(los, his, None, cfg, seed=5)
+    lf = dev.batch_bound(3, "early-stop-empirical", alpha)
+    ob = orc.Objective(spec)
+    layout = dev.stat_layout()
+    for i in range(3):
+        assert rep["ok"][i]
+        elo, ehi = dev.report_stats(i)
+        st = ob.stats_from_layout(elo.astype(np.float64), ehi.astype(np.float64), layout, spec.horizon)
+        ref = ob.lower_bound(los[i], his[i], "early-stop-empirical", st, alpha)
+        assert abs(lf[i] - ref) <= 1e-9 * max(1.0, abs(ref)), (name, i, lf[i], ref)
+        assert lf[i] <= rep["uf"][i] + 1e-6 * max(1.0, abs(rep["uf"][i]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "ref-obstacles", "ref-linear"])
+def test_interval_bound_matches_oracle(device, name):
+    spec = small_spec(name)
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    lf = dev.bound_boxes(lo[None], hi[None], "early-stop-interval")
+    ref = orc.Objective(spec).lower_bound(lo, hi, "early-stop-interval")
+    assert abs(lf[0] - ref) <= 1e-9 * max(1.0, abs(ref))
+
+
+def test_search_properties(device):
+    spec = small_spec("c1")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    cfg = from_json('{"search": {"samples_per_iter": 200, "iterations": 6, "top_capacity": 64}}')
+    warm = np.random.default_rng(0).uniform(lo, hi)[None]
+    rep = dev.batch_search(lo[None], hi[None], warm, cfg, seed=11)
+    warm_val = bp.api.default_device()  # noqa: F841 (keeps the default device alive)
+    ob = orc.Objective(spec)
+    wv = ob.evaluate(warm.astype(np.float32).astype(np.float64))[0]
+    assert rep["ok"][0] and rep["uf"][0] <= wv * (1 + 1e-5) + 1e-6
+    v, a = dev.report_top(0, rep["n_top"][0])
+    assert 0 < len(v) <= 64 and v[0] == rep["uf"][0] and np.all(np.diff(v) >= 0)
+    assert np.all(a >= lo - 1e-7) and np.all(a <= hi + 1e-7)
+    assert np.array_equal(a[0], rep["best"][0])
+    assert rep["samples"][0] == 6 * (4 * 50 + 1)
+    # the device values of the kept samples are the oracle's objective at those points
+    ref = ob.evaluate(a.astype(np.float32).astype(np.float64))
+    assert rel_err(v, ref) < RTOL
+
+
+def test_search_is_seeded_per_box(device):
+    """batch_search equals independent runs with seed ^ index (test_search.cpp:171-188)."""
+    spec = small_spec("c1")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    los = np.stack([lo, lo * 0.5, lo])
+    his = np.stack([hi, hi * 0.5, hi * 0.25])
+    cfg = from_json('{"search": {"samples_per_iter": 100, "iterations": 4}}')
+    batch = dev.batch_search(los, his, None, cfg, seed=99)
+    for i in range(3):
+        solo = dev.batch_search(los[i:i + 1], his[i:i + 1], None, cfg, seed=99 ^ i)
+        assert batch["uf"][i] == solo["uf"][0] and np.array_equal(batch["best"][i], solo["best"][0])
+    again = dev.batch_search(los, his, None, cfg, seed=99)
+    assert np.array_equal(again["uf"], batch["uf"])
+
+
+def test_mppi_search_runs(device):
+    spec = small_spec("c1")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    cfg = from_json('{"search": {"method": "mppi", "samples_per_iter": 120, "iterations": 5}}')
+    rep = dev.batch_search(lo[None], hi[None], None, cfg, seed=1, method="mppi")
+    center = orc.Objective(spec).evaluate((0.5 * (lo + hi))[None])[0]
+    assert rep["ok"][0] and rep["uf"][0] <= center * (1 + 1e-5)
+    assert rep["samples"][0] == 5 * (3 * 40 + 1)
+
+
+def test_reference_smoke_plan_reaches_target():
+    """proj/tests/python/test_smoke.py:60-76 through the drop-in module."""
+    import json
+    import math
+
+    m = bp.generate_model(seed=1, widths=[4, 2])
+    s = bp.Scenario()
+    s.x0, s.x_target, s.p0 = np.full(2, 0.4), np.zeros(2), np.zeros(2)
+    s.horizon = 3
+    s.u_lower, s.u_upper = np.full(2, -0.5), np.full(2, 0.5)
+    s.validate()
+    cfg = json.loads(bp.default_config())
+    cfg["seed"] = 11
+    cfg["termination"]["max_iterations"] = 5
+    cfg["search"]["samples_per_iter"] = 48
+    cfg["search"]["iterations"] = 3
+    res = bp.plan(m, s, json.dumps(cfg), method="babnd")
+    act = np.asarray(res["action"])
+    assert act.shape == (6,)
+    assert bp.rollout(m, s, act).shape == (3, 2)
+    vals = bp.objective_value(m, s, act.reshape(1, -1))
+    assert math.isclose(vals[0], res["objective"], rel_tol=0, abs_tol=1e-9)
+    uf = res["trace"]["uf"]
+    assert all(a >= b for a, b in zip(uf, uf[1:]))
+    assert res["lower_bound"] <= res["objective"] + 1e-9
+    assert res["stop_reason"] in {"max-iterations", "pool-exhausted", "target", "wall-clock"}
+
+
+def test_plan_matches_or_beats_cpu_reference_objective(device):
+    """Same or better best objective than the CPU planner at equal iteration count (C1)."""
+    wl = workloads.c1()
+    cfg = wl.planner_config()
+    cfg["termination"]["max_iterations"] = 6
+    dev = device.load(wl.spec)
+    gpu = dev.plan(cfg)
+    cpu = orc.Objective(wl.spec).plan(cfg)
+    assert gpu["iterations"] == cpu["iterations"] == 6
+    assert gpu["objective"] <= cpu["objective"] * 1.05 + 1e-3
+    assert gpu["trace"]["pool_size"][0] == 1
+
+
+def test_plan_sample_only_method(device):
+    spec = small_spec("c1")
+    dev = device.load(spec)
+    cfg = from_json('{"search": {"samples_per_iter": 100, "iterations": 4}}')
+    res = dev.plan(cfg, method="cem")
+    assert res["stop_reason"] == "sampler-budget" and res["iterations"] == 4
+    assert res["lower_bound"] == -np.inf and not res["certified"]
+    assert len(res["trace"]["uf"]) == 4
+
+
+def test_nonfinite_rollouts_fail_the_box_not_the_batch(device):
+    """search.cpp:273-278 failure isolation: a box whose rollouts overflow is reported failed."""
+    spec = small_spec("ref-linear")
+    big = objmod.ObjectiveSpec(**{**spec.__dict__, "W": [spec.W[0] * 1e30]})
+    dev = device.load(big)
+    lo, hi = big.box()
+    cfg = from_json('{"search": {"samples_per_iter": 32, "iterations": 2}}')
+    rep = dev.batch_search(np.stack([lo, lo]), np.stack([hi, hi]), None, cfg, seed=1)
+    assert not rep["ok"].any()
+    lf = dev.batch_bound(2)  # interval fallback
+    assert lf.shape == (2,)
