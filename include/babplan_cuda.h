@@ -166,6 +166,12 @@ size_t bp_get_last_error(char* buf, size_t cap);
 /* Optional NCCL sharding: rank r of world w; unique_id is the 128-byte ncclUniqueId. */
 bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* nccl_unique_id);
 
+/* Launch the context's work on an external stream (NULL = its own stream),
+ * e.g. torch.cuda.current_stream(), so caller-side CUDA events time it. */
+bp_status bp_set_stream(bp_ctx* ctx, void* cuda_stream);
+/* Host<->device bytes the library copied since the previous call. */
+bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h);
+
 /* Uploads weights / cost program; derives stop and watch sets. */
 bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc);
 /* Number of recorded (watched) coordinates per rollout step, and the layout
@@ -202,6 +208,14 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
 typedef struct bp_result bp_result;
 bp_status bp_plan(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm, int method_babnd,
                   bp_result** out);
+/* plan() one iteration at a time: create runs the root search + bound, each
+ * step one pick / split / search / bound / merge / prune iteration (stepped =
+ * 0 once a termination rule fired), finish the remaining iterations. */
+typedef struct bp_planner bp_planner;
+bp_status bp_planner_create(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm, bp_planner** out);
+bp_status bp_planner_step(bp_planner* p, int* stepped, int* children, int* pool_size);
+bp_status bp_planner_finish(bp_planner* p, bp_result** out);
+bp_status bp_planner_destroy(bp_planner* p);
 bp_status bp_result_summary(const bp_result* r, double* uf, double* min_lf, int* certified,
                             int64_t* samples, int* iterations, char* stop_reason, size_t cap,
                             int* n_trace, int* d);
@@ -213,6 +227,10 @@ bp_status bp_result_free(bp_result* r);
  * kernel family; rollout is the dominant kernel). */
 bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms,
                     double* search_ms, int64_t* launches);
+
+/* Diagnostics: sustained FP32 FMA throughput of the device (TFLOP/s), the
+ * roofline denominator of the SIMT rollout kernel. */
+bp_status bp_measure_fp32_peak(int device, double* tflops, double* ms);
 
 /* Host-side pool primitives (bit-exact restatements, exposed for parity). */
 typedef struct {

@@ -86,12 +86,14 @@ class PoolMeta(C.Structure):
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
-    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_comm", "bp_load_objective",
+    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_comm", "bp_set_stream", "bp_io_bytes",
+    "bp_load_objective",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
-    "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_result_summary", "bp_result_best",
+    "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
+    "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
     "bp_result_trace", "bp_result_free", "bp_timing", "bp_rng_new", "bp_rng_free",
     "bp_rng_uniform", "bp_rng_normal", "bp_rng_bits", "bp_rng_fill", "bp_mix_seed", "bp_pick_out",
-    "bp_split_axis", "bp_generate_model",
+    "bp_split_axis", "bp_generate_model", "bp_measure_fp32_peak",
 ]
 
 _lib = None
@@ -119,6 +121,8 @@ def load() -> C.CDLL:
             "bp_destroy": (C.c_int, [vp]),
             "bp_get_last_error": (C.c_size_t, [C.c_char_p, C.c_size_t]),
             "bp_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+            "bp_set_stream": (C.c_int, [vp, vp]),
+            "bp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_load_objective": (C.c_int, [vp, C.POINTER(ObjectiveDesc)]),
             "bp_stat_layout": (C.c_int, [vp, _ip, _ip, _ip, _ip, _ip, _ip, C.c_int]),
             "bp_rollout": (C.c_int, [vp, C.c_int, C.c_int, _fp, _fp, _fp, _fp, _fp, _ip]),
@@ -129,6 +133,10 @@ def load() -> C.CDLL:
             "bp_batch_bound": (C.c_int, [vp, C.c_int, C.c_int, _dp]),
             "bp_bound_boxes": (C.c_int, [vp, C.c_int, _dp, _dp, C.c_int, C.c_int, _dp]),
             "bp_plan": (C.c_int, [vp, C.POINTER(PlannerConfig), _dp, C.c_int, C.POINTER(vp)]),
+            "bp_planner_create": (C.c_int, [vp, C.POINTER(PlannerConfig), _dp, C.POINTER(vp)]),
+            "bp_planner_step": (C.c_int, [vp, _ip, _ip, _ip]),
+            "bp_planner_finish": (C.c_int, [vp, C.POINTER(vp)]),
+            "bp_planner_destroy": (C.c_int, [vp]),
             "bp_result_summary": (C.c_int, [vp, _dp, _dp, _ip, C.POINTER(C.c_int64), _ip,
                                             C.c_char_p, C.c_size_t, _ip, _ip]),
             "bp_result_best": (C.c_int, [vp, _dp]),
@@ -147,6 +155,7 @@ def load() -> C.CDLL:
             "bp_split_axis": (C.c_int, [C.c_int, _dp, _dp, C.c_int, _dp, C.c_int64, C.c_double,
                                         C.c_double, C.c_int, _ip, _dp, C.POINTER(C.c_ubyte)]),
             "bp_generate_model": (C.c_int, [C.c_uint64, C.c_int, _ip, _dp]),
+            "bp_measure_fp32_peak": (C.c_int, [C.c_int, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

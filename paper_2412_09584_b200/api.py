@@ -143,29 +143,23 @@ class Device:
         w = None if warm is None else np.ascontiguousarray(warm, dtype=np.float64)
         res = C.c_void_p()
         check(self.lib.bp_plan(self.h, packed.ref(), _capi.dptr(w), 1 if method == "babnd" else 0, C.byref(res)))
-        try:
-            uf, mlf = C.c_double(), C.c_double()
-            cert, iters, ntr, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
-            samples = C.c_int64()
-            stop = C.create_string_buffer(64)
-            check(self.lib.bp_result_summary(res, C.byref(uf), C.byref(mlf), C.byref(cert), C.byref(samples),
-                                             C.byref(iters), stop, 64, C.byref(ntr), C.byref(d)))
-            best = np.zeros(d.value)
-            check(self.lib.bp_result_best(res, _capi.dptr(best)))
-            rows = (_capi.TraceRow * max(1, ntr.value))()
-            check(self.lib.bp_result_trace(res, rows, ntr.value))
-        finally:
-            self.lib.bp_result_free(res)
-        tr = rows[:ntr.value]
-        trace = {
-            "iter": [r.iter for r in tr], "uf": [r.uf for r in tr], "min_lf": [r.min_lf for r in tr],
-            "pruned_vol": [r.pruned_vol for r in tr], "selected_vol": [r.selected_vol for r in tr],
-            "pool_size": [r.pool_size for r in tr], "samples": [r.samples for r in tr],
-            "wall_ms": [r.wall_ms for r in tr],
-        }
-        return {"objective": uf.value, "action": best, "lower_bound": mlf.value, "certified": bool(cert.value),
-                "samples": samples.value, "iterations": iters.value, "stop_reason": stop.value.decode(),
-                "trace": trace}
+        return _result_dict(self.lib, res)
+
+    def planner(self, cfg: dict, warm: Optional[np.ndarray] = None) -> "Planner":
+        """plan() driven one BaB iteration at a time (the bench steps it)."""
+        return Planner(self, cfg, warm)
+
+    def set_stream(self, stream_handle: Optional[int]) -> None:
+        """Run on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        check(self.lib.bp_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
+
+    @staticmethod
+    def io_bytes():
+        """(h2d, d2h) bytes copied by the library since the previous call."""
+        lib = _capi.load()
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.bp_io_bytes(C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def timing(self) -> dict:
         """Device time since the previous call: rollout ms and launches, bound ms, search wall ms."""
@@ -174,6 +168,61 @@ class Device:
         check(self.lib.bp_timing(self.h, C.byref(r), C.byref(rl), C.byref(b), C.byref(s), C.byref(l)))
         return {"rollout_ms": r.value, "rollout_launches": rl.value, "bound_ms": b.value, "search_ms": s.value,
                 "launches": l.value}
+
+
+def _result_dict(lib, res) -> dict:
+    try:
+        uf, mlf = C.c_double(), C.c_double()
+        cert, iters, ntr, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        samples = C.c_int64()
+        stop = C.create_string_buffer(64)
+        check(lib.bp_result_summary(res, C.byref(uf), C.byref(mlf), C.byref(cert), C.byref(samples),
+                                    C.byref(iters), stop, 64, C.byref(ntr), C.byref(d)))
+        best = np.zeros(d.value)
+        check(lib.bp_result_best(res, _capi.dptr(best)))
+        rows = (_capi.TraceRow * max(1, ntr.value))()
+        check(lib.bp_result_trace(res, rows, ntr.value))
+    finally:
+        lib.bp_result_free(res)
+    tr = rows[:ntr.value]
+    trace = {k: [getattr(r, k) for r in tr] for k in
+             ("iter", "uf", "min_lf", "pruned_vol", "selected_vol", "pool_size", "samples", "wall_ms")}
+    return {"objective": uf.value, "action": best, "lower_bound": mlf.value, "certified": bool(cert.value),
+            "samples": samples.value, "iterations": iters.value, "stop_reason": stop.value.decode(),
+            "trace": trace}
+
+
+class Planner:
+    """bp_planner handle: root search + bound on creation, then step()."""
+
+    def __init__(self, dev: Device, cfg: dict, warm=None):
+        self.dev, self.lib = dev, dev.lib
+        self._packed = _config.PackedConfig(cfg)
+        self._w = None if warm is None else np.ascontiguousarray(warm, dtype=np.float64)
+        self.h = C.c_void_p()
+        check(self.lib.bp_planner_create(dev.h, self._packed.ref(), _capi.dptr(self._w), C.byref(self.h)))
+
+    def step(self):
+        """One BaB iteration -> (stepped, children searched+bounded, pool size)."""
+        st, ch, ps = C.c_int(), C.c_int(), C.c_int()
+        check(self.lib.bp_planner_step(self.h, C.byref(st), C.byref(ch), C.byref(ps)))
+        return bool(st.value), ch.value, ps.value
+
+    def finish(self) -> dict:
+        res = C.c_void_p()
+        check(self.lib.bp_planner_finish(self.h, C.byref(res)))
+        return _result_dict(self.lib, res)
+
+    def close(self):
+        if self.h:
+            self.lib.bp_planner_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _default: Optional[Device] = None

@@ -37,6 +37,7 @@ struct DevObjective {
   int w_smem_off[kMaxLayers];             // float offset of layer l inside the resident smem image
   int w_smem_total;                       // floats in the resident image (0 when streamed)
   int w_max_layer;                        // floats of the largest single layer image
+  int red_w;                              // column stride of the fused-extrema scratch (4 x red_w ints)
   // backward weights: W [out][in] row-major and b, double arena offsets
   int wd[kMaxLayers], bd[kMaxLayers];
   // per-row scratch layout in the activation buffer

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -120,6 +121,14 @@ bp_status guard(F&& f) {
     g_last_error = e.what();
     return BP_RUNTIME;
   }
+}
+
+// Host<->device bytes moved by the library (e2e accounting, bp_io_bytes).
+std::atomic<int64_t> g_h2d{0}, g_d2h{0};
+cudaError_t memcpy_counted(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t st) {
+  if (kind == cudaMemcpyHostToDevice) g_h2d += static_cast<int64_t>(n);
+  if (kind == cudaMemcpyDeviceToHost) g_d2h += static_cast<int64_t>(n);
+  return cudaMemcpyAsync(dst, src, n, kind, st);
 }
 
 int r4(int x) { return (x + 3) & ~3; }
@@ -424,7 +433,10 @@ Compiled compile(const bp_objective_desc& d) {
 
   // rollout tile and shared-memory plan
   c.R = bp::rollout_rows_per_tile(c.nq);
-  const size_t base_bytes = (static_cast<size_t>(c.R) * o.S + static_cast<size_t>(c.R) * 8) * sizeof(float);
+  o.red_w = 4;
+  for (int l = 0; l < d.n_layers; ++l)
+    if (o.relu[l]) o.red_w = std::max(o.red_w, o.nstr[l]);
+  const size_t base_bytes = (static_cast<size_t>(c.R) * o.S + static_cast<size_t>(c.R) * 9 + 4 * o.red_w) * sizeof(float);
   const size_t resident = base_bytes + static_cast<size_t>(o.w_smem_total) * sizeof(float);
   const size_t cap = 227 * 1024;
   if (resident <= cap) {
@@ -464,6 +476,7 @@ struct bp_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
   bool loaded = false;
   Compiled comp;
   DBuf<float> d_fa;
@@ -500,7 +513,7 @@ struct bp_ctx {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
   }
   void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
   bp::DevObjective dev() {
@@ -609,22 +622,22 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   a.seeds = c->seeds.get(static_cast<size_t>(n));
   a.lo = c->lo_f.get(nd);
   a.hi = c->hi_f.get(nd);
-  ck(cudaMemcpyAsync(const_cast<unsigned long long*>(a.seeds), seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
-  ck(cudaMemcpyAsync(const_cast<float*>(a.lo), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(cudaMemcpyAsync(const_cast<float*>(a.hi), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(cudaMemcpyAsync(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
-  ck(cudaMemcpyAsync(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(const_cast<unsigned long long*>(a.seeds), seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(const_cast<float*>(a.lo), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(const_cast<float*>(a.hi), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
   a.warm = nullptr;
   std::vector<float> w32;
   if (warm != nullptr) {
     w32.resize(nd);
     for (size_t i = 0; i < nd; ++i) w32[i] = static_cast<float>(warm[i]);
     a.warm = c->warm_f.get(nd);
-    ck(cudaMemcpyAsync(const_cast<float*>(a.warm), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(const_cast<float*>(a.warm), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
   }
   if (!ratios.empty()) {
     float* r = c->ratios.get(ratios.size());
-    ck(cudaMemcpyAsync(r, ratios.data(), ratios.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(r, ratios.data(), ratios.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
     a.noise_ratios = r;
     a.temp_ratios = r + a.n_noise;
   }
@@ -659,14 +672,14 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
     c->rollout(a.actions, const_cast<float*>(a.costs), nullptr, smin, smax, a.failed,
                static_cast<long long>(n) * a.rows, a.rows);
     ck(bp::launch_search_update(a, st), "search update");
-    ck(cudaMemcpyAsync(ufh + static_cast<size_t>(it) * n, a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st), "D2D");
+    ck(memcpy_counted(ufh + static_cast<size_t>(it) * n, a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st), "D2D");
     c->launches += 2;
     a.cur ^= 1;
   }
   c->cur = a.cur;
   c->searched = true;
   c->h_failed.assign(static_cast<size_t>(n), 0);
-  ck(cudaMemcpyAsync(c->h_failed.data(), a.failed, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(c->h_failed.data(), a.failed, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
   if (out == nullptr) {
     ck(cudaStreamSynchronize(st), "sync");
     return;
@@ -674,13 +687,13 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   // harvest reports
   std::vector<float> uf(static_cast<size_t>(n)), best(nd), hist(static_cast<size_t>(n) * cfg.iterations);
   std::vector<int> cnt(static_cast<size_t>(n));
-  ck(cudaMemcpyAsync(uf.data(), a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(cudaMemcpyAsync(best.data(), a.best, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(cudaMemcpyAsync(cnt.data(), a.top_cnt, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(cudaMemcpyAsync(hist.data(), ufh, hist.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(uf.data(), a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(best.data(), a.best, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(cnt.data(), a.top_cnt, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(hist.data(), ufh, hist.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
   std::vector<float> tv(tk), ta(tk * d);
-  ck(cudaMemcpyAsync(tv.data(), a.top_val[a.cur], tk * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(cudaMemcpyAsync(ta.data(), a.top_act[a.cur], tk * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(tv.data(), a.top_val[a.cur], tk * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(ta.data(), a.top_act[a.cur], tk * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
   ck(cudaStreamSynchronize(st), "sync");
   out->assign(static_cast<size_t>(n), Report());
   for (int i = 0; i < n; ++i) {
@@ -715,7 +728,7 @@ void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
   std::vector<int> use(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) use[static_cast<size_t>(i)] = c->h_failed[static_cast<size_t>(i)] ? 0 : 1;
   int* du = c->use_flags.get(static_cast<size_t>(n));
-  ck(cudaMemcpyAsync(du, use.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(memcpy_counted(du, use.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
   bp::BoundArgs a{c->lo_d.p, c->hi_d.p, c->stat_min.p, c->stat_max.p, du,
                   c->ivl_lo.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
                   c->ivl_hi.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
@@ -724,7 +737,7 @@ void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
   ck(bp::launch_bound(c->dev(), a, n, c->stream), "bound launch");
   if (c->timing) ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
-  ck(cudaMemcpyAsync(lf_out, a.lf, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(memcpy_counted(lf_out, a.lf, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "sync");
   if (c->timing) {
     float ms = 0.f;
@@ -989,30 +1002,37 @@ std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec>& boxes, c
   return reps;
 }
 
-void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start, bp_result& result) {
-  // bab.cpp:266-415
-  const int d = c->comp.d;
-  if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
-  if (cfg.bound_mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
-  const auto t0 = std::chrono::steady_clock::now();
-  auto elapsed_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+// plan() (bab.cpp:266-415) as a steppable object: the constructor runs the
+// root search + bound, step() one pick -> split -> search -> bound -> merge ->
+// prune iteration, finish() the result fields.
+struct Planner {
+  bp_ctx* c;
+  bp_planner_config cfg;
+  int d;
+  std::chrono::steady_clock::time_point t0;
   std::vector<Rec> pool;
-  bp_rng pick_rng(mix_seed(cfg.seed, 1));
+  bp_rng pick_rng;
   int64_t next_id = 1;
   double pruned_cum = 0.0;
   double retired_min_lf = std::numeric_limits<double>::infinity();
-  auto pool_min_lf = [&] {
-    double m = std::numeric_limits<double>::infinity();
+  bp_result result;
+  std::string stop;
+  int iter = 0;
+  bool done = false;
+  int64_t children_bounded = 0;  // subdomains searched + bounded so far (root included)
+  int last_children = 0;
+
+  double elapsed_ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  double current_min_lf() const {
+    double m = retired_min_lf;
     for (const auto& r : pool) m = std::min(m, r.lf);
-    return m;
-  };
-  auto current_min_lf = [&] {
-    const double m = std::min(pool_min_lf(), retired_min_lf);
     return std::isfinite(m) || !pool.empty() ? m : result.uf;
-  };
-  auto push_trace = [&](int iter, double selected_vol) {
+  }
+  void push_trace(int it, double selected_vol) {
     bp_trace_row row{};
-    row.iter = iter;
+    row.iter = it;
     row.uf = result.uf;
     row.min_lf = current_min_lf();
     row.pruned_vol = pruned_cum;
@@ -1021,8 +1041,8 @@ void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start,
     row.samples = result.samples;
     row.wall_ms = elapsed_ms();
     result.trace.push_back(row);
-  };
-  auto prune = [&]() {  // bab.cpp:225-241
+  }
+  double prune() {  // bab.cpp:225-241
     double removed = 0.0;
     std::vector<Rec> keep;
     keep.reserve(pool.size());
@@ -1034,8 +1054,12 @@ void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start,
     }
     pool = std::move(keep);
     return removed;
-  };
-  {
+  }
+
+  Planner(bp_ctx* ctx, const bp_planner_config& config, const double* warm_start)
+      : c(ctx), cfg(config), d(ctx->comp.d), t0(std::chrono::steady_clock::now()), pick_rng(mix_seed(config.seed, 1)) {
+    if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
+    if (cfg.bound_mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
     Rec root;
     root.lo.resize(static_cast<size_t>(d));
     root.hi.resize(static_cast<size_t>(d));
@@ -1059,19 +1083,26 @@ void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start,
     result.best = root.best;
     result.samples = root.samples;
     pool.push_back(std::move(root));
+    children_bounded = 1;
+    last_children = 1;
     pruned_cum += prune();
     push_trace(0, 1.0);
   }
-  std::string stop;
-  int iter = 0;
-  std::vector<bp_pool_meta> meta;
-  while (true) {
-    if (result.uf <= cfg.target_objective) { stop = "target"; break; }
-    if (pool.empty()) { stop = "pool-exhausted"; break; }
-    if (iter >= cfg.max_iterations) { stop = "max-iterations"; break; }
-    if (cfg.wall_clock_ms > 0.0 && elapsed_ms() >= cfg.wall_clock_ms) { stop = "wall-clock"; break; }
+
+  // One BaB iteration; returns false (and records the stop reason) when the
+  // termination checks of bab.cpp:343-358 end the run.
+  bool step() {
+    if (done) return false;
+    if (result.uf <= cfg.target_objective) stop = "target";
+    else if (pool.empty()) stop = "pool-exhausted";
+    else if (iter >= cfg.max_iterations) stop = "max-iterations";
+    else if (cfg.wall_clock_ms > 0.0 && elapsed_ms() >= cfg.wall_clock_ms) stop = "wall-clock";
+    if (!stop.empty()) {
+      done = true;
+      return false;
+    }
     ++iter;
-    meta.resize(pool.size());
+    std::vector<bp_pool_meta> meta(pool.size());
     for (size_t i = 0; i < pool.size(); ++i) meta[i] = {pool[i].lf, pool[i].uf, pool[i].id, pool[i].log_vol};
     const std::vector<int> chosen = pick_indices(meta.data(), static_cast<int>(pool.size()), cfg.batch, cfg.eta, cfg.temperature, pick_rng);
     std::vector<char> taken(pool.size(), 0);
@@ -1100,6 +1131,7 @@ void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start,
       children.push_back(std::move(a));
       children.push_back(std::move(b));
     }
+    last_children = static_cast<int>(children.size());
     if (!children.empty()) {
       std::vector<const std::vector<double>*> warms;
       for (const auto& ch : children) warms.push_back(ch.best.empty() ? nullptr : &ch.best);
@@ -1118,14 +1150,27 @@ void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start,
         }
         pool.push_back(std::move(ch));
       }
+      children_bounded += static_cast<int64_t>(children.size());
     }
     pruned_cum += prune();
     push_trace(iter, selected_vol);
+    return true;
   }
-  result.min_lf = current_min_lf();
-  result.certified = cfg.bound_mode != BP_BOUND_EMPIRICAL;
-  result.iterations = iter;
-  result.stop_reason = stop;
+
+  void finish() {
+    while (step()) {
+    }
+    result.min_lf = current_min_lf();
+    result.certified = cfg.bound_mode != BP_BOUND_EMPIRICAL;
+    result.iterations = iter;
+    result.stop_reason = stop;
+  }
+};
+
+void run_plan(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start, bp_result& result) {
+  Planner p(c, cfg, warm_start);
+  p.finish();
+  result = std::move(p.result);
 }
 
 void run_sample_only(bp_ctx* c, const bp_planner_config& cfg, const double* warm_start, bp_result& result) {
@@ -1192,7 +1237,8 @@ bp_status bp_init(int device, bp_ctx** out) {
     ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major < 10) fail(BP_CUDA, "bp_init: device is not sm_100 class (B200 required)");
     c->sms = prop.multiProcessorCount;
-    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
     ck(cudaEventCreate(&c->ev1), "event");
     *out = c.release();
@@ -1216,6 +1262,20 @@ bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* uid) {
   });
 }
 
+bp_status bp_set_stream(bp_ctx* ctx, void* stream) {
+  return guard([&] {
+    check_ctx(ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->stream = stream != nullptr ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = g_h2d.exchange(0);
+  if (d2h) *d2h = g_d2h.exchange(0);
+  return BP_OK;
+}
+
 bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
   return guard([&] {
     check_ctx(ctx);
@@ -1224,9 +1284,9 @@ bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
     float* f = ctx->d_fa.get(cp.fa.size());
     double* dd = ctx->d_da.get(cp.da.size());
     int* iv = ctx->d_ia.get(cp.ia.size());
-    ck(cudaMemcpyAsync(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    ck(cudaMemcpyAsync(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    ck(cudaMemcpyAsync(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->comp = std::move(cp);
     ctx->loaded = true;
@@ -1270,18 +1330,18 @@ bp_status bp_rollout(bp_ctx* ctx, int n_sub, int rows, const float* actions, flo
     fill_int(mn, nstat, bp::enc_f_host(INFINITY), st);
     fill_int(mx, nstat, bp::enc_f_host(-INFINITY), st);
     ck(cudaMemsetAsync(fl, 0, static_cast<size_t>(n_sub) * 4, st), "memset");
-    ck(cudaMemcpyAsync(da, actions, static_cast<size_t>(nr) * cp.d * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(da, actions, static_cast<size_t>(nr) * cp.d * 4, cudaMemcpyHostToDevice, st), "H2D");
     ctx->rollout(da, dc, ds, mn, mx, fl, nr, rows);
-    ck(cudaMemcpyAsync(costs, dc, static_cast<size_t>(nr) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    if (states) ck(cudaMemcpyAsync(states, ds, static_cast<size_t>(nr) * cp.o.H * cp.o.ks * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(memcpy_counted(costs, dc, static_cast<size_t>(nr) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    if (states) ck(memcpy_counted(states, ds, static_cast<size_t>(nr) * cp.o.H * cp.o.ks * 4, cudaMemcpyDeviceToHost, st), "D2H");
     std::vector<int> hmn, hmx, hfl(static_cast<size_t>(n_sub));
     if (emp_lo || emp_hi) {
       hmn.resize(static_cast<size_t>(nstat));
       hmx.resize(static_cast<size_t>(nstat));
-      ck(cudaMemcpyAsync(hmn.data(), mn, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-      ck(cudaMemcpyAsync(hmx.data(), mx, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(hmn.data(), mn, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(hmx.data(), mx, static_cast<size_t>(nstat) * 4, cudaMemcpyDeviceToHost, st), "D2H");
     }
-    ck(cudaMemcpyAsync(hfl.data(), fl, static_cast<size_t>(n_sub) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(memcpy_counted(hfl.data(), fl, static_cast<size_t>(n_sub) * 4, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");
     ctx->harvest_roll_events();
     for (long long i = 0; i < nstat; ++i) {
@@ -1366,8 +1426,8 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
     for (size_t i = 0; i < nd; ++i)
       if (!(lo[i] <= hi[i]) || !std::isfinite(lo[i]) || !std::isfinite(hi[i]))
         fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
-    ck(cudaMemcpyAsync(ctx->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    ck(cudaMemcpyAsync(ctx->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(ctx->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(ctx->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ctx->n = n_boxes;
     ctx->searched = true;  // boxes resident; no statistics
     ctx->h_failed.assign(static_cast<size_t>(n_boxes), 1);
@@ -1387,6 +1447,45 @@ bp_status bp_plan(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm,
       run_sample_only(ctx, *cfg, warm, *r);
     *out = r.release();
   });
+}
+
+struct bp_planner {
+  std::unique_ptr<Planner> p;
+};
+
+bp_status bp_planner_create(bp_ctx* ctx, const bp_planner_config* cfg, const double* warm, bp_planner** out) {
+  return guard([&] {
+    check_loaded(ctx);
+    if (cfg == nullptr || out == nullptr) fail(BP_INVALID_ARGUMENT, "bp_planner_create: null argument");
+    auto h = std::make_unique<bp_planner>();
+    h->p = std::make_unique<Planner>(ctx, *cfg, warm);
+    *out = h.release();
+  });
+}
+
+bp_status bp_planner_step(bp_planner* h, int* stepped, int* children, int* pool_size) {
+  return guard([&] {
+    if (h == nullptr) fail(BP_INVALID_ARGUMENT, "null planner");
+    h->p->c->use();
+    const bool ok = h->p->step();
+    if (stepped) *stepped = ok ? 1 : 0;
+    if (children) *children = ok ? h->p->last_children : 0;
+    if (pool_size) *pool_size = static_cast<int>(h->p->pool.size());
+  });
+}
+
+bp_status bp_planner_finish(bp_planner* h, bp_result** out) {
+  return guard([&] {
+    if (h == nullptr || out == nullptr) fail(BP_INVALID_ARGUMENT, "null planner");
+    h->p->c->use();
+    h->p->finish();
+    *out = new bp_result(h->p->result);
+  });
+}
+
+bp_status bp_planner_destroy(bp_planner* h) {
+  delete h;
+  return BP_OK;
 }
 
 bp_status bp_result_summary(const bp_result* r, double* uf, double* min_lf, int* certified, int64_t* samples,

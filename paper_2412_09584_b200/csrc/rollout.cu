@@ -44,27 +44,31 @@ __device__ __forceinline__ float f4get(const float4& v, int k) {
 }
 
 // Register-tiled layer: rows ty + 16 i (i < TM), columns q*64 + tx*4 + c.
-template <int TM, int NQ>
+// FULL: every column quad q < NQ holds live columns (no per-quad predicate).
+template <int TM, int NQ, bool FULL>
 __device__ __forceinline__ void kloop_wide(const float* __restrict__ act, int S, const float* __restrict__ W,
                                            int NS, int k0, int k1, float (&acc)[TM][NQ * 4]) {
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  const float* xr = act + ty * S;
+  const float* wr = W + tx * 4;
+#pragma unroll 1
   for (int k = k0; k < k1; k += 4) {
     float4 xv[TM];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) xv[i] = *reinterpret_cast<const float4*>(act + (ty + 16 * i) * S + k);
+    for (int i = 0; i < TM; ++i) xv[i] = *reinterpret_cast<const float4*>(xr + 16 * i * S + k);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       float4 wv[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
-        wv[q] = (q * 64 < NS) ? *reinterpret_cast<const float4*>(W + (k - k0 + kk) * NS + q * 64 + tx * 4)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        wv[q] = (FULL || q * 64 < NS) ? *reinterpret_cast<const float4*>(wr + (k - k0 + kk) * NS + q * 64)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const float xs = f4get(xv[i], kk);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          if (q * 64 < NS) {
+          if (FULL || q * 64 < NS) {
             acc[i][q * 4 + 0] = fmaf(xs, wv[q].x, acc[i][q * 4 + 0]);
             acc[i][q * 4 + 1] = fmaf(xs, wv[q].y, acc[i][q * 4 + 1]);
             acc[i][q * 4 + 2] = fmaf(xs, wv[q].z, acc[i][q * 4 + 2]);
@@ -76,6 +80,15 @@ __device__ __forceinline__ void kloop_wide(const float* __restrict__ act, int S,
   }
 }
 
+template <int TM, int NQ>
+__device__ __forceinline__ void kloop_any(const float* act, int S, const float* W, int NS, int k0, int k1,
+                                          float (&acc)[TM][NQ * 4]) {
+  if (NS > 64 * (NQ - 1))
+    kloop_wide<TM, NQ, true>(act, S, W, NS, k0, k1, acc);
+  else
+    kloop_wide<TM, NQ, false>(act, S, W, NS, k0, k1, acc);
+}
+
 // Cooperative global -> shared copy of n floats (16B aligned).
 __device__ __forceinline__ void copy_f4(float* dst, const float* __restrict__ src, int n) {
   const int n4 = n >> 2;
@@ -83,12 +96,23 @@ __device__ __forceinline__ void copy_f4(float* dst, const float* __restrict__ sr
     reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
 }
 
+// Rows of a tile split into at most two subdomains: rows [0, bnd) belong to
+// subdomain seg0, rows [bnd, nvalid) to seg0 + 1 (bnd = nvalid when one).
+struct TileSeg {
+  long long seg0;
+  int bnd, nvalid;
+  bool two;  // the tile fits the two-segment form (rows_per_sub >= R)
+};
+
+// Wide layer with the fused epilogue: bias in the accumulator, per-column
+// extrema of the pre-activations (register -> xor-16 shuffle -> shared
+// atomics -> one global atomic per column and subdomain), ReLU applied on
+// the way back to shared memory.
 template <int TM, int NQ, bool STREAM>
-__device__ void layer_wide(const DevObjective& o, float* act, float* wsm, int l, int kslab) {
-  constexpr int R = 16 * TM;
-  (void)R;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int K4 = o.kpad[l], NS = o.nstr[l], S = o.S;
+__device__ void layer_wide(const DevObjective& o, const RolloutArgs& a, float* act, float* wsm, int* red, int l,
+                           const TileSeg& ts, int t) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4, lane = threadIdx.x & 31;
+  const int K4 = o.kpad[l], NS = o.nstr[l], S = o.S, N = o.widths[l + 1], RW = o.red_w;
   const float* __restrict__ bias = o.f + o.bias[l];
   float acc[TM][NQ * 4];
 #pragma unroll
@@ -104,15 +128,52 @@ __device__ void layer_wide(const DevObjective& o, float* act, float* wsm, int l,
     }
   }
   if constexpr (!STREAM) {
-    kloop_wide<TM, NQ>(act, S, wsm + o.w_smem_off[l], NS, 0, K4, acc);
+    kloop_any<TM, NQ>(act, S, wsm + o.w_smem_off[l], NS, 0, K4, acc);
   } else {
     const float* __restrict__ wg = o.f + o.wt[l];
-    for (int k0 = 0; k0 < K4; k0 += kslab) {
-      const int k1 = min(K4, k0 + kslab);
+    for (int k0 = 0; k0 < K4; k0 += a.kslab) {
+      const int k1 = min(K4, k0 + a.kslab);
       __syncthreads();  // previous slab fully consumed
       copy_f4(wsm, wg + static_cast<size_t>(k0) * NS, (k1 - k0) * NS);
       __syncthreads();
-      kloop_wide<TM, NQ>(act, S, wsm, NS, k0, k1, acc);
+      kloop_any<TM, NQ>(act, S, wsm, NS, k0, k1, acc);
+    }
+  }
+  const bool relu = o.relu[l] != 0;
+  const int stat = o.pre_stat[l];
+  const bool rec = ts.two && relu && stat >= 0 && a.stat_min != nullptr;
+  const bool apply_relu = relu && ts.two;  // otherwise the column pass records, then rectifies
+  if (rec) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (q * 64 >= NS) continue;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const int r = ty + 16 * i;
+          const float v = acc[i][q * 4 + c];
+          if (r < ts.bnd) {
+            mn0 = fminf(mn0, v);
+            mx0 = fmaxf(mx0, v);
+          } else if (r < ts.nvalid) {
+            mn1 = fminf(mn1, v);
+            mx1 = fmaxf(mx1, v);
+          }
+        }
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 16));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 16));
+        mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, 16));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 16));
+        const int col = q * 64 + tx * 4 + c;
+        if (lane < 16 && col < N) {
+          atomicMin(red + col, enc_f(mn0));
+          atomicMax(red + RW + col, enc_f(mx0));
+          atomicMin(red + 2 * RW + col, enc_f(mn1));
+          atomicMax(red + 3 * RW + col, enc_f(mx1));
+        }
+      }
     }
   }
   __syncthreads();  // every row's inputs consumed: write in place
@@ -121,9 +182,29 @@ __device__ void layer_wide(const DevObjective& o, float* act, float* wsm, int l,
     const int col = q * 64 + tx * 4;
     if (col < NS) {
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
-        *reinterpret_cast<float4*>(act + (ty + 16 * i) * S + col) =
-            make_float4(acc[i][q * 4 + 0], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
+      for (int i = 0; i < TM; ++i) {
+        float4 v = make_float4(acc[i][q * 4 + 0], acc[i][q * 4 + 1], acc[i][q * 4 + 2], acc[i][q * 4 + 3]);
+        if (apply_relu) {
+          v.x = fmaxf(v.x, 0.f);
+          v.y = fmaxf(v.y, 0.f);
+          v.z = fmaxf(v.z, 0.f);
+          v.w = fmaxf(v.w, 0.f);
+        }
+        *reinterpret_cast<float4*>(act + (ty + 16 * i) * S + col) = v;
+      }
+    }
+  }
+  if (rec) {  // flush this layer's extrema and reset the shared buffer
+    const long long SPH = static_cast<long long>(o.SP) * o.H;
+    for (int item = threadIdx.x; item < 2 * N; item += kThreads) {
+      const int sg = item / N, col = item % N;
+      const int vmin = red[2 * sg * RW + col], vmax = red[(2 * sg + 1) * RW + col];
+      red[2 * sg * RW + col] = enc_f(INFINITY);
+      red[(2 * sg + 1) * RW + col] = enc_f(-INFINITY);
+      if (sg == 1 && ts.bnd >= ts.nvalid) continue;
+      const long long idx = (ts.seg0 + sg) * SPH + t * o.SP + stat + col;
+      atomicMin(a.stat_min + idx, vmin);
+      atomicMax(a.stat_max + idx, vmax);
     }
   }
   __syncthreads();
@@ -184,29 +265,31 @@ __device__ void layer_narrow(const DevObjective& o, float* act, float* wsm, int 
 
 // Column pass over act[:, col0 : col0+ncols): per-subdomain extrema of the
 // valid rows into the global record (stat >= 0) and optional in-place ReLU.
+// segl[r] is the tile-local subdomain of row r (-1 past the last valid row);
+// seg0 the subdomain of the tile's first row.
 template <int R>
-__device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* act, int col0, int ncols, int stat,
-                            bool relu, int t, long long row0, int nvalid) {
-  const bool rec0 = stat >= 0 && a.stat_min != nullptr;
-  if (ncols <= 0 || (!rec0 && !relu)) return;  // uniform across the CTA
+__device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* act, const int* segl, long long seg0,
+                            int col0, int ncols, int stat, bool relu, int t) {
+  const bool rec = stat >= 0 && a.stat_min != nullptr;
+  if (ncols <= 0 || (!rec && !relu)) return;  // uniform across the CTA
   const int S = o.S;
   const int groups = max(1, min(R, kThreads / ncols));
   const int rpg = (R + groups - 1) / groups;
-  const bool rec = stat >= 0 && a.stat_min != nullptr;
-  const int SPH = o.SP * o.H;
+  const long long SPH = static_cast<long long>(o.SP) * o.H;
+  const int soff = t * o.SP + stat;
   for (int item = threadIdx.x; item < ncols * groups; item += kThreads) {
     const int c = item % ncols, g = item / ncols;
     const int rb = g * rpg, re = min(R, rb + rpg);
     float mn = INFINITY, mx = -INFINITY;
-    long long seg = -1;
-    for (int r = rb; r < re; ++r) {
-      float* p = act + r * S + col0 + c;
+    int seg = -1;
+    float* p = act + rb * S + col0 + c;
+    for (int r = rb; r < re; ++r, p += S) {
       const float v = *p;
-      if (rec && r < nvalid) {
-        const long long s = (row0 + r) / a.rows_per_sub;
+      if (rec) {
+        const int s = segl[r];
         if (s != seg) {
           if (seg >= 0) {
-            const long long idx = seg * SPH + static_cast<long long>(t) * o.SP + stat + c;
+            const long long idx = (seg0 + seg) * SPH + soff + c;
             atomicMin(a.stat_min + idx, enc_f(mn));
             atomicMax(a.stat_max + idx, enc_f(mx));
           }
@@ -220,7 +303,7 @@ __device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* 
       if (relu) *p = fmaxf(v, 0.f);
     }
     if (rec && seg >= 0) {
-      const long long idx = seg * SPH + static_cast<long long>(t) * o.SP + stat + c;
+      const long long idx = (seg0 + seg) * SPH + soff + c;
       atomicMin(a.stat_min + idx, enc_f(mn));
       atomicMax(a.stat_max + idx, enc_f(mx));
     }
@@ -307,7 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
   extern __shared__ __align__(16) float smem[];
   float* act = smem;                                // [R][S]
   float* prow = act + R * o.S;                      // [R][8] effector
-  float* wsm = prow + R * 8;                        // weights (resident image or slab)
+  int* segl = reinterpret_cast<int*>(prow + R * 8);  // [R] tile-local subdomain per row
+  int* red = segl + R;                              // [2 seg][min|max][red_w] fused-extrema scratch
+  float* wsm = prow + R * 9 + 4 * o.red_w;          // weights (resident image or slab)
   const long long row0 = static_cast<long long>(blockIdx.x) * R;
   const long long rem_rows = a.n_rows - row0;
   const int nvalid = static_cast<int>(rem_rows < R ? rem_rows : R);
@@ -323,6 +408,18 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
   }
 
   for (int i = tid; i < R * o.S; i += kThreads) act[i] = 0.f;
+  const long long seg0 = row0 / a.rows_per_sub;
+  if (tid < R) segl[tid] = tid < nvalid ? static_cast<int>((row0 + tid) / a.rows_per_sub - seg0) : -1;
+  for (int i = tid; i < 4 * o.red_w; i += kThreads) red[i] = enc_f(((i / o.red_w) & 1) ? -INFINITY : INFINITY);
+  TileSeg ts;
+  ts.seg0 = seg0;
+  ts.nvalid = nvalid;
+  {
+    const long long first_next = (seg0 + 1) * a.rows_per_sub;  // first row of the next subdomain
+    const long long b = first_next - row0;
+    ts.bnd = static_cast<int>(b < nvalid ? b : nvalid);
+    ts.two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
+  }
   if constexpr (!STREAM) copy_f4(wsm, o.f + o.wt[0] - o.w_smem_off[0], o.w_smem_total);
   __syncthreads();
 
@@ -343,8 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
       if (o.nstr[l] <= 16)
         layer_narrow<R, STREAM>(o, act, wsm, l, a.kslab);
       else
-        layer_wide<TM, NQ, STREAM>(o, act, wsm, l, a.kslab);
-      if (o.relu[l]) column_pass<R>(o, a, act, 0, o.widths[l + 1], o.pre_stat[l], true, t, row0, nvalid);
+        layer_wide<TM, NQ, STREAM>(o, a, act, wsm, red, l, ts, t);
+      // narrow hidden layers, or tiles spanning more than two subdomains
+      if (o.relu[l] && (o.nstr[l] <= 16 || !ts.two))
+        column_pass<R>(o, a, act, segl, seg0, 0, o.widths[l + 1], o.pre_stat[l], true, t);
     }
     // x_t in act[:, 0:ks).  Cost program with u_t, p_t in the row scratch.
     if (tid < R) {
@@ -359,11 +458,11 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
       cost += cost_program(o, row, t);
     }
     __syncthreads();
-    column_pass<R>(o, a, act, 0, ks, o.x_stat, false, t, row0, nvalid);
-    if (o.u_stat >= 0) column_pass<R>(o, a, act, o.ucol, ka, o.u_stat, false, t, row0, nvalid);
-    if (o.p_stat >= 0) column_pass<R>(o, a, act, o.pcol, kd, o.p_stat, false, t, row0, nvalid);
+    column_pass<R>(o, a, act, segl, seg0, 0, ks, o.x_stat, false, t);
+    if (o.u_stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.ucol, ka, o.u_stat, false, t);
+    if (o.p_stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.pcol, kd, o.p_stat, false, t);
     for (int i = 0; i < o.n_ops; ++i)
-      if (o.ops[i].stat >= 0) column_pass<R>(o, a, act, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t, row0, nvalid);
+      if (o.ops[i].stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t);
     if (tid < R) {
       float* row = act + tid * o.S;
       if (a.states != nullptr && row_ok)
