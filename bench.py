@@ -11,8 +11,10 @@ the launching stream, L2 flushed between steps, max over ranks.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun): each rank runs its own planner replica on its own
-device (weak scaling; the NCCL-sharded planner is the next step).
+Multi-GPU (torchrun): one planner sharded over the ranks -- every iteration's
+children go round-robin to the GPUs and their reports are allgathered over
+NCCL (paper_2412_09584_b200.parallel); the batch grows with the GPU count so
+each GPU keeps D=512 children per step (weak scaling).
 """
 from __future__ import annotations
 
@@ -156,11 +158,14 @@ def main():
         _capi.check(_capi.load().bp_measure_fp32_peak(local, C.byref(t), C.byref(ms)))
         peak = t.value
 
+    from paper_2412_09584_b200 import parallel
+
     dev = bp.Device(local).load(wl.spec)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
+    parallel.attach(dev)
     cfg = wl.planner_config()
-    cfg["seed"] = 2 + rank
+    cfg["batch"] = cfg["batch"] * world
     cfg["termination"]["max_iterations"] = 10**6
     planner = dev.planner(cfg)
     batch = cfg["batch"]
@@ -196,18 +201,17 @@ def main():
     if world > 1:
         mx = stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = stats.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        total_ms_max, children_all = mx[0].item(), sm[1].item()
+        total_ms_max = mx[0].item()
     else:
-        total_ms_max, children_all = total_ms, float(children)
+        total_ms_max = total_ms
+    children_all = float(children)  # the planner's global child count (identical on every rank)
     rows = wl.rows_per_search_iter
     H = wl.spec.horizon
     iters = cfg["search"]["iterations"]
     value = children_all / (total_ms_max / 1e3)
     sample_steps = children_all * rows * iters * H / (total_ms_max / 1e3)
     # roofline of the dominant kernel (rollout): algorithmic FLOPs / device time of its launches
-    flop = children * rows * iters * H * wl.flops_per_sample_step
+    flop = children / world * rows * iters * H * wl.flops_per_sample_step  # this rank's share
     achieved = flop / (tm["rollout_ms"] / 1e3) / 1e12 if tm["rollout_ms"] > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "rollout_ncu_summary.json")
@@ -219,8 +223,9 @@ def main():
         # end to end through the public API: objective upload, plan() from the root for the same number
         # of iterations, host buffers in and the result dict out, wall clock around the whole call.
         dev2 = bp.Device(local)
+        parallel.attach(dev2)
         cfg2 = wl.planner_config()
-        cfg2["seed"] = 2 + rank
+        cfg2["batch"] = cfg2["batch"] * world
         n_it = setup + args.warmup + args.steps
         cfg2["termination"]["max_iterations"] = n_it
         bp.Device.io_bytes()
@@ -258,9 +263,9 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded He-init weights, x0/goal/obstacles from the reference Rng)",
             "config": {"workload": f"{wl.name} (BASELINE.json configs[1])", "widths": wl.spec.widths,
-                       "H": H, "M": wl.samples_per_iter, "D_per_step": children / args.steps,
+                       "H": H, "M": wl.samples_per_iter, "D_per_step": children / args.steps, "D_per_gpu": children / args.steps / world,
                        "cem_iterations": iters, "batch": batch, "setup_iterations": setup,
-                       "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{world}"},
+                       "l2": "flushed (256 MB write) between timed steps", "parallelism": f"subdomain-sharded x{world}" if world > 1 else "1 GPU"},
             "sample_steps_per_s": sample_steps,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,

@@ -163,8 +163,14 @@ bp_status bp_init(int device, bp_ctx** out);
 bp_status bp_destroy(bp_ctx* ctx);
 /* Thread-local message of the last failing call (empty when none). */
 size_t bp_get_last_error(char* buf, size_t cap);
-/* Optional NCCL sharding: rank r of world w; unique_id is the 128-byte ncclUniqueId. */
-bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* nccl_unique_id);
+/* Subdomain sharding across ranks (one process per GPU).  With world > 1 the
+ * planner assigns child k of every BaB iteration to rank k % world, searches
+ * and bounds its own children on the device, and calls fn to allgather the
+ * packed reports: fn(user, send, bytes, recv) must fill recv (world * bytes)
+ * with every rank's send buffer in rank order and return 0.  The runtime's
+ * hook is torch.distributed.all_gather_into_tensor over NCCL (NVLink). */
+typedef int (*bp_exchange_fn)(void* user, const void* send, size_t bytes, void* recv);
+bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, void* user);
 
 /* Launch the context's work on an external stream (NULL = its own stream),
  * e.g. torch.cuda.current_stream(), so caller-side CUDA events time it. */

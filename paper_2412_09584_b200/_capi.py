@@ -80,13 +80,16 @@ class TraceRow(C.Structure):
     ]
 
 
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
 class PoolMeta(C.Structure):
     _fields_ = [("lf", C.c_double), ("uf", C.c_double), ("id", C.c_int64), ("log_vol", C.c_double)]
 
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
-    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_comm", "bp_set_stream", "bp_io_bytes",
+    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_io_bytes",
     "bp_load_objective",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
@@ -120,7 +123,7 @@ def load() -> C.CDLL:
             "bp_init": (C.c_int, [C.c_int, C.POINTER(vp)]),
             "bp_destroy": (C.c_int, [vp]),
             "bp_get_last_error": (C.c_size_t, [C.c_char_p, C.c_size_t]),
-            "bp_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+            "bp_set_exchange": (C.c_int, [vp, C.c_int, C.c_int, EXCHANGE_FN, vp]),
             "bp_set_stream": (C.c_int, [vp, vp]),
             "bp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_load_objective": (C.c_int, [vp, C.POINTER(ObjectiveDesc)]),

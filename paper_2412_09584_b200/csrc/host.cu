@@ -495,6 +495,10 @@ struct bp_ctx {
   std::vector<double> h_lo, h_hi;
   std::vector<int> h_failed;
   std::vector<Report> reports;
+  // sharding: rank / world and the allgather hook (host buffers)
+  int rank = 0, world = 1;
+  bp_exchange_fn exchange = nullptr;
+  void* exchange_user = nullptr;
   // scratch for bp_rollout
   DBuf<float> r_actions, r_costs, r_states;
   DBuf<int> r_min, r_max;
@@ -568,7 +572,7 @@ void check_loaded(bp_ctx* c) {
 
 // Device batch search (batch_search, search.cpp:262-282, with run_cem / run_mppi).
 void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm,
-                         const bp_search_config& cfg, std::vector<Report>* out) {
+                         const bp_search_config& cfg, std::vector<Report>* out, const int64_t* seed_index = nullptr) {
   const Compiled& cp = c->comp;
   const int d = cp.d;
   if (cfg.iterations <= 0 || cfg.samples_per_iter <= 0)
@@ -618,7 +622,9 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
     hf32[i] = static_cast<float>(hi[i]);
   }
   std::vector<unsigned long long> seeds(static_cast<size_t>(n));
-  for (int i = 0; i < n; ++i) seeds[static_cast<size_t>(i)] = cfg.seed ^ static_cast<unsigned long long>(i);
+  // derive_seed(seed, i) (rng.hpp:37-39) with i the box's index in the caller's batch
+  for (int i = 0; i < n; ++i)
+    seeds[static_cast<size_t>(i)] = cfg.seed ^ static_cast<unsigned long long>(seed_index ? seed_index[i] : i);
   a.seeds = c->seeds.get(static_cast<size_t>(n));
   a.lo = c->lo_f.get(nd);
   a.hi = c->hi_f.get(nd);
@@ -974,32 +980,111 @@ void merge_report(Rec& rec, Report&& rep, int top_capacity, int d) {  // bab.cpp
   }
 }
 
+// One child's search result as exchanged between ranks (fixed size).
+struct PackedReport {
+  static size_t bytes(int d, int K) { return sizeof(double) * (6 + static_cast<size_t>(d)) + sizeof(float) * static_cast<size_t>(K) * (1 + d); }
+  static void pack(unsigned char* p, int64_t index, const Report& r, double lf, int d, int K) {
+    double* h = reinterpret_cast<double*>(p);
+    const int nt = static_cast<int>(r.top_val.size());
+    h[0] = static_cast<double>(index);
+    h[1] = r.ok ? 1.0 : 0.0;
+    h[2] = static_cast<double>(r.samples);
+    h[3] = r.uf;
+    h[4] = lf;
+    h[5] = nt;
+    for (int j = 0; j < d; ++j) h[6 + j] = r.best.empty() ? std::nan("") : r.best[static_cast<size_t>(j)];
+    float* f = reinterpret_cast<float*>(h + 6 + d);
+    std::copy(r.top_val.begin(), r.top_val.end(), f);
+    std::copy(r.top_act.begin(), r.top_act.end(), f + K);
+  }
+  static int64_t unpack(const unsigned char* p, Report& r, double& lf, int d, int K) {
+    const double* h = reinterpret_cast<const double*>(p);
+    const int64_t index = static_cast<int64_t>(h[0]);
+    if (index < 0) return -1;
+    r = Report();
+    r.ok = h[1] != 0.0;
+    if (!r.ok) r.error = "evaluate: non-finite objective value (malformed weights?)";
+    r.samples = static_cast<int64_t>(h[2]);
+    r.uf = h[3];
+    lf = h[4];
+    const int nt = static_cast<int>(h[5]);
+    if (r.ok) r.best.assign(h + 6, h + 6 + d);
+    const float* f = reinterpret_cast<const float*>(h + 6 + d);
+    r.top_val.assign(f, f + nt);
+    r.top_act.assign(f + K, f + K + static_cast<size_t>(nt) * d);
+    return index;
+  }
+};
+
 std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec>& boxes, const std::vector<const std::vector<double>*>& warms,
                                      const bp_search_config& scfg, int mode, int alpha, std::vector<double>* lfs) {
   const int d = c->comp.d;
-  const int n = static_cast<int>(boxes.size());
+  const int n_all = static_cast<int>(boxes.size());
+  const bool shard = c->world > 1 && c->exchange != nullptr && n_all > 1;
+  // children of the global pick order go round-robin to the ranks; a child's
+  // sampler stream is keyed by its global index, so results do not depend on
+  // the number of ranks.
+  std::vector<int64_t> mine;
+  for (int i = 0; i < n_all; ++i)
+    if (!shard || i % c->world == c->rank) mine.push_back(i);
+  const int n = static_cast<int>(mine.size());
   std::vector<double> lo(static_cast<size_t>(n) * d), hi(static_cast<size_t>(n) * d), warm(static_cast<size_t>(n) * d);
   bool any_warm = false;
-  for (int i = 0; i < n; ++i) {
-    std::copy(boxes[static_cast<size_t>(i)].lo.begin(), boxes[static_cast<size_t>(i)].lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(i) * d);
-    std::copy(boxes[static_cast<size_t>(i)].hi.begin(), boxes[static_cast<size_t>(i)].hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(i) * d);
-    const std::vector<double>* w = warms[static_cast<size_t>(i)];
+  for (int k = 0; k < n; ++k) {
+    const size_t i = static_cast<size_t>(mine[static_cast<size_t>(k)]);
+    std::copy(boxes[i].lo.begin(), boxes[i].lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(k) * d);
+    std::copy(boxes[i].hi.begin(), boxes[i].hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(k) * d);
+    const std::vector<double>* w = warms[i];
     if (w != nullptr && !w->empty()) {
       any_warm = true;
-      std::copy(w->begin(), w->end(), warm.begin() + static_cast<std::ptrdiff_t>(i) * d);
+      std::copy(w->begin(), w->end(), warm.begin() + static_cast<std::ptrdiff_t>(k) * d);
     } else {
-      std::fill(warm.begin() + static_cast<std::ptrdiff_t>(i) * d, warm.begin() + static_cast<std::ptrdiff_t>(i + 1) * d,
+      std::fill(warm.begin() + static_cast<std::ptrdiff_t>(k) * d, warm.begin() + static_cast<std::ptrdiff_t>(k + 1) * d,
                 std::numeric_limits<double>::quiet_NaN());
     }
   }
   std::vector<Report> reps;
+  std::vector<double> my_lf(static_cast<size_t>(n), 0.0);
   const auto t0 = std::chrono::steady_clock::now();
-  device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps);
-  lfs->assign(static_cast<size_t>(n), 0.0);
-  device_batch_bound(c, mode, alpha, lfs->data());
+  if (n > 0) {
+    device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps, mine.data());
+    device_batch_bound(c, mode, alpha, my_lf.data());
+  }
   c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   c->harvest_roll_events();
-  return reps;
+  if (!shard) {
+    *lfs = std::move(my_lf);
+    return reps;
+  }
+  // allgather of the packed reports (every rank then replays the same host logic)
+  const int K = std::max(scfg.top_capacity, 1);
+  const size_t rb = PackedReport::bytes(d, K);
+  const int per_rank = (n_all + c->world - 1) / c->world;
+  std::vector<unsigned char> send(rb * static_cast<size_t>(per_rank), 0), recv(send.size() * static_cast<size_t>(c->world), 0);
+  for (int k = 0; k < per_rank; ++k) {
+    unsigned char* p = send.data() + rb * static_cast<size_t>(k);
+    if (k < n)
+      PackedReport::pack(p, mine[static_cast<size_t>(k)], reps[static_cast<size_t>(k)], my_lf[static_cast<size_t>(k)], d, K);
+    else
+      reinterpret_cast<double*>(p)[0] = -1.0;
+  }
+  if (c->exchange(c->exchange_user, send.data(), send.size(), recv.data()) != 0)
+    fail(BP_NCCL, "exchange: allgather of child reports failed");
+  std::vector<Report> all(static_cast<size_t>(n_all));
+  lfs->assign(static_cast<size_t>(n_all), 0.0);
+  std::vector<char> seen(static_cast<size_t>(n_all), 0);
+  for (size_t k = 0; k < static_cast<size_t>(per_rank) * c->world; ++k) {
+    Report r;
+    double lf = 0.0;
+    const int64_t idx = PackedReport::unpack(recv.data() + rb * k, r, lf, d, K);
+    if (idx < 0) continue;
+    if (idx >= n_all || seen[static_cast<size_t>(idx)]) fail(BP_NCCL, "exchange: inconsistent child reports");
+    seen[static_cast<size_t>(idx)] = 1;
+    all[static_cast<size_t>(idx)] = std::move(r);
+    (*lfs)[static_cast<size_t>(idx)] = lf;
+  }
+  if (std::find(seen.begin(), seen.end(), 0) != seen.end()) fail(BP_NCCL, "exchange: missing child reports");
+  return all;
 }
 
 // plan() (bab.cpp:266-415) as a steppable object: the constructor runs the
@@ -1254,11 +1339,15 @@ bp_status bp_destroy(bp_ctx* ctx) {
   });
 }
 
-bp_status bp_set_comm(bp_ctx* ctx, int rank, int world, const void* uid) {
+bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, void* user) {
   return guard([&] {
     check_ctx(ctx);
-    (void)rank, (void)world, (void)uid;
-    fail(BP_UNSUPPORTED, "bp_set_comm: NCCL sharding is driven from the host runtime (paper_2412_09584_b200.parallel)");
+    if (world < 1 || rank < 0 || rank >= world) fail(BP_INVALID_ARGUMENT, "bp_set_exchange: bad rank / world");
+    if (world > 1 && fn == nullptr) fail(BP_INVALID_ARGUMENT, "bp_set_exchange: null exchange for world > 1");
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->exchange = fn;
+    ctx->exchange_user = user;
   });
 }
 
