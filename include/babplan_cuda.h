@@ -175,6 +175,10 @@ bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, v
 /* Launch the context's work on an external stream (NULL = its own stream),
  * e.g. torch.cuda.current_stream(), so caller-side CUDA events time it. */
 bp_status bp_set_stream(bp_ctx* ctx, void* cuda_stream);
+/* Rollout kernel selection: path 0 = auto (tcgen05 3xTF32 when every layer
+ * width is <= 128 and it fits shared memory, else SIMT FP32), 1 = SIMT only,
+ * -1 = query.  *active (optional) = 2 tcgen05, 1 SIMT for the loaded objective. */
+bp_status bp_set_rollout_path(bp_ctx* ctx, int path, int* active);
 /* Host<->device bytes the library copied since the previous call. */
 bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h);
 

@@ -153,6 +153,13 @@ class Device:
         """Run on an external CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
         check(self.lib.bp_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
 
+    def rollout_path(self, path: Optional[str] = None) -> str:
+        """Select ("auto" | "simt") and report ("tcgen05" | "simt") the rollout kernel."""
+        code = {None: -1, "auto": 0, "simt": 1}[path]
+        active = C.c_int()
+        check(self.lib.bp_set_rollout_path(self.h, code, C.byref(active)))
+        return "tcgen05" if active.value == 2 else "simt"
+
     @staticmethod
     def io_bytes():
         """(h2d, d2h) bytes copied by the library since the previous call."""

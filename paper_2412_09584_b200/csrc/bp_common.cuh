@@ -53,6 +53,10 @@ struct DevObjective {
   int stop_layer;   // hidden layer whose ReLU output at step H is the last-ReLU stop (-1)
   int stop_op;      // RELU cost op that is the last-ReLU stop at step H (-1)
   int xstop;        // int arena offset: H flags, x_t is a stop node
+  // tcgen05 (3xTF32) rollout: per layer a K-block image [kb][hi|lo][npad rows x 32 tf32, 128B-swizzled]
+  int tc;                    // eligible (all widths <= 128)
+  int tc_w[kMaxLayers], tc_bias[kMaxLayers], tc_npad[kMaxLayers], tc_kb[kMaxLayers], tc_ksteps[kMaxLayers];
+  int tc_kbmax, tc_npadmax, tc_S, tc_cols;
   // constants
   int x0, p0, step_w;        // float arena offsets
   int x0d, p0d;              // double arena offsets

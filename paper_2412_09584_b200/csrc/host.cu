@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -80,6 +81,8 @@ struct SearchArgs {
   int n_noise;
 };
 cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, bool stream, size_t smem, cudaStream_t st);
+cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
+size_t rollout_tc_smem(const DevObjective& o);
 int rollout_rows_per_tile(int nq);
 cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st);
 size_t bound_smem_bytes();
@@ -132,6 +135,15 @@ cudaError_t memcpy_counted(void* dst, const void* src, size_t n, cudaMemcpyKind 
 }
 
 int r4(int x) { return (x + 3) & ~3; }
+int r16(int x) { return (x + 15) & ~15; }
+float rna_tf32_host(float x) {  // cvt.rna.tf32.f32: round the 13 dropped mantissa bits, ties away
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  b = (b + 0x1000u) & ~0x1FFFu;
+  float r;
+  std::memcpy(&r, &b, 4);
+  return r;
+}
 int r8(int x) { return (x + 7) & ~7; }
 
 // Grow-only device buffer.
@@ -180,6 +192,7 @@ struct Compiled {
   size_t smem = 0;
   int kslab = 0;
   int R = 0;
+  size_t tc_smem = 0;
   // stat layout (for bp_stat_layout): kind 0 preact(layer), 1 x, 2 u, 3 p, 4 op(index)
   std::vector<int> slot_kind, slot_index, slot_dim, slot_off;
   std::vector<double> x0, p0, ulo, uhi;
@@ -455,6 +468,49 @@ Compiled compile(const bp_objective_desc& d) {
     c.kslab = ksl;
     c.smem = base_bytes + (static_cast<size_t>(ksl) * maxNS + pad) * sizeof(float);
   }
+  // tcgen05 (3xTF32) rollout: every layer K, N <= 128, and its shared memory fits
+  {
+    bool ok = true;
+    int kbmax = 1, npadmax = 16;
+    for (int l = 0; l < d.n_layers; ++l) {
+      const int K = d.widths[l], N = d.widths[l + 1];
+      if (K > 128 || N > 128) ok = false;
+      kbmax = std::max({kbmax, (K + 31) / 32, (N + 31) / 32});
+      npadmax = std::max(npadmax, std::max(16, r16(N)));
+    }
+    o.tc = 0;
+    if (ok) {
+      o.tc_kbmax = kbmax;
+      o.tc_npadmax = npadmax;
+      o.tc_S = r8(std::max(col, r4(d.ks))) + 4;
+      o.tc_cols = 32;
+      while (o.tc_cols < npadmax) o.tc_cols *= 2;
+      for (int l = 0; l < d.n_layers; ++l) {
+        const int K = d.widths[l], N = d.widths[l + 1];
+        const int npad = std::max(16, r16(N)), kb = (K + 31) / 32;
+        o.tc_npad[l] = npad;
+        o.tc_kb[l] = kb;
+        o.tc_ksteps[l] = (K + 7) / 8;
+        std::vector<double> img(static_cast<size_t>(kb) * 2 * npad * 32, 0.0);
+        for (int b = 0; b < kb; ++b)
+          for (int n = 0; n < npad; ++n)
+            for (int cc = 0; cc < 32; ++cc) {
+              const int k = b * 32 + cc;
+              const float w = (n < N && k < K) ? static_cast<float>(d.W[l][static_cast<size_t>(n) * K + k]) : 0.f;
+              const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
+              const size_t pos = static_cast<size_t>(n) * 32 + (((cc >> 2) ^ (n & 7)) << 2) + (cc & 3);
+              img[static_cast<size_t>(b) * 2 * npad * 32 + pos] = hi;
+              img[static_cast<size_t>(b) * 2 * npad * 32 + static_cast<size_t>(npad) * 32 + pos] = lo;
+            }
+        o.tc_w[l] = push_f(c.fa, img.data(), img.size());
+        std::vector<double> bp(static_cast<size_t>(npad), 0.0);
+        for (int n = 0; n < N; ++n) bp[static_cast<size_t>(n)] = d.b[l][n];
+        o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
+      }
+      c.tc_smem = bp::rollout_tc_smem(o);
+      o.tc = c.tc_smem <= cap ? 1 : 0;
+    }
+  }
   return c;
 }
 
@@ -509,6 +565,7 @@ struct bp_ctx {
   double rollout_ms = 0, bound_ms = 0, search_ms = 0;
   int64_t rollout_launches = 0, launches = 0;
   bool timing = true;
+  bool force_simt = false;  // BP_ROLLOUT=simt or bp_set_rollout_path
 
   ~bp_ctx() {
     for (auto& e : roll_events) {
@@ -552,7 +609,10 @@ struct bp_ctx {
       ev = roll_event();
       ck(cudaEventRecord(ev.first, stream), "event");
     }
-    ck(bp::launch_rollout(dev(), a, comp.nq, comp.stream, comp.smem, stream), "rollout launch");
+    if (comp.o.tc && !force_simt)
+      ck(bp::launch_rollout_tc(dev(), a, stream), "rollout (tcgen05) launch");
+    else
+      ck(bp::launch_rollout(dev(), a, comp.nq, comp.stream, comp.smem, stream), "rollout launch");
     if (timing) ck(cudaEventRecord(ev.second, stream), "event");
     ++rollout_launches;
     ++launches;
@@ -1322,6 +1382,7 @@ bp_status bp_init(int device, bp_ctx** out) {
     ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major < 10) fail(BP_CUDA, "bp_init: device is not sm_100 class (B200 required)");
     c->sms = prop.multiProcessorCount;
+    if (const char* env = std::getenv("BP_ROLLOUT")) c->force_simt = std::string(env) == "simt";
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
@@ -1356,6 +1417,15 @@ bp_status bp_set_stream(bp_ctx* ctx, void* stream) {
     check_ctx(ctx);
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->stream = stream != nullptr ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+bp_status bp_set_rollout_path(bp_ctx* ctx, int path, int* active) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (path == 0) ctx->force_simt = false;
+    if (path == 1) ctx->force_simt = true;
+    if (active) *active = (ctx->loaded && ctx->comp.o.tc && !ctx->force_simt) ? 2 : 1;
   });
 }
 

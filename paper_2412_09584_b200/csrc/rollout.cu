@@ -21,21 +21,9 @@
 
 #include <cstdint>
 
-#include "bp_common.cuh"
+#include "rollout_common.cuh"
 
 namespace bp {
-
-struct RolloutArgs {
-  const float* actions;  // [n_rows][d]
-  float* costs;          // [n_rows]
-  float* states;         // optional [n_rows][H][ks]
-  int* stat_min;         // [n_sub][H*SP] (enc_f), may be null
-  int* stat_max;
-  int* failed;           // [n_sub], may be null: set when a row's objective is non-finite
-  long long n_rows;
-  int rows_per_sub;
-  int kslab;             // streamed mode: K rows per weight slab
-};
 
 namespace {
 
@@ -95,14 +83,6 @@ __device__ __forceinline__ void copy_f4(float* dst, const float* __restrict__ sr
   for (int i = threadIdx.x; i < n4; i += kThreads)
     reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
 }
-
-// Rows of a tile split into at most two subdomains: rows [0, bnd) belong to
-// subdomain seg0, rows [bnd, nvalid) to seg0 + 1 (bnd = nvalid when one).
-struct TileSeg {
-  long long seg0;
-  int bnd, nvalid;
-  bool two;  // the tile fits the two-segment form (rows_per_sub >= R)
-};
 
 // Wide layer with the fused epilogue: bias in the accumulator, per-column
 // extrema of the pre-activations (register -> xor-16 shuffle -> shared
@@ -263,127 +243,6 @@ __device__ void layer_narrow(const DevObjective& o, float* act, float* wsm, int 
   __syncthreads();
 }
 
-// Column pass over act[:, col0 : col0+ncols): per-subdomain extrema of the
-// valid rows into the global record (stat >= 0) and optional in-place ReLU.
-// segl[r] is the tile-local subdomain of row r (-1 past the last valid row);
-// seg0 the subdomain of the tile's first row.
-template <int R>
-__device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* act, const int* segl, long long seg0,
-                            int col0, int ncols, int stat, bool relu, int t) {
-  const bool rec = stat >= 0 && a.stat_min != nullptr;
-  if (ncols <= 0 || (!rec && !relu)) return;  // uniform across the CTA
-  const int S = o.S;
-  const int groups = max(1, min(R, kThreads / ncols));
-  const int rpg = (R + groups - 1) / groups;
-  const long long SPH = static_cast<long long>(o.SP) * o.H;
-  const int soff = t * o.SP + stat;
-  for (int item = threadIdx.x; item < ncols * groups; item += kThreads) {
-    const int c = item % ncols, g = item / ncols;
-    const int rb = g * rpg, re = min(R, rb + rpg);
-    float mn = INFINITY, mx = -INFINITY;
-    int seg = -1;
-    float* p = act + rb * S + col0 + c;
-    for (int r = rb; r < re; ++r, p += S) {
-      const float v = *p;
-      if (rec) {
-        const int s = segl[r];
-        if (s != seg) {
-          if (seg >= 0) {
-            const long long idx = (seg0 + seg) * SPH + soff + c;
-            atomicMin(a.stat_min + idx, enc_f(mn));
-            atomicMax(a.stat_max + idx, enc_f(mx));
-          }
-          seg = s;
-          mn = INFINITY;
-          mx = -INFINITY;
-        }
-        mn = fminf(mn, v);
-        mx = fmaxf(mx, v);
-      }
-      if (relu) *p = fmaxf(v, 0.f);
-    }
-    if (rec && seg >= 0) {
-      const long long idx = (seg0 + seg) * SPH + soff + c;
-      atomicMin(a.stat_min + idx, enc_f(mn));
-      atomicMax(a.stat_max + idx, enc_f(mx));
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ const float* val_ptr(const DevObjective& o, const float* row, int id) {
-  if (id == 0) return row;                 // x_t
-  if (id == 1) return row + o.ucol;        // u_t
-  if (id == 2) return row + o.pcol;        // p_t
-  return row + o.ops[id - 3].col;          // op output
-}
-
-// The step's cost program for one row (reference node semantics, graph.cpp:293-347).
-__device__ float cost_program(const DevObjective& o, float* row, int t) {
-  float cost = 0.f;
-  for (int i = 0; i < o.n_ops; ++i) {
-    const DevOp& op = o.ops[i];
-    const float* src = val_ptr(o, row, op.src0);
-    float* dst = row + op.col;
-    float v = 0.f;
-    switch (op.kind) {
-      case 0: {  // LINEAR
-        const float* W = o.f + op.w;
-        const float* b = o.f + op.b;
-        for (int r = 0; r < op.dim; ++r) {
-          float s = 0.f;
-          for (int j = 0; j < op.in_dim; ++j) s = fmaf(__ldg(W + r * op.in_dim + j), src[j], s);
-          dst[r] = s + __ldg(b + r);
-        }
-        v = dst[0];
-        break;
-      }
-      case 1:  // RELU
-        for (int j = 0; j < op.dim; ++j) dst[j] = fmaxf(src[j], 0.f);
-        v = dst[0];
-        break;
-      case 2: {  // SUM
-        const float* s1 = op.src1 >= 0 ? val_ptr(o, row, op.src1) : nullptr;
-        for (int j = 0; j < op.dim; ++j) dst[j] = s1 ? src[j] + s1[j] : src[j];
-        v = dst[0];
-        break;
-      }
-      case 3:  // SCALAR_AFFINE
-        for (int j = 0; j < op.dim; ++j) dst[j] = op.scale * src[j] + op.offset;
-        v = dst[0];
-        break;
-      case 4: {  // SQDIST
-        const float* tg = o.f + op.tgt;
-        const float* wt = o.f + op.wt + (op.weight_by_step ? t * op.in_dim : 0);
-        float acc = 0.f;
-        for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - __ldg(tg + j);
-          acc += __ldg(wt + j) * d * d;
-        }
-        dst[0] = v = acc;
-        break;
-      }
-      case 5: {  // HINGE
-        const float* c = o.f + op.ctr;
-        float acc = 0.f;
-        for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - __ldg(c + j);
-          acc += d * d;
-        }
-        const float m = op.radius - sqrtf(acc);
-        dst[0] = v = m > 0.f ? op.penalty * m : 0.f;
-        break;
-      }
-      case 6:  // SLICE
-        for (int j = 0; j < op.dim; ++j) dst[j] = src[op.begin + j];
-        v = dst[0];
-        break;
-    }
-    if (op.is_term) cost += v;
-  }
-  return cost;
-}
-
 template <int TM, int NQ, bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective o, const RolloutArgs a) {
   constexpr int R = 16 * TM;
@@ -443,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
         layer_wide<TM, NQ, STREAM>(o, a, act, wsm, red, l, ts, t);
       // narrow hidden layers, or tiles spanning more than two subdomains
       if (o.relu[l] && (o.nstr[l] <= 16 || !ts.two))
-        column_pass<R>(o, a, act, segl, seg0, 0, o.widths[l + 1], o.pre_stat[l], true, t);
+        column_pass<R>(o, a, act, o.S, segl, seg0, 0, o.widths[l + 1], o.pre_stat[l], true, t);
     }
     // x_t in act[:, 0:ks).  Cost program with u_t, p_t in the row scratch.
     if (tid < R) {
@@ -458,11 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
       cost += cost_program(o, row, t);
     }
     __syncthreads();
-    column_pass<R>(o, a, act, segl, seg0, 0, ks, o.x_stat, false, t);
-    if (o.u_stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.ucol, ka, o.u_stat, false, t);
-    if (o.p_stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.pcol, kd, o.p_stat, false, t);
+    column_pass<R>(o, a, act, o.S, segl, seg0, 0, ks, o.x_stat, false, t);
+    if (o.u_stat >= 0) column_pass<R>(o, a, act, o.S, segl, seg0, o.ucol, ka, o.u_stat, false, t);
+    if (o.p_stat >= 0) column_pass<R>(o, a, act, o.S, segl, seg0, o.pcol, kd, o.p_stat, false, t);
     for (int i = 0; i < o.n_ops; ++i)
-      if (o.ops[i].stat >= 0) column_pass<R>(o, a, act, segl, seg0, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t);
+      if (o.ops[i].stat >= 0) column_pass<R>(o, a, act, o.S, segl, seg0, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t);
     if (tid < R) {
       float* row = act + tid * o.S;
       if (a.states != nullptr && row_ok)

@@ -1,0 +1,484 @@
+// rollout_tc.cu -- K1 on the 5th-generation tensor cores: the same fused
+// H-step rollout as rollout.cu (reference evaluate / forward_chunk,
+// proj/src/graph.cpp:252-401, on the build_objective graph, model.cpp:310-387),
+// with every Linear layer done by tcgen05.mma (kind::tf32) into a TMEM
+// accumulator.
+//
+// Precision: 3xTF32.  Activations and weights are split into hi = rna_tf32(x)
+// and lo = rna_tf32(x - hi); D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi keeps
+// ~2^-21 relative per product (FP32 is 2^-24), inside the 1e-5 parity bar.
+//
+// One CTA = 128 rows (the MMA M), warp-specialized:
+//   warps 0-3  row work: warp w owns TMEM lanes 32w..32w+31 = rows 32w..32w+31;
+//              the fused epilogue reads the accumulator (tcgen05.ld), adds the
+//              bias, reduces per-column sample extrema (butterfly
+//              transpose-reduce -> shared atomics -> one global atomic per
+//              column and subdomain), applies ReLU and writes the hi / lo split
+//              of the next layer's input straight back into TMEM (tcgen05.st),
+//              where the next MMAs read it as their A operand; after the output
+//              layer it runs the per-row cost program (rollout_common.cuh).
+//   warp 4     producer: streams the weight K-blocks (hi and lo, host-side
+//              pre-swizzled to the 128B K-major UMMA layout) into a ring of
+//              shared-memory stages with cp.async.bulk + mbarrier tx counts,
+//              running ahead across layers and steps.
+//   warp 5     MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
+//              TMEM, B from shared memory) per K=8 step; tcgen05.commit frees
+//              the weight stage and, at the end of a layer, hands the
+//              accumulator to the epilogue.
+// TMEM: columns [0,128) accumulator D, [128,256) A_hi, [256,384) A_lo.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rollout_common.cuh"
+
+namespace bp {
+
+namespace {
+
+constexpr int kTcThreads = 192;  // 4 row warps + producer warp + MMA warp
+constexpr int kStages = 4;
+constexpr uint32_t kColD = 0, kColAhi = 128, kColAlo = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;                    // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>((1024u >> 4) & 0x3FFFu) << 32;  // SBO
+  d |= static_cast<uint64_t>(1u) << 46;                    // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2u) << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=n.
+__device__ __forceinline__ uint32_t tf32_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  for (long long spin = 0; !done; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (spin > (1ll << 28)) asm volatile("trap;");  // never hang the device on a lost arrival
+  }
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+  for (int j = 16; j < 32; ++j) v[j] = 0.f;
+}
+
+// Butterfly transpose-reduce: lane l ends with the min (max) over the warp's
+// 32 rows of column l.  31 shuffles per reduction instead of 32 x 5.
+__device__ __forceinline__ void warp_colreduce(float (&mn)[32], float (&mx)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float smn = upper ? mn[i] : mn[i + s];
+      const float smx = upper ? mx[i] : mx[i + s];
+      const float rmn = __shfl_xor_sync(0xffffffffu, smn, s);
+      const float rmx = __shfl_xor_sync(0xffffffffu, smx, s);
+      mn[i] = fminf(upper ? mn[i + s] : mn[i], rmn);
+      mx[i] = fmaxf(upper ? mx[i + s] : mx[i], rmx);
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31])));
+}
+
+// Writes 32 consecutive K-values of this thread's row as the hi / lo A operand in TMEM.
+__device__ __forceinline__ void store_operand_tmem(uint32_t tlane, int chunk, const float (&v)[32]) {
+  float h[32], l[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    h[j] = rna_tf32(v[j]);
+    l[j] = rna_tf32(v[j] - h[j]);
+  }
+  tmem_st32(tlane + kColAhi + 32 * chunk, h);
+  tmem_st32(tlane + kColAlo + 32 * chunk, l);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct TcSmem {
+  unsigned char* w;    // [kStages][hi | lo][npadmax rows x 128 B]
+  float* sc;           // [128][tc_S] per-row scratch (x_t, u_t, p_t, cost-op values)
+  float* bias;         // [L][npadmax]
+  int* red;            // [2][2][red_w]
+  int* segl;           // [128]
+  float* prow;         // [128][8]
+  uint64_t* full;      // [kStages] weight stage landed
+  uint64_t* empty;     // [kStages] weight stage consumed by the MMAs
+  uint64_t* d_full;    // accumulator ready for the epilogue
+  uint64_t* a_full;    // A operand written (and D drained) by the 128 row threads
+  uint32_t* tmem_slot;
+};
+
+__device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
+  const uint32_t s0 = smem_u32(raw);
+  unsigned char* base = raw + (((s0 + 1023u) & ~1023u) - s0);
+  TcSmem m;
+  m.w = base;
+  m.sc = reinterpret_cast<float*>(m.w + kStages * 2 * o.tc_npadmax * 128);
+  m.bias = m.sc + 128 * o.tc_S;
+  m.red = reinterpret_cast<int*>(m.bias + o.L * o.tc_npadmax);
+  m.segl = m.red + 4 * o.red_w;
+  m.prow = reinterpret_cast<float*>(m.segl + 128);
+  m.full = reinterpret_cast<uint64_t*>(m.prow + 128 * 8);
+  m.empty = m.full + kStages;
+  m.d_full = m.empty + kStages;
+  m.a_full = m.d_full + 1;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(m.a_full + 1);
+  return m;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObjective o, const RolloutArgs a) {
+  extern __shared__ unsigned char smraw[];
+  const TcSmem m = carve(o, smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long row0 = static_cast<long long>(blockIdx.x) * 128;
+  const long long rem_rows = a.n_rows - row0;
+  const int nvalid = static_cast<int>(rem_rows < 128 ? rem_rows : 128);
+  const int ks = o.ks, ka = o.ka, kd = o.kd, d = o.d, S = o.tc_S, L = o.L, H = o.H;
+
+  if (a.failed != nullptr) {  // skip tiles whose subdomains already failed
+    const long long s0 = row0 / a.rows_per_sub, s1 = (row0 + nvalid - 1) / a.rows_per_sub;
+    bool all_failed = true;
+    for (long long s = s0; s <= s1; ++s) all_failed = all_failed && a.failed[s] != 0;
+    if (all_failed) return;
+  }
+
+  const long long seg0 = row0 / a.rows_per_sub;
+  if (tid < 128) m.segl[tid] = tid < nvalid ? static_cast<int>((row0 + tid) / a.rows_per_sub - seg0) : -1;
+  for (int i = tid; i < 4 * o.red_w; i += kTcThreads) m.red[i] = enc_f(((i / o.red_w) & 1) ? -INFINITY : INFINITY);
+  for (int i = tid; i < 128 * S; i += kTcThreads) m.sc[i] = 0.f;
+  for (int i = tid; i < L * o.tc_npadmax; i += kTcThreads) {
+    const int l = i / o.tc_npadmax, j = i % o.tc_npadmax;
+    m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(m.full + s, 1);
+      mbar_init(m.empty + s, 1);
+    }
+    mbar_init(m.d_full, 1);
+    mbar_init(m.a_full, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *m.tmem_slot;
+  const int stage_bytes = 2 * o.tc_npadmax * 128;
+
+  if (warp == 4) {
+    // ------------------------------------------------ producer: weight K-blocks
+    if (lane == 0) {
+      int it = 0;
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l < L; ++l) {
+          const int npad = o.tc_npad[l];
+          const uint32_t bytes = 2u * npad * 128u;
+          for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
+            const int s = it % kStages;
+            if (it >= kStages) mbar_wait(m.empty + s, static_cast<uint32_t>((it / kStages - 1) & 1));
+            mbar_expect_tx(m.full + s, bytes);
+            bulk_g2s(m.w + s * stage_bytes, o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32, bytes, m.full + s);
+          }
+        }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int it = 0, layer_it = 0;
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l < L; ++l, ++layer_it) {
+          const int npad = o.tc_npad[l];
+          const uint32_t idesc = tf32_idesc(npad);
+          mbar_wait(m.a_full, static_cast<uint32_t>(layer_it & 1));  // A written, D drained
+          fence_after();
+          for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
+            const int s = it % kStages;
+            mbar_wait(m.full + s, static_cast<uint32_t>((it / kStages) & 1));
+            fence_after();
+            const uint32_t wb_hi = smem_u32(m.w + s * stage_bytes), wb_lo = wb_hi + npad * 128;
+            for (int q = 0; q < 4; ++q) {
+              const int kstep = kb * 4 + q;
+              if (kstep >= o.tc_ksteps[l]) break;
+              const uint64_t bh = sw128_desc(wb_hi + 32 * q), bl = sw128_desc(wb_lo + 32 * q);
+              const uint32_t ah = tmem + kColAhi + 8 * kstep, al = tmem + kColAlo + 8 * kstep;
+              mma_tf32_ts(tmem + kColD, ah, bh, idesc, kstep > 0 ? 1u : 0u);
+              mma_tf32_ts(tmem + kColD, ah, bl, idesc, 1u);
+              mma_tf32_ts(tmem + kColD, al, bh, idesc, 1u);
+            }
+            mma_commit(m.empty + s);  // stage free once these MMAs retire
+          }
+          mma_commit(m.d_full);  // accumulator complete
+        }
+    }
+  } else {
+    // ------------------------------------------------ row threads (epilogue + cost program)
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    TileSeg ts;
+    ts.seg0 = seg0;
+    ts.nvalid = nvalid;
+    {
+      const long long b = (seg0 + 1) * a.rows_per_sub - row0;
+      ts.bnd = static_cast<int>(b < nvalid ? b : nvalid);
+      ts.two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
+    }
+    const bool row_ok = tid < nvalid;
+    const float* urow = row_ok ? a.actions + (row0 + tid) * d : nullptr;
+    float* srow = m.sc + tid * S;
+    for (int j = 0; j < kd; ++j) m.prow[tid * 8 + j] = o.f[o.p0 + j];
+    for (int j = 0; j < ks; ++j) srow[j] = o.f[o.x0 + j];
+    float ucur[8], unext[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ucur[j] = (row_ok && j < ka) ? __ldg(urow + j) : 0.f;
+    float cost = 0.f;
+    int layer_it = 0;
+    const int SPH = o.SP * H;
+    for (int t = 0; t < H; ++t) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) unext[j] = (row_ok && j < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+      // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
+      for (int kb = 0; kb < o.tc_kb[0]; ++kb) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = kb * 32 + j;
+          float x = 0.f;
+          if (k < ks) {
+            x = srow[k] - (o.rel ? m.prow[tid * 8 + k % kd] : 0.f);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (k - ks == q && q < ka) x = ucur[q];
+          }
+          v[j] = x;
+        }
+        store_operand_tmem(tlane, kb, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_before();
+      mbar_arrive(m.a_full);
+      for (int l = 0; l < L; ++l, ++layer_it) {
+        const int N = o.widths[l + 1], npad = o.tc_npad[l];
+        mbar_wait(m.d_full, static_cast<uint32_t>(layer_it & 1));
+        fence_after();
+        const bool hidden = l + 1 < L;
+        const bool relu = o.relu[l] != 0;
+        const int stat = o.pre_stat[l];
+        const bool rec = relu && stat >= 0 && a.stat_min != nullptr;
+        const float* bias = m.bias + l * o.tc_npadmax;
+        const int nchunk = (npad + 31) / 32;
+        for (int cb = 0; cb < nchunk; ++cb) {
+          float v[32];
+          if (npad - cb * 32 >= 32)
+            tmem_ld32(tlane + kColD + cb * 32, v);
+          else
+            tmem_ld16(tlane + kColD + cb * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (cb * 32 + j < N) ? v[j] + bias[cb * 32 + j] : 0.f;
+          if (rec) {
+            const int lastrow = min(32 * warp + 31, nvalid - 1);
+            const int sfirst = m.segl[32 * warp], slast = lastrow >= 32 * warp ? m.segl[lastrow] : -1;
+            for (int sg = sfirst; sg <= slast && sg >= 0; ++sg) {
+              float mn[32], mx[32];
+              const bool mine = m.segl[tid] == sg;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                mn[j] = mine ? v[j] : INFINITY;
+                mx[j] = mine ? v[j] : -INFINITY;
+              }
+              warp_colreduce(mn, mx, lane);
+              const int col = cb * 32 + lane;
+              if (col < N) {
+                if (ts.two) {
+                  atomicMin(m.red + 2 * sg * o.red_w + col, enc_f(mn[0]));
+                  atomicMax(m.red + (2 * sg + 1) * o.red_w + col, enc_f(mx[0]));
+                } else {
+                  const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
+                  atomicMin(a.stat_min + idx, enc_f(mn[0]));
+                  atomicMax(a.stat_max + idx, enc_f(mx[0]));
+                }
+              }
+            }
+          }
+          if (relu) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+          }
+          if (hidden) {
+            store_operand_tmem(tlane, cb, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cb * 32 + j < ks) srow[cb * 32 + j] = v[j];
+          }
+        }
+        if (hidden) {
+          // next layer's A is in TMEM and D has been read: hand both to the MMA warp
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          fence_before();
+          mbar_arrive(m.a_full);
+        }
+        if (rec && ts.two) {  // flush this layer's shared extrema, reset
+          row_sync<1>();
+          for (int item = tid; item < 2 * N; item += 128) {
+            const int sg = item / N, col = item % N;
+            const int vmin = m.red[2 * sg * o.red_w + col], vmax = m.red[(2 * sg + 1) * o.red_w + col];
+            m.red[2 * sg * o.red_w + col] = enc_f(INFINITY);
+            m.red[(2 * sg + 1) * o.red_w + col] = enc_f(-INFINITY);
+            if (sg == 1 && ts.bnd >= ts.nvalid) continue;
+            const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
+            atomicMin(a.stat_min + idx, vmin);
+            atomicMax(a.stat_max + idx, vmax);
+          }
+          row_sync<1>();
+        }
+      }
+      // x_t in srow[0:ks): cost program with u_t, p_t in the scratch row
+      for (int j = 0; j < ka; ++j) {
+        srow[o.ucol + j] = ucur[j];
+        const float p = m.prow[tid * 8 + j] + ucur[j];
+        m.prow[tid * 8 + j] = p;
+        srow[o.pcol + j] = p;
+      }
+      cost += cost_program(o, srow, t);
+      row_sync<1>();
+      column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, 0, ks, o.x_stat, false, t);
+      if (o.u_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ucol, ka, o.u_stat, false, t);
+      if (o.p_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.pcol, kd, o.p_stat, false, t);
+      for (int i = 0; i < o.n_ops; ++i)
+        if (o.ops[i].stat >= 0)
+          column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t);
+      if (a.states != nullptr && row_ok)
+        for (int j = 0; j < ks; ++j) a.states[((row0 + tid) * H + t) * ks + j] = srow[j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ucur[j] = unext[j];
+    }
+    if (row_ok) {
+      a.costs[row0 + tid] = cost;
+      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + tid) / a.rows_per_sub, 1);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+}  // namespace
+
+size_t rollout_tc_smem(const DevObjective& o) {
+  return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
+         sizeof(float) * o.L * o.tc_npadmax + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 128 * 8 +
+         sizeof(uint64_t) * (2 * kStages + 2) + 16;
+}
+
+cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
+  const size_t smem = rollout_tc_smem(o);
+  cudaError_t e = cudaFuncSetAttribute(rollout_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long grid = (a.n_rows + 127) / 128;
+  if (grid <= 0) return cudaSuccess;
+  rollout_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, smem, st>>>(o, a);
+  return cudaGetLastError();
+}
+
+}  // namespace bp

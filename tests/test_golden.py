@@ -35,7 +35,8 @@ def test_device_matches_golden(device, name):
     costs, _, _, _, bad = dev.rollout(np.array(g["actions"], dtype=np.float32)[None])
     ref = np.array(g["costs"])
     assert not bad.any()
-    assert np.max(np.abs(costs[0] - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5
+    tol = 5e-5 if dev.rollout_path() == "tcgen05" else 1e-5  # 3xTF32 vs FP32 bar
+    assert np.max(np.abs(costs[0] - ref) / np.maximum(np.abs(ref), 1.0)) < tol
     lo, hi = spec.box()
     lf = dev.bound_boxes(lo[None], hi[None], "early-stop-interval")[0]
     assert abs(lf - g["lf_interval"]) <= 1e-9 * max(1.0, abs(g["lf_interval"]))

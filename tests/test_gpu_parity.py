@@ -17,6 +17,14 @@ from paper_2412_09584_b200.config import from_json
 pytestmark = pytest.mark.gpu
 
 RTOL = 1e-5
+# The tcgen05 path computes every Linear layer in 3xTF32 (~2^-21 per product
+# instead of FP32's 2^-24); the north star allows a looser stated tolerance
+# for it: 5e-5 relative.
+RTOL_TC = 5e-5
+
+
+def rtol_for(dev):
+    return RTOL_TC if dev.rollout_path() == "tcgen05" else RTOL
 
 
 def rel_err(got, ref):
@@ -70,13 +78,14 @@ def test_rollout_costs_and_extrema_match_oracle(device, name):
     for s in range(3):
         st = orc.Stats()
         ref = ob.evaluate(acts[s].astype(np.float64), st)
-        assert rel_err(costs[s], ref) < RTOL, name
+        tol = rtol_for(dev)
+        assert rel_err(costs[s], ref) < tol, name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
         # the device records x_t at every step; the oracle watches it only where
         # a bound reads it (stop steps, quadratic / ReLU arguments)
         seen = ~np.isnan(rlo)
         assert seen.mean() > 0.5
-        assert rel_err(elo[s][seen], rlo[seen]) < RTOL and rel_err(ehi[s][seen], rhi[seen]) < RTOL, name
+        assert rel_err(elo[s][seen], rlo[seen]) < tol and rel_err(ehi[s][seen], rhi[seen]) < tol, name
 
 
 def test_rollout_rows_are_batch_invariant(device):
@@ -159,7 +168,7 @@ def test_search_properties(device):
     assert rep["samples"][0] == 6 * (4 * 50 + 1)
     # the device values of the kept samples are the oracle's objective at those points
     ref = ob.evaluate(a.astype(np.float32).astype(np.float64))
-    assert rel_err(v, ref) < RTOL
+    assert rel_err(v, ref) < rtol_for(dev)
 
 
 def test_search_is_seeded_per_box(device):
@@ -251,3 +260,22 @@ def test_nonfinite_rollouts_fail_the_box_not_the_batch(device):
     assert not rep["ok"].any()
     lf = dev.batch_bound(2)  # interval fallback
     assert lf.shape == (2,)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "ref-obstacles", "ref-linear"])
+def test_tcgen05_and_simt_rollouts_agree(device, name):
+    """The tcgen05 3xTF32 kernel and the SIMT FP32 kernel against the oracle and each other."""
+    spec = small_spec(name)
+    dev = device.load(spec)
+    assert dev.rollout_path("auto") == "tcgen05"
+    lo, hi = spec.box()
+    acts = np.random.default_rng(3).uniform(lo, hi, size=(2, 300, spec.d)).astype(np.float32)
+    c_tc, _, lo_tc, hi_tc, _ = dev.rollout(acts)
+    assert dev.rollout_path("simt") == "simt"
+    c_simt, _, lo_s, hi_s, _ = dev.rollout(acts)
+    dev.rollout_path("auto")
+    ob = orc.Objective(spec)
+    for s in range(2):
+        ref = ob.evaluate(acts[s].astype(np.float64))
+        assert rel_err(c_tc[s], ref) < RTOL_TC and rel_err(c_simt[s], ref) < RTOL
+    assert rel_err(lo_tc, lo_s) < RTOL_TC and rel_err(hi_tc, hi_s) < RTOL_TC

@@ -10,6 +10,8 @@ D = int(sys.argv[2]) if len(sys.argv) > 2 else None
 wl = workloads.ALL[name]() if name != "c5" else workloads.c5(D or 1024)
 D = D or wl.children
 dev = bp.Device(0).load(wl.spec)
+if len(sys.argv) > 3: dev.rollout_path(sys.argv[3])
+print("rollout path:", dev.rollout_path(), flush=True)
 los, his = workloads.presplit_boxes(wl.spec, D)
 cfg = wl.planner_config()
 for it in range(3):
