@@ -57,6 +57,7 @@ struct DevObjective {
   int tc;                    // eligible (all widths <= 128)
   int tc_w[kMaxLayers], tc_bias[kMaxLayers], tc_npad[kMaxLayers], tc_kb[kMaxLayers], tc_ksteps[kMaxLayers];
   int tc_kbmax, tc_npadmax, tc_S, tc_cols;
+  int sc_list, n_sc;  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
   // constants
   int x0, p0, step_w;        // float arena offsets
   int x0d, p0d;              // double arena offsets

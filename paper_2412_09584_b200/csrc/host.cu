@@ -37,6 +37,7 @@ struct RolloutArgs {
   long long n_rows;
   int rows_per_sub;
   int kslab;
+  long long* timeline;
 };
 struct BoundArgs {
   const double* lo;
@@ -443,6 +444,21 @@ Compiled compile(const bp_objective_desc& d) {
   for (int i = 0; i < d.n_ops; ++i)
     if (need[static_cast<size_t>(3 + i)]) o.ops[i].stat = rec(4, i, o.ops[i].dim);
   o.SP = sp;
+  {  // recorded scratch columns: x_t, u_t, p_t and cost-op values (fused stats pass of the tcgen05 kernel)
+    std::vector<int> pairs;
+    auto add = [&](int col0, int stat, int dim) {
+      if (stat < 0) return;
+      for (int j = 0; j < dim; ++j) pairs.push_back(col0 + j), pairs.push_back(stat + j);
+    };
+    add(0, o.x_stat, d.ks);
+    add(o.ucol, o.u_stat, d.ka);
+    add(o.pcol, o.p_stat, d.kd);
+    for (int i = 0; i < d.n_ops; ++i) add(o.ops[i].col, o.ops[i].stat, o.ops[i].dim);
+    while (c.ia.size() % 4) c.ia.push_back(0);
+    o.sc_list = static_cast<int>(c.ia.size());
+    o.n_sc = static_cast<int>(pairs.size() / 2);
+    c.ia.insert(c.ia.end(), pairs.begin(), pairs.end());
+  }
 
   // rollout tile and shared-memory plan
   c.R = bp::rollout_rows_per_tile(c.nq);
@@ -557,6 +573,7 @@ struct bp_ctx {
   void* exchange_user = nullptr;
   // scratch for bp_rollout
   DBuf<float> r_actions, r_costs, r_states;
+  DBuf<long long> timeline;
   DBuf<int> r_min, r_max;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -603,7 +620,12 @@ struct bp_ctx {
   }
   void rollout(const float* actions, float* costs, float* states, int* smin, int* smax, int* fail_flags,
                long long n_rows, int rows_per_sub) {
-    bp::RolloutArgs a{actions, costs, states, smin, smax, fail_flags, n_rows, rows_per_sub, comp.kslab};
+    bp::RolloutArgs a{actions, costs, states, smin, smax, fail_flags, n_rows, rows_per_sub, comp.kslab, nullptr};
+    static const bool want_tl = std::getenv("BP_TC_TIMELINE") != nullptr;
+    if (want_tl && comp.o.tc && !force_simt) {
+      a.timeline = timeline.get(4096);
+      ck(cudaMemsetAsync(a.timeline, 0, 4096 * 8, stream), "memset");
+    }
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
     if (timing) {
       ev = roll_event();
@@ -614,6 +636,16 @@ struct bp_ctx {
     else
       ck(bp::launch_rollout(dev(), a, comp.nq, comp.stream, comp.smem, stream), "rollout launch");
     if (timing) ck(cudaEventRecord(ev.second, stream), "event");
+    if (a.timeline) {  // debug: print CTA 0's phase marks of step 3
+      std::vector<long long> tl(4096);
+      ck(cudaMemcpyAsync(tl.data(), a.timeline, 4096 * 8, cudaMemcpyDeviceToHost, stream), "D2H");
+      ck(cudaStreamSynchronize(stream), "sync");
+      const long long t0 = tl[0];
+      std::fprintf(stderr, "[timeline] role,mark,cycles-from-step-start:");
+      for (int i = 0; i < 4096; ++i)
+        if (tl[i] != 0) std::fprintf(stderr, " %d:%lld", i, tl[i] - t0);
+      std::fprintf(stderr, "\n");
+    }
     ++rollout_launches;
     ++launches;
   }

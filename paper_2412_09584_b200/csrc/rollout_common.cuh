@@ -22,6 +22,7 @@ struct RolloutArgs {
   long long n_rows;
   int rows_per_sub;
   int kslab;             // streamed mode: K rows per weight slab
+  long long* timeline;   // optional (BP_TC_TIMELINE): clock64 marks of CTA 0, see rollout_tc.cu
 };
 
 // Rows of a tile split into at most two subdomains: rows [0, bnd) belong to
@@ -90,19 +91,20 @@ __device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* 
   row_sync<BAR>();
 }
 
-__device__ __forceinline__ const float* val_ptr(const DevObjective& o, const float* row, int id) {
+__device__ __forceinline__ const float* val_ptr(const DevObjective& o, const DevOp* ops, const float* row, int id) {
   if (id == 0) return row;                 // x_t
   if (id == 1) return row + o.ucol;        // u_t
   if (id == 2) return row + o.pcol;        // p_t
-  return row + o.ops[id - 3].col;          // op output
+  return row + ops[id - 3].col;            // op output
 }
 
 // The step's cost program for one row (reference node semantics, graph.cpp:293-347).
-__device__ __forceinline__ float cost_program(const DevObjective& o, float* row, int t) {
+// ops: the objective's op table (kernel parameters, or a shared-memory copy).
+__device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp* ops, float* row, int t) {
   float cost = 0.f;
   for (int i = 0; i < o.n_ops; ++i) {
-    const DevOp& op = o.ops[i];
-    const float* src = val_ptr(o, row, op.src0);
+    const DevOp& op = ops[i];
+    const float* src = val_ptr(o, ops, row, op.src0);
     float* dst = row + op.col;
     float v = 0.f;
     switch (op.kind) {
@@ -122,7 +124,7 @@ __device__ __forceinline__ float cost_program(const DevObjective& o, float* row,
         v = dst[0];
         break;
       case 2: {  // SUM
-        const float* s1 = op.src1 >= 0 ? val_ptr(o, row, op.src1) : nullptr;
+        const float* s1 = op.src1 >= 0 ? val_ptr(o, ops, row, op.src1) : nullptr;
         for (int j = 0; j < op.dim; ++j) dst[j] = s1 ? src[j] + s1[j] : src[j];
         v = dst[0];
         break;

@@ -9,7 +9,8 @@
 // ~2^-21 relative per product (FP32 is 2^-24), inside the 1e-5 parity bar.
 //
 // One CTA = 128 rows (the MMA M), warp-specialized:
-//   warps 0-3  row work: warp w owns TMEM lanes 32w..32w+31 = rows 32w..32w+31;
+//   warps 0-7  row work: warp w owns TMEM lanes 32(w%4).. = rows 32(w%4)..+31 and
+//              the 32-column chunks cb with cb%2 == w/4 (two warps per SMSP);
 //              the fused epilogue reads the accumulator (tcgen05.ld), adds the
 //              bias, reduces per-column sample extrema (butterfly
 //              transpose-reduce -> shared atomics -> one global atomic per
@@ -17,15 +18,20 @@
 //              of the next layer's input straight back into TMEM (tcgen05.st),
 //              where the next MMAs read it as their A operand; after the output
 //              layer it runs the per-row cost program (rollout_common.cuh).
-//   warp 4     producer: streams the weight K-blocks (hi and lo, host-side
+//   warp 8     producer: streams the weight K-blocks (hi and lo, host-side
 //              pre-swizzled to the 128B K-major UMMA layout) into a ring of
 //              shared-memory stages with cp.async.bulk + mbarrier tx counts,
 //              running ahead across layers and steps.
-//   warp 5     MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
+//   warp 9     MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
 //              TMEM, B from shared memory) per K=8 step; tcgen05.commit frees
 //              the weight stage and, at the end of a layer, hands the
 //              accumulator to the epilogue.
-// TMEM: columns [0,128) accumulator D, [128,256) A_hi, [256,384) A_lo.
+// TMEM: columns [0,128) and [128,256) two accumulators used by alternate
+// layers, [256,384) A_hi, [384,512) A_lo.  The epilogue of layer l reads its
+// accumulator 32 columns at a time and writes the matching 32-column K-block
+// of layer l+1's A operand, arriving on that K-block's mbarrier; the MMAs of
+// layer l+1 (into the other accumulator) start on each K-block as soon as it
+// lands, so the tensor pipe and the epilogue overlap within one tile.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -36,9 +42,12 @@ namespace bp {
 
 namespace {
 
-constexpr int kTcThreads = 192;  // 4 row warps + producer warp + MMA warp
+constexpr int kTcThreads = 320;  // 8 epilogue warps + producer warp + MMA warp
+constexpr int kProducerWarp = 8, kMmaWarp = 9;
 constexpr int kStages = 4;
-constexpr uint32_t kColD = 0, kColAhi = 128, kColAlo = 256;
+// TMEM columns: two accumulators (layers alternate) and the hi / lo A operand
+constexpr uint32_t kColD0 = 0, kColD1 = 128, kColAhi = 256, kColAlo = 384;
+constexpr int kMaxChunks = 4;  // A operand K-blocks of 32 (widths <= 128)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -187,6 +196,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Debug timeline (BP_TC_TIMELINE): CTA 0, step 3; slots: 0 step start,
+// 100+10l+{0,1} MMA layer l first issue / commit (MMA warp),
+// 200+10l+{0,1,2} epilogue layer l wait-done / chunks done / flush done (warp 0),
+// 300+10l warp 4 epilogue wait-done, 400 cost start, 401 cost done, 402 passes done,
+// 403 features done.
+__device__ __forceinline__ void mark(const RolloutArgs& a, int t, int slot) {
+  if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = clock64();
+}
+
 struct TcSmem {
   unsigned char* w;    // [kStages][hi | lo][npadmax rows x 128 B]
   float* sc;           // [128][tc_S] per-row scratch (x_t, u_t, p_t, cost-op values)
@@ -196,9 +214,11 @@ struct TcSmem {
   float* prow;         // [128][8]
   uint64_t* full;      // [kStages] weight stage landed
   uint64_t* empty;     // [kStages] weight stage consumed by the MMAs
-  uint64_t* d_full;    // accumulator ready for the epilogue
-  uint64_t* a_full;    // A operand written (and D drained) by the 128 row threads
+  uint64_t* d_full;    // [2] accumulator ready for the epilogue
+  uint64_t* a_chunk;   // [kMaxChunks] A operand K-block written by the 128 row threads
   uint32_t* tmem_slot;
+  DevOp* ops;          // [n_ops] op table copy
+  int* red2;           // [2 seg][min|max][n_sc] fused scratch extrema
 };
 
 __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
@@ -214,8 +234,10 @@ __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
   m.full = reinterpret_cast<uint64_t*>(m.prow + 128 * 8);
   m.empty = m.full + kStages;
   m.d_full = m.empty + kStages;
-  m.a_full = m.d_full + 1;
-  m.tmem_slot = reinterpret_cast<uint32_t*>(m.a_full + 1);
+  m.a_chunk = m.d_full + 2;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(m.a_chunk + kMaxChunks);
+  m.ops = reinterpret_cast<DevOp*>(m.tmem_slot + 4);
+  m.red2 = reinterpret_cast<int*>(m.ops + o.n_ops);
   return m;
 }
 
@@ -243,13 +265,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     const int l = i / o.tc_npadmax, j = i % o.tc_npadmax;
     m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
   }
+  for (int i = tid; i < o.n_ops * static_cast<int>(sizeof(DevOp) / 4); i += kTcThreads)
+    reinterpret_cast<int*>(m.ops)[i] = reinterpret_cast<const int*>(o.ops)[i];
+  for (int i = tid; i < 4 * o.n_sc; i += kTcThreads) m.red2[i] = enc_f(((i / o.n_sc) & 1) ? -INFINITY : INFINITY);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(m.full + s, 1);
       mbar_init(m.empty + s, 1);
     }
-    mbar_init(m.d_full, 1);
-    mbar_init(m.a_full, 128);
+    mbar_init(m.d_full + 0, 1);
+    mbar_init(m.d_full + 1, 1);
+    for (int c = 0; c < kMaxChunks; ++c) mbar_init(m.a_chunk + c, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -263,7 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
   const uint32_t tmem = *m.tmem_slot;
   const int stage_bytes = 2 * o.tc_npadmax * 128;
 
-  if (warp == 4) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------ producer: weight K-blocks
     if (lane == 0) {
       int it = 0;
@@ -279,17 +305,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           }
         }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       int it = 0, layer_it = 0;
+      int a_cnt[kMaxChunks] = {0, 0, 0, 0};
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l, ++layer_it) {
           const int npad = o.tc_npad[l];
           const uint32_t idesc = tf32_idesc(npad);
-          mbar_wait(m.a_full, static_cast<uint32_t>(layer_it & 1));  // A written, D drained
-          fence_after();
+          const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
           for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
+            mbar_wait(m.a_chunk + kb, static_cast<uint32_t>(a_cnt[kb]++ & 1));  // this K-block of A landed
+            if (kb == 0) mark(a, t, 100 + 10 * l);
             const int s = it % kStages;
             mbar_wait(m.full + s, static_cast<uint32_t>((it / kStages) & 1));
             fence_after();
@@ -299,18 +327,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
               if (kstep >= o.tc_ksteps[l]) break;
               const uint64_t bh = sw128_desc(wb_hi + 32 * q), bl = sw128_desc(wb_lo + 32 * q);
               const uint32_t ah = tmem + kColAhi + 8 * kstep, al = tmem + kColAlo + 8 * kstep;
-              mma_tf32_ts(tmem + kColD, ah, bh, idesc, kstep > 0 ? 1u : 0u);
-              mma_tf32_ts(tmem + kColD, ah, bl, idesc, 1u);
-              mma_tf32_ts(tmem + kColD, al, bh, idesc, 1u);
+              mma_tf32_ts(tmem + dcol, ah, bh, idesc, kstep > 0 ? 1u : 0u);
+              mma_tf32_ts(tmem + dcol, ah, bl, idesc, 1u);
+              mma_tf32_ts(tmem + dcol, al, bh, idesc, 1u);
             }
             mma_commit(m.empty + s);  // stage free once these MMAs retire
           }
-          mma_commit(m.d_full);  // accumulator complete
+          mma_commit(m.d_full + (layer_it & 1));  // accumulator complete
+          mark(a, t, 101 + 10 * l);
         }
     }
   } else {
     // ------------------------------------------------ row threads (epilogue + cost program)
-    const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column-chunk parity
+    const int row = 32 * g + lane;
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * g) << 16);
     TileSeg ts;
     ts.seg0 = seg0;
     ts.nvalid = nvalid;
@@ -319,11 +350,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       ts.bnd = static_cast<int>(b < nvalid ? b : nvalid);
       ts.two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
     }
-    const bool row_ok = tid < nvalid;
-    const float* urow = row_ok ? a.actions + (row0 + tid) * d : nullptr;
-    float* srow = m.sc + tid * S;
-    for (int j = 0; j < kd; ++j) m.prow[tid * 8 + j] = o.f[o.p0 + j];
-    for (int j = 0; j < ks; ++j) srow[j] = o.f[o.x0 + j];
+    const bool row_ok = row < nvalid;
+    const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
+    float* srow = m.sc + row * S;
+    if (h == 0) {
+      for (int j = 0; j < kd; ++j) m.prow[row * 8 + j] = o.f[o.p0 + j];
+      for (int j = 0; j < ks; ++j) srow[j] = o.f[o.x0 + j];
+    }
+    asm volatile("bar.sync 2, 256;" ::: "memory");
     float ucur[8], unext[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) ucur[j] = (row_ok && j < ka) ? __ldg(urow + j) : 0.f;
@@ -331,17 +365,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     int layer_it = 0;
     const int SPH = o.SP * H;
     for (int t = 0; t < H; ++t) {
+      if (warp == 0) mark(a, t, 0);
 #pragma unroll
       for (int j = 0; j < 8; ++j) unext[j] = (row_ok && j < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
       // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
-      for (int kb = 0; kb < o.tc_kb[0]; ++kb) {
+      for (int kb = h; kb < o.tc_kb[0]; kb += 2) {
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int k = kb * 32 + j;
           float x = 0.f;
           if (k < ks) {
-            x = srow[k] - (o.rel ? m.prow[tid * 8 + k % kd] : 0.f);
+            x = srow[k] - (o.rel ? m.prow[row * 8 + k % kd] : 0.f);
           } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -350,34 +385,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           v[j] = x;
         }
         store_operand_tmem(tlane, kb, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_before();
+        mbar_arrive(m.a_chunk + kb);
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      fence_before();
-      mbar_arrive(m.a_full);
+      if (warp == 0) mark(a, t, 403);
       for (int l = 0; l < L; ++l, ++layer_it) {
         const int N = o.widths[l + 1], npad = o.tc_npad[l];
-        mbar_wait(m.d_full, static_cast<uint32_t>(layer_it & 1));
+        const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
+        mbar_wait(m.d_full + (layer_it & 1), static_cast<uint32_t>((layer_it >> 1) & 1));
         fence_after();
+        if (warp == 0) mark(a, t, 200 + 10 * l);
+        if (warp == 4) mark(a, t, 300 + 10 * l);
         const bool hidden = l + 1 < L;
         const bool relu = o.relu[l] != 0;
         const int stat = o.pre_stat[l];
         const bool rec = relu && stat >= 0 && a.stat_min != nullptr;
         const float* bias = m.bias + l * o.tc_npadmax;
         const int nchunk = (npad + 31) / 32;
-        for (int cb = 0; cb < nchunk; ++cb) {
+        for (int cb = h; cb < nchunk; cb += 2) {
           float v[32];
           if (npad - cb * 32 >= 32)
-            tmem_ld32(tlane + kColD + cb * 32, v);
+            tmem_ld32(tlane + dcol + cb * 32, v);
           else
-            tmem_ld16(tlane + kColD + cb * 32, v);
+            tmem_ld16(tlane + dcol + cb * 32, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = (cb * 32 + j < N) ? v[j] + bias[cb * 32 + j] : 0.f;
           if (rec) {
-            const int lastrow = min(32 * warp + 31, nvalid - 1);
-            const int sfirst = m.segl[32 * warp], slast = lastrow >= 32 * warp ? m.segl[lastrow] : -1;
+            const int lastrow = min(32 * g + 31, nvalid - 1);
+            const int sfirst = m.segl[32 * g], slast = lastrow >= 32 * g ? m.segl[lastrow] : -1;
             for (int sg = sfirst; sg <= slast && sg >= 0; ++sg) {
               float mn[32], mx[32];
-              const bool mine = m.segl[tid] == sg;
+              const bool mine = m.segl[row] == sg;
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 mn[j] = mine ? v[j] : INFINITY;
@@ -403,21 +442,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           }
           if (hidden) {
             store_operand_tmem(tlane, cb, v);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
+            mbar_arrive(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (cb * 32 + j < ks) srow[cb * 32 + j] = v[j];
           }
         }
-        if (hidden) {
-          // next layer's A is in TMEM and D has been read: hand both to the MMA warp
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          fence_before();
-          mbar_arrive(m.a_full);
-        }
+        if (warp == 0) mark(a, t, 201 + 10 * l);
         if (rec && ts.two) {  // flush this layer's shared extrema, reset
-          row_sync<1>();
-          for (int item = tid; item < 2 * N; item += 128) {
+          asm volatile("bar.sync 2, 256;" ::: "memory");
+          for (int item = threadIdx.x; item < 2 * N; item += 256) {
             const int sg = item / N, col = item % N;
             const int vmin = m.red[2 * sg * o.red_w + col], vmax = m.red[(2 * sg + 1) * o.red_w + col];
             m.red[2 * sg * o.red_w + col] = enc_f(INFINITY);
@@ -427,32 +464,80 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             atomicMin(a.stat_min + idx, vmin);
             atomicMax(a.stat_max + idx, vmax);
           }
-          row_sync<1>();
+          asm volatile("bar.sync 2, 256;" ::: "memory");
         }
+        if (warp == 0) mark(a, t, 202 + 10 * l);
       }
-      // x_t in srow[0:ks): cost program with u_t, p_t in the scratch row
-      for (int j = 0; j < ka; ++j) {
-        srow[o.ucol + j] = ucur[j];
-        const float p = m.prow[tid * 8 + j] + ucur[j];
-        m.prow[tid * 8 + j] = p;
-        srow[o.pcol + j] = p;
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // x_t of every row is in the scratch
+      if (warp == 0) mark(a, t, 400);
+      if (h == 0) {
+        // cost program with u_t, p_t in the scratch row (one thread per row)
+        for (int j = 0; j < ka; ++j) {
+          srow[o.ucol + j] = ucur[j];
+          const float p = m.prow[row * 8 + j] + ucur[j];
+          m.prow[row * 8 + j] = p;
+          srow[o.pcol + j] = p;
+        }
+        cost += cost_program(o, m.ops, srow, t);
+        if (warp == 0) mark(a, t, 401);
+        if (a.stat_min != nullptr && o.n_sc > 0) {
+          if (ts.two) {
+            // one fused pass over every recorded scratch column: redux.sync per
+            // column and subdomain -> shared atomics -> one global atomic each
+            const int sg = m.segl[row];
+            const unsigned has0 = __ballot_sync(0xffffffffu, sg == 0), has1 = __ballot_sync(0xffffffffu, sg == 1);
+            const int* pairs = o.iv + o.sc_list;
+            for (int i = 0; i < o.n_sc; ++i) {
+              const int e = enc_f(srow[pairs[2 * i]]);
+              if (has0) {
+                const int mn = __reduce_min_sync(0xffffffffu, sg == 0 ? e : 0x7fffffff);
+                const int mx = __reduce_max_sync(0xffffffffu, sg == 0 ? e : static_cast<int>(0x80000000u));
+                if (lane == 0) {
+                  atomicMin(m.red2 + i, mn);
+                  atomicMax(m.red2 + o.n_sc + i, mx);
+                }
+              }
+              if (has1) {
+                const int mn = __reduce_min_sync(0xffffffffu, sg == 1 ? e : 0x7fffffff);
+                const int mx = __reduce_max_sync(0xffffffffu, sg == 1 ? e : static_cast<int>(0x80000000u));
+                if (lane == 0) {
+                  atomicMin(m.red2 + 2 * o.n_sc + i, mn);
+                  atomicMax(m.red2 + 3 * o.n_sc + i, mx);
+                }
+              }
+            }
+            row_sync<1>();
+            for (int item = row; item < 2 * o.n_sc; item += 128) {
+              const int s2 = item / o.n_sc, i = item % o.n_sc;
+              const int vmin = m.red2[2 * s2 * o.n_sc + i], vmax = m.red2[(2 * s2 + 1) * o.n_sc + i];
+              m.red2[2 * s2 * o.n_sc + i] = enc_f(INFINITY);
+              m.red2[(2 * s2 + 1) * o.n_sc + i] = enc_f(-INFINITY);
+              if (s2 == 1 && ts.bnd >= ts.nvalid) continue;
+              const long long idx = (seg0 + s2) * SPH + t * o.SP + pairs[2 * i + 1];
+              atomicMin(a.stat_min + idx, vmin);
+              atomicMax(a.stat_max + idx, vmax);
+            }
+          } else {
+            row_sync<1>();
+            column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, 0, ks, o.x_stat, false, t);
+            if (o.u_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ucol, ka, o.u_stat, false, t);
+            if (o.p_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.pcol, kd, o.p_stat, false, t);
+            for (int i = 0; i < o.n_ops; ++i)
+              if (m.ops[i].stat >= 0)
+                column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, m.ops[i].col, m.ops[i].dim, m.ops[i].stat, false, t);
+          }
+        }
+        if (a.states != nullptr && row_ok)
+          for (int j = 0; j < ks; ++j) a.states[((row0 + row) * H + t) * ks + j] = srow[j];
       }
-      cost += cost_program(o, srow, t);
-      row_sync<1>();
-      column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, 0, ks, o.x_stat, false, t);
-      if (o.u_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ucol, ka, o.u_stat, false, t);
-      if (o.p_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.pcol, kd, o.p_stat, false, t);
-      for (int i = 0; i < o.n_ops; ++i)
-        if (o.ops[i].stat >= 0)
-          column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ops[i].col, o.ops[i].dim, o.ops[i].stat, false, t);
-      if (a.states != nullptr && row_ok)
-        for (int j = 0; j < ks; ++j) a.states[((row0 + tid) * H + t) * ks + j] = srow[j];
+      if (warp == 0) mark(a, t, 402);
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // next step's features read the scratch
 #pragma unroll
       for (int j = 0; j < 8; ++j) ucur[j] = unext[j];
     }
-    if (row_ok) {
-      a.costs[row0 + tid] = cost;
-      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + tid) / a.rows_per_sub, 1);
+    if (h == 0 && row_ok) {
+      a.costs[row0 + row] = cost;
+      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + row) / a.rows_per_sub, 1);
     }
   }
   fence_before();
@@ -468,7 +553,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 size_t rollout_tc_smem(const DevObjective& o) {
   return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
          sizeof(float) * o.L * o.tc_npadmax + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 128 * 8 +
-         sizeof(uint64_t) * (2 * kStages + 2) + 16;
+         sizeof(uint64_t) * (2 * kStages + 2 + kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc;
 }
 
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
