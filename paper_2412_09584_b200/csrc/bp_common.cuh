@@ -56,8 +56,9 @@ struct DevObjective {
   // tcgen05 (3xTF32) rollout: per layer a K-block image [kb][hi|lo][npad rows x 32 tf32, 128B-swizzled]
   int tc;                    // eligible (all widths <= 128)
   int tc_w[kMaxLayers], tc_bias[kMaxLayers], tc_npad[kMaxLayers], tc_kb[kMaxLayers], tc_ksteps[kMaxLayers];
-  int tc_kbmax, tc_npadmax, tc_S, tc_cols;
-  int sc_list, n_sc;  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
+  int tc_kbmax, tc_npadmax, tc_S, tc_cols, tc_xs;
+  int sc_list, n_sc;
+  int cost_f0, cost_f1;  // float arena range holding every cost-op constant (copied to smem by the tcgen05 kernel)  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
   // constants
   int x0, p0, step_w;        // float arena offsets
   int x0d, p0d;              // double arena offsets

@@ -306,6 +306,8 @@ Compiled compile(const bp_objective_desc& d) {
   std::vector<int> vdim = {d.ks, d.ka, d.kd};
   std::vector<char> need(static_cast<size_t>(3 + d.n_ops), 0);
   bool any_term = false;
+  while (c.fa.size() % 4) c.fa.push_back(0.f);
+  o.cost_f0 = static_cast<int>(c.fa.size());
   for (int i = 0; i < d.n_ops; ++i) {
     const bp_cost_op& s = d.ops[i];
     bp::DevOp& p = o.ops[i];
@@ -389,9 +391,10 @@ Compiled compile(const bp_objective_desc& d) {
     any_term = any_term || s.is_term;
     p.dim = dim;
     p.col = col;
-    col += r4(dim);
+    col += dim;  // scalar access only: packed
     vdim.push_back(dim);
   }
+  o.cost_f1 = static_cast<int>(c.fa.size());
   if (!any_term) fail(BP_INVALID_ARGUMENT, "objective: cost program has no terms");
   o.S = r8(std::max({maxK4, r4(maxw), col})) + 4;
 
@@ -498,7 +501,8 @@ Compiled compile(const bp_objective_desc& d) {
     if (ok) {
       o.tc_kbmax = kbmax;
       o.tc_npadmax = npadmax;
-      o.tc_S = r8(std::max(col, r4(d.ks))) + 4;
+      o.tc_S = std::max(col, d.ks) | 1;  // odd row stride: one row per thread, conflict-free
+      o.tc_xs = r4(d.ks) + 1;
       o.tc_cols = 32;
       while (o.tc_cols < npadmax) o.tc_cols *= 2;
       for (int l = 0; l < d.n_layers; ++l) {

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const DevObjective
         prow[tid * 8 + j] = p;
         row[o.pcol + j] = p;
       }
-      cost += cost_program(o, o.ops, row, t);
+      cost += cost_program(o, o.ops, o.f, row, t);
     }
     __syncthreads();
     column_pass<R>(o, a, act, o.S, segl, seg0, 0, ks, o.x_stat, false, t);

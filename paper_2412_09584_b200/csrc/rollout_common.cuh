@@ -99,8 +99,11 @@ __device__ __forceinline__ const float* val_ptr(const DevObjective& o, const Dev
 }
 
 // The step's cost program for one row (reference node semantics, graph.cpp:293-347).
-// ops: the objective's op table (kernel parameters, or a shared-memory copy).
-__device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp* ops, float* row, int t) {
+// ops: the objective's op table (kernel parameters, or a shared-memory copy);
+// cf: base such that cf + op.<offset> addresses the op constants (o.f, or a
+// shared-memory copy of the arena range [cost_f0, cost_f1) shifted by -cost_f0).
+__device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp* ops, const float* cf, float* row,
+                                             int t) {
   float cost = 0.f;
   for (int i = 0; i < o.n_ops; ++i) {
     const DevOp& op = ops[i];
@@ -109,12 +112,12 @@ __device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp
     float v = 0.f;
     switch (op.kind) {
       case 0: {  // LINEAR
-        const float* W = o.f + op.w;
-        const float* b = o.f + op.b;
+        const float* W = cf + op.w;
+        const float* b = cf + op.b;
         for (int r = 0; r < op.dim; ++r) {
           float s = 0.f;
-          for (int j = 0; j < op.in_dim; ++j) s = fmaf(__ldg(W + r * op.in_dim + j), src[j], s);
-          dst[r] = s + __ldg(b + r);
+          for (int j = 0; j < op.in_dim; ++j) s = fmaf(W[r * op.in_dim + j], src[j], s);
+          dst[r] = s + b[r];
         }
         v = dst[0];
         break;
@@ -134,21 +137,21 @@ __device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp
         v = dst[0];
         break;
       case 4: {  // SQDIST
-        const float* tg = o.f + op.tgt;
-        const float* wt = o.f + op.wt + (op.weight_by_step ? t * op.in_dim : 0);
+        const float* tg = cf + op.tgt;
+        const float* wt = cf + op.wt + (op.weight_by_step ? t * op.in_dim : 0);
         float acc = 0.f;
         for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - __ldg(tg + j);
-          acc += __ldg(wt + j) * d * d;
+          const float d = src[j] - tg[j];
+          acc += wt[j] * d * d;
         }
         dst[0] = v = acc;
         break;
       }
       case 5: {  // HINGE
-        const float* c = o.f + op.ctr;
+        const float* c = cf + op.ctr;
         float acc = 0.f;
         for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - __ldg(c + j);
+          const float d = src[j] - c[j];
           acc += d * d;
         }
         const float m = op.radius - sqrtf(acc);

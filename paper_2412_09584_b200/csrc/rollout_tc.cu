@@ -11,18 +11,20 @@
 // One CTA = 128 rows (the MMA M), warp-specialized:
 //   warps 0-7  row work: warp w owns TMEM lanes 32(w%4).. = rows 32(w%4)..+31 and
 //              the 32-column chunks cb with cb%2 == w/4 (two warps per SMSP);
+//              they stage recorded pre-activations for the extrema warps;
 //              the fused epilogue reads the accumulator (tcgen05.ld), adds the
-//              bias, reduces per-column sample extrema (butterfly
-//              transpose-reduce -> shared atomics -> one global atomic per
-//              column and subdomain), applies ReLU and writes the hi / lo split
+//              bias, applies ReLU and writes the hi / lo split
 //              of the next layer's input straight back into TMEM (tcgen05.st),
 //              where the next MMAs read it as their A operand; after the output
 //              layer it runs the per-row cost program (rollout_common.cuh).
-//   warp 8     producer: streams the weight K-blocks (hi and lo, host-side
+//   warps 8-11 extrema: warp 8+c reduces 32-column chunk c of every recorded
+//              pre-activation, staged in shared memory by the epilogue, over
+//              the tile's rows (lane = column), off the layer-to-layer path.
+//   warp 12    producer: streams the weight K-blocks (hi and lo, host-side
 //              pre-swizzled to the 128B K-major UMMA layout) into a ring of
 //              shared-memory stages with cp.async.bulk + mbarrier tx counts,
 //              running ahead across layers and steps.
-//   warp 9     MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
+//   warp 13    MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
 //              TMEM, B from shared memory) per K=8 step; tcgen05.commit frees
 //              the weight stage and, at the end of a layer, hands the
 //              accumulator to the epilogue.
@@ -42,9 +44,10 @@ namespace bp {
 
 namespace {
 
-constexpr int kTcThreads = 320;  // 8 epilogue warps + producer warp + MMA warp
-constexpr int kProducerWarp = 8, kMmaWarp = 9;
-constexpr int kStages = 4;
+constexpr int kTcThreads = 448;  // 8 epilogue warps + 4 aux warps + producer warp + MMA warp
+constexpr int kAuxWarp0 = 8, kProducerWarp = 12, kMmaWarp = 13;
+constexpr int kStgStride = 36;  // staging row stride (floats): 16B rows, conflict-free column reads
+constexpr int kStages = 3;
 // TMEM columns: two accumulators (layers alternate) and the hi / lo A operand
 constexpr uint32_t kColD0 = 0, kColD1 = 128, kColAhi = 256, kColAlo = 384;
 constexpr int kMaxChunks = 4;  // A operand K-blocks of 32 (widths <= 128)
@@ -126,24 +129,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
   for (int j = 16; j < 32; ++j) v[j] = 0.f;
 }
 
-// Butterfly transpose-reduce: lane l ends with the min (max) over the warp's
-// 32 rows of column l.  31 shuffles per reduction instead of 32 x 5.
-__device__ __forceinline__ void warp_colreduce(float (&mn)[32], float (&mx)[32], int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool upper = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float smn = upper ? mn[i] : mn[i + s];
-      const float smx = upper ? mx[i] : mx[i + s];
-      const float rmn = __shfl_xor_sync(0xffffffffu, smn, s);
-      const float rmx = __shfl_xor_sync(0xffffffffu, smx, s);
-      mn[i] = fminf(upper ? mn[i + s] : mn[i], rmn);
-      mx[i] = fmaxf(upper ? mx[i + s] : mx[i], rmx);
-    }
-  }
-}
-
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -219,6 +204,14 @@ struct TcSmem {
   uint32_t* tmem_slot;
   DevOp* ops;          // [n_ops] op table copy
   int* red2;           // [2 seg][min|max][n_sc] fused scratch extrema
+  float* stg;          // [kMaxChunks][128 rows][kStgStride] staged pre-activations
+  float* cconst;       // cost-op constants, arena range [cost_f0, cost_f1)
+  int* pairs;          // [n_sc][2] recorded scratch columns
+  uint64_t* stg_full;  // [kMaxChunks] chunk staged (128 epilogue threads)
+  uint64_t* stg_empty; // [kMaxChunks] chunk consumed by its extrema warp
+  float* xbuf;         // [2][128][tc_xs] x_t hand-off to the aux warps (by step parity)
+  uint64_t* x_full;    // [2]
+  uint64_t* x_empty;   // [2]
 };
 
 __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
@@ -226,18 +219,26 @@ __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
   unsigned char* base = raw + (((s0 + 1023u) & ~1023u) - s0);
   TcSmem m;
   m.w = base;
-  m.sc = reinterpret_cast<float*>(m.w + kStages * 2 * o.tc_npadmax * 128);
+  m.stg = reinterpret_cast<float*>(m.w + kStages * 2 * o.tc_npadmax * 128);
+  m.sc = m.stg + kMaxChunks * 128 * kStgStride;
   m.bias = m.sc + 128 * o.tc_S;
   m.red = reinterpret_cast<int*>(m.bias + o.L * o.tc_npadmax);
   m.segl = m.red + 4 * o.red_w;
   m.prow = reinterpret_cast<float*>(m.segl + 128);
-  m.full = reinterpret_cast<uint64_t*>(m.prow + 128 * 8);
+  m.full = reinterpret_cast<uint64_t*>(m.prow + 3 * 128 * 8);  // prow [128][8] then u_t [2][128][8]
   m.empty = m.full + kStages;
   m.d_full = m.empty + kStages;
   m.a_chunk = m.d_full + 2;
-  m.tmem_slot = reinterpret_cast<uint32_t*>(m.a_chunk + kMaxChunks);
+  m.stg_full = m.a_chunk + kMaxChunks;
+  m.stg_empty = m.stg_full + kMaxChunks;
+  m.x_full = m.stg_empty + kMaxChunks;
+  m.x_empty = m.x_full + 2;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(m.x_empty + 2);
   m.ops = reinterpret_cast<DevOp*>(m.tmem_slot + 4);
   m.red2 = reinterpret_cast<int*>(m.ops + o.n_ops);
+  m.pairs = m.red2 + 4 * o.n_sc;
+  m.cconst = reinterpret_cast<float*>(m.pairs + 2 * o.n_sc);
+  m.xbuf = m.cconst + (o.cost_f1 - o.cost_f0);
   return m;
 }
 
@@ -268,6 +269,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
   for (int i = tid; i < o.n_ops * static_cast<int>(sizeof(DevOp) / 4); i += kTcThreads)
     reinterpret_cast<int*>(m.ops)[i] = reinterpret_cast<const int*>(o.ops)[i];
   for (int i = tid; i < 4 * o.n_sc; i += kTcThreads) m.red2[i] = enc_f(((i / o.n_sc) & 1) ? -INFINITY : INFINITY);
+  for (int i = tid; i < 2 * o.n_sc; i += kTcThreads) m.pairs[i] = o.iv[o.sc_list + i];
+  for (int i = tid; i < o.cost_f1 - o.cost_f0; i += kTcThreads) m.cconst[i] = o.f[o.cost_f0 + i];
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(m.full + s, 1);
@@ -275,7 +278,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     }
     mbar_init(m.d_full + 0, 1);
     mbar_init(m.d_full + 1, 1);
-    for (int c = 0; c < kMaxChunks; ++c) mbar_init(m.a_chunk + c, 128);
+    for (int c = 0; c < kMaxChunks; ++c) {
+      mbar_init(m.a_chunk + c, 128);
+      mbar_init(m.stg_full + c, 128);
+      mbar_init(m.stg_empty + c, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(m.x_full + b, 256);
+      mbar_init(m.x_empty + b, 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -337,37 +348,200 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           mark(a, t, 101 + 10 * l);
         }
     }
-  } else {
-    // ------------------------------------------------ row threads (epilogue + cost program)
-    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column-chunk parity
-    const int row = 32 * g + lane;
-    const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * g) << 16);
-    TileSeg ts;
-    ts.seg0 = seg0;
-    ts.nvalid = nvalid;
-    {
-      const long long b = (seg0 + 1) * a.rows_per_sub - row0;
-      ts.bnd = static_cast<int>(b < nvalid ? b : nvalid);
-      ts.two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
-    }
+  } else if (warp >= kAuxWarp0) {
+    // ------------------------------------------------ aux: extrema + cost program (off the layer path)
+    const int c = warp - kAuxWarp0;      // extrema chunk, and rows 32c..32c+31 of the cost program
+    const int row = 32 * c + lane;
+    const long long b1 = (seg0 + 1) * a.rows_per_sub - row0;
+    const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
+    const bool two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
+    const int SPH = o.SP * H;
     const bool row_ok = row < nvalid;
     const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
     float* srow = m.sc + row * S;
+    float p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = j < kd ? o.f[o.p0 + j] : 0.f;
+    float cost = 0.f;
+    int use = 0;
+    for (int t = 0; t < H; ++t) {
+      for (int l = 0; l + 1 < L; ++l) {
+        const int stat = o.pre_stat[l];
+        const bool rec = o.relu[l] != 0 && stat >= 0 && a.stat_min != nullptr;
+        if (!rec || c >= (o.tc_npad[l] + 31) / 32) continue;
+        mbar_wait(m.stg_full + c, static_cast<uint32_t>(use & 1));
+        ++use;
+        const int col = c * 32 + lane, N = o.widths[l + 1];
+        const float* colp = m.stg + c * 128 * kStgStride + lane;
+        if (two) {
+          float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+#pragma unroll 8
+          for (int r = 0; r < bnd; ++r) {
+            const float v = colp[r * kStgStride];
+            mn0 = fminf(mn0, v);
+            mx0 = fmaxf(mx0, v);
+          }
+#pragma unroll 8
+          for (int r = bnd; r < nvalid; ++r) {
+            const float v = colp[r * kStgStride];
+            mn1 = fminf(mn1, v);
+            mx1 = fmaxf(mx1, v);
+          }
+          if (col < N) {
+            if (bnd > 0) {
+              const long long idx = seg0 * SPH + t * o.SP + stat + col;
+              atomicMin(a.stat_min + idx, enc_f(mn0));
+              atomicMax(a.stat_max + idx, enc_f(mx0));
+            }
+            if (bnd < nvalid) {
+              const long long idx = (seg0 + 1) * SPH + t * o.SP + stat + col;
+              atomicMin(a.stat_min + idx, enc_f(mn1));
+              atomicMax(a.stat_max + idx, enc_f(mx1));
+            }
+          }
+        } else {  // many small subdomains in the tile (parity-test sizes)
+          float mn = INFINITY, mx = -INFINITY;
+          int sg = -1;
+          for (int r = 0; r < nvalid; ++r) {
+            const int s2 = m.segl[r];
+            if (s2 != sg) {
+              if (sg >= 0 && col < N) {
+                const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
+                atomicMin(a.stat_min + idx, enc_f(mn));
+                atomicMax(a.stat_max + idx, enc_f(mx));
+              }
+              sg = s2;
+              mn = INFINITY;
+              mx = -INFINITY;
+            }
+            const float v = colp[r * kStgStride];
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+          }
+          if (sg >= 0 && col < N) {
+            const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
+            atomicMin(a.stat_min + idx, enc_f(mn));
+            atomicMax(a.stat_max + idx, enc_f(mx));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(m.stg_empty + c);
+      }
+      // ---- step t's cost program for this warp's rows, from the x_t hand-off
+      const int xb = t & 1;
+      mbar_wait(m.x_full + xb, static_cast<uint32_t>((t >> 1) & 1));
+      if (warp == kAuxWarp0) mark(a, t, 400);
+      for (int j = 0; j < ks; ++j) srow[j] = m.xbuf[(xb * 128 + row) * o.tc_xs + j];
+      mbar_arrive(m.x_empty + xb);
+      for (int j = 0; j < ka; ++j) {
+        const float u = row_ok ? __ldg(urow + t * ka + j) : 0.f;
+        srow[o.ucol + j] = u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q == j) p[q] += u;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kd) srow[o.pcol + q] = p[q];
+      cost += cost_program(o, m.ops, m.cconst - o.cost_f0, srow, t);
+      if (warp == kAuxWarp0) mark(a, t, 401);
+      if (a.stat_min != nullptr && o.n_sc > 0) {
+        if (two) {
+          // fused pass over every recorded scratch column: redux.sync per column
+          // and subdomain -> shared atomics -> one global atomic each
+          const int sg = m.segl[row];
+          const unsigned has0 = __ballot_sync(0xffffffffu, sg == 0), has1 = __ballot_sync(0xffffffffu, sg == 1);
+          for (int i = 0; i < o.n_sc; ++i) {
+            const int e = enc_f(srow[m.pairs[2 * i]]);
+            if (has0) {
+              const int mn = __reduce_min_sync(0xffffffffu, sg == 0 ? e : 0x7fffffff);
+              const int mx = __reduce_max_sync(0xffffffffu, sg == 0 ? e : static_cast<int>(0x80000000u));
+              if (lane == 0) {
+                atomicMin(m.red2 + i, mn);
+                atomicMax(m.red2 + o.n_sc + i, mx);
+              }
+            }
+            if (has1) {
+              const int mn = __reduce_min_sync(0xffffffffu, sg == 1 ? e : 0x7fffffff);
+              const int mx = __reduce_max_sync(0xffffffffu, sg == 1 ? e : static_cast<int>(0x80000000u));
+              if (lane == 0) {
+                atomicMin(m.red2 + 2 * o.n_sc + i, mn);
+                atomicMax(m.red2 + 3 * o.n_sc + i, mx);
+              }
+            }
+          }
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          for (int item = row; item < 2 * o.n_sc; item += 128) {
+            const int s2 = item / o.n_sc, i = item % o.n_sc;
+            const int vmin = m.red2[2 * s2 * o.n_sc + i], vmax = m.red2[(2 * s2 + 1) * o.n_sc + i];
+            m.red2[2 * s2 * o.n_sc + i] = enc_f(INFINITY);
+            m.red2[(2 * s2 + 1) * o.n_sc + i] = enc_f(-INFINITY);
+            if (s2 == 1 && bnd >= nvalid) continue;
+            const long long idx = (seg0 + s2) * SPH + t * o.SP + m.pairs[2 * i + 1];
+            atomicMin(a.stat_min + idx, vmin);
+            atomicMax(a.stat_max + idx, vmax);
+          }
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+        } else {
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          for (int i = row; i < o.n_sc; i += 128) {  // one recorded column per thread: segment walk (small tiles)
+            const int colsc = m.pairs[2 * i], off = m.pairs[2 * i + 1];
+            float mn = INFINITY, mx = -INFINITY;
+            int sg = -1;
+            for (int r = 0; r < nvalid; ++r) {
+              const int s2 = m.segl[r];
+              if (s2 != sg) {
+                if (sg >= 0) {
+                  const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
+                  atomicMin(a.stat_min + idx, enc_f(mn));
+                  atomicMax(a.stat_max + idx, enc_f(mx));
+                }
+                sg = s2;
+                mn = INFINITY;
+                mx = -INFINITY;
+              }
+              const float v = m.sc[r * S + colsc];
+              mn = fminf(mn, v);
+              mx = fmaxf(mx, v);
+            }
+            if (sg >= 0) {
+              const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
+              atomicMin(a.stat_min + idx, enc_f(mn));
+              atomicMax(a.stat_max + idx, enc_f(mx));
+            }
+          }
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+        }
+      }
+      if (warp == kAuxWarp0) mark(a, t, 402);
+      if (a.states != nullptr && row_ok)
+        for (int j = 0; j < ks; ++j) a.states[((row0 + row) * H + t) * ks + j] = srow[j];
+    }
+    if (row_ok) {
+      a.costs[row0 + row] = cost;
+      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + row) / a.rows_per_sub, 1);
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps: layer to layer
+    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column-chunk parity
+    const int row = 32 * g + lane;
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * g) << 16);
+    const bool row_ok = row < nvalid;
+    const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
+    float* prow = m.prow + row * 8;      // effector p_{t-1} (h == 0 threads)
+    float* ubuf = m.prow + 128 * 8;      // [2][128][8] u_t by step parity
     if (h == 0) {
-      for (int j = 0; j < kd; ++j) m.prow[row * 8 + j] = o.f[o.p0 + j];
-      for (int j = 0; j < ks; ++j) srow[j] = o.f[o.x0 + j];
+      for (int j = 0; j < 8; ++j) prow[j] = j < kd ? o.f[o.p0 + j] : 0.f;
+      for (int j = 0; j < 8; ++j) ubuf[row * 8 + j] = (row_ok && j < ka) ? __ldg(urow + j) : 0.f;
+      for (int j = 0; j < ks; ++j) m.xbuf[(128 + row) * o.tc_xs + j] = o.f[o.x0 + j];  // x_0 in the odd slot
     }
     asm volatile("bar.sync 2, 256;" ::: "memory");
-    float ucur[8], unext[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ucur[j] = (row_ok && j < ka) ? __ldg(urow + j) : 0.f;
-    float cost = 0.f;
     int layer_it = 0;
-    const int SPH = o.SP * H;
+    int stg_use[kMaxChunks] = {0, 0, 0, 0};
     for (int t = 0; t < H; ++t) {
       if (warp == 0) mark(a, t, 0);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) unext[j] = (row_ok && j < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+      const float* ucur = ubuf + (t & 1) * 128 * 8 + row * 8;
+      const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // x_{t-1} (x_0 at t = 0)
       // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
       for (int kb = h; kb < o.tc_kb[0]; kb += 2) {
         float v[32];
@@ -375,13 +549,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         for (int j = 0; j < 32; ++j) {
           const int k = kb * 32 + j;
           float x = 0.f;
-          if (k < ks) {
-            x = srow[k] - (o.rel ? m.prow[row * 8 + k % kd] : 0.f);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (k - ks == q && q < ka) x = ucur[q];
-          }
+          if (k < ks)
+            x = xprev[k] - (o.rel ? prow[k % kd] : 0.f);
+          else if (k < ks + ka)
+            x = ucur[k - ks];
           v[j] = x;
         }
         store_operand_tmem(tlane, kb, v);
@@ -390,17 +561,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         mbar_arrive(m.a_chunk + kb);
       }
       if (warp == 0) mark(a, t, 403);
+      // p_t and u_{t+1} for the next step's features
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow / ucur above
+      if (h == 0) {
+        for (int j = 0; j < ka; ++j) prow[j] += ucur[j];
+        float* unx = ubuf + ((t + 1) & 1) * 128 * 8 + row * 8;
+        for (int j = 0; j < ka; ++j) unx[j] = (row_ok && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+      }
       for (int l = 0; l < L; ++l, ++layer_it) {
         const int N = o.widths[l + 1], npad = o.tc_npad[l];
         const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
+        const bool hidden = l + 1 < L;
+        if (!hidden) {  // x_t hand-off slot must be free (the aux warps consumed step t-2)
+          if (t >= 2) mbar_wait(m.x_empty + (t & 1), static_cast<uint32_t>(((t >> 1) - 1) & 1));
+        }
         mbar_wait(m.d_full + (layer_it & 1), static_cast<uint32_t>((layer_it >> 1) & 1));
         fence_after();
         if (warp == 0) mark(a, t, 200 + 10 * l);
-        if (warp == 4) mark(a, t, 300 + 10 * l);
-        const bool hidden = l + 1 < L;
         const bool relu = o.relu[l] != 0;
         const int stat = o.pre_stat[l];
-        const bool rec = relu && stat >= 0 && a.stat_min != nullptr;
+        const bool rec = relu && stat >= 0 && a.stat_min != nullptr && hidden;
         const float* bias = m.bias + l * o.tc_npadmax;
         const int nchunk = (npad + 31) / 32;
         for (int cb = h; cb < nchunk; cb += 2) {
@@ -411,30 +591,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             tmem_ld16(tlane + dcol + cb * 32, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = (cb * 32 + j < N) ? v[j] + bias[cb * 32 + j] : 0.f;
-          if (rec) {
-            const int lastrow = min(32 * g + 31, nvalid - 1);
-            const int sfirst = m.segl[32 * g], slast = lastrow >= 32 * g ? m.segl[lastrow] : -1;
-            for (int sg = sfirst; sg <= slast && sg >= 0; ++sg) {
-              float mn[32], mx[32];
-              const bool mine = m.segl[row] == sg;
+          if (rec) {  // stage the pre-activations for this chunk's aux warp
+            if (stg_use[cb] > 0) mbar_wait(m.stg_empty + cb, static_cast<uint32_t>((stg_use[cb] - 1) & 1));
+            ++stg_use[cb];
+            float4* dst = reinterpret_cast<float4*>(m.stg + (cb * 128 + row) * kStgStride);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                mn[j] = mine ? v[j] : INFINITY;
-                mx[j] = mine ? v[j] : -INFINITY;
-              }
-              warp_colreduce(mn, mx, lane);
-              const int col = cb * 32 + lane;
-              if (col < N) {
-                if (ts.two) {
-                  atomicMin(m.red + 2 * sg * o.red_w + col, enc_f(mn[0]));
-                  atomicMax(m.red + (2 * sg + 1) * o.red_w + col, enc_f(mx[0]));
-                } else {
-                  const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
-                  atomicMin(a.stat_min + idx, enc_f(mn[0]));
-                  atomicMax(a.stat_max + idx, enc_f(mx[0]));
-                }
-              }
-            }
+            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            mbar_arrive(m.stg_full + cb);
           }
           if (relu) {
 #pragma unroll
@@ -446,100 +609,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             fence_before();
             mbar_arrive(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
           } else {
+            float* xo = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (cb * 32 + j < ks) srow[cb * 32 + j] = v[j];
+              if (cb * 32 + j < ks) xo[cb * 32 + j] = v[j];
           }
         }
         if (warp == 0) mark(a, t, 201 + 10 * l);
-        if (rec && ts.two) {  // flush this layer's shared extrema, reset
-          asm volatile("bar.sync 2, 256;" ::: "memory");
-          for (int item = threadIdx.x; item < 2 * N; item += 256) {
-            const int sg = item / N, col = item % N;
-            const int vmin = m.red[2 * sg * o.red_w + col], vmax = m.red[(2 * sg + 1) * o.red_w + col];
-            m.red[2 * sg * o.red_w + col] = enc_f(INFINITY);
-            m.red[(2 * sg + 1) * o.red_w + col] = enc_f(-INFINITY);
-            if (sg == 1 && ts.bnd >= ts.nvalid) continue;
-            const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
-            atomicMin(a.stat_min + idx, vmin);
-            atomicMax(a.stat_max + idx, vmax);
-          }
+        if (!hidden) {  // x_t of every row written: hand it to the aux warps and to the next features
+          fence_before();
+          mbar_arrive(m.x_full + (t & 1));
           asm volatile("bar.sync 2, 256;" ::: "memory");
         }
-        if (warp == 0) mark(a, t, 202 + 10 * l);
       }
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // x_t of every row is in the scratch
-      if (warp == 0) mark(a, t, 400);
-      if (h == 0) {
-        // cost program with u_t, p_t in the scratch row (one thread per row)
-        for (int j = 0; j < ka; ++j) {
-          srow[o.ucol + j] = ucur[j];
-          const float p = m.prow[row * 8 + j] + ucur[j];
-          m.prow[row * 8 + j] = p;
-          srow[o.pcol + j] = p;
-        }
-        cost += cost_program(o, m.ops, srow, t);
-        if (warp == 0) mark(a, t, 401);
-        if (a.stat_min != nullptr && o.n_sc > 0) {
-          if (ts.two) {
-            // one fused pass over every recorded scratch column: redux.sync per
-            // column and subdomain -> shared atomics -> one global atomic each
-            const int sg = m.segl[row];
-            const unsigned has0 = __ballot_sync(0xffffffffu, sg == 0), has1 = __ballot_sync(0xffffffffu, sg == 1);
-            const int* pairs = o.iv + o.sc_list;
-            for (int i = 0; i < o.n_sc; ++i) {
-              const int e = enc_f(srow[pairs[2 * i]]);
-              if (has0) {
-                const int mn = __reduce_min_sync(0xffffffffu, sg == 0 ? e : 0x7fffffff);
-                const int mx = __reduce_max_sync(0xffffffffu, sg == 0 ? e : static_cast<int>(0x80000000u));
-                if (lane == 0) {
-                  atomicMin(m.red2 + i, mn);
-                  atomicMax(m.red2 + o.n_sc + i, mx);
-                }
-              }
-              if (has1) {
-                const int mn = __reduce_min_sync(0xffffffffu, sg == 1 ? e : 0x7fffffff);
-                const int mx = __reduce_max_sync(0xffffffffu, sg == 1 ? e : static_cast<int>(0x80000000u));
-                if (lane == 0) {
-                  atomicMin(m.red2 + 2 * o.n_sc + i, mn);
-                  atomicMax(m.red2 + 3 * o.n_sc + i, mx);
-                }
-              }
-            }
-            row_sync<1>();
-            for (int item = row; item < 2 * o.n_sc; item += 128) {
-              const int s2 = item / o.n_sc, i = item % o.n_sc;
-              const int vmin = m.red2[2 * s2 * o.n_sc + i], vmax = m.red2[(2 * s2 + 1) * o.n_sc + i];
-              m.red2[2 * s2 * o.n_sc + i] = enc_f(INFINITY);
-              m.red2[(2 * s2 + 1) * o.n_sc + i] = enc_f(-INFINITY);
-              if (s2 == 1 && ts.bnd >= ts.nvalid) continue;
-              const long long idx = (seg0 + s2) * SPH + t * o.SP + pairs[2 * i + 1];
-              atomicMin(a.stat_min + idx, vmin);
-              atomicMax(a.stat_max + idx, vmax);
-            }
-          } else {
-            row_sync<1>();
-            column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, 0, ks, o.x_stat, false, t);
-            if (o.u_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.ucol, ka, o.u_stat, false, t);
-            if (o.p_stat >= 0) column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, o.pcol, kd, o.p_stat, false, t);
-            for (int i = 0; i < o.n_ops; ++i)
-              if (m.ops[i].stat >= 0)
-                column_pass<128, 1>(o, a, m.sc, S, m.segl, seg0, m.ops[i].col, m.ops[i].dim, m.ops[i].stat, false, t);
-          }
-        }
-        if (a.states != nullptr && row_ok)
-          for (int j = 0; j < ks; ++j) a.states[((row0 + row) * H + t) * ks + j] = srow[j];
-      }
-      if (warp == 0) mark(a, t, 402);
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // next step's features read the scratch
-#pragma unroll
-      for (int j = 0; j < 8; ++j) ucur[j] = unext[j];
-    }
-    if (h == 0 && row_ok) {
-      a.costs[row0 + row] = cost;
-      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + row) / a.rows_per_sub, 1);
     }
   }
+
   fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -552,8 +637,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 
 size_t rollout_tc_smem(const DevObjective& o) {
   return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
-         sizeof(float) * o.L * o.tc_npadmax + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 128 * 8 +
-         sizeof(uint64_t) * (2 * kStages + 2 + kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc;
+         sizeof(float) * o.L * o.tc_npadmax + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 2 * 128 * 8 +
+         sizeof(uint64_t) * (2 * kStages + 2 + 3 * kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc +
+         sizeof(float) * kMaxChunks * 128 * kStgStride + sizeof(int) * 2 * o.n_sc +
+         sizeof(float) * (o.cost_f1 - o.cost_f0) + sizeof(float) * 2 * 128 * o.tc_xs + sizeof(uint64_t) * 4 +
+         sizeof(float) * 128 * 8;
 }
 
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
