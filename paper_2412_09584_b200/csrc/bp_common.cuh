@@ -16,6 +16,7 @@ struct DevOp {
   int kind, src0, src1, dim, in_dim, begin;
   int is_term, weight_by_step;
   int col;       // column of this op's output inside the per-row scratch
+  int c0, c1;    // scratch columns of src0 / src1 (c1 = -1 without a second argument)
   int stat;      // offset of its recorded extrema within one step's record, -1 if not recorded
   int stop;      // RELU op anchored as the last-ReLU stop at step H
   // float arena offsets (forward)

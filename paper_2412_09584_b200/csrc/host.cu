@@ -395,6 +395,11 @@ Compiled compile(const bp_objective_desc& d) {
     vdim.push_back(dim);
   }
   o.cost_f1 = static_cast<int>(c.fa.size());
+  auto val_col = [&](int id) { return id < 0 ? -1 : id == 0 ? 0 : id == 1 ? o.ucol : id == 2 ? o.pcol : o.ops[id - 3].col; };
+  for (int i = 0; i < d.n_ops; ++i) {
+    o.ops[i].c0 = val_col(o.ops[i].src0);
+    o.ops[i].c1 = val_col(o.ops[i].src1);
+  }
   if (!any_term) fail(BP_INVALID_ARGUMENT, "objective: cost program has no terms");
   o.S = r8(std::max({maxK4, r4(maxw), col})) + 4;
 

@@ -91,81 +91,122 @@ __device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* 
   row_sync<BAR>();
 }
 
-__device__ __forceinline__ const float* val_ptr(const DevObjective& o, const DevOp* ops, const float* row, int id) {
-  if (id == 0) return row;                 // x_t
-  if (id == 1) return row + o.ucol;        // u_t
-  if (id == 2) return row + o.pcol;        // p_t
-  return row + ops[id - 3].col;            // op output
-}
-
-// The step's cost program for one row (reference node semantics, graph.cpp:293-347).
+// The step's cost program for NR rows of one thread, interleaved so the rows'
+// dependent chains overlap (reference node semantics, graph.cpp:293-347).
 // ops: the objective's op table (kernel parameters, or a shared-memory copy);
 // cf: base such that cf + op.<offset> addresses the op constants (o.f, or a
 // shared-memory copy of the arena range [cost_f0, cost_f1) shifted by -cost_f0).
-__device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp* ops, const float* cf, float* row,
-                                             int t) {
-  float cost = 0.f;
+template <int NR>
+__device__ __forceinline__ void cost_program_n(const DevObjective& o, const DevOp* ops, const float* cf,
+                                               float* const (&row)[NR], int t, float (&cost)[NR]) {
   for (int i = 0; i < o.n_ops; ++i) {
     const DevOp& op = ops[i];
-    const float* src = val_ptr(o, ops, row, op.src0);
-    float* dst = row + op.col;
-    float v = 0.f;
+    const int c0 = op.c0, c1 = op.c1, oc = op.col, dim = op.dim, in = op.in_dim;
+    float v[NR];
     switch (op.kind) {
       case 0: {  // LINEAR
         const float* W = cf + op.w;
         const float* b = cf + op.b;
-        for (int r = 0; r < op.dim; ++r) {
-          float s = 0.f;
-          for (int j = 0; j < op.in_dim; ++j) s = fmaf(W[r * op.in_dim + j], src[j], s);
-          dst[r] = s + b[r];
+        for (int r = 0; r < dim; ++r) {
+          float s[NR];
+#pragma unroll
+          for (int q = 0; q < NR; ++q) s[q] = 0.f;
+          for (int j = 0; j < in; ++j) {
+            const float w = W[r * in + j];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) s[q] = fmaf(w, row[q][c0 + j], s[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < NR; ++q) row[q][oc + r] = s[q] + b[r];
         }
-        v = dst[0];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
         break;
       }
       case 1:  // RELU
-        for (int j = 0; j < op.dim; ++j) dst[j] = fmaxf(src[j], 0.f);
-        v = dst[0];
+        for (int j = 0; j < dim; ++j)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) row[q][oc + j] = fmaxf(row[q][c0 + j], 0.f);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
         break;
-      case 2: {  // SUM
-        const float* s1 = op.src1 >= 0 ? val_ptr(o, ops, row, op.src1) : nullptr;
-        for (int j = 0; j < op.dim; ++j) dst[j] = s1 ? src[j] + s1[j] : src[j];
-        v = dst[0];
+      case 2:  // SUM
+        for (int j = 0; j < dim; ++j)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) row[q][oc + j] = c1 >= 0 ? row[q][c0 + j] + row[q][c1 + j] : row[q][c0 + j];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
+        break;
+      case 3: {  // SCALAR_AFFINE
+        const float sc = op.scale, of = op.offset;
+        for (int j = 0; j < dim; ++j)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) row[q][oc + j] = sc * row[q][c0 + j] + of;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
         break;
       }
-      case 3:  // SCALAR_AFFINE
-        for (int j = 0; j < op.dim; ++j) dst[j] = op.scale * src[j] + op.offset;
-        v = dst[0];
-        break;
       case 4: {  // SQDIST
         const float* tg = cf + op.tgt;
-        const float* wt = cf + op.wt + (op.weight_by_step ? t * op.in_dim : 0);
-        float acc = 0.f;
-        for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - tg[j];
-          acc += wt[j] * d * d;
+        const float* wt = cf + op.wt + (op.weight_by_step ? t * in : 0);
+        float acc[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) acc[q] = 0.f;
+        for (int j = 0; j < in; ++j) {
+          const float g = tg[j], w = wt[j];
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            const float dd = row[q][c0 + j] - g;
+            acc[q] += w * dd * dd;
+          }
         }
-        dst[0] = v = acc;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) row[q][oc] = v[q] = acc[q];
         break;
       }
       case 5: {  // HINGE
         const float* c = cf + op.ctr;
-        float acc = 0.f;
-        for (int j = 0; j < op.in_dim; ++j) {
-          const float d = src[j] - c[j];
-          acc += d * d;
+        float acc[NR];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) acc[q] = 0.f;
+        for (int j = 0; j < in; ++j) {
+          const float g = c[j];
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            const float dd = row[q][c0 + j] - g;
+            acc[q] += dd * dd;
+          }
         }
-        const float m = op.radius - sqrtf(acc);
-        dst[0] = v = m > 0.f ? op.penalty * m : 0.f;
+        const float rad = op.radius, pen = op.penalty;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const float mg = rad - sqrtf(acc[q]);
+          row[q][oc] = v[q] = mg > 0.f ? pen * mg : 0.f;
+        }
         break;
       }
-      case 6:  // SLICE
-        for (int j = 0; j < op.dim; ++j) dst[j] = src[op.begin + j];
-        v = dst[0];
+      default: {  // SLICE
+        const int b0 = c0 + op.begin;
+        for (int j = 0; j < dim; ++j)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) row[q][oc + j] = row[q][b0 + j];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
         break;
+      }
     }
-    if (op.is_term) cost += v;
+    if (op.is_term)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) cost[q] += v[q];
   }
-  return cost;
+}
+
+__device__ __forceinline__ float cost_program(const DevObjective& o, const DevOp* ops, const float* cf, float* row,
+                                             int t) {
+  float* const rows[1] = {row};
+  float c[1] = {0.f};
+  cost_program_n<1>(o, ops, cf, rows, t, c);
+  return c[0];
 }
 
 

@@ -45,7 +45,10 @@ namespace bp {
 namespace {
 
 constexpr int kTcThreads = 448;  // 8 epilogue warps + 4 aux warps + producer warp + MMA warp
-constexpr int kAuxWarp0 = 8, kProducerWarp = 12, kMmaWarp = 13;
+// Warps issue from sub-partition warp % 4.  The MMA warp's sub-partition carries no
+// aux warp: an issue-starved MMA thread halves the tensor pipe's rate (tools/mma_rate.cu).
+constexpr int kAuxWarp0 = 8, kProducerWarp = 9, kMmaWarp = 13;
+__device__ __forceinline__ int aux_index(int warp) { return warp == 8 ? 0 : warp - 9; }  // warps 8, 10, 11, 12
 constexpr int kStgStride = 36;  // staging row stride (floats): 16B rows, conflict-free column reads
 constexpr int kStages = 3;
 // TMEM columns: two accumulators (layers alternate) and the hi / lo A operand
@@ -56,10 +59,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Round to TF32, nearest with ties away (cvt.rna.tf32.f32 on finite values) in two
+// integer ops.  Non-finite inputs stay non-finite through lo = x - hi.
 __device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
@@ -88,10 +91,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   for (long long spin = 0; !done; ++spin) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}\n"
         : "=r"(done)
-        : "r"(a), "r"(phase)
+        : "r"(a), "r"(phase), "r"(0x989680u)  // suspend in hardware until the phase flips
         : "memory");
     if (spin > (1ll << 28)) asm volatile("trap;");  // never hang the device on a lost arrival
   }
@@ -135,6 +138,28 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// The three 3xTF32 MMAs of one K-step (A_hi.B_hi, A_hi.B_lo, A_lo.B_hi), issued by one
+// elected lane of a converged warp.
+__device__ __forceinline__ void mma3_tf32_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                             uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, one;\n\t}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
@@ -190,6 +215,9 @@ __device__ __forceinline__ void mark(const RolloutArgs& a, int t, int slot) {
   if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = clock64();
 }
 
+// Bias rows padded to whole 32-column chunks (float4 reads of a full chunk).
+__host__ __device__ __forceinline__ int bias_stride(const DevObjective& o) { return (o.tc_npadmax + 31) & ~31; }
+
 struct TcSmem {
   unsigned char* w;    // [kStages][hi | lo][npadmax rows x 128 B]
   float* sc;           // [128][tc_S] per-row scratch (x_t, u_t, p_t, cost-op values)
@@ -222,7 +250,7 @@ __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
   m.stg = reinterpret_cast<float*>(m.w + kStages * 2 * o.tc_npadmax * 128);
   m.sc = m.stg + kMaxChunks * 128 * kStgStride;
   m.bias = m.sc + 128 * o.tc_S;
-  m.red = reinterpret_cast<int*>(m.bias + o.L * o.tc_npadmax);
+  m.red = reinterpret_cast<int*>(m.bias + o.L * bias_stride(o));
   m.segl = m.red + 4 * o.red_w;
   m.prow = reinterpret_cast<float*>(m.segl + 128);
   m.full = reinterpret_cast<uint64_t*>(m.prow + 3 * 128 * 8);  // prow [128][8] then u_t [2][128][8]
@@ -262,8 +290,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
   if (tid < 128) m.segl[tid] = tid < nvalid ? static_cast<int>((row0 + tid) / a.rows_per_sub - seg0) : -1;
   for (int i = tid; i < 4 * o.red_w; i += kTcThreads) m.red[i] = enc_f(((i / o.red_w) & 1) ? -INFINITY : INFINITY);
   for (int i = tid; i < 128 * S; i += kTcThreads) m.sc[i] = 0.f;
-  for (int i = tid; i < L * o.tc_npadmax; i += kTcThreads) {
-    const int l = i / o.tc_npadmax, j = i % o.tc_npadmax;
+  for (int i = tid; i < L * bias_stride(o); i += kTcThreads) {
+    const int l = i / bias_stride(o), j = i % bias_stride(o);
     m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
   }
   for (int i = tid; i < o.n_ops * static_cast<int>(sizeof(DevOp) / 4); i += kTcThreads)
@@ -285,7 +313,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(m.x_full + b, 256);
-      mbar_init(m.x_empty + b, 128);
+      mbar_init(m.x_empty + b, 64);  // the two cost warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -311,215 +339,232 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
             const int s = it % kStages;
             if (it >= kStages) mbar_wait(m.empty + s, static_cast<uint32_t>((it / kStages - 1) & 1));
+            if (l == 1) mark(a, t, 520 + kb);
             mbar_expect_tx(m.full + s, bytes);
             bulk_g2s(m.w + s * stage_bytes, o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32, bytes, m.full + s);
           }
         }
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int it = 0, layer_it = 0;
-      int a_cnt[kMaxChunks] = {0, 0, 0, 0};
-      for (int t = 0; t < H; ++t)
-        for (int l = 0; l < L; ++l, ++layer_it) {
-          const int npad = o.tc_npad[l];
-          const uint32_t idesc = tf32_idesc(npad);
-          const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
-          for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
-            mbar_wait(m.a_chunk + kb, static_cast<uint32_t>(a_cnt[kb]++ & 1));  // this K-block of A landed
-            if (kb == 0) mark(a, t, 100 + 10 * l);
-            const int s = it % kStages;
-            mbar_wait(m.full + s, static_cast<uint32_t>((it / kStages) & 1));
-            fence_after();
-            const uint32_t wb_hi = smem_u32(m.w + s * stage_bytes), wb_lo = wb_hi + npad * 128;
-            for (int q = 0; q < 4; ++q) {
-              const int kstep = kb * 4 + q;
-              if (kstep >= o.tc_ksteps[l]) break;
-              const uint64_t bh = sw128_desc(wb_hi + 32 * q), bl = sw128_desc(wb_lo + 32 * q);
-              const uint32_t ah = tmem + kColAhi + 8 * kstep, al = tmem + kColAlo + 8 * kstep;
-              mma_tf32_ts(tmem + dcol, ah, bh, idesc, kstep > 0 ? 1u : 0u);
-              mma_tf32_ts(tmem + dcol, ah, bl, idesc, 1u);
-              mma_tf32_ts(tmem + dcol, al, bh, idesc, 1u);
-            }
-            mma_commit(m.empty + s);  // stage free once these MMAs retire
+    // ------------------------------------------------ MMA issuer: the whole warp runs the
+    // (uniform) loop so descriptors stay in uniform registers; one elected lane issues.
+    int it = 0, layer_it = 0;
+    int a_cnt[kMaxChunks] = {0, 0, 0, 0};
+    const uint64_t wdesc0 = sw128_desc(smem_u32(m.w));
+    for (int t = 0; t < H; ++t)
+      for (int l = 0; l < L; ++l, ++layer_it) {
+        const int npad = o.tc_npad[l], ksteps = o.tc_ksteps[l];
+        const uint32_t idesc = tf32_idesc(npad);
+        const uint32_t dst = tmem + ((layer_it & 1) ? kColD1 : kColD0);
+        const uint64_t lo_off = static_cast<uint64_t>(npad * 128) >> 4;
+        for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
+          mbar_wait(m.a_chunk + kb, static_cast<uint32_t>(a_cnt[kb]++ & 1));  // this K-block of A landed
+          if (kb == 0) mark(a, t, 100 + 10 * l);
+          if (l == 1) mark(a, t, 500 + 2 * kb);
+          const int s = it % kStages;
+          mbar_wait(m.full + s, static_cast<uint32_t>((it / kStages) & 1));
+          if (l == 1) mark(a, t, 501 + 2 * kb);
+          fence_after();
+          const uint64_t bh0 = wdesc0 + (static_cast<uint64_t>(s * stage_bytes) >> 4);
+          const int nq = min(4, ksteps - kb * 4);
+          for (int q = 0; q < nq; ++q) {
+            const int kstep = kb * 4 + q;
+            const uint64_t bh = bh0 + 2 * q;  // +32 B along K inside the 128 B swizzle atom
+            mma3_tf32_ts(dst, tmem + kColAhi + 8 * kstep, tmem + kColAlo + 8 * kstep, bh, bh + lo_off, idesc,
+                         kstep > 0 ? 1u : 0u);
           }
-          mma_commit(m.d_full + (layer_it & 1));  // accumulator complete
-          mark(a, t, 101 + 10 * l);
+          mma_commit_elect(m.empty + s);  // stage free once these MMAs retire
         }
-    }
-  } else if (warp >= kAuxWarp0) {
-    // ------------------------------------------------ aux: extrema + cost program (off the layer path)
-    const int c = warp - kAuxWarp0;      // extrema chunk, and rows 32c..32c+31 of the cost program
-    const int row = 32 * c + lane;
+        mma_commit_elect(m.d_full + (layer_it & 1));  // accumulator complete
+        mark(a, t, 101 + 10 * l);
+      }
+  } else if (warp >= 8) {
+    const int ai = aux_index(warp);
     const long long b1 = (seg0 + 1) * a.rows_per_sub - row0;
     const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
     const bool two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
-    const int SPH = o.SP * H;
-    const bool row_ok = row < nvalid;
-    const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
-    float* srow = m.sc + row * S;
-    float p[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) p[j] = j < kd ? o.f[o.p0 + j] : 0.f;
-    float cost = 0.f;
-    int use = 0;
-    for (int t = 0; t < H; ++t) {
-      for (int l = 0; l + 1 < L; ++l) {
-        const int stat = o.pre_stat[l];
-        const bool rec = o.relu[l] != 0 && stat >= 0 && a.stat_min != nullptr;
-        if (!rec || c >= (o.tc_npad[l] + 31) / 32) continue;
-        mbar_wait(m.stg_full + c, static_cast<uint32_t>(use & 1));
-        ++use;
-        const int col = c * 32 + lane, N = o.widths[l + 1];
-        const float* colp = m.stg + c * 128 * kStgStride + lane;
-        if (two) {
-          float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+    const long long SPH = static_cast<long long>(o.SP) * H;
+    if (ai < 2) {
+      // ---------------------------------------------- extrema warps: chunks ai and ai + 2 of
+      // every recorded hidden pre-activation, one column per lane over the 128 staged rows
+      int use[2] = {0, 0};
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l + 1 < L; ++l) {
+          const int stat = o.pre_stat[l];
+          if (o.relu[l] == 0 || stat < 0 || a.stat_min == nullptr) continue;
+          const int nch = (o.tc_npad[l] + 31) / 32, N = o.widths[l + 1];
+          for (int u = 0; u < 2; ++u) {
+            const int c = ai + 2 * u;
+            if (c >= nch) break;
+            mbar_wait(m.stg_full + c, static_cast<uint32_t>(use[u]++ & 1));
+            const int col = c * 32 + lane;
+            const float* colp = m.stg + c * 128 * kStgStride + lane;
+            if (two) {
+              float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
 #pragma unroll 8
-          for (int r = 0; r < bnd; ++r) {
-            const float v = colp[r * kStgStride];
-            mn0 = fminf(mn0, v);
-            mx0 = fmaxf(mx0, v);
-          }
+              for (int r = 0; r < bnd; ++r) {
+                const float v = colp[r * kStgStride];
+                mn0 = fminf(mn0, v);
+                mx0 = fmaxf(mx0, v);
+              }
 #pragma unroll 8
-          for (int r = bnd; r < nvalid; ++r) {
-            const float v = colp[r * kStgStride];
-            mn1 = fminf(mn1, v);
-            mx1 = fmaxf(mx1, v);
-          }
-          if (col < N) {
-            if (bnd > 0) {
-              const long long idx = seg0 * SPH + t * o.SP + stat + col;
-              atomicMin(a.stat_min + idx, enc_f(mn0));
-              atomicMax(a.stat_max + idx, enc_f(mx0));
-            }
-            if (bnd < nvalid) {
-              const long long idx = (seg0 + 1) * SPH + t * o.SP + stat + col;
-              atomicMin(a.stat_min + idx, enc_f(mn1));
-              atomicMax(a.stat_max + idx, enc_f(mx1));
-            }
-          }
-        } else {  // many small subdomains in the tile (parity-test sizes)
-          float mn = INFINITY, mx = -INFINITY;
-          int sg = -1;
-          for (int r = 0; r < nvalid; ++r) {
-            const int s2 = m.segl[r];
-            if (s2 != sg) {
+              for (int r = bnd; r < nvalid; ++r) {
+                const float v = colp[r * kStgStride];
+                mn1 = fminf(mn1, v);
+                mx1 = fmaxf(mx1, v);
+              }
+              if (col < N) {
+                if (bnd > 0) {
+                  const long long idx = seg0 * SPH + t * o.SP + stat + col;
+                  atomicMin(a.stat_min + idx, enc_f(mn0));
+                  atomicMax(a.stat_max + idx, enc_f(mx0));
+                }
+                if (bnd < nvalid) {
+                  const long long idx = (seg0 + 1) * SPH + t * o.SP + stat + col;
+                  atomicMin(a.stat_min + idx, enc_f(mn1));
+                  atomicMax(a.stat_max + idx, enc_f(mx1));
+                }
+              }
+            } else {  // many small subdomains in the tile (parity-test sizes)
+              float mn = INFINITY, mx = -INFINITY;
+              int sg = -1;
+              for (int r = 0; r < nvalid; ++r) {
+                const int s2 = m.segl[r];
+                if (s2 != sg) {
+                  if (sg >= 0 && col < N) {
+                    const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
+                    atomicMin(a.stat_min + idx, enc_f(mn));
+                    atomicMax(a.stat_max + idx, enc_f(mx));
+                  }
+                  sg = s2;
+                  mn = INFINITY;
+                  mx = -INFINITY;
+                }
+                const float v = colp[r * kStgStride];
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+              }
               if (sg >= 0 && col < N) {
                 const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
                 atomicMin(a.stat_min + idx, enc_f(mn));
                 atomicMax(a.stat_max + idx, enc_f(mx));
               }
-              sg = s2;
-              mn = INFINITY;
-              mx = -INFINITY;
             }
-            const float v = colp[r * kStgStride];
-            mn = fminf(mn, v);
-            mx = fmaxf(mx, v);
-          }
-          if (sg >= 0 && col < N) {
-            const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
-            atomicMin(a.stat_min + idx, enc_f(mn));
-            atomicMax(a.stat_max + idx, enc_f(mx));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(m.stg_empty + c);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(m.stg_empty + c);
-      }
-      // ---- step t's cost program for this warp's rows, from the x_t hand-off
-      const int xb = t & 1;
-      mbar_wait(m.x_full + xb, static_cast<uint32_t>((t >> 1) & 1));
-      if (warp == kAuxWarp0) mark(a, t, 400);
-      for (int j = 0; j < ks; ++j) srow[j] = m.xbuf[(xb * 128 + row) * o.tc_xs + j];
-      mbar_arrive(m.x_empty + xb);
-      for (int j = 0; j < ka; ++j) {
-        const float u = row_ok ? __ldg(urow + t * ka + j) : 0.f;
-        srow[o.ucol + j] = u;
+    } else {
+      // ---------------------------------------------- cost warps: two rows per thread
+      // (rows 64w + lane and 64w + 32 + lane), the step's cost program from the x_t hand-off
+      const int cw = ai - 2, ctid = 32 * cw + lane;
+      const int rA = 64 * cw + lane, rB = rA + 32;
+      float* const rows[2] = {m.sc + rA * S, m.sc + rB * S};
+      const bool ok[2] = {rA < nvalid, rB < nvalid};
+      const float* ur[2] = {ok[0] ? a.actions + (row0 + rA) * d : nullptr, ok[1] ? a.actions + (row0 + rB) * d : nullptr};
+      const int sgA = m.segl[rA], sgB = m.segl[rB];
+      float p[2][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q == j) p[q] += u;
-      }
+      for (int j = 0; j < 8; ++j) p[0][j] = p[1][j] = j < kd ? o.f[o.p0 + j] : 0.f;
+      float cost[2] = {0.f, 0.f};
+      for (int t = 0; t < H; ++t) {
+        const int xb = t & 1;
+        mbar_wait(m.x_full + xb, static_cast<uint32_t>((t >> 1) & 1));
+        if (warp == 11) mark(a, t, 400);
+        for (int j = 0; j < ks; ++j) {
+          rows[0][j] = m.xbuf[(xb * 128 + rA) * o.tc_xs + j];
+          rows[1][j] = m.xbuf[(xb * 128 + rB) * o.tc_xs + j];
+        }
+        mbar_arrive(m.x_empty + xb);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < kd) srow[o.pcol + q] = p[q];
-      cost += cost_program(o, m.ops, m.cconst - o.cost_f0, srow, t);
-      if (warp == kAuxWarp0) mark(a, t, 401);
-      if (a.stat_min != nullptr && o.n_sc > 0) {
-        if (two) {
-          // fused pass over every recorded scratch column: redux.sync per column
-          // and subdomain -> shared atomics -> one global atomic each
-          const int sg = m.segl[row];
-          const unsigned has0 = __ballot_sync(0xffffffffu, sg == 0), has1 = __ballot_sync(0xffffffffu, sg == 1);
-          for (int i = 0; i < o.n_sc; ++i) {
-            const int e = enc_f(srow[m.pairs[2 * i]]);
-            if (has0) {
-              const int mn = __reduce_min_sync(0xffffffffu, sg == 0 ? e : 0x7fffffff);
-              const int mx = __reduce_max_sync(0xffffffffu, sg == 0 ? e : static_cast<int>(0x80000000u));
-              if (lane == 0) {
-                atomicMin(m.red2 + i, mn);
-                atomicMax(m.red2 + o.n_sc + i, mx);
-              }
-            }
-            if (has1) {
-              const int mn = __reduce_min_sync(0xffffffffu, sg == 1 ? e : 0x7fffffff);
-              const int mx = __reduce_max_sync(0xffffffffu, sg == 1 ? e : static_cast<int>(0x80000000u));
-              if (lane == 0) {
-                atomicMin(m.red2 + 2 * o.n_sc + i, mn);
-                atomicMax(m.red2 + 3 * o.n_sc + i, mx);
-              }
-            }
+        for (int q = 0; q < 2; ++q) {
+          for (int j = 0; j < ka; ++j) {
+            const float u = ok[q] ? __ldg(ur[q] + t * ka + j) : 0.f;
+            rows[q][o.ucol + j] = u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (e == j) p[q][e] += u;
           }
-          asm volatile("bar.sync 3, 128;" ::: "memory");
-          for (int item = row; item < 2 * o.n_sc; item += 128) {
-            const int s2 = item / o.n_sc, i = item % o.n_sc;
-            const int vmin = m.red2[2 * s2 * o.n_sc + i], vmax = m.red2[(2 * s2 + 1) * o.n_sc + i];
-            m.red2[2 * s2 * o.n_sc + i] = enc_f(INFINITY);
-            m.red2[(2 * s2 + 1) * o.n_sc + i] = enc_f(-INFINITY);
-            if (s2 == 1 && bnd >= nvalid) continue;
-            const long long idx = (seg0 + s2) * SPH + t * o.SP + m.pairs[2 * i + 1];
-            atomicMin(a.stat_min + idx, vmin);
-            atomicMax(a.stat_max + idx, vmax);
-          }
-          asm volatile("bar.sync 3, 128;" ::: "memory");
-        } else {
-          asm volatile("bar.sync 3, 128;" ::: "memory");
-          for (int i = row; i < o.n_sc; i += 128) {  // one recorded column per thread: segment walk (small tiles)
-            const int colsc = m.pairs[2 * i], off = m.pairs[2 * i + 1];
-            float mn = INFINITY, mx = -INFINITY;
-            int sg = -1;
-            for (int r = 0; r < nvalid; ++r) {
-              const int s2 = m.segl[r];
-              if (s2 != sg) {
-                if (sg >= 0) {
-                  const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
-                  atomicMin(a.stat_min + idx, enc_f(mn));
-                  atomicMax(a.stat_max + idx, enc_f(mx));
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (e < kd) rows[q][o.pcol + e] = p[q][e];
+        }
+        cost_program_n<2>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
+        if (warp == 11) mark(a, t, 401);
+        if (a.stat_min != nullptr && o.n_sc > 0) {
+          if (two) {
+            // every recorded scratch column: redux.sync per column and subdomain, one
+            // global atomic pair per warp
+            const bool in0 = sgA == 0 || sgB == 0, in1 = sgA == 1 || sgB == 1;
+            const unsigned has0 = __ballot_sync(0xffffffffu, in0), has1 = __ballot_sync(0xffffffffu, in1);
+            for (int i = 0; i < o.n_sc; ++i) {
+              const int col = m.pairs[2 * i];
+              const long long idx0 = seg0 * SPH + t * o.SP + m.pairs[2 * i + 1];
+              const int eA = enc_f(rows[0][col]), eB = enc_f(rows[1][col]);
+              if (has0) {
+                const int lo = min(sgA == 0 ? eA : 0x7fffffff, sgB == 0 ? eB : 0x7fffffff);
+                const int hi = max(sgA == 0 ? eA : static_cast<int>(0x80000000u), sgB == 0 ? eB : static_cast<int>(0x80000000u));
+                const int mn = __reduce_min_sync(0xffffffffu, lo), mx = __reduce_max_sync(0xffffffffu, hi);
+                if (lane == 0) {
+                  atomicMin(a.stat_min + idx0, mn);
+                  atomicMax(a.stat_max + idx0, mx);
                 }
-                sg = s2;
-                mn = INFINITY;
-                mx = -INFINITY;
               }
-              const float v = m.sc[r * S + colsc];
-              mn = fminf(mn, v);
-              mx = fmaxf(mx, v);
+              if (has1) {
+                const int lo = min(sgA == 1 ? eA : 0x7fffffff, sgB == 1 ? eB : 0x7fffffff);
+                const int hi = max(sgA == 1 ? eA : static_cast<int>(0x80000000u), sgB == 1 ? eB : static_cast<int>(0x80000000u));
+                const int mn = __reduce_min_sync(0xffffffffu, lo), mx = __reduce_max_sync(0xffffffffu, hi);
+                if (lane == 0) {
+                  atomicMin(a.stat_min + idx0 + SPH, mn);
+                  atomicMax(a.stat_max + idx0 + SPH, mx);
+                }
+              }
             }
-            if (sg >= 0) {
-              const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
-              atomicMin(a.stat_min + idx, enc_f(mn));
-              atomicMax(a.stat_max + idx, enc_f(mx));
+          } else {
+            asm volatile("bar.sync 3, 64;" ::: "memory");
+            for (int i = ctid; i < o.n_sc; i += 64) {  // one recorded column per thread: segment walk (small tiles)
+              const int colsc = m.pairs[2 * i], off = m.pairs[2 * i + 1];
+              float mn = INFINITY, mx = -INFINITY;
+              int sg = -1;
+              for (int r = 0; r < nvalid; ++r) {
+                const int s2 = m.segl[r];
+                if (s2 != sg) {
+                  if (sg >= 0) {
+                    const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
+                    atomicMin(a.stat_min + idx, enc_f(mn));
+                    atomicMax(a.stat_max + idx, enc_f(mx));
+                  }
+                  sg = s2;
+                  mn = INFINITY;
+                  mx = -INFINITY;
+                }
+                const float v = m.sc[r * S + colsc];
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+              }
+              if (sg >= 0) {
+                const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
+                atomicMin(a.stat_min + idx, enc_f(mn));
+                atomicMax(a.stat_max + idx, enc_f(mx));
+              }
             }
+            asm volatile("bar.sync 3, 64;" ::: "memory");
           }
-          asm volatile("bar.sync 3, 128;" ::: "memory");
         }
+        if (warp == 11) mark(a, t, 402);
+        if (a.states != nullptr)
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (ok[q])
+              for (int j = 0; j < ks; ++j) a.states[((row0 + (q ? rB : rA)) * H + t) * ks + j] = rows[q][j];
       }
-      if (warp == kAuxWarp0) mark(a, t, 402);
-      if (a.states != nullptr && row_ok)
-        for (int j = 0; j < ks; ++j) a.states[((row0 + row) * H + t) * ks + j] = srow[j];
-    }
-    if (row_ok) {
-      a.costs[row0 + row] = cost;
-      if (a.failed != nullptr && !isfinite(cost)) atomicOr(a.failed + (row0 + row) / a.rows_per_sub, 1);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (ok[q]) {
+          const long long r = row0 + (q ? rB : rA);
+          a.costs[r] = cost[q];
+          if (a.failed != nullptr && !isfinite(cost[q])) atomicOr(a.failed + r / a.rows_per_sub, 1);
+        }
     }
   } else {
     // ------------------------------------------------ epilogue warps: layer to layer
@@ -581,16 +626,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         const bool relu = o.relu[l] != 0;
         const int stat = o.pre_stat[l];
         const bool rec = relu && stat >= 0 && a.stat_min != nullptr && hidden;
-        const float* bias = m.bias + l * o.tc_npadmax;
+        const float* bias = m.bias + l * bias_stride(o);
         const int nchunk = (npad + 31) / 32;
         for (int cb = h; cb < nchunk; cb += 2) {
           float v[32];
-          if (npad - cb * 32 >= 32)
+          if (npad - cb * 32 >= 32) {
             tmem_ld32(tlane + dcol + cb * 32, v);
-          else
+          } else {
             tmem_ld16(tlane + dcol + cb * 32, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = (cb * 32 + j < N) ? v[j] + bias[cb * 32 + j] : 0.f;
+            for (int j = 16; j < 32; ++j) v[j] = 0.f;
+          }
+          // columns in [N, npad) are exact zeros: zero weight rows and zero bias padding
+          const float4* b4 = reinterpret_cast<const float4*>(bias + cb * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 bb = b4[q];
+            v[4 * q] += bb.x;
+            v[4 * q + 1] += bb.y;
+            v[4 * q + 2] += bb.z;
+            v[4 * q + 3] += bb.w;
+          }
           if (rec) {  // stage the pre-activations for this chunk's aux warp
             if (stg_use[cb] > 0) mbar_wait(m.stg_empty + cb, static_cast<uint32_t>((stg_use[cb] - 1) & 1));
             ++stg_use[cb];
@@ -637,7 +693,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 
 size_t rollout_tc_smem(const DevObjective& o) {
   return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
-         sizeof(float) * o.L * o.tc_npadmax + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 2 * 128 * 8 +
+         sizeof(float) * o.L * bias_stride(o) + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 2 * 128 * 8 +
          sizeof(uint64_t) * (2 * kStages + 2 + 3 * kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc +
          sizeof(float) * kMaxChunks * 128 * kStgStride + sizeof(int) * 2 * o.n_sc +
          sizeof(float) * (o.cost_f1 - o.cost_f0) + sizeof(float) * 2 * 128 * o.tc_xs + sizeof(uint64_t) * 4 +
