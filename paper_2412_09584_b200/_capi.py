@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbabplan_cuda.so")
+LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(_HERE, "_lib", "libbabplan_cuda.so")  # override: dev variants
 
 BP_OK, BP_INVALID_ARGUMENT, BP_LOGIC, BP_RUNTIME, BP_CUDA, BP_NCCL, BP_UNSUPPORTED = range(7)
 BP_FEATURE_RELATIVE, BP_FEATURE_ABSOLUTE = 0, 1

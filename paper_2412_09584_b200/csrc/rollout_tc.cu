@@ -5,29 +5,36 @@
 // accumulator.
 //
 // Precision: 3xTF32.  Activations and weights are split into hi = rna_tf32(x)
-// and lo = rna_tf32(x - hi); D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi keeps
-// ~2^-21 relative per product (FP32 is 2^-24), inside the 1e-5 parity bar.
+// and lo = x - hi (the tensor core reads lo's top 19 bits); D += A_hi.B_hi +
+// A_hi.B_lo + A_lo.B_hi keeps ~2^-21 relative per product (FP32 is 2^-24).
+// Measured against the FP64 oracle: <= 1e-5 relative on the parity cases; the
+// tests state 5e-5 for this path.
 //
-// One CTA = 128 rows (the MMA M), warp-specialized:
-//   warps 0-7  row work: warp w owns TMEM lanes 32(w%4).. = rows 32(w%4)..+31 and
-//              the 32-column chunks cb with cb%2 == w/4 (two warps per SMSP);
-//              they stage recorded pre-activations for the extrema warps;
-//              the fused epilogue reads the accumulator (tcgen05.ld), adds the
-//              bias, applies ReLU and writes the hi / lo split
-//              of the next layer's input straight back into TMEM (tcgen05.st),
-//              where the next MMAs read it as their A operand; after the output
-//              layer it runs the per-row cost program (rollout_common.cuh).
-//   warps 8-11 extrema: warp 8+c reduces 32-column chunk c of every recorded
-//              pre-activation, staged in shared memory by the epilogue, over
-//              the tile's rows (lane = column), off the layer-to-layer path.
-//   warp 12    producer: streams the weight K-blocks (hi and lo, host-side
-//              pre-swizzled to the 128B K-major UMMA layout) into a ring of
-//              shared-memory stages with cp.async.bulk + mbarrier tx counts,
-//              running ahead across layers and steps.
-//   warp 13    MMA issuer: one thread issues 3 tcgen05.mma (kind::tf32, A from
-//              TMEM, B from shared memory) per K=8 step; tcgen05.commit frees
-//              the weight stage and, at the end of a layer, hands the
-//              accumulator to the epilogue.
+// One CTA = 128 rows (the MMA M), 14 warps, warp-specialized:
+//   warps 0-7   epilogue: warp w owns TMEM lanes 32(w%4).. = rows 32(w%4)..+31
+//               and the 32-column chunks cb with cb%2 == w/4.  Per layer it
+//               reads the accumulator (tcgen05.ld), adds the bias, stages the
+//               recorded pre-activations for the extrema warps, applies ReLU and
+//               writes the hi / lo split of the next layer's input straight back
+//               into TMEM (tcgen05.st) as the next MMAs' A operand.  The output
+//               layer's x_t goes to a shared-memory hand-off (double-buffered by
+//               step) and the next step's features are built from it at once.
+//   warps 8, 10 extrema: column extrema of staged chunks {0, 2} / {1, 3} of
+//               every recorded pre-activation over the tile's rows (lane =
+//               column), off the layer-to-layer path.
+//   warps 11,12 cost: two rows per thread, the per-row cost program of step t
+//               (rollout_common.cuh) from the x_t hand-off, the recorded scratch
+//               extrema (redux.sync per column), the states output.
+//   warp 9      producer: streams the weight K-blocks (hi and lo, host-side
+//               pre-swizzled to the 128B K-major UMMA layout) into a ring of
+//               shared-memory stages with cp.async.bulk + mbarrier tx counts,
+//               running ahead across layers and steps.
+//   warp 13     MMA issuer: one elected lane issues 3 tcgen05.mma (kind::tf32,
+//               A from TMEM, B from shared memory) per K=8 step; tcgen05.commit
+//               frees the weight stage and, at the end of a layer, hands the
+//               accumulator to the epilogue.  Its sub-partition (warp % 4 == 1)
+//               carries no extrema or cost warp: an issue-starved MMA thread
+//               halves the tensor pipe's rate (tools/mma_rate.cu).
 // TMEM: columns [0,128) and [128,256) two accumulators used by alternate
 // layers, [256,384) A_hi, [384,512) A_lo.  The epilogue of layer l reads its
 // accumulator 32 columns at a time and writes the matching 32-column K-block
@@ -45,9 +52,7 @@ namespace bp {
 namespace {
 
 constexpr int kTcThreads = 448;  // 8 epilogue warps + 4 aux warps + producer warp + MMA warp
-// Warps issue from sub-partition warp % 4.  The MMA warp's sub-partition carries no
-// aux warp: an issue-starved MMA thread halves the tensor pipe's rate (tools/mma_rate.cu).
-constexpr int kAuxWarp0 = 8, kProducerWarp = 9, kMmaWarp = 13;
+constexpr int kProducerWarp = 9, kMmaWarp = 13;  // aux warps: 8, 10, 11, 12
 __device__ __forceinline__ int aux_index(int warp) { return warp == 8 ? 0 : warp - 9; }  // warps 8, 10, 11, 12
 constexpr int kStgStride = 36;  // staging row stride (floats): 16B rows, conflict-free column reads
 constexpr int kStages = 3;
@@ -78,11 +83,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=n.
 __device__ __forceinline__ uint32_t tf32_idesc(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | ((128u >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
@@ -132,14 +132,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
   for (int j = 16; j < 32; ++j) v[j] = 0.f;
 }
 
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
-}
-
 // The three 3xTF32 MMAs of one K-step (A_hi.B_hi, A_hi.B_lo, A_lo.B_hi), issued by one
 // elected lane of a converged warp.
 __device__ __forceinline__ void mma3_tf32_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
@@ -184,7 +176,7 @@ __device__ __forceinline__ void store_operand_tmem(uint32_t tlane, int chunk, co
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     h[j] = rna_tf32(v[j]);
-    l[j] = rna_tf32(v[j] - h[j]);
+    l[j] = v[j] - h[j];  // exact; kind::tf32 reads its top 19 bits (truncation, measured: tools/tc_err.py)
   }
   tmem_st32(tlane + kColAhi + 32 * chunk, h);
   tmem_st32(tlane + kColAlo + 32 * chunk, l);
@@ -253,7 +245,7 @@ __device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
   m.red = reinterpret_cast<int*>(m.bias + o.L * bias_stride(o));
   m.segl = m.red + 4 * o.red_w;
   m.prow = reinterpret_cast<float*>(m.segl + 128);
-  m.full = reinterpret_cast<uint64_t*>(m.prow + 3 * 128 * 8);  // prow [128][8] then u_t [2][128][8]
+  m.full = reinterpret_cast<uint64_t*>(m.prow + 128 * 8);  // prow [128][8]
   m.empty = m.full + kStages;
   m.d_full = m.empty + kStages;
   m.a_chunk = m.d_full + 2;
@@ -574,47 +566,70 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     const bool row_ok = row < nvalid;
     const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
     float* prow = m.prow + row * 8;      // effector p_{t-1} (h == 0 threads)
-    float* ubuf = m.prow + 128 * 8;      // [2][128][8] u_t by step parity
+    // xbuf row of slot b: [x | u] -- x_t (output of step t, slot t&1) and u_{t+1} (the
+    // next step's action); step t's features read slot (t+1)&1 = [x_{t-1} | u_t]
     if (h == 0) {
+      float* xr = m.xbuf + (128 + row) * o.tc_xs;  // slot 1: x_0, u_0
       for (int j = 0; j < 8; ++j) prow[j] = j < kd ? o.f[o.p0 + j] : 0.f;
-      for (int j = 0; j < 8; ++j) ubuf[row * 8 + j] = (row_ok && j < ka) ? __ldg(urow + j) : 0.f;
-      for (int j = 0; j < ks; ++j) m.xbuf[(128 + row) * o.tc_xs + j] = o.f[o.x0 + j];  // x_0 in the odd slot
+      for (int j = 0; j < ks; ++j) xr[j] = o.f[o.x0 + j];
+      for (int j = 0; j < ka; ++j) xr[ks + j] = row_ok ? __ldg(urow + j) : 0.f;
     }
     asm volatile("bar.sync 2, 256;" ::: "memory");
     int layer_it = 0;
     int stg_use[kMaxChunks] = {0, 0, 0, 0};
     for (int t = 0; t < H; ++t) {
       if (warp == 0) mark(a, t, 0);
-      const float* ucur = ubuf + (t & 1) * 128 * 8 + row * 8;
-      const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // x_{t-1} (x_0 at t = 0)
+      const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // [x_{t-1} | u_t]
+      float un[8];  // u_{t+1}, loaded now so the global latency overlaps the features
+#pragma unroll
+      for (int j = 0; j < 8; ++j) un[j] = (h == 0 && row_ok && j < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+      if (warp == 0) mark(a, t, 407);
       // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
       for (int kb = h; kb < o.tc_kb[0]; kb += 2) {
+        // every load is issued unconditionally from a clamped address (no predicated
+        // loads, no branches), so they pipeline; the selects come after
         float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = xprev[min(kb * 32 + j, ks + ka - 1)];
+        if (o.rel) {  // x - tile(p_{t-1}): p index k mod kd, stepped with k, selected from registers
+          float pa[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pa[e] = prow[e];
+          int km = (kb * 32) % kd;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float pv = pa[0];
+#pragma unroll
+            for (int e = 1; e < 8; ++e) pv = km == e ? pa[e] : pv;
+            if (kb * 32 + j < ks) v[j] -= pv;
+            km = km + 1 == kd ? 0 : km + 1;
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int k = kb * 32 + j;
-          float x = 0.f;
-          if (k < ks)
-            x = xprev[k] - (o.rel ? prow[k % kd] : 0.f);
-          else if (k < ks + ka)
-            x = ucur[k - ks];
-          v[j] = x;
+          v[j] = k < ks + ka ? v[j] : 0.f;
         }
+        if (warp == 0) mark(a, t, 404);
         store_operand_tmem(tlane, kb, v);
+        if (warp == 0) mark(a, t, 405);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (warp == 0) mark(a, t, 406);
         fence_before();
         mbar_arrive(m.a_chunk + kb);
       }
       if (warp == 0) mark(a, t, 403);
       // p_t and u_{t+1} for the next step's features
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow / ucur above
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow / xprev above
       if (h == 0) {
-        for (int j = 0; j < ka; ++j) prow[j] += ucur[j];
-        float* unx = ubuf + ((t + 1) & 1) * 128 * 8 + row * 8;
-        for (int j = 0; j < ka; ++j) unx[j] = (row_ok && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+        for (int j = 0; j < ka; ++j) prow[j] += xprev[ks + j];
+        float* unx = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs + ks;  // u_{t+1} beside x_t's slot
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < ka) unx[j] = un[j];
       }
       for (int l = 0; l < L; ++l, ++layer_it) {
-        const int N = o.widths[l + 1], npad = o.tc_npad[l];
+        const int npad = o.tc_npad[l];
         const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
         const bool hidden = l + 1 < L;
         if (!hidden) {  // x_t hand-off slot must be free (the aux warps consumed step t-2)
@@ -693,7 +708,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 
 size_t rollout_tc_smem(const DevObjective& o) {
   return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
-         sizeof(float) * o.L * bias_stride(o) + sizeof(int) * (4 * o.red_w + 128) + sizeof(float) * 2 * 128 * 8 +
+         sizeof(float) * o.L * bias_stride(o) + sizeof(int) * (4 * o.red_w + 128) +
          sizeof(uint64_t) * (2 * kStages + 2 + 3 * kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc +
          sizeof(float) * kMaxChunks * 128 * kStgStride + sizeof(int) * 2 * o.n_sc +
          sizeof(float) * (o.cost_f1 - o.cost_f0) + sizeof(float) * 2 * 128 * o.tc_xs + sizeof(uint64_t) * 4 +
