@@ -507,7 +507,7 @@ Compiled compile(const bp_objective_desc& d) {
       o.tc_kbmax = kbmax;
       o.tc_npadmax = npadmax;
       o.tc_S = std::max(col, d.ks) | 1;  // odd row stride: one row per thread, conflict-free
-      o.tc_xs = (d.ks + d.ka) | 1;  // x_t hand-off row [x | u], odd stride
+      o.tc_xs = d.ks | 1;  // x_t hand-off rows, odd stride
       o.tc_cols = 32;
       while (o.tc_cols < npadmax) o.tc_cols *= 2;
       for (int l = 0; l < d.n_layers; ++l) {

@@ -91,16 +91,43 @@ __device__ void column_pass(const DevObjective& o, const RolloutArgs& a, float* 
   row_sync<BAR>();
 }
 
+// Forward-only op record (80 B): what the cost program reads of a DevOp, loaded
+// with five 16-byte shared-memory loads issued back to back.
+struct alignas(16) FwdOp {
+  int kind, c0, c1, col, dim, in_dim, begin, is_term;
+  int weight_by_step, w, b, tgt, wt, ctr, pad0, pad1;
+  float scale, offset, radius, penalty;
+};
+
+__device__ __forceinline__ FwdOp to_fwd(const DevOp& d) {
+  FwdOp f;
+  f.kind = d.kind, f.c0 = d.c0, f.c1 = d.c1, f.col = d.col, f.dim = d.dim, f.in_dim = d.in_dim, f.begin = d.begin;
+  f.is_term = d.is_term, f.weight_by_step = d.weight_by_step, f.w = d.w, f.b = d.b, f.tgt = d.tgt, f.wt = d.wt;
+  f.ctr = d.ctr, f.pad0 = 0, f.pad1 = 0;
+  f.scale = d.scale, f.offset = d.offset, f.radius = d.radius, f.penalty = d.penalty;
+  return f;
+}
+
+__device__ __forceinline__ FwdOp load_op(const FwdOp* p) {
+  FwdOp r;
+  const int4* s = reinterpret_cast<const int4*>(p);
+  int4* d = reinterpret_cast<int4*>(&r);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) d[q] = s[q];
+  return r;
+}
+__device__ __forceinline__ const DevOp& load_op(const DevOp* p) { return *p; }
+
 // The step's cost program for NR rows of one thread, interleaved so the rows'
 // dependent chains overlap (reference node semantics, graph.cpp:293-347).
 // ops: the objective's op table (kernel parameters, or a shared-memory copy);
 // cf: base such that cf + op.<offset> addresses the op constants (o.f, or a
 // shared-memory copy of the arena range [cost_f0, cost_f1) shifted by -cost_f0).
-template <int NR>
-__device__ __forceinline__ void cost_program_n(const DevObjective& o, const DevOp* ops, const float* cf,
+template <int NR, class OpT>
+__device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT* ops, const float* cf,
                                                float* const (&row)[NR], int t, float (&cost)[NR]) {
   for (int i = 0; i < o.n_ops; ++i) {
-    const DevOp& op = ops[i];
+    const auto& op = load_op(ops + i);
     const int c0 = op.c0, c1 = op.c1, oc = op.col, dim = op.dim, in = op.in_dim;
     float v[NR];
     switch (op.kind) {

@@ -55,7 +55,19 @@ constexpr int kTcThreads = 448;  // 8 epilogue warps + 4 aux warps + producer wa
 constexpr int kProducerWarp = 9, kMmaWarp = 13;  // aux warps: 8, 10, 11, 12
 __device__ __forceinline__ int aux_index(int warp) { return warp == 8 ? 0 : warp - 9; }  // warps 8, 10, 11, 12
 constexpr int kStgStride = 36;  // staging row stride (floats): 16B rows, conflict-free column reads
-constexpr int kStages = 3;
+constexpr int kStages = 3;   // weight ring capacity, in K-blocks of the widest layer
+constexpr int kSlots = 8;    // K-blocks in flight in the ring at most (mbarrier pairs)
+
+// Weight ring: K-blocks of 2 * npad * 128 bytes (hi | lo) placed back to back in
+// a byte ring of kStages widest blocks, wrapping to 0 when a block does not fit,
+// so narrow layers keep more blocks in flight.  Producer and MMA issuer walk the
+// same sequence and place block by block with this function.
+__device__ __forceinline__ uint32_t ring_place(uint32_t& pos, uint32_t bytes, uint32_t ring) {
+  if (pos + bytes > ring) pos = 0;
+  const uint32_t at = pos;
+  pos += bytes;
+  return at;
+}
 // TMEM columns: two accumulators (layers alternate) and the hi / lo A operand
 constexpr uint32_t kColD0 = 0, kColD1 = 128, kColAhi = 256, kColAlo = 384;
 constexpr int kMaxChunks = 4;  // A operand K-blocks of 32 (widths <= 128)
@@ -172,13 +184,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 
 // Writes 32 consecutive K-values of this thread's row as the hi / lo A operand in TMEM.
 __device__ __forceinline__ void store_operand_tmem(uint32_t tlane, int chunk, const float (&v)[32]) {
-  float h[32], l[32];
+  // hi = v as stored: kind::tf32 reads the top 19 bits (truncation); lo = v - trunc(v),
+  // exact, read the same way.  Error ~2^-21 relative per product (tools/tc_err.py).
+  tmem_st32(tlane + kColAhi + 32 * chunk, v);
+  float l[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    h[j] = rna_tf32(v[j]);
-    l[j] = v[j] - h[j];  // exact; kind::tf32 reads its top 19 bits (truncation, measured: tools/tc_err.py)
-  }
-  tmem_st32(tlane + kColAhi + 32 * chunk, h);
+  for (int j = 0; j < 32; ++j) l[j] = v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
   tmem_st32(tlane + kColAlo + 32 * chunk, l);
 }
 
@@ -211,60 +222,131 @@ __device__ __forceinline__ void mark(const RolloutArgs& a, int t, int slot) {
 __host__ __device__ __forceinline__ int bias_stride(const DevObjective& o) { return (o.tc_npadmax + 31) & ~31; }
 
 struct TcSmem {
-  unsigned char* w;    // [kStages][hi | lo][npadmax rows x 128 B]
-  float* sc;           // [128][tc_S] per-row scratch (x_t, u_t, p_t, cost-op values)
-  float* bias;         // [L][npadmax]
-  int* red;            // [2][2][red_w]
-  int* segl;           // [128]
-  float* prow;         // [128][8]
-  uint64_t* full;      // [kStages] weight stage landed
-  uint64_t* empty;     // [kStages] weight stage consumed by the MMAs
-  uint64_t* d_full;    // [2] accumulator ready for the epilogue
-  uint64_t* a_chunk;   // [kMaxChunks] A operand K-block written by the 128 row threads
-  uint32_t* tmem_slot;
-  DevOp* ops;          // [n_ops] op table copy
-  int* red2;           // [2 seg][min|max][n_sc] fused scratch extrema
+  unsigned char* w;    // weight ring: kStages x (hi | lo)[npadmax rows x 128 B] bytes
   float* stg;          // [kMaxChunks][128 rows][kStgStride] staged pre-activations
+  float* sc;           // [128][tc_S] per-row scratch of the cost warps (x_t, u_t, p_t, op values)
+  float* bias;         // [L][bias_stride]
+  float* xbuf;         // [2][128][tc_xs] x_t hand-off rows, by step parity
+  float* ubuf;         // [2][128][ustr] u_t rows for the features, by step parity (written by the cost warps)
+  float* prow;         // [128][8] effector p_{t-1} of the epilogue
   float* cconst;       // cost-op constants, arena range [cost_f0, cost_f1)
-  int* pairs;          // [n_sc][2] recorded scratch columns
+  FwdOp* ops;          // [n_ops] forward op table
+  int* segl;           // [128] tile-local subdomain of each row (-1 past the last)
+  int* pairs;          // [n_sc][2] recorded scratch columns (column, record offset)
+  uint64_t* full;      // [kSlots] weight K-block landed
+  uint64_t* empty;     // [kSlots] weight K-block consumed by the MMAs
+  uint64_t* d_full;    // [2] accumulator ready for the epilogue
+  uint64_t* a_chunk;   // [kMaxChunks] A operand K-block written by its 128 epilogue threads
   uint64_t* stg_full;  // [kMaxChunks] chunk staged (128 epilogue threads)
   uint64_t* stg_empty; // [kMaxChunks] chunk consumed by its extrema warp
-  float* xbuf;         // [2][128][tc_xs] x_t hand-off to the aux warps (by step parity)
-  uint64_t* x_full;    // [2]
-  uint64_t* x_empty;   // [2]
+  uint64_t* x_full;    // [2] x_t rows written (256 epilogue threads)
+  uint64_t* x_empty;   // [2] x_t rows copied by the cost warps (64)
+  uint64_t* sc_full;   // [2] step's scratch rows complete (64 cost threads)
+  uint64_t* sc_empty;  // [2] step's scratch extrema taken (64 extrema threads)
+  uint64_t* u_full;    // [2] u rows of the slot written (64 cost threads)
+  uint32_t* tmem_slot;
+  size_t bytes;        // total, from the 1024-aligned base
 };
 
-__device__ TcSmem carve(const DevObjective& o, unsigned char* raw) {
-  const uint32_t s0 = smem_u32(raw);
-  unsigned char* base = raw + (((s0 + 1023u) & ~1023u) - s0);
+// Extrema of one column over the tile's valid rows (v = col[r * stride]) into the
+// per-subdomain record at offset `off` within a subdomain's [H * SP] block: the
+// two-subdomain form (rows [0, bnd) / [bnd, nvalid)) or, for tiles spanning more
+// subdomains (parity-test sizes), a walk over segl.  `valid` gates the atomics.
+__device__ __forceinline__ void column_extrema(const RolloutArgs& a, const float* col, int stride, bool valid, bool two,
+                                               int bnd, int nvalid, const int* segl, long long seg0, long long SPH,
+                                               long long off) {
+  if (two) {
+    float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+#pragma unroll 8
+    for (int r = 0; r < bnd; ++r) {
+      const float v = col[r * stride];
+      mn0 = fminf(mn0, v);
+      mx0 = fmaxf(mx0, v);
+    }
+#pragma unroll 8
+    for (int r = bnd; r < nvalid; ++r) {
+      const float v = col[r * stride];
+      mn1 = fminf(mn1, v);
+      mx1 = fmaxf(mx1, v);
+    }
+    if (valid) {
+      if (bnd > 0) {
+        atomicMin(a.stat_min + seg0 * SPH + off, enc_f(mn0));
+        atomicMax(a.stat_max + seg0 * SPH + off, enc_f(mx0));
+      }
+      if (bnd < nvalid) {
+        atomicMin(a.stat_min + (seg0 + 1) * SPH + off, enc_f(mn1));
+        atomicMax(a.stat_max + (seg0 + 1) * SPH + off, enc_f(mx1));
+      }
+    }
+    return;
+  }
+  float mn = INFINITY, mx = -INFINITY;
+  int sg = -1;
+  for (int r = 0; r < nvalid; ++r) {
+    const int s2 = segl[r];
+    if (s2 != sg) {
+      if (sg >= 0 && valid) {
+        atomicMin(a.stat_min + (seg0 + sg) * SPH + off, enc_f(mn));
+        atomicMax(a.stat_max + (seg0 + sg) * SPH + off, enc_f(mx));
+      }
+      sg = s2;
+      mn = INFINITY;
+      mx = -INFINITY;
+    }
+    const float v = col[r * stride];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  if (sg >= 0 && valid) {
+    atomicMin(a.stat_min + (seg0 + sg) * SPH + off, enc_f(mn));
+    atomicMax(a.stat_max + (seg0 + sg) * SPH + off, enc_f(mx));
+  }
+}
+
+__host__ __device__ __forceinline__ int ustride(const DevObjective& o) { return o.ka | 1; }
+
+// One carve for the kernel and the host-side size: 16-byte aligned regions.
+__host__ __device__ inline TcSmem carve(const DevObjective& o, unsigned char* base) {
   TcSmem m;
-  m.w = base;
-  m.stg = reinterpret_cast<float*>(m.w + kStages * 2 * o.tc_npadmax * 128);
-  m.sc = m.stg + kMaxChunks * 128 * kStgStride;
-  m.bias = m.sc + 128 * o.tc_S;
-  m.red = reinterpret_cast<int*>(m.bias + o.L * bias_stride(o));
-  m.segl = m.red + 4 * o.red_w;
-  m.prow = reinterpret_cast<float*>(m.segl + 128);
-  m.full = reinterpret_cast<uint64_t*>(m.prow + 128 * 8);  // prow [128][8]
-  m.empty = m.full + kStages;
-  m.d_full = m.empty + kStages;
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    unsigned char* p = base + off;
+    off = (off + n + 15) & ~static_cast<size_t>(15);
+    return p;
+  };
+  m.w = take(static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128);
+  m.stg = reinterpret_cast<float*>(take(sizeof(float) * kMaxChunks * 128 * kStgStride));
+  m.sc = reinterpret_cast<float*>(take(sizeof(float) * 128 * o.tc_S));
+  m.bias = reinterpret_cast<float*>(take(sizeof(float) * o.L * bias_stride(o)));
+  m.xbuf = reinterpret_cast<float*>(take(sizeof(float) * 2 * 128 * o.tc_xs));
+  m.ubuf = reinterpret_cast<float*>(take(sizeof(float) * 2 * 128 * ustride(o)));
+  m.prow = reinterpret_cast<float*>(take(sizeof(float) * 128 * 8));
+  m.cconst = reinterpret_cast<float*>(take(sizeof(float) * (o.cost_f1 - o.cost_f0)));
+  m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops));
+  m.segl = reinterpret_cast<int*>(take(sizeof(int) * 128));
+  m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kSlots + 2 + 3 * kMaxChunks + 10)));
+  m.full = bars;
+  m.empty = m.full + kSlots;
+  m.d_full = m.empty + kSlots;
   m.a_chunk = m.d_full + 2;
   m.stg_full = m.a_chunk + kMaxChunks;
   m.stg_empty = m.stg_full + kMaxChunks;
   m.x_full = m.stg_empty + kMaxChunks;
   m.x_empty = m.x_full + 2;
-  m.tmem_slot = reinterpret_cast<uint32_t*>(m.x_empty + 2);
-  m.ops = reinterpret_cast<DevOp*>(m.tmem_slot + 4);
-  m.red2 = reinterpret_cast<int*>(m.ops + o.n_ops);
-  m.pairs = m.red2 + 4 * o.n_sc;
-  m.cconst = reinterpret_cast<float*>(m.pairs + 2 * o.n_sc);
-  m.xbuf = m.cconst + (o.cost_f1 - o.cost_f0);
+  m.sc_full = m.x_empty + 2;
+  m.sc_empty = m.sc_full + 2;
+  m.u_full = m.sc_empty + 2;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(take(16));
+  m.bytes = off;
   return m;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObjective o, const RolloutArgs a) {
   extern __shared__ unsigned char smraw[];
-  const TcSmem m = carve(o, smraw);
+  const uint32_t s0 = smem_u32(smraw);
+  const TcSmem m = carve(o, smraw + (((s0 + 1023u) & ~1023u) - s0));  // SW128 stages: 1024-aligned
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long row0 = static_cast<long long>(blockIdx.x) * 128;
   const long long rem_rows = a.n_rows - row0;
@@ -280,19 +362,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 
   const long long seg0 = row0 / a.rows_per_sub;
   if (tid < 128) m.segl[tid] = tid < nvalid ? static_cast<int>((row0 + tid) / a.rows_per_sub - seg0) : -1;
-  for (int i = tid; i < 4 * o.red_w; i += kTcThreads) m.red[i] = enc_f(((i / o.red_w) & 1) ? -INFINITY : INFINITY);
   for (int i = tid; i < 128 * S; i += kTcThreads) m.sc[i] = 0.f;
   for (int i = tid; i < L * bias_stride(o); i += kTcThreads) {
     const int l = i / bias_stride(o), j = i % bias_stride(o);
     m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
   }
-  for (int i = tid; i < o.n_ops * static_cast<int>(sizeof(DevOp) / 4); i += kTcThreads)
-    reinterpret_cast<int*>(m.ops)[i] = reinterpret_cast<const int*>(o.ops)[i];
-  for (int i = tid; i < 4 * o.n_sc; i += kTcThreads) m.red2[i] = enc_f(((i / o.n_sc) & 1) ? -INFINITY : INFINITY);
+  for (int i = tid; i < o.n_ops; i += kTcThreads) m.ops[i] = to_fwd(o.ops[i]);
   for (int i = tid; i < 2 * o.n_sc; i += kTcThreads) m.pairs[i] = o.iv[o.sc_list + i];
   for (int i = tid; i < o.cost_f1 - o.cost_f0; i += kTcThreads) m.cconst[i] = o.f[o.cost_f0 + i];
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       mbar_init(m.full + s, 1);
       mbar_init(m.empty + s, 1);
     }
@@ -306,6 +385,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     for (int b = 0; b < 2; ++b) {
       mbar_init(m.x_full + b, 256);
       mbar_init(m.x_empty + b, 64);  // the two cost warps
+      mbar_init(m.sc_full + b, 64);
+      mbar_init(m.sc_empty + b, 64);  // the two extrema warps
+      mbar_init(m.u_full + b, 64);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -318,22 +400,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
   __syncthreads();
   fence_after();
   const uint32_t tmem = *m.tmem_slot;
-  const int stage_bytes = 2 * o.tc_npadmax * 128;
+  const uint32_t ring_bytes = static_cast<uint32_t>(kStages) * 2u * o.tc_npadmax * 128u;
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------ producer: weight K-blocks
     if (lane == 0) {
-      int it = 0;
+      // in-flight blocks [head, it): their byte ranges, oldest first (FIFO order of
+      // the ring); block it waits for every older block whose bytes it overlaps
+      uint32_t pos = 0, lo_b[kSlots], hi_b[kSlots];
+      int it = 0, head = 0;
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l) {
           const int npad = o.tc_npad[l];
           const uint32_t bytes = 2u * npad * 128u;
           for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
-            const int s = it % kStages;
-            if (it >= kStages) mbar_wait(m.empty + s, static_cast<uint32_t>((it / kStages - 1) & 1));
-            if (l == 1) mark(a, t, 520 + kb);
+            const uint32_t at = ring_place(pos, bytes, ring_bytes);
+            while (head < it) {
+              const int hs = head % kSlots;
+              if (it - head < kSlots && (hi_b[hs] <= at || lo_b[hs] >= at + bytes)) break;
+              mbar_wait(m.empty + hs, static_cast<uint32_t>((head / kSlots) & 1));
+              ++head;
+            }
+            const int s = it % kSlots;
+            lo_b[s] = at;
+            hi_b[s] = at + bytes;
+            if (l == L - 1) mark(a, t, 520 + kb);
             mbar_expect_tx(m.full + s, bytes);
-            bulk_g2s(m.w + s * stage_bytes, o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32, bytes, m.full + s);
+            bulk_g2s(m.w + at, o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32, bytes, m.full + s);
           }
         }
     }
@@ -341,6 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     // ------------------------------------------------ MMA issuer: the whole warp runs the
     // (uniform) loop so descriptors stay in uniform registers; one elected lane issues.
     int it = 0, layer_it = 0;
+    uint32_t pos = 0;
     int a_cnt[kMaxChunks] = {0, 0, 0, 0};
     const uint64_t wdesc0 = sw128_desc(smem_u32(m.w));
     for (int t = 0; t < H; ++t)
@@ -352,12 +446,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
           mbar_wait(m.a_chunk + kb, static_cast<uint32_t>(a_cnt[kb]++ & 1));  // this K-block of A landed
           if (kb == 0) mark(a, t, 100 + 10 * l);
-          if (l == 1) mark(a, t, 500 + 2 * kb);
-          const int s = it % kStages;
-          mbar_wait(m.full + s, static_cast<uint32_t>((it / kStages) & 1));
-          if (l == 1) mark(a, t, 501 + 2 * kb);
+          if (l == L - 1) mark(a, t, 500 + 2 * kb);
+          const int s = it % kSlots;
+          const uint32_t at = ring_place(pos, 2u * npad * 128u, ring_bytes);
+          mbar_wait(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
+          if (l == L - 1) mark(a, t, 501 + 2 * kb);
           fence_after();
-          const uint64_t bh0 = wdesc0 + (static_cast<uint64_t>(s * stage_bytes) >> 4);
+          const uint64_t bh0 = wdesc0 + (static_cast<uint64_t>(at) >> 4);
           const int nq = min(4, ksteps - kb * 4);
           for (int q = 0; q < nq; ++q) {
             const int kstep = kb * 4 + q;
@@ -365,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             mma3_tf32_ts(dst, tmem + kColAhi + 8 * kstep, tmem + kColAlo + 8 * kstep, bh, bh + lo_off, idesc,
                          kstep > 0 ? 1u : 0u);
           }
-          mma_commit_elect(m.empty + s);  // stage free once these MMAs retire
+          mma_commit_elect(m.empty + s);  // block's bytes free once these MMAs retire
         }
         mma_commit_elect(m.d_full + (layer_it & 1));  // accumulator complete
         mark(a, t, 101 + 10 * l);
@@ -376,91 +471,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
     const bool two = (row0 + nvalid - 1) / a.rows_per_sub - seg0 <= 1;
     const long long SPH = static_cast<long long>(o.SP) * H;
+    const bool rec_any = a.stat_min != nullptr;
     if (ai < 2) {
-      // ---------------------------------------------- extrema warps: chunks ai and ai + 2 of
-      // every recorded hidden pre-activation, one column per lane over the 128 staged rows
+      // ---------------------------------------------- extrema warps: per step, chunks ai and
+      // ai + 2 of every recorded hidden pre-activation (staged by the epilogue), then the
+      // recorded scratch columns of the previous step (written by the cost warps);
+      // lane = column, over the tile's rows
       int use[2] = {0, 0};
-      for (int t = 0; t < H; ++t)
+      const int n_sc = rec_any ? o.n_sc : 0;
+      auto scratch = [&](int ts) {
+        mbar_wait(m.sc_full + (ts & 1), static_cast<uint32_t>((ts >> 1) & 1));
+        for (int i = 32 * ai + lane; i < n_sc; i += 64)
+          column_extrema(a, m.sc + m.pairs[2 * i], o.tc_S, true, two, bnd, nvalid, m.segl, seg0, SPH,
+                         ts * o.SP + m.pairs[2 * i + 1]);
+        mbar_arrive(m.sc_empty + (ts & 1));
+      };
+      for (int t = 0; t < H; ++t) {
         for (int l = 0; l + 1 < L; ++l) {
           const int stat = o.pre_stat[l];
-          if (o.relu[l] == 0 || stat < 0 || a.stat_min == nullptr) continue;
+          if (o.relu[l] == 0 || stat < 0 || !rec_any) continue;
           const int nch = (o.tc_npad[l] + 31) / 32, N = o.widths[l + 1];
           for (int u = 0; u < 2; ++u) {
             const int c = ai + 2 * u;
             if (c >= nch) break;
             mbar_wait(m.stg_full + c, static_cast<uint32_t>(use[u]++ & 1));
             const int col = c * 32 + lane;
-            const float* colp = m.stg + c * 128 * kStgStride + lane;
-            if (two) {
-              float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
-#pragma unroll 8
-              for (int r = 0; r < bnd; ++r) {
-                const float v = colp[r * kStgStride];
-                mn0 = fminf(mn0, v);
-                mx0 = fmaxf(mx0, v);
-              }
-#pragma unroll 8
-              for (int r = bnd; r < nvalid; ++r) {
-                const float v = colp[r * kStgStride];
-                mn1 = fminf(mn1, v);
-                mx1 = fmaxf(mx1, v);
-              }
-              if (col < N) {
-                if (bnd > 0) {
-                  const long long idx = seg0 * SPH + t * o.SP + stat + col;
-                  atomicMin(a.stat_min + idx, enc_f(mn0));
-                  atomicMax(a.stat_max + idx, enc_f(mx0));
-                }
-                if (bnd < nvalid) {
-                  const long long idx = (seg0 + 1) * SPH + t * o.SP + stat + col;
-                  atomicMin(a.stat_min + idx, enc_f(mn1));
-                  atomicMax(a.stat_max + idx, enc_f(mx1));
-                }
-              }
-            } else {  // many small subdomains in the tile (parity-test sizes)
-              float mn = INFINITY, mx = -INFINITY;
-              int sg = -1;
-              for (int r = 0; r < nvalid; ++r) {
-                const int s2 = m.segl[r];
-                if (s2 != sg) {
-                  if (sg >= 0 && col < N) {
-                    const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
-                    atomicMin(a.stat_min + idx, enc_f(mn));
-                    atomicMax(a.stat_max + idx, enc_f(mx));
-                  }
-                  sg = s2;
-                  mn = INFINITY;
-                  mx = -INFINITY;
-                }
-                const float v = colp[r * kStgStride];
-                mn = fminf(mn, v);
-                mx = fmaxf(mx, v);
-              }
-              if (sg >= 0 && col < N) {
-                const long long idx = (seg0 + sg) * SPH + t * o.SP + stat + col;
-                atomicMin(a.stat_min + idx, enc_f(mn));
-                atomicMax(a.stat_max + idx, enc_f(mx));
-              }
-            }
+            column_extrema(a, m.stg + c * 128 * kStgStride + lane, kStgStride, col < N, two, bnd, nvalid, m.segl, seg0,
+                           SPH, t * o.SP + stat + col);
             __syncwarp();
             if (lane == 0) mbar_arrive(m.stg_empty + c);
           }
         }
+        if (t >= 1) scratch(t - 1);
+      }
+      scratch(H - 1);
     } else {
       // ---------------------------------------------- cost warps: two rows per thread
       // (rows 64w + lane and 64w + 32 + lane), the step's cost program from the x_t hand-off
-      const int cw = ai - 2, ctid = 32 * cw + lane;
+      const int cw = ai - 2;
       const int rA = 64 * cw + lane, rB = rA + 32;
       float* const rows[2] = {m.sc + rA * S, m.sc + rB * S};
       const bool ok[2] = {rA < nvalid, rB < nvalid};
       const float* ur[2] = {ok[0] ? a.actions + (row0 + rA) * d : nullptr, ok[1] ? a.actions + (row0 + rB) * d : nullptr};
-      const int sgA = m.segl[rA], sgB = m.segl[rB];
       float p[2][8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) p[0][j] = p[1][j] = j < kd ? o.f[o.p0 + j] : 0.f;
       float cost[2] = {0.f, 0.f};
+      const int us = ustride(o);
+      for (int b = 0; b < 2; ++b) {  // u_0, u_1 for the epilogue's features
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          for (int j = 0; j < ka; ++j)
+            m.ubuf[(b * 128 + (q ? rB : rA)) * us + j] = (ok[q] && b < H) ? __ldg(ur[q] + b * ka + j) : 0.f;
+        mbar_arrive(m.u_full + b);
+      }
       for (int t = 0; t < H; ++t) {
         const int xb = t & 1;
+        float un[2][8];  // u_t (this iteration) and u_{t+2} (the epilogue's features two steps on)
+        float u2[2][8];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            un[q][j] = j < ka ? m.ubuf[(xb * 128 + (q ? rB : rA)) * us + j] : 0.f;
+            u2[q][j] = (ok[q] && j < ka && t + 2 < H) ? __ldg(ur[q] + (t + 2) * ka + j) : 0.f;
+          }
+        if (t >= 1) mbar_wait(m.sc_empty + ((t - 1) & 1), static_cast<uint32_t>(((t - 1) >> 1) & 1));
         mbar_wait(m.x_full + xb, static_cast<uint32_t>((t >> 1) & 1));
         if (warp == 11) mark(a, t, 400);
         for (int j = 0; j < ks; ++j) {
@@ -468,87 +544,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           rows[1][j] = m.xbuf[(xb * 128 + rB) * o.tc_xs + j];
         }
         mbar_arrive(m.x_empty + xb);
+        // x_full(t): the epilogue has read u_t (features, p update), so the slot takes u_{t+2}
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < ka) m.ubuf[(xb * 128 + (q ? rB : rA)) * us + j] = u2[q][j];
+        mbar_arrive(m.u_full + xb);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          for (int j = 0; j < ka; ++j) {
-            const float u = ok[q] ? __ldg(ur[q] + t * ka + j) : 0.f;
-            rows[q][o.ucol + j] = u;
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (e == j) p[q][e] += u;
-          }
+          for (int j = 0; j < 8; ++j)
+            if (j < ka) {
+              rows[q][o.ucol + j] = un[q][j];
+              p[q][j] += un[q][j];
+            }
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             if (e < kd) rows[q][o.pcol + e] = p[q][e];
         }
         cost_program_n<2>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
         if (warp == 11) mark(a, t, 401);
-        if (a.stat_min != nullptr && o.n_sc > 0) {
-          if (two) {
-            // every recorded scratch column: redux.sync per column and subdomain, one
-            // global atomic pair per warp
-            const bool in0 = sgA == 0 || sgB == 0, in1 = sgA == 1 || sgB == 1;
-            const unsigned has0 = __ballot_sync(0xffffffffu, in0), has1 = __ballot_sync(0xffffffffu, in1);
-            for (int i = 0; i < o.n_sc; ++i) {
-              const int col = m.pairs[2 * i];
-              const long long idx0 = seg0 * SPH + t * o.SP + m.pairs[2 * i + 1];
-              const int eA = enc_f(rows[0][col]), eB = enc_f(rows[1][col]);
-              if (has0) {
-                const int lo = min(sgA == 0 ? eA : 0x7fffffff, sgB == 0 ? eB : 0x7fffffff);
-                const int hi = max(sgA == 0 ? eA : static_cast<int>(0x80000000u), sgB == 0 ? eB : static_cast<int>(0x80000000u));
-                const int mn = __reduce_min_sync(0xffffffffu, lo), mx = __reduce_max_sync(0xffffffffu, hi);
-                if (lane == 0) {
-                  atomicMin(a.stat_min + idx0, mn);
-                  atomicMax(a.stat_max + idx0, mx);
-                }
-              }
-              if (has1) {
-                const int lo = min(sgA == 1 ? eA : 0x7fffffff, sgB == 1 ? eB : 0x7fffffff);
-                const int hi = max(sgA == 1 ? eA : static_cast<int>(0x80000000u), sgB == 1 ? eB : static_cast<int>(0x80000000u));
-                const int mn = __reduce_min_sync(0xffffffffu, lo), mx = __reduce_max_sync(0xffffffffu, hi);
-                if (lane == 0) {
-                  atomicMin(a.stat_min + idx0 + SPH, mn);
-                  atomicMax(a.stat_max + idx0 + SPH, mx);
-                }
-              }
-            }
-          } else {
-            asm volatile("bar.sync 3, 64;" ::: "memory");
-            for (int i = ctid; i < o.n_sc; i += 64) {  // one recorded column per thread: segment walk (small tiles)
-              const int colsc = m.pairs[2 * i], off = m.pairs[2 * i + 1];
-              float mn = INFINITY, mx = -INFINITY;
-              int sg = -1;
-              for (int r = 0; r < nvalid; ++r) {
-                const int s2 = m.segl[r];
-                if (s2 != sg) {
-                  if (sg >= 0) {
-                    const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
-                    atomicMin(a.stat_min + idx, enc_f(mn));
-                    atomicMax(a.stat_max + idx, enc_f(mx));
-                  }
-                  sg = s2;
-                  mn = INFINITY;
-                  mx = -INFINITY;
-                }
-                const float v = m.sc[r * S + colsc];
-                mn = fminf(mn, v);
-                mx = fmaxf(mx, v);
-              }
-              if (sg >= 0) {
-                const long long idx = (seg0 + sg) * SPH + t * o.SP + off;
-                atomicMin(a.stat_min + idx, enc_f(mn));
-                atomicMax(a.stat_max + idx, enc_f(mx));
-              }
-            }
-            asm volatile("bar.sync 3, 64;" ::: "memory");
-          }
-        }
-        if (warp == 11) mark(a, t, 402);
         if (a.states != nullptr)
 #pragma unroll
           for (int q = 0; q < 2; ++q)
             if (ok[q])
               for (int j = 0; j < ks; ++j) a.states[((row0 + (q ? rB : rA)) * H + t) * ks + j] = rows[q][j];
+        mbar_arrive(m.sc_full + xb);  // scratch rows of step t complete: the extrema warps take them
       }
 #pragma unroll
       for (int q = 0; q < 2; ++q)
@@ -566,23 +588,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     const bool row_ok = row < nvalid;
     const float* urow = row_ok ? a.actions + (row0 + row) * d : nullptr;
     float* prow = m.prow + row * 8;      // effector p_{t-1} (h == 0 threads)
-    // xbuf row of slot b: [x | u] -- x_t (output of step t, slot t&1) and u_{t+1} (the
-    // next step's action); step t's features read slot (t+1)&1 = [x_{t-1} | u_t]
+    // x_t goes to xbuf slot t&1; step t's features read x_{t-1} from slot (t+1)&1
+    // (x_0 in slot 1) and u_t from ubuf slot t&1
     if (h == 0) {
-      float* xr = m.xbuf + (128 + row) * o.tc_xs;  // slot 1: x_0, u_0
       for (int j = 0; j < 8; ++j) prow[j] = j < kd ? o.f[o.p0 + j] : 0.f;
-      for (int j = 0; j < ks; ++j) xr[j] = o.f[o.x0 + j];
-      for (int j = 0; j < ka; ++j) xr[ks + j] = row_ok ? __ldg(urow + j) : 0.f;
+      for (int j = 0; j < ks; ++j) m.xbuf[(128 + row) * o.tc_xs + j] = o.f[o.x0 + j];
     }
+    const int us = ustride(o);
     asm volatile("bar.sync 2, 256;" ::: "memory");
     int layer_it = 0;
     int stg_use[kMaxChunks] = {0, 0, 0, 0};
     for (int t = 0; t < H; ++t) {
       if (warp == 0) mark(a, t, 0);
-      const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // [x_{t-1} | u_t]
-      float un[8];  // u_{t+1}, loaded now so the global latency overlaps the features
-#pragma unroll
-      for (int j = 0; j < 8; ++j) un[j] = (h == 0 && row_ok && j < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + j) : 0.f;
+      const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // x_{t-1}
+      const float* ucur = m.ubuf + ((t & 1) * 128 + row) * us;               // u_t
+      mbar_wait(m.u_full + (t & 1), static_cast<uint32_t>((t >> 1) & 1));  // written a step ago
       if (warp == 0) mark(a, t, 407);
       // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
       for (int kb = h; kb < o.tc_kb[0]; kb += 2) {
@@ -590,7 +610,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         // loads, no branches), so they pipeline; the selects come after
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = xprev[min(kb * 32 + j, ks + ka - 1)];
+        for (int j = 0; j < 32; ++j) {
+          const int k = kb * 32 + j;
+          v[j] = k < ks ? xprev[min(k, ks - 1)] : ucur[min(max(k - ks, 0), ka - 1)];
+        }
         if (o.rel) {  // x - tile(p_{t-1}): p index k mod kd, stepped with k, selected from registers
           float pa[8];
 #pragma unroll
@@ -620,14 +643,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       }
       if (warp == 0) mark(a, t, 403);
       // p_t and u_{t+1} for the next step's features
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow / xprev above
-      if (h == 0) {
-        for (int j = 0; j < ka; ++j) prow[j] += xprev[ks + j];
-        float* unx = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs + ks;  // u_{t+1} beside x_t's slot
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < ka) unx[j] = un[j];
-      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow above
+      if (h == 0)
+        for (int j = 0; j < ka; ++j) prow[j] += ucur[j];
       for (int l = 0; l < L; ++l, ++layer_it) {
         const int npad = o.tc_npad[l];
         const uint32_t dcol = (layer_it & 1) ? kColD1 : kColD0;
@@ -706,14 +724,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 
 }  // namespace
 
-size_t rollout_tc_smem(const DevObjective& o) {
-  return 1024 + static_cast<size_t>(kStages) * 2 * o.tc_npadmax * 128 + sizeof(float) * 128 * o.tc_S +
-         sizeof(float) * o.L * bias_stride(o) + sizeof(int) * (4 * o.red_w + 128) +
-         sizeof(uint64_t) * (2 * kStages + 2 + 3 * kMaxChunks) + 16 + sizeof(DevOp) * o.n_ops + sizeof(int) * 4 * o.n_sc +
-         sizeof(float) * kMaxChunks * 128 * kStgStride + sizeof(int) * 2 * o.n_sc +
-         sizeof(float) * (o.cost_f1 - o.cost_f0) + sizeof(float) * 2 * 128 * o.tc_xs + sizeof(uint64_t) * 4 +
-         sizeof(float) * 128 * 8;
-}
+size_t rollout_tc_smem(const DevObjective& o) { return 1024 + carve(o, nullptr).bytes; }
 
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
   const size_t smem = rollout_tc_smem(o);
