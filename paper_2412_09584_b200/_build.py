@@ -45,3 +45,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _mtime(LIB) < max(_mtime(o) for o in objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs])
     return LIB
+
+
+def build_variant(name: str, defines: list) -> str:
+    """Dev helper: the library compiled with extra -D flags into _lib/variant_<name>.so
+    (load it with BP_LIB_PATH); the product library is untouched."""
+    obj_dir = os.path.join(OBJ_DIR, name)
+    os.makedirs(obj_dir, exist_ok=True)
+    out = os.path.join(OUT_DIR, f"variant_{name}.so")
+    cmds = [[NVCC, *ARCH, *FLAGS, *defines, "-c", os.path.join(CSRC, s), "-o", os.path.join(obj_dir, s.replace(".cu", ".o"))]
+            for s in SOURCES]
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(run, cmds))
+    run([NVCC, *ARCH, "-shared", "-o", out, *[os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES]])
+    return out

@@ -199,6 +199,13 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+
+// One arrival per warp, after every lane's prior writes: __syncwarp orders the
+// lanes' accesses before lane 0's release-arrive (barrier counts are in warps).
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -209,14 +216,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Debug timeline (BP_TC_TIMELINE): CTA 0, step 3; slots: 0 step start,
-// 100+10l+{0,1} MMA layer l first issue / commit (MMA warp),
-// 200+10l+{0,1,2} epilogue layer l wait-done / chunks done / flush done (warp 0),
-// 300+10l warp 4 epilogue wait-done, 400 cost start, 401 cost done, 402 passes done,
-// 403 features done.
+// Debug timeline: compiled in with -DBP_TC_TIMELINE (_build.build_variant, used by
+// tools/tc_timeline.py) and enabled by the BP_TC_TIMELINE environment variable;
+// clock64 marks of CTA 0, step 3.  Slots: 0 step start, 100+10l+{0,1} MMA layer l
+// first issue / commit, 200+10l+{0,1} epilogue layer l wake / chunks done (warp 0),
+// 400/401 cost program start / done (warp 11), 403-407 features, 500+ MMA waits of
+// the last layer, 520+ producer issues of the last layer, 600+ epilogue chunk phases.
+#ifdef BP_TC_TIMELINE
 __device__ __forceinline__ void mark(const RolloutArgs& a, int t, int slot) {
   if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = clock64();
 }
+#else
+__device__ __forceinline__ void mark(const RolloutArgs&, int, int) {}  // timeline marks compiled out
+#endif
 
 // Bias rows padded to whole 32-column chunks (float4 reads of a full chunk).
 __host__ __device__ __forceinline__ int bias_stride(const DevObjective& o) { return (o.tc_npadmax + 31) & ~31; }
@@ -236,15 +248,16 @@ struct TcSmem {
   uint64_t* full;      // [kSlots] weight K-block landed
   uint64_t* empty;     // [kSlots] weight K-block consumed by the MMAs
   uint64_t* d_full;    // [2] accumulator ready for the epilogue
-  uint64_t* a_chunk;   // [kMaxChunks] A operand K-block written by its 128 epilogue threads
-  uint64_t* stg_full;  // [kMaxChunks] chunk staged (128 epilogue threads)
+  uint64_t* a_chunk;   // [kMaxChunks] A operand K-block written by its 4 epilogue warps
+  uint64_t* stg_full;  // [kMaxChunks] chunk staged (4 epilogue warps)
   uint64_t* stg_empty; // [kMaxChunks] chunk consumed by its extrema warp
-  uint64_t* x_full;    // [2] x_t rows written (256 epilogue threads)
-  uint64_t* x_empty;   // [2] x_t rows copied by the cost warps (64)
-  uint64_t* sc_full;   // [2] step's scratch rows complete (64 cost threads)
-  uint64_t* sc_empty;  // [2] step's scratch extrema taken (64 extrema threads)
-  uint64_t* u_full;    // [2] u rows of the slot written (64 cost threads)
+  uint64_t* x_full;    // [2] x_t rows written (8 epilogue warps)
+  uint64_t* x_empty;   // [2] x_t rows copied by the 2 cost warps
+  uint64_t* sc_full;   // [2] step's scratch rows complete (2 cost warps)
+  uint64_t* sc_empty;  // [2] step's scratch extrema taken (2 extrema warps)
+  uint64_t* u_full;    // [2] u rows of the slot written (2 cost warps)
   uint32_t* tmem_slot;
+  uint32_t* ring;      // [2][kSlots] producer bookkeeping
   size_t bytes;        // total, from the 1024-aligned base
 };
 
@@ -339,6 +352,7 @@ __host__ __device__ inline TcSmem carve(const DevObjective& o, unsigned char* ba
   m.sc_empty = m.sc_full + 2;
   m.u_full = m.sc_empty + 2;
   m.tmem_slot = reinterpret_cast<uint32_t*>(take(16));
+  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2 * kSlots));
   m.bytes = off;
   return m;
 }
@@ -378,16 +392,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     mbar_init(m.d_full + 0, 1);
     mbar_init(m.d_full + 1, 1);
     for (int c = 0; c < kMaxChunks; ++c) {
-      mbar_init(m.a_chunk + c, 128);
-      mbar_init(m.stg_full + c, 128);
+      mbar_init(m.a_chunk + c, 4);  // arrivals are per warp
+      mbar_init(m.stg_full + c, 4);
       mbar_init(m.stg_empty + c, 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(m.x_full + b, 256);
-      mbar_init(m.x_empty + b, 64);  // the two cost warps
-      mbar_init(m.sc_full + b, 64);
-      mbar_init(m.sc_empty + b, 64);  // the two extrema warps
-      mbar_init(m.u_full + b, 64);
+      mbar_init(m.x_full + b, 8);
+      mbar_init(m.x_empty + b, 2);  // the two cost warps
+      mbar_init(m.sc_full + b, 2);
+      mbar_init(m.sc_empty + b, 2);  // the two extrema warps
+      mbar_init(m.u_full + b, 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -407,7 +421,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     if (lane == 0) {
       // in-flight blocks [head, it): their byte ranges, oldest first (FIFO order of
       // the ring); block it waits for every older block whose bytes it overlaps
-      uint32_t pos = 0, lo_b[kSlots], hi_b[kSlots];
+      uint32_t pos = 0;
+      uint32_t* lo_b = m.ring;  // [kSlots] byte ranges of the in-flight blocks
+      uint32_t* hi_b = m.ring + kSlots;
       int it = 0, head = 0;
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l) {
@@ -484,7 +500,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         for (int i = 32 * ai + lane; i < n_sc; i += 64)
           column_extrema(a, m.sc + m.pairs[2 * i], o.tc_S, true, two, bnd, nvalid, m.segl, seg0, SPH,
                          ts * o.SP + m.pairs[2 * i + 1]);
-        mbar_arrive(m.sc_empty + (ts & 1));
+        mbar_arrive_warp(m.sc_empty + (ts & 1));
       };
       for (int t = 0; t < H; ++t) {
         for (int l = 0; l + 1 < L; ++l) {
@@ -523,7 +539,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         for (int q = 0; q < 2; ++q)
           for (int j = 0; j < ka; ++j)
             m.ubuf[(b * 128 + (q ? rB : rA)) * us + j] = (ok[q] && b < H) ? __ldg(ur[q] + b * ka + j) : 0.f;
-        mbar_arrive(m.u_full + b);
+        mbar_arrive_warp(m.u_full + b);
       }
       for (int t = 0; t < H; ++t) {
         const int xb = t & 1;
@@ -543,14 +559,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           rows[0][j] = m.xbuf[(xb * 128 + rA) * o.tc_xs + j];
           rows[1][j] = m.xbuf[(xb * 128 + rB) * o.tc_xs + j];
         }
-        mbar_arrive(m.x_empty + xb);
+        mbar_arrive_warp(m.x_empty + xb);
         // x_full(t): the epilogue has read u_t (features, p update), so the slot takes u_{t+2}
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (j < ka) m.ubuf[(xb * 128 + (q ? rB : rA)) * us + j] = u2[q][j];
-        mbar_arrive(m.u_full + xb);
+        mbar_arrive_warp(m.u_full + xb);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -570,7 +586,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           for (int q = 0; q < 2; ++q)
             if (ok[q])
               for (int j = 0; j < ks; ++j) a.states[((row0 + (q ? rB : rA)) * H + t) * ks + j] = rows[q][j];
-        mbar_arrive(m.sc_full + xb);  // scratch rows of step t complete: the extrema warps take them
+        mbar_arrive_warp(m.sc_full + xb);  // scratch rows of step t complete: the extrema warps take them
       }
 #pragma unroll
       for (int q = 0; q < 2; ++q)
@@ -639,7 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (warp == 0) mark(a, t, 406);
         fence_before();
-        mbar_arrive(m.a_chunk + kb);
+        mbar_arrive_warp(m.a_chunk + kb);
       }
       if (warp == 0) mark(a, t, 403);
       // p_t and u_{t+1} for the next step's features
@@ -663,6 +679,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         const int nchunk = (npad + 31) / 32;
         for (int cb = h; cb < nchunk; cb += 2) {
           float v[32];
+          float4 bb[8];  // bias loads issued first: their latency overlaps the TMEM load
+          const float4* b4 = reinterpret_cast<const float4*>(bias + cb * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) bb[q] = b4[q];
           if (npad - cb * 32 >= 32) {
             tmem_ld32(tlane + dcol + cb * 32, v);
           } else {
@@ -670,33 +690,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
 #pragma unroll
             for (int j = 16; j < 32; ++j) v[j] = 0.f;
           }
+          const bool mk = warp == 0 && l == 1;
+          if (mk) mark(a, t, 600 + 10 * (cb >> 1));
           // columns in [N, npad) are exact zeros: zero weight rows and zero bias padding
-          const float4* b4 = reinterpret_cast<const float4*>(bias + cb * 32);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float4 bb = b4[q];
-            v[4 * q] += bb.x;
-            v[4 * q + 1] += bb.y;
-            v[4 * q + 2] += bb.z;
-            v[4 * q + 3] += bb.w;
+            v[4 * q] += bb[q].x;
+            v[4 * q + 1] += bb[q].y;
+            v[4 * q + 2] += bb[q].z;
+            v[4 * q + 3] += bb[q].w;
           }
+          if (mk) mark(a, t, 604 + 10 * (cb >> 1));
           if (rec) {  // stage the pre-activations for this chunk's aux warp
             if (stg_use[cb] > 0) mbar_wait(m.stg_empty + cb, static_cast<uint32_t>((stg_use[cb] - 1) & 1));
+            if (mk) mark(a, t, 605 + 10 * (cb >> 1));
             ++stg_use[cb];
             float4* dst = reinterpret_cast<float4*>(m.stg + (cb * 128 + row) * kStgStride);
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            mbar_arrive(m.stg_full + cb);
+            mbar_arrive_warp(m.stg_full + cb);
           }
+          if (mk) mark(a, t, 601 + 10 * (cb >> 1));
           if (relu) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
           }
           if (hidden) {
             store_operand_tmem(tlane, cb, v);
+            if (mk) mark(a, t, 602 + 10 * (cb >> 1));
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (mk) mark(a, t, 603 + 10 * (cb >> 1));
             fence_before();
-            mbar_arrive(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
+            mbar_arrive_warp(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
           } else {
             float* xo = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs;
 #pragma unroll
@@ -707,7 +732,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         if (warp == 0) mark(a, t, 201 + 10 * l);
         if (!hidden) {  // x_t of every row written: hand it to the aux warps and to the next features
           fence_before();
-          mbar_arrive(m.x_full + (t & 1));
+          mbar_arrive_warp(m.x_full + (t & 1));
           asm volatile("bar.sync 2, 256;" ::: "memory");
         }
       }

@@ -1,6 +1,11 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["BP_TC_TIMELINE"] = "1"
+# the marks are compiled in only in the timeline variant:
+#   python -c "from paper_2412_09584_b200 import _build; _build.build_variant('timeline', ['-DBP_TC_TIMELINE'])"
+_v = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2412_09584_b200", "_lib", "variant_timeline.so")
+if os.path.exists(_v):
+    os.environ.setdefault("BP_LIB_PATH", _v)
 import numpy as np
 import paper_2412_09584_b200 as bp
 from paper_2412_09584_b200 import workloads
