@@ -22,6 +22,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <thread>
+#include <mutex>
+#include <exception>
 
 #include "../../include/babplan_cuda.h"
 #include "bp_common.cuh"
@@ -169,6 +172,65 @@ struct DBuf {
     return p;
   }
 };
+
+// Pinned host staging (device->host report copies run at full DMA rate).
+template <class T>
+struct HBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  T* get(size_t want) {
+    if (want > n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(want, 1) * sizeof(T), cudaHostAllocDefault),
+         "cudaHostAlloc");
+      n = want;
+    }
+    return p;
+  }
+};
+
+// Host threads for the per-subdomain report / merge / split work of a BaB step
+// (independent items; results land in per-item slots, so the outcome does not
+// depend on the thread count).
+int host_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("BP_HOST_THREADS");
+    const int v = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
+    return std::clamp(v, 1, 64);
+  }();
+  return n;
+}
+
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int nt = std::min(host_threads(), n / 8);  // below ~8 items per thread, stay serial
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        for (int i = t; i < n; i += nt) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
 
 __global__ void fill_int_kernel(int* p, long long n, int v) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -573,6 +635,8 @@ struct bp_ctx {
   DBuf<int> failed, top_seq0, top_seq1, top_cnt, stat_min, stat_max, use_flags;
   DBuf<double> lo_d, hi_d, ivl_lo, ivl_hi, lf;
   DBuf<float> uf_hist;
+  HBuf<float> h_uf, h_best, h_hist, h_tv, h_ta;  // pinned report staging
+  HBuf<int> h_cnt;
   std::vector<double> h_lo, h_hi;
   std::vector<int> h_failed;
   std::vector<Report> reports;
@@ -792,38 +856,55 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
     return;
   }
   // harvest reports
-  std::vector<float> uf(static_cast<size_t>(n)), best(nd), hist(static_cast<size_t>(n) * cfg.iterations);
-  std::vector<int> cnt(static_cast<size_t>(n));
-  ck(memcpy_counted(uf.data(), a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(memcpy_counted(best.data(), a.best, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(memcpy_counted(cnt.data(), a.top_cnt, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(memcpy_counted(hist.data(), ufh, hist.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  std::vector<float> tv(tk), ta(tk * d);
-  ck(memcpy_counted(tv.data(), a.top_val[a.cur], tk * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  ck(memcpy_counted(ta.data(), a.top_act[a.cur], tk * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  float* uf = c->h_uf.get(static_cast<size_t>(n));
+  float* best = c->h_best.get(nd);
+  float* hist = c->h_hist.get(static_cast<size_t>(n) * cfg.iterations);
+  int* cnt = c->h_cnt.get(static_cast<size_t>(n));
+  ck(memcpy_counted(uf, a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(best, a.best, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(cnt, a.top_cnt, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(memcpy_counted(hist, ufh, static_cast<size_t>(n) * cfg.iterations * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  // only the filled part of each top list crosses: counts first, then per-box extents
   ck(cudaStreamSynchronize(st), "sync");
+  float* tv = c->h_tv.get(tk);
+  float* ta = c->h_ta.get(tk * d);
+  {
+    int kmax = 0;
+    for (int i = 0; i < n; ++i) kmax = std::max(kmax, cnt[i]);
+    if (kmax == a.top_cap) {
+      ck(memcpy_counted(tv, a.top_val[a.cur], tk * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(ta, a.top_act[a.cur], tk * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    } else if (kmax > 0) {  // 2D copies of the first kmax entries of every box
+      ck(cudaMemcpy2DAsync(tv, static_cast<size_t>(a.top_cap) * 4, a.top_val[a.cur], static_cast<size_t>(a.top_cap) * 4,
+                           static_cast<size_t>(kmax) * 4, static_cast<size_t>(n), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaMemcpy2DAsync(ta, static_cast<size_t>(a.top_cap) * d * 4, a.top_act[a.cur],
+                           static_cast<size_t>(a.top_cap) * d * 4, static_cast<size_t>(kmax) * d * 4, static_cast<size_t>(n),
+                           cudaMemcpyDeviceToHost, st), "D2H");
+      g_d2h += static_cast<int64_t>(n) * kmax * (d + 1) * 4;
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+  }
   out->assign(static_cast<size_t>(n), Report());
-  for (int i = 0; i < n; ++i) {
+  parallel_for(n, [&](int i) {
     Report& r = (*out)[static_cast<size_t>(i)];
     if (c->h_failed[static_cast<size_t>(i)]) {
       r.ok = false;
       r.error = "evaluate: non-finite objective value (malformed weights?)";
-      continue;
+      return;
     }
-    r.uf = uf[static_cast<size_t>(i)];
-    r.best.assign(best.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * d),
-                  best.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i + 1) * d));
-    const int k = cnt[static_cast<size_t>(i)];
-    r.top_val.assign(tv.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap),
-                     tv.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap + k));
-    r.top_act.assign(ta.begin() + static_cast<std::ptrdiff_t>(static_cast<size_t>(i) * a.top_cap * d),
-                     ta.begin() + static_cast<std::ptrdiff_t>((static_cast<size_t>(i) * a.top_cap + k) * d));
+    r.uf = uf[i];
+    r.best.assign(best + static_cast<size_t>(i) * d, best + static_cast<size_t>(i + 1) * d);
+    const int k = cnt[i];
+    r.top_val.assign(tv + static_cast<size_t>(i) * a.top_cap, tv + static_cast<size_t>(i) * a.top_cap + k);
+    r.top_act.assign(ta + static_cast<size_t>(i) * a.top_cap * d, ta + (static_cast<size_t>(i) * a.top_cap + k) * d);
     r.samples = static_cast<int64_t>(cfg.iterations) * a.rows;
+    r.uf_history.resize(static_cast<size_t>(cfg.iterations));
+    r.samples_history.resize(static_cast<size_t>(cfg.iterations));
     for (int it = 0; it < cfg.iterations; ++it) {
-      r.uf_history.push_back(hist[static_cast<size_t>(it) * n + i]);
-      r.samples_history.push_back(static_cast<int64_t>(it + 1) * a.rows);
+      r.uf_history[static_cast<size_t>(it)] = hist[static_cast<size_t>(it) * n + i];
+      r.samples_history[static_cast<size_t>(it)] = static_cast<int64_t>(it + 1) * a.rows;
     }
-  }
+  });
 }
 
 void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
@@ -1305,18 +1386,20 @@ struct Planner {
     }
     double selected_vol = 0.0;
     for (const auto& r : picked) selected_vol += std::exp(r.log_vol);
-    std::vector<Rec> children;
+    std::vector<Rec*> to_split;
     for (Rec& rec : picked) {
       if (rec.max_width() <= cfg.min_width) {
         retired_min_lf = std::min(retired_min_lf, rec.lf);
         continue;
       }
-      Rec a, b;
-      split_rec(rec, d, cfg.top_percent, cfg.min_width, next_id, cfg.split_rule, a, b);
-      next_id += 2;
-      children.push_back(std::move(a));
-      children.push_back(std::move(b));
+      to_split.push_back(&rec);
     }
+    std::vector<Rec> children(2 * to_split.size());
+    parallel_for(static_cast<int>(to_split.size()), [&](int i) {  // ids by pick order, as the serial loop
+      split_rec(*to_split[static_cast<size_t>(i)], d, cfg.top_percent, cfg.min_width, next_id + 2 * i, cfg.split_rule,
+                children[2 * static_cast<size_t>(i)], children[2 * static_cast<size_t>(i) + 1]);
+    });
+    next_id += 2 * static_cast<int64_t>(to_split.size());
     last_children = static_cast<int>(children.size());
     if (!children.empty()) {
       std::vector<const std::vector<double>*> warms;
@@ -1325,11 +1408,13 @@ struct Planner {
       scfg.seed = mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1);
       std::vector<double> lfs;
       std::vector<Report> reps = search_and_bound(c, children, warms, scfg, cfg.bound_mode, cfg.alpha, &lfs);
+      parallel_for(static_cast<int>(children.size()), [&](int i) {
+        children[static_cast<size_t>(i)].lf = lfs[static_cast<size_t>(i)];
+        merge_report(children[static_cast<size_t>(i)], std::move(reps[static_cast<size_t>(i)]), cfg.search.top_capacity, d);
+      });
       for (size_t i = 0; i < children.size(); ++i) {
         Rec& ch = children[i];
         result.samples += reps[i].samples;
-        ch.lf = lfs[i];
-        merge_report(ch, std::move(reps[i]), cfg.search.top_capacity, d);
         if (ch.uf < result.uf) {
           result.uf = ch.uf;
           result.best = ch.best;
