@@ -34,6 +34,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 
+TF32_DENSE_TFLOPS = 1100.0  # /opt/skills/guides/B200_PROFILING.md, dense (non-sparse) TF32
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -150,17 +153,20 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2412_09584_b200 as bp
 
-    peak = None
+    peak_fp32 = peak_tf32 = None
     if rank == 0:
         import ctypes as C
         from paper_2412_09584_b200 import _capi
         t, ms = C.c_double(), C.c_double()
         _capi.check(_capi.load().bp_measure_fp32_peak(local, C.byref(t), C.byref(ms)))
-        peak = t.value
+        peak_fp32 = t.value
+        _capi.check(_capi.load().bp_measure_tf32_peak(local, C.byref(t), C.byref(ms)))
+        peak_tf32 = t.value
 
     from paper_2412_09584_b200 import parallel
 
     dev = bp.Device(local).load(wl.spec)
+    path = dev.rollout_path()  # "tcgen05" (3xTF32 tensor cores) or "simt" (FP32 FFMA)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
     parallel.attach(dev)
@@ -214,9 +220,27 @@ def main():
     flop = children / world * rows * iters * H * wl.flops_per_sample_step  # this rank's share
     achieved = flop / (tm["rollout_ms"] / 1e3) / 1e12 if tm["rollout_ms"] > 0 else None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "rollout_ncu_summary.json")
+    tp = os.path.join(ROOT, "profiles", "rollout_tc_ncu_summary.json" if path == "tcgen05" else "rollout_ncu_summary.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if path == "tcgen05":
+        # 3xTF32: three dense kind::tf32 MMAs per FP32 product, so the ceiling for the
+        # algorithmic (FP32) FLOP rate is the TF32 tensor peak / 3.
+        roof = {"bound": "tensor", "achieved": achieved, "peak": TF32_DENSE_TFLOPS / 3.0, "unit": "TFLOP/s",
+                "kernel": "rollout_tc_kernel (K1, tcgen05 kind::tf32, 3xTF32)",
+                "peak_source": "B200_PROFILING.md fallback: dense TF32 1100 TFLOP/s (MEASURED_PEAKS.json has no TF32 "
+                               "entry) / 3 MMAs per FP32 product",
+                "peak_measured_live": (peak_tf32 / 3.0) if peak_tf32 else None,
+                "tensor_tflops_executed": 3.0 * achieved if achieved else None}
+    else:
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
+                "kernel": "rollout_kernel (K1, SIMT FFMA)",
+                "peak_source": "bp_measure_fp32_peak: FFMA microbenchmark run live in this process "
+                               "(MEASURED_PEAKS.json has no FP32 SIMT entry)"}
+    roof["frac"] = (roof["achieved"] / roof["peak"]) if (roof["achieved"] and roof["peak"]) else None
+    roof["traffic"] = traffic
+    roof.update({"flop_per_sample_step": wl.flops_per_sample_step, "rollout_ms": tm["rollout_ms"],
+                 "rollout_launches": tm["rollout_launches"]})
 
     e2e = None
     if not args.no_e2e:
@@ -260,20 +284,14 @@ def main():
         line = {
             "metric": "subdomains_bounded_per_s", "value": value, "unit": "subdomains/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if path == "simt" else "tf32x3",
             "data": "synthetic (seeded He-init weights, x0/goal/obstacles from the reference Rng)",
             "config": {"workload": f"{wl.name} (BASELINE.json configs[1])", "widths": wl.spec.widths,
                        "H": H, "M": wl.samples_per_iter, "D_per_step": children / args.steps, "D_per_gpu": children / args.steps / world,
                        "cem_iterations": iters, "batch": batch, "setup_iterations": setup,
                        "l2": "flushed (256 MB write) between timed steps", "parallelism": f"subdomain-sharded x{world}" if world > 1 else "1 GPU"},
             "sample_steps_per_s": sample_steps,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                         "kernel": "rollout_kernel (K1)",
-                         "peak_source": "bp_measure_fp32_peak: FFMA microbenchmark run live in this process "
-                                        "(MEASURED_PEAKS.json has no FP32 SIMT entry)",
-                         "flop_per_sample_step": wl.flops_per_sample_step,
-                         "rollout_ms": tm["rollout_ms"], "rollout_launches": tm["rollout_launches"]},
+            "roofline": roof,
             "e2e": e2e, "gpu_launches": int(tm["launches"]), "clocks": clk, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

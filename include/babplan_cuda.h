@@ -241,6 +241,9 @@ bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, 
 /* Diagnostics: sustained FP32 FMA throughput of the device (TFLOP/s), the
  * roofline denominator of the SIMT rollout kernel. */
 bp_status bp_measure_fp32_peak(int device, double* tflops, double* ms);
+/* Dense kind::tf32 tcgen05.mma throughput (TFLOP/s, M=128 N=128 K=8, one CTA
+ * per SM), the roofline denominator of the tensor-core rollout. */
+bp_status bp_measure_tf32_peak(int device, double* tflops, double* ms);
 
 /* Host-side pool primitives (bit-exact restatements, exposed for parity). */
 typedef struct {

@@ -96,7 +96,7 @@ EXPORTS = [
     "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
     "bp_result_trace", "bp_result_free", "bp_timing", "bp_rng_new", "bp_rng_free",
     "bp_rng_uniform", "bp_rng_normal", "bp_rng_bits", "bp_rng_fill", "bp_mix_seed", "bp_pick_out",
-    "bp_split_axis", "bp_generate_model", "bp_measure_fp32_peak",
+    "bp_split_axis", "bp_generate_model", "bp_measure_fp32_peak", "bp_measure_tf32_peak",
 ]
 
 _lib = None
@@ -160,6 +160,7 @@ def load() -> C.CDLL:
                                         C.c_double, C.c_int, _ip, _dp, C.POINTER(C.c_ubyte)]),
             "bp_generate_model": (C.c_int, [C.c_uint64, C.c_int, _ip, _dp]),
             "bp_measure_fp32_peak": (C.c_int, [C.c_int, _dp, _dp]),
+            "bp_measure_tf32_peak": (C.c_int, [C.c_int, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     // (uniform) loop so descriptors stay in uniform registers; one elected lane issues.
     int it = 0, layer_it = 0;
     uint32_t pos = 0;
-    int a_cnt[kMaxChunks] = {0, 0, 0, 0};
+    uint32_t a_par = 0;  // bit kb: phase parity of a_chunk[kb] (registers, no local array)
     const uint64_t wdesc0 = sw128_desc(smem_u32(m.w));
     for (int t = 0; t < H; ++t)
       for (int l = 0; l < L; ++l, ++layer_it) {
@@ -460,7 +460,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         const uint32_t dst = tmem + ((layer_it & 1) ? kColD1 : kColD0);
         const uint64_t lo_off = static_cast<uint64_t>(npad * 128) >> 4;
         for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
-          mbar_wait(m.a_chunk + kb, static_cast<uint32_t>(a_cnt[kb]++ & 1));  // this K-block of A landed
+          mbar_wait(m.a_chunk + kb, (a_par >> kb) & 1u);  // this K-block of A landed
+          a_par ^= 1u << kb;
           if (kb == 0) mark(a, t, 100 + 10 * l);
           if (l == L - 1) mark(a, t, 500 + 2 * kb);
           const int s = it % kSlots;
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       // ai + 2 of every recorded hidden pre-activation (staged by the epilogue), then the
       // recorded scratch columns of the previous step (written by the cost warps);
       // lane = column, over the tile's rows
-      int use[2] = {0, 0};
+      uint32_t use_par = 0;  // bit u: phase parity of stg_full[ai + 2u]
       const int n_sc = rec_any ? o.n_sc : 0;
       auto scratch = [&](int ts) {
         mbar_wait(m.sc_full + (ts & 1), static_cast<uint32_t>((ts >> 1) & 1));
@@ -510,10 +511,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           for (int u = 0; u < 2; ++u) {
             const int c = ai + 2 * u;
             if (c >= nch) break;
-            mbar_wait(m.stg_full + c, static_cast<uint32_t>(use[u]++ & 1));
+            mbar_wait(m.stg_full + c, (use_par >> u) & 1u);
+            use_par ^= 1u << u;
             const int col = c * 32 + lane;
-            column_extrema(a, m.stg + c * 128 * kStgStride + lane, kStgStride, col < N, two, bnd, nvalid, m.segl, seg0,
-                           SPH, t * o.SP + stat + col);
+            column_extrema(a, m.stg + c * 128 * kStgStride + lane, kStgStride, col < N, two, bnd, nvalid, m.segl, seg0, SPH,
+                           t * o.SP + stat + col);
             __syncwarp();
             if (lane == 0) mbar_arrive(m.stg_empty + c);
           }
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     const int us = ustride(o);
     asm volatile("bar.sync 2, 256;" ::: "memory");
     int layer_it = 0;
-    int stg_use[kMaxChunks] = {0, 0, 0, 0};
+    uint32_t stg_used = 0, stg_par = 0;  // bit cb: chunk staged before / parity of its last use
     for (int t = 0; t < H; ++t) {
       if (warp == 0) mark(a, t, 0);
       const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // x_{t-1}
@@ -702,9 +704,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           }
           if (mk) mark(a, t, 604 + 10 * (cb >> 1));
           if (rec) {  // stage the pre-activations for this chunk's aux warp
-            if (stg_use[cb] > 0) mbar_wait(m.stg_empty + cb, static_cast<uint32_t>((stg_use[cb] - 1) & 1));
+            if ((stg_used >> cb) & 1u) mbar_wait(m.stg_empty + cb, ((stg_par >> cb) & 1u) ^ 1u);
             if (mk) mark(a, t, 605 + 10 * (cb >> 1));
-            ++stg_use[cb];
+            stg_used |= 1u << cb;
+            stg_par ^= 1u << cb;
             float4* dst = reinterpret_cast<float4*>(m.stg + (cb * 128 + row) * kStgStride);
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
