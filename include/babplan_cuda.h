@@ -175,10 +175,14 @@ bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, v
 /* Launch the context's work on an external stream (NULL = its own stream),
  * e.g. torch.cuda.current_stream(), so caller-side CUDA events time it. */
 bp_status bp_set_stream(bp_ctx* ctx, void* cuda_stream);
-/* Rollout kernel selection: path 0 = auto (tcgen05 3xTF32 when every layer
- * width is <= 128 and it fits shared memory, else SIMT FP32), 1 = SIMT only,
- * -1 = query.  *active (optional) = 2 tcgen05, 1 SIMT for the loaded objective. */
+/* Rollout kernel selection: path 0 = auto (tcgen05 3xTF32 v2 when every layer
+ * width is <= 256 and it fits shared memory, else v1 at widths <= 128, else
+ * SIMT FP32), 1 = SIMT only, 2 = tcgen05 v1, 3 = tcgen05 v2, -1 = query.
+ * *active (optional) = 3 tcgen05 v2, 2 tcgen05 v1, 1 SIMT for the loaded objective. */
 bp_status bp_set_rollout_path(bp_ctx* ctx, int path, int* active);
+/* The rollout kernel of the loaded objective (as *active above), its 128-row tiles per
+ * CTA, rows per CTA and dynamic shared memory per CTA (bytes).  Any pointer may be NULL. */
+bp_status bp_rollout_info(bp_ctx* ctx, int* kernel, int* tiles_per_cta, int* rows_per_cta, int64_t* smem_bytes);
 /* Host<->device bytes the library copied since the previous call. */
 bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h);
 

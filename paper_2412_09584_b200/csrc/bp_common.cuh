@@ -58,6 +58,10 @@ struct DevObjective {
   int tc;                    // eligible (all widths <= 128)
   int tc_w[kMaxLayers], tc_bias[kMaxLayers], tc_npad[kMaxLayers], tc_kb[kMaxLayers], tc_ksteps[kMaxLayers];
   int tc_kbmax, tc_npadmax, tc_S, tc_cols, tc_xs;
+  // tcgen05 v2 (rollout_tc2.cu): tiles per CTA (2: widths <= 128, 1: widths <= 256; 0 ineligible) and the
+  // weight ring bytes.  The tc_w images of layers wider than 128 hold per K-block two N halves
+  // [kb][half][hi|lo][rows x 32] (half 0 = 128 rows); narrower layers are the v1 layout.
+  int tc2, tc2_rw, tc2_ring;  // tc2_rw: TMEM region width (128 or 256 columns)
   int sc_list, n_sc;
   int cost_f0, cost_f1;  // float arena range holding every cost-op constant (copied to smem by the tcgen05 kernel)  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
   // constants

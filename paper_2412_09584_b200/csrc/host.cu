@@ -87,6 +87,9 @@ struct SearchArgs {
 cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, bool stream, size_t smem, cudaStream_t st);
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
 size_t rollout_tc_smem(const DevObjective& o);
+cudaError_t launch_rollout_tc2(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
+size_t rollout_tc2_fixed_smem(const DevObjective& o);
+size_t rollout_tc2_smem(const DevObjective& o);
 int rollout_rows_per_tile(int nq);
 cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st);
 size_t bound_smem_bytes();
@@ -554,18 +557,24 @@ Compiled compile(const bp_objective_desc& d) {
     c.kslab = ksl;
     c.smem = base_bytes + (static_cast<size_t>(ksl) * maxNS + pad) * sizeof(float);
   }
-  // tcgen05 (3xTF32) rollout: every layer K, N <= 128, and its shared memory fits
+  // tcgen05 (3xTF32) rollouts: v1 (rollout_tc.cu) when every layer K, N <= 128; v2
+  // (rollout_tc2.cu) when every K, N <= 256 -- two 128-row tiles per CTA at widths <= 128,
+  // one at widths <= 256 -- and its shared memory leaves a weight ring of >= 3 blocks.
   {
-    bool ok = true;
+    bool ok1 = true, ok2 = true;
     int kbmax = 1, npadmax = 16;
     for (int l = 0; l < d.n_layers; ++l) {
       const int K = d.widths[l], N = d.widths[l + 1];
-      if (K > 128 || N > 128) ok = false;
+      if (K > 128 || N > 128) ok1 = false;
+      if (K > 256 || N > 256) ok2 = false;
       kbmax = std::max({kbmax, (K + 31) / 32, (N + 31) / 32});
       npadmax = std::max(npadmax, std::max(16, r16(N)));
     }
     o.tc = 0;
-    if (ok) {
+    o.tc2 = 0;
+    o.tc2_rw = 0;
+    o.tc2_ring = 0;
+    if (ok2) {
       o.tc_kbmax = kbmax;
       o.tc_npadmax = npadmax;
       o.tc_S = std::max(col, d.ks) | 1;  // odd row stride: one row per thread, conflict-free
@@ -578,24 +587,48 @@ Compiled compile(const bp_objective_desc& d) {
         o.tc_npad[l] = npad;
         o.tc_kb[l] = kb;
         o.tc_ksteps[l] = (K + 7) / 8;
+        // per K-block: N halves of <= 128 rows, each [hi rows x 32][lo rows x 32], 128B-swizzled rows
         std::vector<double> img(static_cast<size_t>(kb) * 2 * npad * 32, 0.0);
         for (int b = 0; b < kb; ++b)
-          for (int n = 0; n < npad; ++n)
+          for (int n = 0; n < npad; ++n) {
+            const int half = npad > 128 && n >= 128 ? 1 : 0;
+            const int rows = npad > 128 ? (half ? npad - 128 : 128) : npad;
+            const int nr = n - 128 * half;
+            const size_t blk = static_cast<size_t>(b) * 2 * npad * 32 + (half ? 2 * 128 * 32 : 0);
             for (int cc = 0; cc < 32; ++cc) {
               const int k = b * 32 + cc;
               const float w = (n < N && k < K) ? static_cast<float>(d.W[l][static_cast<size_t>(n) * K + k]) : 0.f;
               const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
-              const size_t pos = static_cast<size_t>(n) * 32 + (((cc >> 2) ^ (n & 7)) << 2) + (cc & 3);
-              img[static_cast<size_t>(b) * 2 * npad * 32 + pos] = hi;
-              img[static_cast<size_t>(b) * 2 * npad * 32 + static_cast<size_t>(npad) * 32 + pos] = lo;
+              const size_t pos = static_cast<size_t>(nr) * 32 + (((cc >> 2) ^ (nr & 7)) << 2) + (cc & 3);
+              img[blk + pos] = hi;
+              img[blk + static_cast<size_t>(rows) * 32 + pos] = lo;
             }
+          }
         o.tc_w[l] = push_f(c.fa, img.data(), img.size());
         std::vector<double> bp(static_cast<size_t>(npad), 0.0);
         for (int n = 0; n < N; ++n) bp[static_cast<size_t>(n)] = d.b[l][n];
         o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
       }
-      c.tc_smem = bp::rollout_tc_smem(o);
-      o.tc = c.tc_smem <= cap ? 1 : 0;
+      if (ok1) {
+        c.tc_smem = bp::rollout_tc_smem(o);
+        o.tc = c.tc_smem <= cap ? 1 : 0;
+      }
+      // two ping-pong tiles when the widths allow it and both tiles' scratch rows fit,
+      // else one tile; the weight ring takes the rest (>= three 128-row blocks)
+      const size_t min_ring = 3 * 128 * 128;
+      const bool narrow = npadmax <= 128 && kbmax <= 4;
+      const int plans[3][2] = {{2, 128}, {1, 128}, {1, 256}};
+      for (const auto& pl : plans) {
+        if (pl[1] == 128 && !narrow) continue;
+        o.tc2 = pl[0];
+        o.tc2_rw = pl[1];
+        const size_t fixed = bp::rollout_tc2_fixed_smem(o);
+        if (fixed + min_ring <= cap) {
+          o.tc2_ring = static_cast<int>((cap - fixed) & ~static_cast<size_t>(1023));
+          break;
+        }
+        o.tc2 = 0;
+      }
     }
   }
   return c;
@@ -655,7 +688,15 @@ struct bp_ctx {
   double rollout_ms = 0, bound_ms = 0, search_ms = 0;
   int64_t rollout_launches = 0, launches = 0;
   bool timing = true;
-  bool force_simt = false;  // BP_ROLLOUT=simt or bp_set_rollout_path
+  int path_mode = 0;  // 0 auto, 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2 (BP_ROLLOUT or bp_set_rollout_path)
+  // rollout kernel for the loaded objective: 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2
+  int kernel() const {
+    if (!loaded || path_mode == 1) return 1;
+    if (path_mode == 2) return comp.o.tc ? 2 : 1;
+    if (path_mode == 3) return comp.o.tc2 ? 3 : 1;
+    // auto: v1 where every width is <= 128 (faster there: rollout_tc2.cu header), else v2
+    return comp.o.tc ? 2 : comp.o.tc2 ? 3 : 1;
+  }
 
   ~bp_ctx() {
     for (auto& e : roll_events) {
@@ -695,7 +736,8 @@ struct bp_ctx {
                long long n_rows, int rows_per_sub) {
     bp::RolloutArgs a{actions, costs, states, smin, smax, fail_flags, n_rows, rows_per_sub, comp.kslab, nullptr};
     static const bool want_tl = std::getenv("BP_TC_TIMELINE") != nullptr;
-    if (want_tl && comp.o.tc && !force_simt) {
+    const int kern = kernel();
+    if (want_tl && kern >= 2) {
       a.timeline = timeline.get(4096);
       ck(cudaMemsetAsync(a.timeline, 0, 4096 * 8, stream), "memset");
     }
@@ -704,7 +746,9 @@ struct bp_ctx {
       ev = roll_event();
       ck(cudaEventRecord(ev.first, stream), "event");
     }
-    if (comp.o.tc && !force_simt)
+    if (kern == 3)
+      ck(bp::launch_rollout_tc2(dev(), a, stream), "rollout (tcgen05 v2) launch");
+    else if (kern == 2)
       ck(bp::launch_rollout_tc(dev(), a, stream), "rollout (tcgen05) launch");
     else
       ck(bp::launch_rollout(dev(), a, comp.nq, comp.stream, comp.smem, stream), "rollout launch");
@@ -716,7 +760,8 @@ struct bp_ctx {
       const long long t0 = tl[0];
       std::fprintf(stderr, "[timeline] role,mark,cycles-from-step-start:");
       for (int i = 0; i < 4096; ++i)
-        if (tl[i] != 0) std::fprintf(stderr, " %d:%lld", i, tl[i] - t0);
+        if (tl[i] != 0)  // values tagged with bit 40 are durations, not clock stamps
+          std::fprintf(stderr, " %d:%lld", i, (tl[i] >> 40) == 1 ? tl[i] - (1ll << 40) : tl[i] - t0);
       std::fprintf(stderr, "\n");
     }
     ++rollout_launches;
@@ -1508,7 +1553,10 @@ bp_status bp_init(int device, bp_ctx** out) {
     ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major < 10) fail(BP_CUDA, "bp_init: device is not sm_100 class (B200 required)");
     c->sms = prop.multiProcessorCount;
-    if (const char* env = std::getenv("BP_ROLLOUT")) c->force_simt = std::string(env) == "simt";
+    if (const char* env = std::getenv("BP_ROLLOUT")) {
+      const std::string e(env);
+      c->path_mode = e == "simt" ? 1 : e == "tc1" ? 2 : e == "tc2" ? 3 : 0;
+    }
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
@@ -1549,9 +1597,22 @@ bp_status bp_set_stream(bp_ctx* ctx, void* stream) {
 bp_status bp_set_rollout_path(bp_ctx* ctx, int path, int* active) {
   return guard([&] {
     check_ctx(ctx);
-    if (path == 0) ctx->force_simt = false;
-    if (path == 1) ctx->force_simt = true;
-    if (active) *active = (ctx->loaded && ctx->comp.o.tc && !ctx->force_simt) ? 2 : 1;
+    if (path >= 0 && path <= 3) ctx->path_mode = path;
+    if (active) *active = ctx->kernel();
+  });
+}
+
+bp_status bp_rollout_info(bp_ctx* ctx, int* kernel, int* tiles_per_cta, int* rows_per_cta, int64_t* smem_bytes) {
+  return guard([&] {
+    check_ctx(ctx);
+    const int k = ctx->kernel();
+    const bp::DevObjective& o = ctx->comp.o;
+    const int tiles = k == 3 ? o.tc2 : k == 2 ? 1 : 0;
+    if (kernel) *kernel = k;
+    if (tiles_per_cta) *tiles_per_cta = tiles;
+    if (rows_per_cta) *rows_per_cta = k == 1 ? ctx->comp.R : 128 * tiles;
+    if (smem_bytes)
+      *smem_bytes = static_cast<int64_t>(k == 3 ? bp::rollout_tc2_smem(o) : k == 2 ? bp::rollout_tc_smem(o) : ctx->comp.smem);
   });
 }
 

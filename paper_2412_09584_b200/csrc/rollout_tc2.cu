@@ -1,0 +1,732 @@
+// rollout_tc2.cu -- K1 v2 on the 5th-generation tensor cores: the fused H-step
+// rollout (reference evaluate / forward_chunk, proj/src/graph.cpp:252-401, on the
+// build_objective graph, model.cpp:310-387) with every Linear layer done by
+// tcgen05.mma (kind::tf32, 3xTF32) into TMEM, for layers up to 256 wide.
+//
+// What changes against rollout_tc.cu (v1, one 128-row tile per CTA, widths <= 128):
+//  * TMEM holds, per 128-row tile, two regions of RW columns that swap roles every
+//    layer: the epilogue converts the accumulator of layer l IN PLACE into the
+//    hi part of layer l+1's A operand, while layer l+1 accumulates into the other
+//    region (which held layer l's A, dead once layer l's MMAs retired).  The lo
+//    part of A lives in shared memory (128B-swizzled K-major, SS MMAs).  That is
+//    2*RW columns per tile instead of 4*128, so
+//      RW = 128 (widths <= 128): TWO tiles per CTA ping-pong -- the MMAs of one
+//           tile run while the epilogue of the other drains, so the tensor pipe
+//           no longer idles through every epilogue (v1's serial chain);
+//      RW = 256 (widths <= 256, C3): one tile, layers issued as N=128 halves.
+//  * Sample extrema of the recorded pre-activations are reduced in the epilogue
+//    registers by a transposing warp butterfly (lane j ends with column j over
+//    the warp's 32 rows) and go straight to the global record with one atomic
+//    pair per column and warp -- no staging buffer, no extrema warps.
+//  * Weight blocks stream as separate hi and lo entries ([rows][128 B] each), so
+//    more of them are in flight in a smaller ring.
+//
+// Precision (unchanged from v1): D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, hi read as
+// the top 19 bits of the FP32 value, lo = x - trunc(x) exact; ~2^-21 relative per
+// product.  The tests state 5e-5 relative for the tensor-core path.
+//
+// Warps (W = 16 epilogue warps; warp w can reach TMEM lanes 32*(w%4)..+31):
+//   0-15   epilogue.  NT=2: tile w/8, chunks c = (w%8)/4 (mod 2);  NT=1: chunks
+//          c = w/4 (mod 4).  Row = 32*(w%4) + lane of its tile.
+//   17     MMA issuer (sub-partition 1), one elected lane issues.
+//   16, (18)  cost warps, one per tile, four rows per thread: the cost program,
+//          the states output and the extrema of the recorded scratch columns
+//          (x_t, u_t, p_t, cost-op values).
+//   last   producer: cp.async.bulk of the weight blocks into the byte ring.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rollout_common.cuh"
+#include "tc_common.cuh"
+
+namespace bp {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kEpiWarps = 16;
+
+// Debug timeline (compiled in with -DBP_TC_TIMELINE, tools/tc_timeline.py): clock64 marks of
+// CTA 0 at step 3.  Slots: 0 step start (epilogue warp 0); 100+20l+10i+{0,1,2} MMA layer l of
+// tile i: A K-block 0 wait begins / ends, commit; 200+20l+10i+{0,1} epilogue of tile i (its
+// first warp) wake / done; 400+10i+{0,1} cost warp of tile i start / done.
+#ifdef BP_TC_TIMELINE
+__device__ __forceinline__ void mark2(const RolloutArgs& a, int t, int slot) {
+  if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = clock64();
+}
+__device__ __forceinline__ long long tl_clock() { return clock64(); }
+__device__ __forceinline__ void put2(const RolloutArgs& a, int t, int slot, long long v) {
+  if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = v;
+}
+#else
+__device__ __forceinline__ void mark2(const RolloutArgs&, int, int) {}
+__device__ __forceinline__ long long tl_clock() { return 0; }
+__device__ __forceinline__ void put2(const RolloutArgs&, int, int, long long) {}
+#endif
+constexpr int kSlots = 8;  // weight blocks in flight at most (mbarrier pairs)
+// __nanosleep backoff (ns) of the long waits: producer / cost warp / epilogue
+constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
+
+template <int NT, int RW_>
+struct Tc2 {
+  static constexpr int RW = RW_;                  // TMEM region width >= widest padded layer
+  static constexpr int KBMAX = RW / 32;           // A operand K-blocks of 32 per tile
+  static constexpr int WPQ = kEpiWarps / (4 * NT);  // epilogue warps per TMEM quadrant per tile
+  static constexpr int kWarps = kEpiWarps + 2 + NT;  // <= 5 warps per sub-partition: 96 registers
+  static constexpr int kThreads = 32 * kWarps;
+  static constexpr int kMmaWarp = 17;
+  static constexpr int kProducerWarp = kWarps - 1;
+  // tile of cost warp w (warps 16 and, for NT = 2, 18)
+  __device__ static int cost_tile(int w) { return w == 16 ? 0 : 1; }
+};
+
+struct Tc2Smem {
+  unsigned char* alo;  // [NT][KBMAX] K-blocks of 128 rows x 128 B (A lo part, SW128 K-major)
+  unsigned char* w;    // weight byte ring
+  float* sc;           // [NT][128][tc_S] per-row scratch of the cost warps (x_t written by the epilogue)
+  float* bias;         // [L][RW]
+  float* cconst;       // cost-op constants, arena range [cost_f0, cost_f1)
+  FwdOp* ops;          // [n_ops]
+  int* segl;           // [NT][128] tile-local subdomain of each row (-1 past the last)
+  int* pairs;          // [n_sc][2] recorded scratch columns (column, record offset)
+  uint64_t* full;      // [kSlots] weight block landed
+  uint64_t* empty;     // [kSlots] weight block consumed by the MMAs
+  uint64_t* d_full;    // [NT][2] accumulator region ready for the epilogue
+  uint64_t* a_chunk;   // [NT][KBMAX] A operand K-block written (4 quadrant warps)
+  uint64_t* x_full;    // [NT] x_t of every row in the scratch (all epilogue warps of the tile)
+  uint64_t* x_empty;   // [NT] step's scratch rows consumed (the tile's cost warp)
+  uint32_t* tmem_slot;
+  uint32_t* ring;      // [2][kSlots] producer bookkeeping
+  size_t bytes;
+};
+
+__host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* base) {
+  const int NT = o.tc2, RW = o.tc2_rw, KBMAX = RW / 32;
+  Tc2Smem m;
+  size_t off = 0;
+  auto take = [&](size_t n, size_t align) {
+    off = (off + align - 1) & ~(align - 1);
+    unsigned char* p = base + off;
+    off += n;
+    return p;
+  };
+  m.alo = take(static_cast<size_t>(NT) * KBMAX * 16384, 1024);
+  m.w = take(static_cast<size_t>(o.tc2_ring), 1024);
+  m.sc = reinterpret_cast<float*>(take(sizeof(float) * NT * 128 * o.tc_S, 16));
+  m.bias = reinterpret_cast<float*>(take(sizeof(float) * o.L * RW, 16));
+  m.cconst = reinterpret_cast<float*>(take(sizeof(float) * (o.cost_f1 - o.cost_f0), 16));
+  m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops, 16));
+  m.segl = reinterpret_cast<int*>(take(sizeof(int) * NT * 128, 16));
+  m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc, 16));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kSlots + NT * (2 + KBMAX + 2)), 16));
+  m.full = bars;
+  m.empty = m.full + kSlots;
+  m.d_full = m.empty + kSlots;
+  m.a_chunk = m.d_full + 2 * NT;
+  m.x_full = m.a_chunk + NT * KBMAX;
+  m.x_empty = m.x_full + NT;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(take(16, 16));
+  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2 * kSlots, 16));
+  m.bytes = off;
+  return m;
+}
+
+// Shared-memory bytes of everything but the weight ring (host planning).
+__host__ inline size_t tc2_fixed_bytes(DevObjective o) {
+  o.tc2_ring = 0;
+  return 1024 + carve2(o, nullptr).bytes + 1024;  // base alignment + ring alignment slack
+}
+
+// Transposing butterfly over the warp for 16 columns: v = this lane's values (one
+// row, columns c0..c0+15); returns in (mn, mx) the min / max over all 32 lanes of
+// column c0 + (lane & 15).  MASK: lanes with incl == false contribute nothing.
+template <bool MASK>
+__device__ __forceinline__ void warp_col_extrema16(const float* v, bool incl, float& mn, float& mx) {
+  const int lane = threadIdx.x & 31;
+  float a[8], b[8];
+  {
+    const bool up = (lane & 8) != 0;
+    if constexpr (MASK) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float l0 = incl ? v[j] : INFINITY, h0 = incl ? v[j + 8] : INFINITY;
+        const float l1 = incl ? v[j] : -INFINITY, h1 = incl ? v[j + 8] : -INFINITY;
+        a[j] = fminf(up ? h0 : l0, __shfl_xor_sync(0xffffffffu, up ? l0 : h0, 8));
+        b[j] = fmaxf(up ? h1 : l1, __shfl_xor_sync(0xffffffffu, up ? l1 : h1, 8));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float r = __shfl_xor_sync(0xffffffffu, up ? v[j] : v[j + 8], 8);
+        const float k = up ? v[j + 8] : v[j];
+        a[j] = fminf(k, r);
+        b[j] = fmaxf(k, r);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const float sa = up ? a[j] : a[j + s], ka = up ? a[j + s] : a[j];
+      const float sb = up ? b[j] : b[j + s], kb = up ? b[j + s] : b[j];
+      a[j] = fminf(ka, __shfl_xor_sync(0xffffffffu, sa, s));
+      b[j] = fmaxf(kb, __shfl_xor_sync(0xffffffffu, sb, s));
+    }
+  }
+  mn = fminf(a[0], __shfl_xor_sync(0xffffffffu, a[0], 16));
+  mx = fmaxf(b[0], __shfl_xor_sync(0xffffffffu, b[0], 16));
+}
+
+// Column extrema of a 32-column chunk over the warp's rows: lane j ends with column j.
+template <bool MASK>
+__device__ __forceinline__ void warp_col_extrema(const float (&v)[32], bool incl, float& mn, float& mx) {
+  float mn0, mx0, mn1, mx1;
+  warp_col_extrema16<MASK>(v, incl, mn0, mx0);
+  warp_col_extrema16<MASK>(v + 16, incl, mn1, mx1);
+  const bool up = (threadIdx.x & 16) != 0;
+  mn = up ? mn1 : mn0;
+  mx = up ? mx1 : mx0;
+}
+
+// Extrema of one scratch column over the tile's valid rows (v = col[r * stride])
+// into the per-subdomain record at offset `off` within a subdomain's [H * SP] block:
+// the unrolled two-subdomain form (rows [0, bnd) / [bnd, nvalid)) or, for tiles
+// spanning more subdomains (parity-test sizes), a walk over segl.
+__device__ __forceinline__ void scratch_column_extrema(const RolloutArgs& a, const float* col, int stride, bool two,
+                                                       int bnd, int nvalid, const int* segl, long long seg0,
+                                                       long long SPH, long long off) {
+  if (two) {
+    float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+#pragma unroll 8
+    for (int r = 0; r < bnd; ++r) {
+      const float v = col[r * stride];
+      mn0 = fminf(mn0, v);
+      mx0 = fmaxf(mx0, v);
+    }
+#pragma unroll 8
+    for (int r = bnd; r < nvalid; ++r) {
+      const float v = col[r * stride];
+      mn1 = fminf(mn1, v);
+      mx1 = fmaxf(mx1, v);
+    }
+    if (bnd > 0) {
+      atomicMin(a.stat_min + seg0 * SPH + off, enc_f(mn0));
+      atomicMax(a.stat_max + seg0 * SPH + off, enc_f(mx0));
+    }
+    if (bnd < nvalid) {
+      atomicMin(a.stat_min + (seg0 + 1) * SPH + off, enc_f(mn1));
+      atomicMax(a.stat_max + (seg0 + 1) * SPH + off, enc_f(mx1));
+    }
+    return;
+  }
+  float mn = INFINITY, mx = -INFINITY;
+  int sg = -1;
+  for (int r = 0; r < nvalid; ++r) {
+    const int s2 = segl[r];
+    if (s2 != sg) {
+      if (sg >= 0) {
+        atomicMin(a.stat_min + (seg0 + sg) * SPH + off, enc_f(mn));
+        atomicMax(a.stat_max + (seg0 + sg) * SPH + off, enc_f(mx));
+      }
+      sg = s2;
+      mn = INFINITY;
+      mx = -INFINITY;
+    }
+    const float v = col[r * stride];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  if (sg >= 0) {
+    atomicMin(a.stat_min + (seg0 + sg) * SPH + off, enc_f(mn));
+    atomicMax(a.stat_max + (seg0 + sg) * SPH + off, enc_f(mx));
+  }
+}
+
+// Column extrema of this warp's 32 rows (v: 32 columns of one row per lane) into the
+// record: lane j handles column c0 + j (< ncols) at record offset off0 + j.
+__device__ __forceinline__ void warp_chunk_extrema(const RolloutArgs& a, const float (&v)[32], bool simple, long long ws0,
+                                                   long long ws1, bool row_ok, long long grow, long long rps,
+                                                   long long SPH, long long off0, int col, int ncols) {
+  if (simple) {
+    float mn, mx;
+    warp_col_extrema<false>(v, true, mn, mx);
+    if (col < ncols) {
+      atomicMin(a.stat_min + ws0 * SPH + off0, enc_f(mn));
+      atomicMax(a.stat_max + ws0 * SPH + off0, enc_f(mx));
+    }
+  } else {
+    for (long long s = ws0; s <= ws1; ++s) {
+      float mn, mx;
+      warp_col_extrema<true>(v, row_ok && grow / rps == s, mn, mx);
+      if (col < ncols) {
+        atomicMin(a.stat_min + s * SPH + off0, enc_f(mn));
+        atomicMax(a.stat_max + s * SPH + off0, enc_f(mx));
+      }
+    }
+  }
+}
+
+// hi / lo parts of one 32-column K-block of this thread's row: hi into TMEM (the
+// tensor core reads its top 19 bits), lo = x - trunc(x) into the row's 128-byte
+// line of the SW128 K-block in shared memory.
+__device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_blk, int row, float (&v)[32]) {
+  tmem_st32(t_hi, v);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
+  float4* line = reinterpret_cast<float4*>(lo_blk + row * 128);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) line[q ^ (row & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+// Publish a written K-block: TMEM stores complete, shared stores visible to the
+// async proxy, then one arrival per warp.
+__device__ __forceinline__ void publish_chunk(uint64_t* bar) {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  fence_proxy_async();
+  fence_before();
+  mbar_arrive_warp(bar);
+}
+
+// Number of N halves of layer l (<= 128 columns per MMA) and the rows of half h.
+__device__ __forceinline__ int n_halves(int npad) { return npad > 128 ? 2 : 1; }
+__device__ __forceinline__ int half_rows(int npad, int h) { return npad > 128 ? (h == 0 ? 128 : npad - 128) : npad; }
+
+template <int NT, int RW_>
+__global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
+  using C = Tc2<NT, RW_>;
+  constexpr int RW = C::RW, KBMAX = C::KBMAX, WPQ = C::WPQ;
+  constexpr uint32_t kTmemCols = 2 * NT * RW;  // a power of two >= 32
+  extern __shared__ unsigned char smraw[];
+  const uint32_t s0 = smem_u32(smraw);
+  const Tc2Smem m = carve2(o, smraw + (((s0 + 1023u) & ~1023u) - s0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long cta_row0 = static_cast<long long>(blockIdx.x) * (128 * NT);
+  const int ks = o.ks, ka = o.ka, kd = o.kd, d = o.d, S = o.tc_S, L = o.L, H = o.H;
+  const long long rps = a.rows_per_sub;
+
+  if (a.failed != nullptr) {  // skip CTAs whose subdomains all failed already
+    const long long last = min(a.n_rows, cta_row0 + 128 * NT) - 1;
+    bool all_failed = true;
+    for (long long s = cta_row0 / rps; s <= last / rps; ++s) all_failed = all_failed && a.failed[s] != 0;
+    if (all_failed) return;
+  }
+
+  for (int i = tid; i < NT * 128; i += C::kThreads) {
+    const long long r = cta_row0 + i;
+    const long long tr0 = cta_row0 + (i / 128) * 128;
+    m.segl[i] = r < a.n_rows ? static_cast<int>(r / rps - tr0 / rps) : -1;
+  }
+  for (int i = tid; i < NT * 128 * S; i += C::kThreads) m.sc[i] = 0.f;
+  for (int i = tid; i < L * RW; i += C::kThreads) {
+    const int l = i / RW, j = i % RW;
+    m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
+  }
+  for (int i = tid; i < o.n_ops; i += C::kThreads) m.ops[i] = to_fwd(o.ops[i]);
+  for (int i = tid; i < 2 * o.n_sc; i += C::kThreads) m.pairs[i] = o.iv[o.sc_list + i];
+  for (int i = tid; i < o.cost_f1 - o.cost_f0; i += C::kThreads) m.cconst[i] = o.f[o.cost_f0 + i];
+  if (tid == 0) {
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(m.full + s, 1);
+      mbar_init(m.empty + s, 1);
+    }
+    for (int i = 0; i < NT; ++i) {
+      mbar_init(m.d_full + 2 * i, 1);
+      mbar_init(m.d_full + 2 * i + 1, 1);
+      for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_chunk + i * KBMAX + c, 4);
+      mbar_init(m.x_full + i, 4 * WPQ);
+      mbar_init(m.x_empty + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *m.tmem_slot;
+  const uint32_t ring_bytes = static_cast<uint32_t>(o.tc2_ring);
+
+  if (warp == C::kProducerWarp) {
+    // ------------------------------------------------ producer: weight blocks, hi then lo
+    if (lane == 0) {
+      uint32_t pos = 0;
+      uint32_t* lo_b = m.ring;  // byte ranges of the in-flight blocks, oldest first
+      uint32_t* hi_b = m.ring + kSlots;
+      int it = 0, head = 0;
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l < L; ++l)
+          for (int i = 0; i < NT; ++i) {
+            const int npad = o.tc_npad[l], nh = n_halves(npad);
+            for (int kb = 0; kb < o.tc_kb[l]; ++kb)
+              for (int h = 0; h < nh; ++h) {
+                const int nr = half_rows(npad, h);
+                const float* src = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32 + (h ? 2 * 128 * 32 : 0);
+                const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
+                for (int part = 0; part < 2; ++part, ++it) {
+                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
+                  while (head < it) {
+                    const int hs = head % kSlots;
+                    if (it - head < kSlots && (hi_b[hs] <= at || lo_b[hs] >= at + bytes)) break;
+                    mbar_wait(m.empty + hs, static_cast<uint32_t>((head / kSlots) & 1), kSleepProducer);
+                    ++head;
+                  }
+                  const int s = it % kSlots;
+                  lo_b[s] = at;
+                  hi_b[s] = at + bytes;
+                  mbar_expect_tx(m.full + s, bytes);
+                  bulk_g2s(m.w + at, src + part * nr * 32, bytes, m.full + s);
+                }
+              }
+          }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ------------------------------------------------ MMA issuer: one thread.  Its
+    // sub-partition is shared with busy epilogue warps, so the issue loop is kept to
+    // a handful of instructions per MMA (tools/mma_rate.cu: ALU-busy neighbours halve
+    // the rate of an issuing warp that spends several instructions per MMA).
+    if (lane == 0) {
+      int it = 0, li = 0;
+      uint32_t pos = 0;
+      uint32_t a_par = 0;  // bit i*KBMAX+kb: phase parity of a_chunk[i][kb]
+      const uint32_t wbase = smem_u32(m.w);
+      const uint32_t abase = smem_u32(m.alo);
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l < L; ++l, ++li)
+          for (int i = 0; i < NT; ++i) {
+            const int npad = o.tc_npad[l], nh = n_halves(npad), ksteps = o.tc_ksteps[l];
+            const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
+            const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
+            long long wfull = 0;  // timeline: cycles waiting for weight blocks
+            for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
+              const int bit = i * KBMAX + kb;
+              if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
+              mbar_wait(m.a_chunk + bit, (a_par >> bit) & 1u);  // this K-block of A written
+              if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
+              a_par ^= 1u << bit;
+              fence_after();
+              const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(bit) * 16384u);
+              const int nq = min(4, ksteps - kb * 4);
+              const uint32_t a0 = areg + 32 * kb;
+              for (int h = 0; h < nh; ++h) {
+                const int nr = half_rows(npad, h);
+                const uint32_t idesc = tf32_idesc(nr);
+                const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
+                const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
+                // hi block: A_hi.B_hi and A_lo.B_hi
+                {
+                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
+                  const int s = it % kSlots;
+                  const long long w0 = tl_clock();
+                  mbar_wait(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
+                  wfull += tl_clock() - w0;
+                  fence_after();
+                  const uint64_t bd = sw128_desc(wbase + at);
+                  mma1_ts(dcol, a0, bd, idesc, kb > 0 ? 1u : 0u);
+                  mma1_ss_acc(dcol, alo_d, bd, idesc);
+                  if (nq > 1) {
+                    mma1_ts_acc(dcol, a0 + 8, bd + 2, idesc);
+                    mma1_ss_acc(dcol, alo_d + 2, bd + 2, idesc);
+                  }
+                  if (nq > 2) {
+                    mma1_ts_acc(dcol, a0 + 16, bd + 4, idesc);
+                    mma1_ss_acc(dcol, alo_d + 4, bd + 4, idesc);
+                  }
+                  if (nq > 3) {
+                    mma1_ts_acc(dcol, a0 + 24, bd + 6, idesc);
+                    mma1_ss_acc(dcol, alo_d + 6, bd + 6, idesc);
+                  }
+                  mma1_commit(m.empty + s);
+                  ++it;
+                }
+                // lo block: A_hi.B_lo
+                {
+                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
+                  const int s = it % kSlots;
+                  const long long w0 = tl_clock();
+                  mbar_wait(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
+                  wfull += tl_clock() - w0;
+                  fence_after();
+                  const uint64_t bd = sw128_desc(wbase + at);
+                  mma1_ts_acc(dcol, a0, bd, idesc);
+                  if (nq > 1) mma1_ts_acc(dcol, a0 + 8, bd + 2, idesc);
+                  if (nq > 2) mma1_ts_acc(dcol, a0 + 16, bd + 4, idesc);
+                  if (nq > 3) mma1_ts_acc(dcol, a0 + 24, bd + 6, idesc);
+                  mma1_commit(m.empty + s);
+                  ++it;
+                }
+              }
+            }
+            mma1_commit(m.d_full + 2 * i + (li & 1));  // accumulator region complete
+            mark2(a, t, 102 + 20 * l + 10 * i);
+            put2(a, t, 300 + 20 * l + 10 * i, wfull + (1ll << 40));
+          }
+    }
+  } else if (warp >= kEpiWarps) {
+    // ------------------------------------------------ cost warp: four rows per thread
+    // (rows lane + 32q); p_t lives in the scratch row (its pcol columns)
+    const int ti = C::cost_tile(warp);
+    const long long row0 = cta_row0 + ti * 128;
+    const long long rem = a.n_rows - row0;
+    const int nvalid = static_cast<int>(rem < 0 ? 0 : rem < 128 ? rem : 128);
+    const long long seg0 = row0 / rps;
+    const long long SPH = static_cast<long long>(o.SP) * H;
+    const bool rec_any = a.stat_min != nullptr;
+    float* sct = m.sc + ti * 128 * S;
+    float* const rows[4] = {sct + lane * S, sct + (lane + 32) * S, sct + (lane + 64) * S, sct + (lane + 96) * S};
+    float cost[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      for (int e = 0; e < kd; ++e) rows[q][o.pcol + e] = o.f[o.p0 + e];
+    const int* segl = m.segl + ti * 128;
+    const int k_first = o.x_stat >= 0 ? ks : 0;  // the x_t columns' extrema come from the epilogue
+    const long long b1 = (seg0 + 1) * rps - row0;
+    const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
+    const bool two = nvalid == 0 || (row0 + nvalid - 1) / rps - seg0 <= 1;
+    for (int t = 0; t < H; ++t) {
+      mbar_wait(m.x_full + ti, static_cast<uint32_t>(t & 1), kSleepCost);  // x_t of the tile's rows in the scratch
+      mark2(a, t, 400 + 10 * ti);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = lane + 32 * q;
+        const float* ur = a.actions + (row0 + r) * d + t * ka;
+        for (int j = 0; j < ka; ++j) {
+          const float u = r < nvalid ? __ldg(ur + j) : 0.f;
+          rows[q][o.ucol + j] = u;
+          if (j < kd) rows[q][o.pcol + j] += u;
+        }
+      }
+      cost_program_n<4>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
+      mark2(a, t, 403 + 10 * ti);
+      if (a.states != nullptr)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (lane + 32 * q < nvalid)
+            for (int j = 0; j < ks; ++j) a.states[((row0 + lane + 32 * q) * H + t) * ks + j] = rows[q][j];
+      if (rec_any) {
+        __syncwarp();
+        for (int k = k_first + lane; k < o.n_sc; k += 32)
+          scratch_column_extrema(a, sct + m.pairs[2 * k], S, two, bnd, nvalid, segl, seg0, SPH,
+                                 t * o.SP + m.pairs[2 * k + 1]);
+      }
+      mark2(a, t, 402 + 10 * ti);
+      mark2(a, t, 401 + 10 * ti);
+      mbar_arrive_warp(m.x_empty + ti);  // scratch of step t consumed
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (lane + 32 * q < nvalid) {
+        const long long r = row0 + lane + 32 * q;
+        a.costs[r] = cost[q];
+        if (a.failed != nullptr && !isfinite(cost[q])) atomicOr(a.failed + r / rps, 1);
+      }
+  } else {
+    // ------------------------------------------------ epilogue warps: layer to layer
+    const int ti = NT == 2 ? warp >> 3 : 0;
+    const int g = warp & 3;
+    const int h = NT == 2 ? (warp >> 2) & 1 : warp >> 2;
+    const int row = 32 * g + lane;
+    const long long row0 = cta_row0 + ti * 128;
+    const long long grow = row0 + row;
+    const bool row_ok = grow < a.n_rows;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(32 * g) << 16) + static_cast<uint32_t>(ti * 2 * RW);
+    unsigned char* alo = m.alo + ti * KBMAX * 16384;
+    float* scrow = m.sc + (ti * 128 + row) * S;
+    const float* urow = row_ok ? a.actions + grow * d : nullptr;
+    // warp's subdomain span (uniform): the common case is one subdomain, all rows valid
+    const long long wr0 = row0 + 32 * g;
+    const long long wr1 = min(wr0 + 31, a.n_rows - 1);
+    const long long ws0 = wr0 / rps, ws1 = wr1 >= wr0 ? wr1 / rps : ws0 - 1;
+    const bool simple = ws0 == ws1 && wr0 + 31 < a.n_rows;
+    const long long SPH = static_cast<long long>(o.SP) * H;
+    const bool x_rec = o.x_stat >= 0 && a.stat_min != nullptr;
+    float pe[8], u_nxt[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      pe[e] = e < kd ? o.f[o.p0 + e] : 0.f;
+      u_nxt[e] = (row_ok && e < ka) ? __ldg(urow + e) : 0.f;  // u_0
+    }
+    // A K-block c of the features concat(x [- tile(p)], u): v holds x in the columns
+    // below ks and zeros above; x - tile(p) in relative mode, then the K-block is
+    // stored with the u_{t+1} columns written by narrow stores over the zeros.
+    auto features_store = [&](int c, float (&v)[32], uint32_t t_hi, unsigned char* lo_blk) {
+      if (o.rel) {
+        int km = (c * 32) % kd;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float pv = pe[0];
+#pragma unroll
+          for (int e = 1; e < 8; ++e) pv = km == e ? pe[e] : pv;
+          if (c * 32 + j < ks) v[j] -= pv;
+          km = km + 1 == kd ? 0 : km + 1;
+        }
+      }
+      store_operand(t_hi, lo_blk, row, v);
+      const int u0 = ks - c * 32;  // column of u_{t+1}[0] inside this K-block (warp-uniform)
+      if (u0 + ka > 0 && u0 < 32) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // the zeros land first
+        float* line = reinterpret_cast<float*>(lo_blk + row * 128);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = u0 + e;
+          if (e < ka && j >= 0 && j < 32) {
+            const float u = u_nxt[e];
+            tmem_st1(t_hi + j, u);
+            line[(((j >> 2) ^ (row & 7)) << 2) + (j & 3)] = u - __uint_as_float(__float_as_uint(u) & 0xffffe000u);
+          }
+        }
+      }
+    };
+    // features of step 0 -> A of layer 0 in region 1
+    for (int c = h; c < o.tc_kb[0]; c += WPQ) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int k = c * 32 + j;
+        v[j] = k < ks ? o.f[o.x0 + min(k, ks - 1)] : 0.f;
+      }
+      features_store(c, v, tl + RW + 32 * c, alo + c * 16384);
+      publish_chunk(m.a_chunk + ti * KBMAX + c);
+    }
+    int li = 0;
+    const bool lead = (warp & 7) == 0;  // first epilogue warp of its tile (timeline)
+    for (int t = 0; t < H; ++t) {
+      if (warp == 0) mark2(a, t, 0);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e < kd && e < ka) pe[e] += u_nxt[e];  // p_t = p_{t-1} + u_t (effector dims: the first kd)
+        u_nxt[e] = (row_ok && e < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + e) : 0.f;  // u_{t+1}
+      }
+      for (int l = 0; l < L; ++l, ++li) {
+        const int npad = o.tc_npad[l];
+        const uint32_t dcol = static_cast<uint32_t>((li & 1) * RW);
+        const bool hidden = l + 1 < L;
+        const float* bias = m.bias + l * RW;
+        const int nch = (npad + 31) / 32;
+        mbar_wait(m.d_full + 2 * ti + (li & 1), static_cast<uint32_t>((li >> 1) & 1), kSleepEpi);
+        fence_after();
+        if (lead) mark2(a, t, 200 + 20 * l + 10 * ti);
+        if (hidden) {
+          const int stat = o.pre_stat[l];
+          const bool rec = o.relu[l] != 0 && stat >= 0 && a.stat_min != nullptr;
+          const bool relu = o.relu[l] != 0;
+          const int N = o.widths[l + 1];
+          for (int c = h; c < nch; c += WPQ) {
+            float v[32];
+            if (npad - c * 32 >= 32)
+              tmem_ld32(tl + dcol + 32 * c, v);
+            else
+              tmem_ld16(tl + dcol + 32 * c, v);
+            const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 bb = b4[q];
+              v[4 * q] += bb.x;
+              v[4 * q + 1] += bb.y;
+              v[4 * q + 2] += bb.z;
+              v[4 * q + 3] += bb.w;
+            }
+            {  // A of layer l+1 first (in place), so its MMAs start before the extrema work
+              float w[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = relu ? fmaxf(v[j], 0.f) : v[j];
+              store_operand(tl + dcol + 32 * c, alo + c * 16384, row, w);
+              publish_chunk(m.a_chunk + ti * KBMAX + c);
+            }
+            if (rec) {
+              const int col = c * 32 + lane;
+              warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                                 static_cast<long long>(t) * o.SP + stat + col, col, N);
+            }
+          }
+        } else {
+          // output layer: x_t -> the cost warps' scratch; features of step t+1 -> A in place
+          const int nf = t + 1 < H ? o.tc_kb[0] : 0;
+          const int ncx = max(nch, nf);
+          if (h * 32 < ks && t >= 1) mbar_wait(m.x_empty + ti, static_cast<uint32_t>((t - 1) & 1), kSleepEpi);
+          for (int c = h; c < ncx; c += WPQ) {
+            float v[32];
+            if (c < nch) {
+              if (npad - c * 32 >= 32)
+                tmem_ld32(tl + dcol + 32 * c, v);
+              else
+                tmem_ld16(tl + dcol + 32 * c, v);
+              const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 bb = b4[q];
+                v[4 * q] += bb.x;
+                v[4 * q + 1] += bb.y;
+                v[4 * q + 2] += bb.z;
+                v[4 * q + 3] += bb.w;
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c * 32 + j < ks) scrow[c * 32 + j] = v[j];
+              if (x_rec && c * 32 < ks)  // x_t extrema here; the cost warp skips the x columns
+                warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                                   static_cast<long long>(t) * o.SP + o.x_stat + c * 32 + lane, c * 32 + lane, ks);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            if (c < nf) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c * 32 + j >= ks) v[j] = 0.f;
+              features_store(c, v, tl + dcol + 32 * c, alo + c * 16384);
+              publish_chunk(m.a_chunk + ti * KBMAX + c);
+            }
+          }
+          mbar_arrive_warp(m.x_full + ti);  // this warp's x_t columns written
+        }
+        if (lead) mark2(a, t, 201 + 20 * l + 10 * ti);
+      }
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+}  // namespace
+
+size_t rollout_tc2_fixed_smem(const DevObjective& o) { return tc2_fixed_bytes(o); }
+size_t rollout_tc2_smem(const DevObjective& o) { return 1024 + carve2(o, nullptr).bytes; }
+
+cudaError_t launch_rollout_tc2(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
+  const size_t smem = rollout_tc2_smem(o);
+  const int nt = o.tc2;
+  const long long rows_per_cta = 128LL * nt;
+  const long long grid = (a.n_rows + rows_per_cta - 1) / rows_per_cta;
+  if (grid <= 0) return cudaSuccess;
+  auto go = [&](auto kern, int threads) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(o, a);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (nt == 2 && o.tc2_rw == 128)
+    e = go(rollout_tc2_kernel<2, 128>, Tc2<2, 128>::kThreads);
+  else if (nt == 1 && o.tc2_rw == 128)
+    e = go(rollout_tc2_kernel<1, 128>, Tc2<1, 128>::kThreads);
+  else if (nt == 1 && o.tc2_rw == 256)
+    e = go(rollout_tc2_kernel<1, 256>, Tc2<1, 256>::kThreads);
+  else
+    return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace bp

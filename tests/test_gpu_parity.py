@@ -88,6 +88,63 @@ def test_rollout_costs_and_extrema_match_oracle(device, name):
         assert rel_err(elo[s][seen], rlo[seen]) < tol and rel_err(ehi[s][seen], rhi[seen]) < tol, name
 
 
+KERNEL_CASES = [("c1", 2), ("c2", 2), ("c4", 1), ("ref-obstacles", 2), ("ref-linear", 2), ("c3", 1)]
+
+
+@pytest.mark.parametrize("name,tiles", KERNEL_CASES)
+@pytest.mark.parametrize("shape", [(3, 37), (2, 300), (1, 700)])
+def test_tcgen05_v2_matches_oracle(device, name, tiles, shape):
+    """rollout_tc2.cu (two ping-pong tiles per CTA at widths <= 128, one 256-wide tile
+    for C3) against the FP64 oracle: subdomains straddling warps and tiles (37 rows),
+    a CTA with one live tile (300 rows), several CTAs (700 rows)."""
+    spec = small_spec(name)
+    dev = device.load(spec)
+    # the default for widths in (128, 256]; selectable wherever every width <= 256
+    assert dev.rollout_kernel() == "tc2" if name in ("c3", "c4") else "tc1"  # C4: v1's smem does not fit
+    assert dev.rollout_path("tc2") == "tcgen05" and dev.rollout_kernel() == "tc2"
+    assert dev.rollout_tiles() == tiles  # C4's wide cost scratch leaves room for one tile
+    n_sub, rows = shape
+    if name == "c3":
+        rows = min(rows, 140)  # the FP64 oracle is slow at width 256
+    lo, hi = spec.box()
+    acts = np.random.default_rng(11).uniform(lo, hi, size=(n_sub, rows, spec.d)).astype(np.float32)
+    costs, states, elo, ehi, bad = dev.rollout(acts, want_states=True)
+    assert not bad.any()
+    ob = orc.Objective(spec)
+    layout = dev.stat_layout()
+    for s in range(n_sub):
+        st = orc.Stats()
+        ref = ob.evaluate(acts[s].astype(np.float64), st)
+        assert rel_err(costs[s], ref) < RTOL_TC, name
+        rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
+        seen = ~np.isnan(rlo)
+        assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
+    # the v2 kernel and the SIMT FP32 kernel see the same rollouts
+    dev.rollout_path("simt")
+    c_s, st_s, lo_s, hi_s, _ = dev.rollout(acts, want_states=True)
+    dev.rollout_path("auto")
+    assert rel_err(costs, c_s) < RTOL_TC and rel_err(states, st_s) < RTOL_TC
+    assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "ref-obstacles"])
+def test_tcgen05_v1_still_matches_oracle(device, name):
+    """The v1 kernel (rollout_tc.cu) stays selectable (BP_ROLLOUT=tc1) and parity-green."""
+    spec = small_spec(name)
+    dev = device.load(spec)
+    assert dev.rollout_path("tc1") == "tcgen05" and dev.rollout_kernel() == "tc1"
+    lo, hi = spec.box()
+    acts = np.random.default_rng(12).uniform(lo, hi, size=(2, 300, spec.d)).astype(np.float32)
+    costs, _, elo, ehi, _ = dev.rollout(acts)
+    dev.rollout_path("auto")
+    c2, _, lo2, hi2, _ = dev.rollout(acts)
+    ob = orc.Objective(spec)
+    for s in range(2):
+        ref = ob.evaluate(acts[s].astype(np.float64))
+        assert rel_err(costs[s], ref) < RTOL_TC
+    assert rel_err(costs, c2) < RTOL_TC and rel_err(elo, lo2) < RTOL_TC and rel_err(ehi, hi2) < RTOL_TC
+
+
 def test_rollout_rows_are_batch_invariant(device):
     spec = small_spec("c2")
     dev = device.load(spec)

@@ -33,6 +33,17 @@ __device__ __forceinline__ void issue(uint32_t d, uint32_t ta, uint64_t da, uint
                  ::"r"(d), "l"(da), "l"(db), "r"(id));
 }
 
+// V 3: TS and SS tf32 alternating (the 3xTF32 hi.hi / lo.hi pattern with lo in smem)
+// V 4: TS, SS, TS per step (hi.hi, lo.hi, hi.lo)
+template <int V>
+__device__ __forceinline__ void issue_mix(int i, uint32_t d, uint32_t ta, uint64_t da, uint64_t db, uint32_t id) {
+  if constexpr (V == 3) {
+    if (i & 1) issue<1>(d, ta, da, db, id); else issue<0>(d, ta, da, db, id);
+  } else {
+    if (i % 3 == 1) issue<1>(d, ta, da, db, id); else issue<0>(d, ta, da, db, id);
+  }
+}
+
 __device__ volatile int g_stop;
 
 // V: 0 TS tf32, 1 SS tf32, 2 SS bf16.  N: MMA N.  I: interference from warps 1-3 while
@@ -107,10 +118,15 @@ __global__ void rate(int n_mma, long long* out) {
     if (acc == 12345.f) out[1] = 1;
   }
   if (threadIdx.x == 0) {
-    const uint32_t id = idesc(V == 2 ? 1 : 2, N);
+    const uint32_t id = idesc(V == 2 ? 1 : 2, N);  // V 3, 4: tf32
     const uint64_t da = sw128(su32(sm)), db = sw128(su32(sm + 32768));
     const long long t0 = clock64();
-    for (int i = 0; i < n_mma; ++i) issue<V>(tm, tm + 256, da + 2 * (i & 3), db + 2 * (i & 3), id);
+    for (int i = 0; i < n_mma; ++i) {
+      if constexpr (V >= 3)
+        issue_mix<V>(i, tm, tm + 256, da + 2 * (i & 3), db + 2 * (i & 3), id);
+      else
+        issue<V>(tm, tm + 256, da + 2 * (i & 3), db + 2 * (i & 3), id);
+    }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
     uint32_t done = 0;
     while (!done)
@@ -145,6 +161,10 @@ void run(const char* name, int grid) {
 }
 
 int main() {
+  run<3, 128>("TS/SS alt N128", 148);
+  run<4, 128>("TS,SS,TS N128", 148);
+  run<3, 128, 3>("TS/SS alt +STS", 148);
+  run<1, 128, 3>("SS N128 +STS", 148);
   run<0, 128, 5>("TS N128 +ALU15", 148);
   run<1, 128, 5>("SS N128 +ALU15", 148);
   run<0, 128, 6>("TS N128 +ALU12 other SPs", 148);
