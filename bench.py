@@ -220,21 +220,29 @@ def main():
     flop = children / world * rows * iters * H * wl.flops_per_sample_step  # this rank's share
     achieved = flop / (tm["rollout_ms"] / 1e3) / 1e12 if tm["rollout_ms"] > 0 else None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "rollout_tc_ncu_summary.json" if path == "tcgen05" else "rollout_ncu_summary.json")
-    if os.path.exists(tp):
+    kern = dev.rollout_kernel()  # "tc1" (rollout_tc.cu), "tc2" (rollout_tc2.cu) or "simt" (rollout.cu)
+    info = dev.rollout_info()
+    # DRAM bytes per launch from the committed ncu --set full capture of this kernel on this workload
+    tp = os.path.join(ROOT, "profiles", {"tc1": "rollout_tc_ncu_summary.json", "simt": "rollout_ncu_summary.json",
+                                         "tc2": f"rollout_tc2_{args.config}_ncu_summary.json"}[kern])
+    if os.path.exists(tp) and (kern == "tc2" or args.config == "c2"):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    kname = {"tc1": "rollout_tc_kernel (K1 v1, rollout_tc.cu: tcgen05 kind::tf32, 3xTF32, one 128-row tile per CTA)",
+             "tc2": f"rollout_tc2_kernel<{info['tiles_per_cta']},{256 if info['tiles_per_cta'] == 1 and max(wl.spec.widths) > 128 else 128}> "
+                    "(K1 v2, rollout_tc2.cu: tcgen05 kind::tf32, 3xTF32, in-place TMEM regions)",
+             "simt": "rollout_kernel (K1, rollout.cu: SIMT FFMA)"}[kern]
     if path == "tcgen05":
         # 3xTF32: three dense kind::tf32 MMAs per FP32 product, so the ceiling for the
         # algorithmic (FP32) FLOP rate is the TF32 tensor peak / 3.
         roof = {"bound": "tensor", "achieved": achieved, "peak": TF32_DENSE_TFLOPS / 3.0, "unit": "TFLOP/s",
-                "kernel": "rollout_tc_kernel (K1, tcgen05 kind::tf32, 3xTF32)",
+                "kernel": kname,
                 "peak_source": "B200_PROFILING.md fallback: dense TF32 1100 TFLOP/s (MEASURED_PEAKS.json has no TF32 "
                                "entry) / 3 MMAs per FP32 product",
                 "peak_measured_live": (peak_tf32 / 3.0) if peak_tf32 else None,
                 "tensor_tflops_executed": 3.0 * achieved if achieved else None}
     else:
         roof = {"bound": "fp32", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
-                "kernel": "rollout_kernel (K1, SIMT FFMA)",
+                "kernel": kname,
                 "peak_source": "bp_measure_fp32_peak: FFMA microbenchmark run live in this process "
                                "(MEASURED_PEAKS.json has no FP32 SIMT entry)"}
     roof["frac"] = (roof["achieved"] / roof["peak"]) if (roof["achieved"] and roof["peak"]) else None

@@ -21,9 +21,12 @@
 //  * Weight blocks stream as separate hi and lo entries ([rows][128 B] each), so
 //    more of them are in flight in a smaller ring.
 //
-// Precision (unchanged from v1): D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, hi read as
-// the top 19 bits of the FP32 value, lo = x - trunc(x) exact; ~2^-21 relative per
-// product.  The tests state 5e-5 relative for the tensor-core path.
+// Precision (as v1): 3xTF32, D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, hi read as the top
+// 19 bits of the FP32 value, lo = x - trunc(x) exact; ~2^-21 relative per product.  The
+// tests state 5e-5 relative for the tensor-core path.
+// Issue order (tools/mma_rate.cu): per K-block the A_hi.B_hi / A_lo.B_hi pairs strictly
+// alternate TS/SS, then the A_hi.B_lo run; a 4xTF32 order with strict alternation runs
+// each MMA faster but costs more in total (measured on C3: 142 vs 159 TFLOP/s).
 //
 // Warps (W = 16 epilogue warps; warp w can reach TMEM lanes 32*(w%4)..+31):
 //   0-15   epilogue.  NT=2: tile w/8, chunks c = (w%8)/4 (mod 2);  NT=1: chunks
@@ -274,9 +277,15 @@ __device__ __forceinline__ void warp_chunk_extrema(const RolloutArgs& a, const f
 // tensor core reads its top 19 bits), lo = x - trunc(x) into the row's 128-byte
 // line of the SW128 K-block in shared memory.
 __device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_blk, int row, float (&v)[32]) {
+#ifndef BP_EXP_NOTMEM
   tmem_st32(t_hi, v);
+#endif
 #pragma unroll
+#ifdef BP_EXP_NOLO
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(__float_as_uint(v[j]) & 0x80001fffu);
+#else
   for (int j = 0; j < 32; ++j) v[j] = v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
+#endif
   float4* line = reinterpret_cast<float4*>(lo_blk + row * 128);
 #pragma unroll
   for (int q = 0; q < 8; ++q) line[q ^ (row & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -364,8 +373,8 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
         for (int l = 0; l < L; ++l)
           for (int i = 0; i < NT; ++i) {
             const int npad = o.tc_npad[l], nh = n_halves(npad);
-            for (int kb = 0; kb < o.tc_kb[l]; ++kb)
-              for (int h = 0; h < nh; ++h) {
+            for (int h = 0; h < nh; ++h)  // N half outer: one accumulator address per pass
+              for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
                 const int nr = half_rows(npad, h);
                 const float* src = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32 + (h ? 2 * 128 * 32 : 0);
                 const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
@@ -380,6 +389,12 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
                   const int s = it % kSlots;
                   lo_b[s] = at;
                   hi_b[s] = at + bytes;
+#ifdef BP_EXP_NOSTREAM
+                  if (it >= 2 * kSlots) {
+                    mbar_arrive(m.full + s);
+                    continue;
+                  }
+#endif
                   mbar_expect_tx(m.full + s, bytes);
                   bulk_g2s(m.w + at, src + part * nr * 32, bytes, m.full + s);
                 }
@@ -387,87 +402,70 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
           }
     }
   } else if (warp == C::kMmaWarp) {
-    // ------------------------------------------------ MMA issuer: one thread.  Its
-    // sub-partition is shared with busy epilogue warps, so the issue loop is kept to
-    // a handful of instructions per MMA (tools/mma_rate.cu: ALU-busy neighbours halve
-    // the rate of an issuing warp that spends several instructions per MMA).
-    if (lane == 0) {
-      int it = 0, li = 0;
-      uint32_t pos = 0;
-      uint32_t a_par = 0;  // bit i*KBMAX+kb: phase parity of a_chunk[i][kb]
-      const uint32_t wbase = smem_u32(m.w);
-      const uint32_t abase = smem_u32(m.alo);
-      for (int t = 0; t < H; ++t)
-        for (int l = 0; l < L; ++l, ++li)
-          for (int i = 0; i < NT; ++i) {
-            const int npad = o.tc_npad[l], nh = n_halves(npad), ksteps = o.tc_ksteps[l];
-            const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
-            const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
-            long long wfull = 0;  // timeline: cycles waiting for weight blocks
+    // ------------------------------------------------ MMA issuer: the whole warp runs the
+    // uniform loop and waits; elect.sync inside the asm picks the issuing lane
+    // (tools/mma_rate.cu: a diverged single issuing thread halves the tensor rate).
+    int it = 0, li = 0;
+    uint32_t pos = 0;
+    uint32_t a_par = 0;  // bit i*KBMAX+kb: phase parity of a_chunk[i][kb]
+    const uint32_t wbase = smem_u32(m.w);
+    const uint32_t abase = smem_u32(m.alo);
+    for (int t = 0; t < H; ++t)
+      for (int l = 0; l < L; ++l, ++li)
+        for (int i = 0; i < NT; ++i) {
+          const int npad = o.tc_npad[l], nh = n_halves(npad), ksteps = o.tc_ksteps[l];
+          const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
+          const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
+          long long wfull = 0;  // timeline: cycles waiting for weight blocks
+          for (int h = 0; h < nh; ++h) {  // N half outer: the accumulator address stays put
+            const int nr = half_rows(npad, h);
+            const uint32_t idesc = tf32_idesc(nr);
+            const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
+            const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
             for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
               const int bit = i * KBMAX + kb;
-              if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
-              mbar_wait(m.a_chunk + bit, (a_par >> bit) & 1u);  // this K-block of A written
-              if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
-              a_par ^= 1u << bit;
-              fence_after();
+              if (h == 0) {  // first pass: this K-block of A written by the epilogue
+                if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
+                mbar_wait_warp(m.a_chunk + bit, (a_par >> bit) & 1u);
+                if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
+                a_par ^= 1u << bit;
+                fence_after();
+              }
               const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(bit) * 16384u);
               const int nq = min(4, ksteps - kb * 4);
               const uint32_t a0 = areg + 32 * kb;
-              for (int h = 0; h < nh; ++h) {
-                const int nr = half_rows(npad, h);
-                const uint32_t idesc = tf32_idesc(nr);
-                const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
-                const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
-                // hi block: A_hi.B_hi and A_lo.B_hi
-                {
-                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
-                  const int s = it % kSlots;
-                  const long long w0 = tl_clock();
-                  mbar_wait(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
-                  wfull += tl_clock() - w0;
-                  fence_after();
-                  const uint64_t bd = sw128_desc(wbase + at);
-                  mma1_ts(dcol, a0, bd, idesc, kb > 0 ? 1u : 0u);
-                  mma1_ss_acc(dcol, alo_d, bd, idesc);
-                  if (nq > 1) {
-                    mma1_ts_acc(dcol, a0 + 8, bd + 2, idesc);
-                    mma1_ss_acc(dcol, alo_d + 2, bd + 2, idesc);
-                  }
-                  if (nq > 2) {
-                    mma1_ts_acc(dcol, a0 + 16, bd + 4, idesc);
-                    mma1_ss_acc(dcol, alo_d + 4, bd + 4, idesc);
-                  }
-                  if (nq > 3) {
-                    mma1_ts_acc(dcol, a0 + 24, bd + 6, idesc);
-                    mma1_ss_acc(dcol, alo_d + 6, bd + 6, idesc);
-                  }
-                  mma1_commit(m.empty + s);
-                  ++it;
-                }
-                // lo block: A_hi.B_lo
-                {
-                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
-                  const int s = it % kSlots;
-                  const long long w0 = tl_clock();
-                  mbar_wait(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
-                  wfull += tl_clock() - w0;
-                  fence_after();
-                  const uint64_t bd = sw128_desc(wbase + at);
-                  mma1_ts_acc(dcol, a0, bd, idesc);
-                  if (nq > 1) mma1_ts_acc(dcol, a0 + 8, bd + 2, idesc);
-                  if (nq > 2) mma1_ts_acc(dcol, a0 + 16, bd + 4, idesc);
-                  if (nq > 3) mma1_ts_acc(dcol, a0 + 24, bd + 6, idesc);
-                  mma1_commit(m.empty + s);
-                  ++it;
-                }
+              // hi block: A_hi.B_hi and A_lo.B_hi as strictly alternating TS/SS pairs
+              {
+                const uint32_t at = ring_place(pos, bytes, ring_bytes);
+                const int s = it % kSlots;
+                const long long w0 = tl_clock();
+                mbar_wait_warp(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
+                wfull += tl_clock() - w0;
+                if (l == 1 && i == 0) mark2(a, t, 600 + 2 * (h * 8 + kb));
+                const uint64_t bd = sw128_desc(wbase + at);
+                for (int q = 0; q < nq; ++q)
+                  mma_pair_elect(dcol, a0 + 8 * q, alo_d + 2 * q, bd + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
+                mma_commit_elect(m.empty + s);
+                ++it;
+              }
+              // lo block: A_hi.B_lo
+              {
+                const uint32_t at = ring_place(pos, bytes, ring_bytes);
+                const int s = it % kSlots;
+                const long long w0 = tl_clock();
+                mbar_wait_warp(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
+                wfull += tl_clock() - w0;
+                const uint64_t bd = sw128_desc(wbase + at);
+                for (int q = 0; q < nq; ++q) mma_ts(dcol, a0 + 8 * q, bd + 2 * q, idesc, 1u);
+                mma_commit_elect(m.empty + s);
+                ++it;
               }
             }
-            mma1_commit(m.d_full + 2 * i + (li & 1));  // accumulator region complete
-            mark2(a, t, 102 + 20 * l + 10 * i);
-            put2(a, t, 300 + 20 * l + 10 * i, wfull + (1ll << 40));
           }
-    }
+          mma_commit_elect(m.d_full + 2 * i + (li & 1));  // accumulator region complete
+          mark2(a, t, 102 + 20 * l + 10 * i);
+          put2(a, t, 300 + 20 * l + 10 * i, wfull + (1ll << 40));
+        }
   } else if (warp >= kEpiWarps) {
     // ------------------------------------------------ cost warp: four rows per thread
     // (rows lane + 32q); p_t lives in the scratch row (its pcol columns)
@@ -619,10 +617,16 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
           const int N = o.widths[l + 1];
           for (int c = h; c < nch; c += WPQ) {
             float v[32];
+#ifdef BP_EXP_NOTMEM
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.001f * (j + c);
+#else
             if (npad - c * 32 >= 32)
               tmem_ld32(tl + dcol + 32 * c, v);
             else
               tmem_ld16(tl + dcol + 32 * c, v);
+#endif
+#ifndef BP_EXP_NOBIAS
             const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -632,6 +636,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
               v[4 * q + 2] += bb.z;
               v[4 * q + 3] += bb.w;
             }
+#endif
             {  // A of layer l+1 first (in place), so its MMAs start before the extrema work
               float w[32];
 #pragma unroll

@@ -131,6 +131,48 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
 
+// Warp-converged forms for the MMA warp: every lane runs them, elect.sync picks the
+// issuing lane inside the asm (tools/mma_rate.cu: MMAs issued from a diverged single
+// thread lose ~half the tensor rate around any wait; from a converged warp none).
+// A_hi.B (A in TMEM) then A_lo.B (A in shared memory), same B and accumulator.
+__device__ __forceinline__ void mma_pair_elect(uint32_t d, uint32_t a_tmem, uint64_t a_lo, uint64_t b, uint32_t idesc,
+                                               uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %4, one;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(a_lo), "l"(b), "r"(idesc), "r"(accum));
+}
+// One k-step of 4xTF32 in the only mixed order the tensor pipe runs at full rate
+// (tools/mma_rate.cu: strict TS/SS alternation; 2 TS : 1 SS orders run at ~half rate):
+// A_hi.B_hi (TS), A_lo.B_hi (SS), A_hi.B_lo (TS), A_lo.B_lo (SS).
+__device__ __forceinline__ void mma_quad_elect(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                               uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %5, one;\n\t}\n" ::"r"(d),
+      "r"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accum));
+}
+// Whole-warp wait in one asm loop (no per-iteration bookkeeping).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(0x989680u)
+      : "memory");
+}
+
 // Single-thread forms (the caller is the one issuing thread).
 __device__ __forceinline__ void mma1_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t accum) {
   asm volatile(

@@ -49,14 +49,20 @@ __device__ volatile int g_stop;
 // V: 0 TS tf32, 1 SS tf32, 2 SS bf16.  N: MMA N.  I: interference from warps 1-3 while
 // the MMAs run (0 none, 1 LDS.128 stream, 2 tcgen05.ld x32 stream, 3 STS.128 stream,
 // 4 tcgen05.st x32 stream).
-template <int V, int N, int I = 0>
+__device__ float g_src[65536];
+
+template <int V, int N, int I = 0, int NI = 3>
 __global__ void rate(int n_mma, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, xbar, ybar;
+  __shared__ int flag;
+  if (threadIdx.x == 0) flag = 7;
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < 96 * 1024; i += blockDim.x) sm[i] = static_cast<unsigned char>((i * 2654435761u) >> 24) & 0x3f;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(su32(&xbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&ybar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (threadIdx.x < 32) {
@@ -70,7 +76,36 @@ __global__ void rate(int n_mma, long long* out) {
   __shared__ volatile int stop;
   if (threadIdx.x == 0) stop = 0;
   __syncthreads();
-  if (I != 0 && threadIdx.x >= 32 && !(I == 6 && (threadIdx.x >> 5) % 4 == 0)) {
+  __shared__ uint64_t cbar[2];
+  if (I == 11 && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  if (I == 11) {
+    if (threadIdx.x == 32) {
+      uint32_t ph[2] = {0, 0};
+      int k = 0;
+      for (int it = 0; !stop && it < 100000; ++it, k ^= 1) {
+        if (it >= 2) {
+          uint32_t done = 0;
+          while (!done)
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&cbar[k])), "r"(ph[k]));
+          ph[k] ^= 1;
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&cbar[k])), "r"(16384));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(sm + 65536 + 16384 * k)), "l"(g_src + 4096 * (it & 7)), "r"(16384), "r"(su32(&cbar[k])));
+      }
+    }
+  }
+  const bool only_sp0 = I >= 7;
+  const int wq = threadIdx.x >> 5;
+  const bool interferer = I != 0 && I != 11 && threadIdx.x >= 32 && !(I == 6 && wq % 4 == 0) &&
+                          (!only_sp0 || (wq % 4 == 0 && wq / 4 <= NI));
+  if (interferer) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float acc = 0.f;
     float4* region = reinterpret_cast<float4*>(sm + 65536);
@@ -94,7 +129,32 @@ __global__ void rate(int n_mma, long long* out) {
               : "r"(tm + 384 + ((32u * w) << 16)));
           asm volatile("tcgen05.wait::ld.sync.aligned;");
           acc += __uint_as_float(x[r & 31]);
-        } else if constexpr (I == 5 || I == 6) {
+        } else if constexpr (I == 8) {  // FMNMX / FSEL chains
+          float b0 = acc, b1 = acc + 1.f, b2 = acc + 2.f, b3 = acc + 3.f;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            b0 = fminf(b1, b0 + 0.5f);
+            b1 = fmaxf(b2, b1 - 0.25f);
+            b2 = (lane & q) ? b3 : b2 * 0.5f;
+            b3 = fminf(b3, b0);
+          }
+          acc = b0 + b1 + b2 + b3;
+        } else if constexpr (I == 9) {  // shuffle butterfly
+          float b0 = acc;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) b0 = fminf(b0, __shfl_xor_sync(0xffffffffu, b0, 1 << (q & 4)));
+          acc += b0;
+        } else if constexpr (I == 10) {  // integer ALU
+          uint32_t x0 = __float_as_uint(acc), x1 = x0 + 7, x2 = x0 ^ 0x55, x3 = x0 * 3;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            x0 = (x0 ^ x1) + q;
+            x1 = (x1 & x2) | x3;
+            x2 = x2 + (x3 >> 1);
+            x3 = x3 ^ (x0 << 2);
+          }
+          acc += __uint_as_float((x0 ^ x1 ^ x2 ^ x3) & 0x3fffffff);
+        } else if constexpr (I == 5 || I == 6 || I == 7) {
           float b0 = acc, b1 = acc + 1.f, b2 = acc + 2.f, b3 = acc + 3.f;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
@@ -117,12 +177,180 @@ __global__ void rate(int n_mma, long long* out) {
     }
     if (acc == 12345.f) out[1] = 1;
   }
-  if (threadIdx.x == 0) {
-    const uint32_t id = idesc(V == 2 ? 1 : 2, N);  // V 3, 4: tf32
+  if (V >= 19 && threadIdx.x < 32) {
+    const int ln = threadIdx.x;
+    const uint32_t id = idesc(2, N);
     const uint64_t da = sw128(su32(sm)), db = sw128(su32(sm + 32768));
     const long long t0 = clock64();
     for (int i = 0; i < n_mma; ++i) {
-      if constexpr (V >= 3)
+      const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
+      const uint64_t aa = da + 2 * (i & 3) + 256 * ((i >> 2) & 3);
+      if (V == 33) {  // 4xTF32 per k-step: TS(hi,Bhi) SS(lo,Bhi) TS(hi,Blo) SS(lo,Blo); commit every 16
+        const int j = i % 16;
+        const int q = j >> 2, p = j & 3;
+        const uint64_t bq = db + 2 * q + 1024 * ((i / 16) & 1) + (p >= 2 ? 512 : 0);
+        if (p & 1)
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm), "l"(da + 2 * q), "l"(bq), "r"(id));
+        else
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm), "r"(tm + 256 + 8 * q), "l"(bq), "r"(id));
+        if (j == 15) {
+          asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+          asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t@!P1 bra WAIT_%=;\n\t}"
+                       ::"r"(su32(&ybar)), "r"(1u), "r"(0x989680u) : "memory");
+        }
+        continue;
+      }
+      if (V == 29 || V == 30 || V == 31 || V == 32) {  // 29: pure TS, A walks 8q, B walks; 30: per k-step TS(hi.hi), SS(lo.hi), TS(hi.lo)
+        const int j = i % 12;
+        const int q = (V == 29 || V >= 31) ? (j & 3) : j / 3;
+        const uint64_t bq = db + 2 * q + 1024 * ((i / 12) & 1) + (V >= 31 && (j >> 2) == 1 ? 512 : 0);
+        const bool ss = (V == 30 && (j % 3) == 1) || (V == 31 && j >= 8) || (V == 32 && j < 4);
+        if (ss)
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm), "l"(da + 2 * q), "l"(bq), "r"(id));
+        else
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm), "r"(tm + 256 + 8 * q), "l"(bq), "r"(id));
+        if (j == 11)
+          asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+        continue;
+      }
+      if (V >= 23 && V <= 28) {  // the v2 kernel pattern: 12 MMAs = 4 x (TS, SS) + 4 x TS, commit+wait after 8 and 12
+        const int j = i % 12;
+        const int q = j < 8 ? (j >> 1) : j - 8;
+        const uint64_t bq = db + 2 * q + 1024 * ((i / 12) & 1);
+        if ((V == 28 ? true : j < 8) && (j & 1))
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm), "l"(da + 2 * q), "l"(bq), "r"(id));
+        else
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm),
+                       "r"(tm + 256 + (V == 25 ? 0 : V == 26 ? 32 * q : 8 * q)), "l"(bq), "r"(id));
+        if ((j == 7 || j == 11) && V != 27) {
+          asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+          if (V == 23)
+            asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t@!P1 bra WAIT_%=;\n\t}"
+                         ::"r"(su32(&ybar)), "r"(1u), "r"(0x989680u) : "memory");
+        }
+        continue;
+      }
+      if (V >= 21) {  // elected lane inside the asm, the whole warp converged (v1 style)
+        if (i & 1)
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm), "l"(aa), "l"(b), "r"(id));
+        else
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm), "r"(tm + 256), "l"(b), "r"(id));
+        if (V >= 21 && i % 12 == 11) {
+          uint32_t done = 0;
+          if (V == 21)
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u), "r"(0x989680u));
+          else
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u));
+          if (!done) out[2] = 1;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+        }
+        continue;
+      }
+      if (ln == 0) {
+        if (i & 1) issue<1>(tm, tm + 256, aa, b, id); else issue<0>(tm, tm + 256, aa, b, id);
+      }
+      if (i % 12 == 11) {
+        uint32_t done = 0;
+        if (ln == 1) {
+          if constexpr (V == 19)
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u));
+          else
+            asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(done) : "r"(su32(&flag)));
+        }
+        done = __shfl_sync(0xffffffffu, done, 1);
+        if (!done) out[2] = 1;
+        if (ln == 0) {
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&xbar)));
+        }
+      }
+    }
+    if (ln == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+      uint32_t dn = 0;
+      while (!dn)
+        asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                     : "=r"(dn) : "r"(su32(&bar)));
+      const long long t1 = clock64();
+      if (blockIdx.x == 0) out[0] = t1 - t0;
+      stop = 1;
+    }
+  } else if (V < 19 && threadIdx.x == 0) {
+    const uint32_t id = idesc(V == 2 ? 1 : 2, N);  // V 3..6: tf32
+    const uint64_t da = sw128(su32(sm)), db = sw128(su32(sm + 32768));
+    const long long t0 = clock64();
+    for (int i = 0; i < n_mma; ++i) {
+      if constexpr (V >= 7) {
+        const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
+        const uint64_t aa = da + 2 * (i & 3) + 256 * ((i >> 2) & 3);
+        if (i & 1) issue<1>(tm, tm + 256, aa, b, id); else issue<0>(tm, tm + 256, aa, b, id);
+        constexpr int P = (V == 13) ? 24 : 12;
+        if (i % P == P - 1) {
+          // V 7 commit, 8 fence, 9 try_wait, 10 test_wait, 11 commit+try_wait, 12 all three, 13 all three per 24
+          if constexpr (V == 7 || V == 11 || V == 12 || V == 13)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&xbar)));
+          if constexpr (V == 9 || V == 11 || V == 12 || V == 13) {
+            uint32_t done = 0;
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u));
+            if (!done) out[2] = 1;
+          }
+          if constexpr (V == 14 || V == 15) {
+            uint32_t done = 0;
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u));
+            if (!done) out[2] = 1;
+          }
+          if constexpr (V == 15) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&xbar)));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          if constexpr (V == 16) {
+            int f;
+            asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(f) : "r"(su32(&flag)));
+            if (f != 7) out[2] = 1;
+          }
+          if constexpr (V == 17) {
+            int f;
+            asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(f) : "r"(su32(&flag)));
+            if (f != 7) out[2] = 1;
+          }
+          if constexpr (V == 18) {
+            int f;
+            asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(f) : "r"(su32(&flag)));
+            if (f != 7) out[2] = 1;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&xbar)));
+          }
+          if constexpr (V == 10) {
+            uint32_t done = 0;
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                         : "=r"(done) : "r"(su32(&ybar)), "r"(1u));
+            if (!done) out[2] = 1;
+          }
+          if constexpr (V == 8 || V == 12 || V == 13) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+      } else if constexpr (V >= 5) {  // fresh operands: B walks 8 K-blocks of 4 KB... (32 KB), A 4 blocks (16 KB)
+        const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
+        const uint64_t aa = da + 2 * (i & 3) + 256 * ((i >> 2) & 3);
+        if (V == 5 || (i & 1)) issue<1>(tm, tm + 256, aa, b, id); else issue<0>(tm, tm + 256, aa, b, id);
+      } else if constexpr (V >= 3)
         issue_mix<V>(i, tm, tm + 256, da + 2 * (i & 3), db + 2 * (i & 3), id);
       else
         issue<V>(tm, tm + 256, da + 2 * (i & 3), db + 2 * (i & 3), id);
@@ -141,11 +369,11 @@ __global__ void rate(int n_mma, long long* out) {
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
-template <int V, int N, int I = 0>
+template <int V, int N, int I = 0, int NI = 3>
 void run(const char* name, int grid) {
   long long* d;
   cudaMalloc(&d, 16);
-  auto k = rate<V, N, I>;
+  auto k = rate<V, N, I, NI>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 97 * 1024);
   for (int n : {64, 1024}) {
     k<<<grid, I >= 5 ? 512 : 128, 97 * 1024>>>(n, d);
@@ -161,27 +389,7 @@ void run(const char* name, int grid) {
 }
 
 int main() {
-  run<3, 128>("TS/SS alt N128", 148);
-  run<4, 128>("TS,SS,TS N128", 148);
-  run<3, 128, 3>("TS/SS alt +STS", 148);
-  run<1, 128, 3>("SS N128 +STS", 148);
-  run<0, 128, 5>("TS N128 +ALU15", 148);
-  run<1, 128, 5>("SS N128 +ALU15", 148);
-  run<0, 128, 6>("TS N128 +ALU12 other SPs", 148);
-  run<0, 128, 1>("TS N128 +LDS", 148);
-  run<0, 128, 2>("TS N128 +LDTM", 148);
-  run<0, 128, 3>("TS N128 +STS", 148);
-  run<0, 128, 4>("TS N128 +STTM", 148);
-  run<1, 128, 1>("SS N128 +LDS", 148);
-  run<1, 128, 3>("SS N128 +STS", 148);
-  for (int grid : {148}) {
-    run<0, 128>("TS tf32 N128", grid);
-    run<1, 128>("SS tf32 N128", grid);
-    run<0, 256>("TS tf32 N256", grid);
-    run<1, 256>("SS tf32 N256", grid);
-    run<0, 64>("TS tf32 N64", grid);
-    run<2, 128>("SS bf16 N128", grid);
-    run<2, 256>("SS bf16 N256", grid);
-  }
+  run<33, 128, 0>("4xTF32 alternating", 148);
+  run<33, 256, 0>("4xTF32 alternating N256", 148);
   return 0;
 }
