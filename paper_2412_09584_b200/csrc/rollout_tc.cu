@@ -703,6 +703,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             v[4 * q + 3] += bb[q].w;
           }
           if (mk) mark(a, t, 604 + 10 * (cb >> 1));
+          if (hidden) {
+            // the next layer's A K-block first (its MMAs start on it), then the staging
+            // of the pre-activations for the extrema warps, off the MMA's critical path
+            float w[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = relu ? fmaxf(v[j], 0.f) : v[j];
+            store_operand_tmem(tlane, cb, w);
+            if (mk) mark(a, t, 602 + 10 * (cb >> 1));
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (mk) mark(a, t, 603 + 10 * (cb >> 1));
+            fence_before();
+            mbar_arrive_warp(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
+          }
           if (rec) {  // stage the pre-activations for this chunk's aux warp
             if ((stg_used >> cb) & 1u) mbar_wait(m.stg_empty + cb, ((stg_par >> cb) & 1u) ^ 1u);
             if (mk) mark(a, t, 605 + 10 * (cb >> 1));
@@ -714,22 +727,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
             mbar_arrive_warp(m.stg_full + cb);
           }
           if (mk) mark(a, t, 601 + 10 * (cb >> 1));
-          if (relu) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-          }
-          if (hidden) {
-            store_operand_tmem(tlane, cb, v);
-            if (mk) mark(a, t, 602 + 10 * (cb >> 1));
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            if (mk) mark(a, t, 603 + 10 * (cb >> 1));
-            fence_before();
-            mbar_arrive_warp(m.a_chunk + cb);  // the next layer's MMAs may start on this K-block
-          } else {
+          if (!hidden) {
             float* xo = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (cb * 32 + j < ks) xo[cb * 32 + j] = v[j];
+              if (cb * 32 + j < ks) xo[cb * 32 + j] = relu ? fmaxf(v[j], 0.f) : v[j];
           }
         }
         if (warp == 0) mark(a, t, 201 + 10 * l);
