@@ -186,6 +186,12 @@ bp_status bp_rollout_info(bp_ctx* ctx, int* kernel, int* tiles_per_cta, int* row
 /* Host<->device bytes the library copied since the previous call. */
 bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h);
 
+/* The separable synthetic objective f(u) = sum_j 5 u_j^2 + cos(50 u_j) on [-1, 1]^d
+ * (replaces build_synthetic / SyntheticObjective, proj/src/model.cpp:407-409,
+ * proj/src/objective.cpp:82-104).  Its bounder is the exact SeparableBounder
+ * (proj/src/bab.cpp:30-83), whatever the configured bound mode. */
+bp_status bp_load_synthetic(bp_ctx* ctx, int dim);
+
 /* Uploads weights / cost program; derives stop and watch sets. */
 bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc);
 /* Number of recorded (watched) coordinates per rollout step, and the layout

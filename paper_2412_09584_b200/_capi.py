@@ -90,7 +90,7 @@ class PoolMeta(C.Structure):
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
     "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes",
-    "bp_load_objective",
+    "bp_load_objective", "bp_load_synthetic",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
     "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
@@ -129,6 +129,7 @@ def load() -> C.CDLL:
             "bp_rollout_info": (C.c_int, [vp, _ip, _ip, _ip, C.POINTER(C.c_int64)]),
             "bp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_load_objective": (C.c_int, [vp, C.POINTER(ObjectiveDesc)]),
+            "bp_load_synthetic": (C.c_int, [vp, C.c_int]),
             "bp_stat_layout": (C.c_int, [vp, _ip, _ip, _ip, _ip, _ip, _ip, C.c_int]),
             "bp_rollout": (C.c_int, [vp, C.c_int, C.c_int, _fp, _fp, _fp, _fp, _fp, _ip]),
             "bp_batch_search": (C.c_int, [vp, C.c_int, _dp, _dp, _dp, C.POINTER(SearchConfig)]),

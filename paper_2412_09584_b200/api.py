@@ -24,6 +24,20 @@ _BOUND = _config.BOUND_MODES
 _ALPHA = _config.ALPHAS
 
 
+class SyntheticSpec:
+    """The separable synthetic objective on [-1, 1]^d (objective.hpp:73-95) as the
+    Device sees it: a one-step "rollout" of d actions, no MLP, no recorded statistics."""
+
+    def __init__(self, dim: int):
+        if dim <= 0:
+            raise ValueError("SyntheticObjective: dimension must be positive")
+        self.d = self.ka = int(dim)
+        self.horizon, self.ks = 1, 0
+
+    def box(self):
+        return np.full(self.d, -1.0), np.full(self.d, 1.0)
+
+
 class Device:
     """One bp_ctx bound to a CUDA device, plus the objective loaded on it."""
 
@@ -57,6 +71,13 @@ class Device:
         packed = spec.to_c()
         check(self.lib.bp_load_objective(self.h, packed.ref()))
         self.spec, self._packed, self._layout = spec, packed, None
+        return self
+
+    def load_synthetic(self, dim: int) -> "Device":
+        """The separable benchmark objective (model.cpp:407-409) with its exact bounder."""
+        spec = SyntheticSpec(dim)
+        check(self.lib.bp_load_synthetic(self.h, spec.d))
+        self.spec, self._packed, self._layout = spec, None, None
         return self
 
     def stat_layout(self):
@@ -166,13 +187,13 @@ class Device:
         "tc1" (tcgen05 v1, rollout_tc.cu) or "simt" (FP32 FFMA, rollout.cu)."""
         active = C.c_int()
         check(self.lib.bp_set_rollout_path(self.h, -1, C.byref(active)))
-        return {1: "simt", 2: "tc1", 3: "tc2"}[active.value]
+        return {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic"}[active.value]
 
     def rollout_info(self) -> dict:
         """Rollout kernel, 128-row tiles per CTA, rows per CTA and shared memory per CTA."""
         k, t, r, sm = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
         check(self.lib.bp_rollout_info(self.h, C.byref(k), C.byref(t), C.byref(r), C.byref(sm)))
-        return {"kernel": {1: "simt", 2: "tc1", 3: "tc2"}[k.value], "tiles_per_cta": t.value,
+        return {"kernel": {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic"}[k.value], "tiles_per_cta": t.value,
                 "rows_per_cta": r.value, "smem_bytes": sm.value}
 
     def rollout_tiles(self) -> int:
@@ -313,7 +334,10 @@ def rollout(model: Model, scenario: Scenario, action) -> np.ndarray:
 
 
 def plan_synthetic(d: int, config: str = "", method: str = "babnd") -> dict:
-    raise NotImplementedError("the synthetic separable objective is a SURVEY 8(f) next row")
+    """pymodule.cpp:162-169: minimise the separable benchmark objective on [-1, 1]^d;
+    babnd uses the exact SeparableBounder (bab.cpp:275-283), on the device."""
+    cfg = _config.from_json(config)
+    return default_device().load_synthetic(int(d)).plan(cfg, None, method)
 
 
 def rrt_plan(*args, **kwargs):

@@ -88,6 +88,10 @@ cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, 
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
 size_t rollout_tc_smem(const DevObjective& o);
 cudaError_t launch_rollout_tc2(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
+cudaError_t launch_synthetic_eval(const float* actions, float* costs, int* failed, long long n_rows, int d,
+                                  int rows_per_sub, cudaStream_t st);
+cudaError_t launch_separable_bound(const double* lo, const double* hi, int n, int d, const double* crit, int ncrit,
+                                   const int* use, double* lf, cudaStream_t st);
 size_t rollout_tc2_fixed_smem(const DevObjective& o);
 size_t rollout_tc2_smem(const DevObjective& o);
 int rollout_rows_per_tile(int nq);
@@ -263,7 +267,70 @@ struct Compiled {
   std::vector<int> slot_kind, slot_index, slot_dim, slot_off;
   std::vector<double> x0, p0, ulo, uhi;
   int d = 0;
+  int synth = 0;  // > 0: the separable synthetic objective of this dimension (no MLP, no cost program)
 };
+
+// Critical points of the 1-d synthetic term 5x^2 + cos(50x) on [-1, 1]: the roots of
+// its derivative on a 400000-interval grid refined by 80 bisections, exactly the
+// reference's SeparableBounder table (proj/src/bab.cpp:32-68).  Setup, not hot path:
+// computed once per process and uploaded with the objective.
+const std::vector<double>& separable_critical_points() {
+  static const std::vector<double> pts = [] {
+    auto dg = [](double x) { return 10.0 * x - 50.0 * std::sin(50.0 * x); };
+    std::vector<double> out;
+    const int n = 400000;
+    double px = -1.0, pv = dg(px);
+    for (int i = 1; i <= n; ++i) {
+      const double x = -1.0 + 2.0 * i / n;
+      const double v = dg(x);
+      if (pv == 0.0) {
+        out.push_back(px);
+      } else if ((pv < 0.0) != (v < 0.0)) {
+        double a = px, b = x, fa = pv;
+        for (int it = 0; it < 80; ++it) {
+          const double m = 0.5 * (a + b);
+          const double fm = dg(m);
+          if (fm == 0.0) {
+            a = b = m;
+            break;
+          }
+          if ((fa < 0.0) != (fm < 0.0)) {
+            b = m;
+          } else {
+            a = m;
+            fa = fm;
+          }
+        }
+        out.push_back(0.5 * (a + b));
+      }
+      px = x;
+      pv = v;
+    }
+    if (pv == 0.0) out.push_back(px);
+    return out;
+  }();
+  return pts;
+}
+
+// The synthetic objective (objective.cpp:82-104 / model.cpp build_synthetic): the
+// planner sees a one-step "rollout" of d actions on the box [-1, 1]^d.
+Compiled compile_synthetic(int dim) {
+  if (dim <= 0) fail(BP_INVALID_ARGUMENT, "SyntheticObjective: dimension must be positive");
+  Compiled c;
+  c.synth = dim;
+  c.d = dim;
+  c.o.H = 1;
+  c.o.ka = dim;
+  c.o.kd = dim;
+  c.o.d = dim;
+  c.o.SP = 0;
+  c.ulo.assign(static_cast<size_t>(dim), -1.0);
+  c.uhi.assign(static_cast<size_t>(dim), 1.0);
+  c.fa.push_back(0.f);
+  c.da = separable_critical_points();
+  c.ia.push_back(0);
+  return c;
+}
 
 int push_f(std::vector<float>& a, const double* p, size_t n) {
   while (a.size() % 4) a.push_back(0.f);
@@ -691,6 +758,7 @@ struct bp_ctx {
   int path_mode = 0;  // 0 auto, 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2 (BP_ROLLOUT or bp_set_rollout_path)
   // rollout kernel for the loaded objective: 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2
   int kernel() const {
+    if (comp.synth) return 4;
     if (!loaded || path_mode == 1) return 1;
     if (path_mode == 2) return comp.o.tc ? 2 : 1;
     if (path_mode == 3) return comp.o.tc2 ? 3 : 1;
@@ -746,7 +814,10 @@ struct bp_ctx {
       ev = roll_event();
       ck(cudaEventRecord(ev.first, stream), "event");
     }
-    if (kern == 3)
+    if (comp.synth)
+      ck(bp::launch_synthetic_eval(actions, costs, fail_flags, n_rows, comp.synth, rows_per_sub, stream),
+         "synthetic objective launch");
+    else if (kern == 3)
       ck(bp::launch_rollout_tc2(dev(), a, stream), "rollout (tcgen05 v2) launch");
     else if (kern == 2)
       ck(bp::launch_rollout_tc(dev(), a, stream), "rollout (tcgen05) launch");
@@ -954,9 +1025,25 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
 
 void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
   if (!c->searched) fail(BP_LOGIC, "bound: no batch searched");
-  if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
   const Compiled& cp = c->comp;
   const int n = c->n;
+  if (cp.synth) {  // SeparableBounder (bab.cpp:70-83): exact, needs no search statistics
+    double* lf = c->lf.get(static_cast<size_t>(n));
+    if (c->timing) ck(cudaEventRecord(c->ev0, c->stream), "event");
+    ck(bp::launch_separable_bound(c->lo_d.p, c->hi_d.p, n, cp.d, c->d_da.p, static_cast<int>(cp.da.size()), nullptr,
+                                  lf, c->stream), "separable bound launch");
+    if (c->timing) ck(cudaEventRecord(c->ev1, c->stream), "event");
+    ++c->launches;
+    ck(memcpy_counted(lf_out, lf, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (c->timing) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event");
+      c->bound_ms += ms;
+    }
+    return;
+  }
+  if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
   const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
   std::vector<int> use(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) use[static_cast<size_t>(i)] = c->h_failed[static_cast<size_t>(i)] ? 0 : 1;
@@ -1607,7 +1694,7 @@ bp_status bp_rollout_info(bp_ctx* ctx, int* kernel, int* tiles_per_cta, int* row
     check_ctx(ctx);
     const int k = ctx->kernel();
     const bp::DevObjective& o = ctx->comp.o;
-    const int tiles = k == 3 ? o.tc2 : k == 2 ? 1 : 0;
+    const int tiles = k == 3 ? o.tc2 : k == 2 ? 1 : 0;  // k == 4: synthetic objective
     if (kernel) *kernel = k;
     if (tiles_per_cta) *tiles_per_cta = tiles;
     if (rows_per_cta) *rows_per_cta = k == 1 ? ctx->comp.R : 128 * tiles;
@@ -1627,6 +1714,23 @@ bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
     check_ctx(ctx);
     if (desc == nullptr) fail(BP_INVALID_ARGUMENT, "null objective");
     Compiled cp = compile(*desc);
+    float* f = ctx->d_fa.get(cp.fa.size());
+    double* dd = ctx->d_da.get(cp.da.size());
+    int* iv = ctx->d_ia.get(cp.ia.size());
+    ck(memcpy_counted(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(memcpy_counted(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->comp = std::move(cp);
+    ctx->loaded = true;
+    ctx->searched = false;
+  });
+}
+
+bp_status bp_load_synthetic(bp_ctx* ctx, int dim) {
+  return guard([&] {
+    check_ctx(ctx);
+    Compiled cp = compile_synthetic(dim);
     float* f = ctx->d_fa.get(cp.fa.size());
     double* dd = ctx->d_da.get(cp.da.size());
     int* iv = ctx->d_ia.get(cp.ia.size());
@@ -1766,7 +1870,8 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
   return guard([&] {
     check_loaded(ctx);
     if (n_boxes <= 0) fail(BP_INVALID_ARGUMENT, "bp_bound_boxes: no boxes");
-    if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
+    if (mode == BP_BOUND_FULL_CROWN && !ctx->comp.synth)
+      fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
     const int d = ctx->comp.d;
     const size_t nd = static_cast<size_t>(n_boxes) * d;
     for (size_t i = 0; i < nd; ++i)
