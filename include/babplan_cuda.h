@@ -45,7 +45,10 @@ typedef enum {
 } bp_status;
 
 /* ------------------------------------------------------------- enums */
-enum { BP_FEATURE_RELATIVE = 0, BP_FEATURE_ABSOLUTE = 1 }; /* model.hpp:13-16 */
+/* model.hpp:13-16; BP_FEATURE_NETWORK: a bare network over the action box (horizon 1, the
+ * MLP reads u only), the graph build_network_objective makes (model.cpp:389-405) for
+ * network_lower_bound (pymodule.cpp:192-202); bounds only, no rollouts. */
+enum { BP_FEATURE_RELATIVE = 0, BP_FEATURE_ABSOLUTE = 1, BP_FEATURE_NETWORK = 2 };
 
 /* Value ids inside one rollout step's cost program. */
 enum { BP_VAL_X = 0, BP_VAL_U = 1, BP_VAL_P = 2, BP_VAL_OP0 = 3 };
@@ -223,6 +226,11 @@ bp_status bp_batch_bound(bp_ctx* ctx, int mode, int alpha, double* lf);
  * stats = nullptr), i.e. interval intermediate bounds (crown.cpp:449-461). */
 bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi, int mode, int alpha,
                          double* lf);
+
+/* The intermediate (node) bounds the last bound call used, in the stat layout
+ * [n_boxes][H][per_step]: the interval pass (interval modes, failed searches) or the
+ * full-CROWN node passes (crown_node_bounds, crown.cpp:379-412).  Diagnostic. */
+bp_status bp_node_bounds(bp_ctx* ctx, double* lo, double* hi);
 
 /* Full planner: plan() when method_babnd != 0, else sample_only_plan(). */
 typedef struct bp_result bp_result;

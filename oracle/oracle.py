@@ -321,6 +321,15 @@ class Objective:
                                 vp(stats.h) if stats else None, ALPHAS[alpha], C.byref(out)))
         return out.value
 
+    def crown_node_stats(self, lo, hi, ids, alpha="adaptive") -> Stats:
+        """crown_node_bounds (crown.cpp:379-412) for the given nodes, as watch stats."""
+        lo, hi = _d(lo), _d(hi)
+        ids = np.asarray(list(ids), dtype=np.int32)
+        h = vp()
+        ck(lib().or_crown_node_stats(self.h, lo.ctypes.data_as(dp), hi.ctypes.data_as(dp), ALPHAS[alpha],
+                                     ids.ctypes.data_as(ip), C.c_int(len(ids)), C.byref(h)))
+        return Stats(handle=h.value)
+
     def stats_in_layout(self, stats: Stats, layout, horizon: int):
         """Oracle watch stats rearranged into the device record layout (H x per_step)."""
         per, slots = layout

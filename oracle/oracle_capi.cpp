@@ -441,6 +441,27 @@ int or_lower_bound(void* h, const double* lo, const double* hi, int mode, void* 
                        static_cast<WatchStats*>(stats), alpha_policy(alpha));
   });
 }
+// crown_node_bounds (crown.cpp:379-412) over the given targets, as watch stats
+// (test helper: node-by-node parity of the device's full-CROWN passes).
+int or_crown_node_stats(void* h, const double* lo, const double* hi, int alpha, const int* ids, int n_ids,
+                        void** out) {
+  return guard([&] {
+    if (!O->graph_obj) throw std::invalid_argument("crown_node_bounds: not a graph objective");
+    const int d = O->obj->dim();
+    const std::vector<int> targets(ids, ids + n_ids);
+    PreactBounds pre = crown_node_bounds(O->graph_obj->graph(), BoxDomain(vec_of(lo, d), vec_of(hi, d)), targets,
+                                         alpha_policy(alpha));
+    auto* ws = new WatchStats();
+    for (int id : targets)
+      if (pre.has(id)) {
+        NodeStats& ns = (*ws)[id];
+        ns.min = pre.at(id).first;
+        ns.max = pre.at(id).second;
+        ns.count = 1;
+      }
+    *out = ws;
+  });
+}
 int or_relax_relu(const double* l, const double* u, int n, int policy, double* ls, double* lo, double* us, double* uo) {
   return guard([&] {
     const ReluRelaxation r = relax_relu(vec_of(l, n), vec_of(u, n), alpha_policy(policy));

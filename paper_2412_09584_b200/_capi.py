@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(_HERE, "_lib", "libbabplan_cuda.so")  # override: dev variants
 
 BP_OK, BP_INVALID_ARGUMENT, BP_LOGIC, BP_RUNTIME, BP_CUDA, BP_NCCL, BP_UNSUPPORTED = range(7)
-BP_FEATURE_RELATIVE, BP_FEATURE_ABSOLUTE = 0, 1
+BP_FEATURE_RELATIVE, BP_FEATURE_ABSOLUTE, BP_FEATURE_NETWORK = 0, 1, 2
 BP_VAL_X, BP_VAL_U, BP_VAL_P, BP_VAL_OP0 = 0, 1, 2, 3
 (BP_OP_LINEAR, BP_OP_RELU, BP_OP_SUM, BP_OP_SCALAR_AFFINE, BP_OP_SQDIST, BP_OP_HINGE,
  BP_OP_SLICE) = range(7)
@@ -89,7 +89,7 @@ class PoolMeta(C.Structure):
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
-    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes",
+    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds",
     "bp_load_objective", "bp_load_synthetic",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
@@ -127,6 +127,7 @@ def load() -> C.CDLL:
             "bp_set_stream": (C.c_int, [vp, vp]),
             "bp_set_rollout_path": (C.c_int, [vp, C.c_int, _ip]),
             "bp_rollout_info": (C.c_int, [vp, _ip, _ip, _ip, C.POINTER(C.c_int64)]),
+            "bp_node_bounds": (C.c_int, [vp, _dp, _dp]),
             "bp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_load_objective": (C.c_int, [vp, C.POINTER(ObjectiveDesc)]),
             "bp_load_synthetic": (C.c_int, [vp, C.c_int]),

@@ -18,7 +18,7 @@ import numpy as np
 from . import _capi, config as _config
 from ._capi import check
 from .model import Model, Scenario
-from .objective import ObjectiveSpec, build_objective
+from .objective import ObjectiveSpec, build_network_objective, build_objective
 
 _BOUND = _config.BOUND_MODES
 _ALPHA = _config.ALPHAS
@@ -157,6 +157,14 @@ class Device:
         check(self.lib.bp_bound_boxes(self.h, lo.shape[0], _capi.dptr(lo), _capi.dptr(hi), _BOUND[mode],
                                       _ALPHA[_config._parse_enum(_ALPHA, alpha, "alpha policy")], _capi.dptr(lf)))
         return lf
+
+    def node_bounds(self, n_boxes: int):
+        """The intermediate bounds of the last bound call, (n_boxes, H, per_step) lo / hi."""
+        per, _ = self.stat_layout()
+        lo = np.zeros((n_boxes, self.spec.horizon, per))
+        hi = np.zeros((n_boxes, self.spec.horizon, per))
+        check(self.lib.bp_node_bounds(self.h, _capi.dptr(lo), _capi.dptr(hi)))
+        return lo, hi
 
     # --------------------------------------------------------------------- plan
     def plan(self, cfg: dict, warm: Optional[np.ndarray] = None, method: str = "babnd") -> dict:
@@ -320,7 +328,18 @@ def lower_bound(model: Model, scenario: Scenario, mode: str = "full-crown", alph
 
 
 def network_lower_bound(model: Model, lower, upper, mode: str = "full-crown", alpha: str = "adaptive") -> float:
-    raise NotImplementedError("network_lower_bound (full-crown over a bare network) is a SURVEY 8(f) next row")
+    """pymodule.cpp:192-202: certified lower bound of a scalar-output network over an
+    input box (build_network_objective, model.cpp:389-405), on the device."""
+    if mode not in _BOUND:
+        raise ValueError(f"unknown bound mode '{mode}'")
+    if alpha not in _ALPHA:
+        raise ValueError(f"unknown alpha policy '{alpha}'")
+    spec = build_network_objective(model, lower, upper)
+    dev = default_device().load(spec)
+    lo, hi = spec.box()
+    if not (np.all(np.isfinite(lo)) and np.all(np.isfinite(hi)) and np.all(lo <= hi)):
+        raise ValueError("BoxDomain: invalid bounds")
+    return float(dev.bound_boxes(lo[None], hi[None], mode, alpha)[0])
 
 
 def rollout(model: Model, scenario: Scenario, action) -> np.ndarray:

@@ -23,18 +23,7 @@
 
 namespace bp {
 
-struct BoundArgs {
-  const double* lo;       // [n][d] boxes
-  const double* hi;
-  const int* stat_min;    // [n][H*SP] sample extrema (enc_f) or null
-  const int* stat_max;
-  const int* use_stats;   // [n]: 1 = empirical extrema valid for this subdomain
-  double* ivl_lo;         // [n][H*SP] scratch for interval bounds
-  double* ivl_hi;
-  double* lf;             // [n]
-  int mode;               // BP_BOUND_EMPIRICAL (1) or BP_BOUND_INTERVAL (2)
-  int alpha;              // 0 adaptive, 1 zero, 2 one
-};
+// BoundArgs: bp_common.cuh
 
 namespace {
 
@@ -121,14 +110,15 @@ __device__ void interval_pass(const DevObjective& o, const BoundArgs& a, Smem& s
   for (int t = 0; t < o.H; ++t) {
     const double* ulo = a.lo + boxoff + t * o.ka;
     const double* uhi = a.hi + boxoff + t * o.ka;
-    // features: concat(x - tile(p), u_t) or concat(x, u_t)
-    for (int j = tid; j < o.ks; j += kThreads) {
+    // features: concat(x - tile(p), u_t), concat(x, u_t), or u_t alone (bare network)
+    const int uoff = o.net ? 0 : o.ks;
+    for (int j = tid; j < o.ks && !o.net; j += kThreads) {
       sm.a_lo[j] = o.rel ? sm.x_lo[j] - sm.p_hi[j % o.kd] : sm.x_lo[j];
       sm.a_hi[j] = o.rel ? sm.x_hi[j] - sm.p_lo[j % o.kd] : sm.x_hi[j];
     }
     for (int j = tid; j < o.ka; j += kThreads) {
-      sm.a_lo[o.ks + j] = ulo[j];
-      sm.a_hi[o.ks + j] = uhi[j];
+      sm.a_lo[uoff + j] = ulo[j];
+      sm.a_hi[uoff + j] = uhi[j];
     }
     __syncthreads();
     double *in_lo = sm.a_lo, *in_hi = sm.a_hi, *out_lo = sm.b_lo, *out_hi = sm.b_hi;
@@ -272,34 +262,48 @@ __device__ __forceinline__ int stat_of(const DevObjective& o, int id) {
   return o.ops[id - 3].stat;
 }
 
-__global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, const BoundArgs a) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smraw);
-  const int s = blockIdx.x, tid = threadIdx.x;
-  const bool emp = a.mode == 1 && a.use_stats != nullptr && a.use_stats[s] != 0 && a.stat_min != nullptr;
-  if (!emp) interval_pass(o, a, sm, s);
-  const Bounds B{o, a, static_cast<long long>(s) * o.H * o.SP, emp};
+// One backward sweep (backward_propagate's lower form, crown.cpp:92-292) of a scalar:
+// the objective's output (start_kind < 0) or `sign` times row `row` of a start node.
+// Returns the concretised lower bound (crown.cpp:296-319) on every thread.
+__device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem& sm, const Bounds& B, int s, int row,
+                        double sign) {
+  const int tid = threadIdx.x;
   const long long boxoff = static_cast<long long>(s) * o.d;
+  const bool node = a.start_kind >= 0;
+  const bool stops = a.mode != 0;  // full CROWN: no stop set (crown.cpp:463-464)
+  const int t_top = node ? a.start_t : o.H - 1;
   double bacc = 0.0;  // this thread's share of the offset
   for (int j = tid; j < kMaxW; j += kThreads) sm.lx[j] = 0.0;
   for (int j = tid; j < 16; j += kThreads) sm.lp[j] = 0.0;
   __syncthreads();
 
-  for (int t = o.H - 1; t >= 0; --t) {
+  for (int t = t_top; t >= 0; --t) {
     const bool last = t == o.H - 1;
-    // 1. cost program, reverse op order; terms enter with coefficient 1.
+    const bool top = t == t_top;
+    // 1. cost program, reverse op order; terms enter with coefficient 1 (output pass),
+    //    or the start row of a cost-op node with coefficient `sign`.
     for (int j = tid; j < kMaxW; j += kThreads) sm.lops[j] = 0.0;
     for (int j = tid; j < 16; j += kThreads) {
       sm.lu[j] = 0.0;
       sm.lpt[j] = j < o.kd ? sm.lp[j] : 0.0;  // from step t+1's relative features
     }
     __syncthreads();
-    if (tid == 0)
-      for (int i = 0; i < o.n_ops; ++i)
-        if (o.ops[i].is_term) sm.lops[o.ops[i].col] += 1.0;
+    if (tid == 0) {
+      if (!node) {
+        for (int i = 0; i < o.n_ops; ++i)
+          if (o.ops[i].is_term) sm.lops[o.ops[i].col] += 1.0;
+      } else if (top) {
+        if (a.start_kind == 4) sm.lops[o.ops[a.start_index].col + row] = sign;
+        if (a.start_kind == 1) sm.lx[row] = sign;
+        if (a.start_kind == 2) sm.lu[row] = sign;
+        if (a.start_kind == 3) sm.lpt[row] = sign;
+      }
+    }
     __syncthreads();
-    for (int i = o.n_ops - 1; i >= 0; --i) {
+    const bool ops_live = !node || (top && a.start_kind == 4);  // earlier steps' ops feed nothing upstream
+    for (int i = o.n_ops - 1; i >= 0 && ops_live; --i) {
       const DevOp& op = o.ops[i];
+      if (node && top && i > a.start_index) continue;  // only the start op's ancestors
       const double* lam = sm.lops + op.col;
       double* ls = lam_of(o, sm, op.src0);
       const int st = stat_of(o, op.src0);
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
         case 1:  // RELU: anchor (last-ReLU stop) or sign-selected relaxation
           for (int j = tid; j < op.dim; j += kThreads) {
             const double c = lam[j], l = B.lo(t, st + j), u = B.hi(t, st + j);
-            if (op.stop && last) {
+            if (stops && op.stop && last) {
               bacc += c * (c >= 0.0 ? fmax(l, 0.0) : fmax(u, 0.0));
             } else if (c >= 0.0) {
               ls[j] += c * relu_lower_slope(l, u, a.alpha);
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
           }
           break;
         }
-        case 5:  // HINGE: anchor on its own output extrema
+        case 5:  // HINGE: anchor on its own output bounds
           if (tid == 0) {
             const double c = lam[0];
             bacc += c * (c >= 0.0 ? B.lo(t, op.stat) : B.hi(t, op.stat));
@@ -373,19 +377,26 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
       __syncthreads();
     }
     // 2. x_t as a stop node: anchor on its extrema, nothing flows below.
-    const bool xstop = o.iv[o.xstop + t] != 0;
+    const bool xstop = stops && o.iv[o.xstop + t] != 0;
+    const bool mlp_live = !node || !top || a.start_kind <= 1 || a.start_kind == 4;
     for (int j = tid; j < o.ks; j += kThreads) {
-      sm.lam[j] = sm.lx[j];
+      sm.lam[j] = mlp_live ? sm.lx[j] : 0.0;
       if (xstop) {
         const double c = sm.lx[j];
         bacc += c * (c >= 0.0 ? B.lo(t, o.x_stat + j) : B.hi(t, o.x_stat + j));
         sm.lam[j] = 0.0;
       }
     }
+    // a pre-activation node starts inside the MLP: lam on the output of layer start_index
+    const int l_top = (node && top && a.start_kind == 0) ? a.start_index : o.L - 1;
+    if (node && top && a.start_kind == 0) {
+      __syncthreads();
+      for (int j = tid; j < o.widths[l_top + 1]; j += kThreads) sm.lam[j] = j == row ? sign : 0.0;
+    }
     __syncthreads();
-    // 3. MLP layers L..1
-    bool cut = xstop;
-    for (int l = o.L - 1; l >= 0 && !cut; --l) {
+    // 3. MLP layers l_top..1
+    bool cut = xstop || !mlp_live;
+    for (int l = l_top; l >= 0 && !cut; --l) {
       const int K = o.widths[l], N = o.widths[l + 1];
       const double* W = o.dd + o.wd[l];
       for (int j = tid; j < K; j += kThreads) {
@@ -397,7 +408,7 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
       __syncthreads();
       if (l > 0 && o.relu[l - 1]) {
         const int st = o.pre_stat[l - 1];
-        const bool anchor = last && o.stop_layer == l - 1;
+        const bool anchor = stops && last && o.stop_layer == l - 1;
         for (int j = tid; j < K; j += kThreads) {
           const double c = sm.lam2[j], lo = B.lo(t, st + j), hi = B.hi(t, st + j);
           double out = 0.0;
@@ -419,10 +430,12 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
       }
       __syncthreads();
     }
-    // 4. features -> x_{t-1}, p_{t-1}, u_t ; p_t = p_{t-1} + u_t
-    for (int j = tid; j < o.ks; j += kThreads) sm.lx[j] = cut ? 0.0 : sm.lam[j];
+    // 4. features -> x_{t-1}, p_{t-1}, u_t ; p_t = p_{t-1} + u_t.  A bare network (o.net:
+    //    build_network_objective, model.cpp:389-405) reads u_t only.
+    const int uoff = o.net ? 0 : o.ks;
+    for (int j = tid; j < o.ks; j += kThreads) sm.lx[j] = (cut || o.net) ? 0.0 : sm.lam[j];
     for (int j = tid; j < o.ka; j += kThreads) {
-      double lu = sm.lu[j] + sm.lpt[j] + (cut ? 0.0 : sm.lam[o.ks + j]);
+      double lu = sm.lu[j] + sm.lpt[j] + (cut ? 0.0 : sm.lam[uoff + j]);
       // concretize the input slice u_t on the box (crown.cpp:461, 296-319)
       bacc += lu * (lu >= 0.0 ? a.lo[boxoff + t * o.ka + j] : a.hi[boxoff + t * o.ka + j]);
     }
@@ -441,11 +454,59 @@ __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, c
   for (int off = 16; off > 0; off >>= 1) bacc += __shfl_down_sync(0xffffffffu, bacc, off);
   if ((tid & 31) == 0) sm.red[tid >> 5] = bacc;
   __syncthreads();
-  if (tid == 0) {
-    double tot = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) tot += sm.red[w];
-    a.lf[s] = tot;
+  double tot = 0.0;
+  for (int w = 0; w < kThreads / 32; ++w) tot += sm.red[w];
+  __syncthreads();
+  return tot;
+}
+
+__global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, const BoundArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  if (a.start_kind >= 0) {  // full-CROWN node pass: CTA = (subdomain, row)
+    const int s = blockIdx.x / a.start_dim, row = blockIdx.x % a.start_dim;
+    const Bounds B{o, a, static_cast<long long>(s) * o.H * o.SP, false};
+    double lo = sweep(o, a, sm, B, s, row, 1.0);
+    double hi = -sweep(o, a, sm, B, s, row, -1.0);  // upper(v) = -lower(-v): every relaxation is by sign
+    if (lo > hi) {  // guard against rounding inversions on degenerate coordinates (crown.cpp:406-407)
+      const double tmp = lo;
+      lo = hi;
+      hi = tmp;
+    }
+    if (threadIdx.x == 0) {
+      const long long i = static_cast<long long>(s) * o.H * o.SP + static_cast<long long>(a.start_t) * o.SP +
+                          a.start_slot + row;
+      a.ivl_lo[i] = lo;
+      a.ivl_hi[i] = hi;
+    }
+    return;
   }
+  const int s = blockIdx.x;
+  const bool emp = a.mode == 1 && a.use_stats != nullptr && a.use_stats[s] != 0 && a.stat_min != nullptr;
+  if (!emp && a.mode != 0) interval_pass(o, a, sm, s);  // full CROWN: node bounds already in ivl
+  const Bounds B{o, a, static_cast<long long>(s) * o.H * o.SP, emp};
+  const double tot = sweep(o, a, sm, B, s, 0, 1.0);
+  if (threadIdx.x == 0) a.lf[s] = tot;
+}
+
+// Hinge outputs under full CROWN: enclosed from their argument's bounds, never
+// propagated (crown_node_bounds, crown.cpp:393-400; hinge_interval :360-375).
+__global__ void hinge_bounds_kernel(const DevObjective o, const BoundArgs a, int t, int op_index) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.start_dim) return;  // start_dim = subdomains here
+  const DevOp& op = o.ops[op_index];
+  const long long base = static_cast<long long>(s) * o.H * o.SP + static_cast<long long>(t) * o.SP;
+  const int st = stat_of(o, op.src0);
+  const double* c = o.dd + op.ctrd;
+  double d2l = 0.0, d2h = 0.0;
+  for (int j = 0; j < op.in_dim; ++j) {
+    const double x = a.ivl_lo[base + st + j] - c[j], y = a.ivl_hi[base + st + j] - c[j];
+    d2h += fmax(x * x, y * y);
+    d2l += (x <= 0.0 && y >= 0.0) ? 0.0 : fmin(x * x, y * y);
+  }
+  const double ml = op.radiusd - sqrt(d2h), mh = op.radiusd - sqrt(d2l);
+  a.ivl_lo[base + op.stat] = ml > 0.0 ? op.penaltyd * ml : 0.0;
+  a.ivl_hi[base + op.stat] = mh > 0.0 ? op.penaltyd * mh : 0.0;
 }
 
 }  // namespace
@@ -457,7 +518,14 @@ cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaS
   const size_t smem = sizeof(Smem);
   cudaError_t e = cudaFuncSetAttribute(bound_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  bound_kernel<<<n, kThreads, smem, st>>>(o, a);
+  const long long grid = a.start_kind >= 0 ? static_cast<long long>(n) * a.start_dim : n;
+  bound_kernel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(o, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hinge_bounds(const DevObjective& o, const BoundArgs& a, int t, int op_index, cudaStream_t st) {
+  if (a.start_dim <= 0) return cudaSuccess;
+  hinge_bounds_kernel<<<(a.start_dim + 127) / 128, 128, 0, st>>>(o, a, t, op_index);
   return cudaGetLastError();
 }
 

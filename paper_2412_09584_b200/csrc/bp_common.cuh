@@ -30,6 +30,7 @@ struct DevOp {
 // Compiled objective, passed by value to every kernel (~5 KB of params).
 struct DevObjective {
   int ks, ka, kd, H, rel, L, d;
+  int net;  // bare network (build_network_objective): the MLP reads u_t only, H = 1
   int widths[kMaxLayers + 1];
   int relu[kMaxLayers];
   // forward weights: layer l stored transposed [kpad][nstr] (k-major, zero padded)
@@ -70,6 +71,27 @@ struct DevObjective {
   const float* f;
   const double* dd;
   const int* iv;
+};
+
+// K7 launch arguments (bound.cu; built by host.cu).
+struct BoundArgs {
+  const double* lo;       // [n][d] boxes
+  const double* hi;
+  const int* stat_min;    // [n][H*SP] sample extrema (enc_f) or null
+  const int* stat_max;
+  const int* use_stats;   // [n]: 1 = empirical extrema valid for this subdomain
+  double* ivl_lo;         // [n][H*SP] scratch for interval bounds
+  double* ivl_hi;
+  double* lf;             // [n]
+  int mode;               // BP_BOUND_FULL_CROWN (0), BP_BOUND_EMPIRICAL (1) or BP_BOUND_INTERVAL (2)
+  int alpha;              // 0 adaptive, 1 zero, 2 one
+  // full CROWN (crown_node_bounds, crown.cpp:379-412): ivl_lo/ivl_hi already hold the
+  // bounds of every node the pass reads, so no interval pass and no stop anchors.
+  // start_kind >= 0: a node pass -- the backward sweep starts at row r of the slot's
+  // node at step start_t (one CTA per (subdomain, row)) and writes the node's lower /
+  // upper bound into ivl_lo / ivl_hi; -1: the pass from the objective's output into lf.
+  int start_kind;         // -1 output, 0 pre-activation of layer start_index, 1 x_t, 2 u_t, 3 p_t, 4 cost op start_index
+  int start_t, start_index, start_dim, start_slot;
 };
 
 // Order-preserving float <-> int encoding for atomicMin/atomicMax extrema.

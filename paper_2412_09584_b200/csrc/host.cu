@@ -42,18 +42,7 @@ struct RolloutArgs {
   int kslab;
   long long* timeline;
 };
-struct BoundArgs {
-  const double* lo;
-  const double* hi;
-  const int* stat_min;
-  const int* stat_max;
-  const int* use_stats;
-  double* ivl_lo;
-  double* ivl_hi;
-  double* lf;
-  int mode;
-  int alpha;
-};
+// BoundArgs: bp_common.cuh
 struct SearchArgs {
   int n, d, rows, n_samp;
   int method;
@@ -96,6 +85,7 @@ size_t rollout_tc2_fixed_smem(const DevObjective& o);
 size_t rollout_tc2_smem(const DevObjective& o);
 int rollout_rows_per_tile(int nq);
 cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st);
+cudaError_t launch_hinge_bounds(const DevObjective& o, const BoundArgs& a, int t, int op_index, cudaStream_t st);
 size_t bound_smem_bytes();
 cudaError_t launch_search_init(const SearchArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const SearchArgs& a, int sms, cudaStream_t st);
@@ -354,13 +344,18 @@ Compiled compile(const bp_objective_desc& d) {
   Compiled c;
   bp::DevObjective& o = c.o;
   if (d.ks <= 0 || d.ka <= 0 || d.kd <= 0 || d.horizon < 1) fail(BP_INVALID_ARGUMENT, "objective: bad dimensions");
+  const bool net = d.feature_mode == BP_FEATURE_NETWORK;
   if (d.ka != d.kd) fail(BP_INVALID_ARGUMENT, "objective: action and effector dimensions must match");
-  if (d.ka > 8) fail(BP_UNSUPPORTED, "objective: action dimension above 8");
+  if (d.ka > (net ? 16 : 8)) fail(BP_UNSUPPORTED, "objective: action dimension above 8 (16 for a bare network)");
   if (d.feature_mode == BP_FEATURE_RELATIVE && d.ks % d.kd != 0)
     fail(BP_INVALID_ARGUMENT, "objective: state must be whole keypoints of workspace dimension");
   if (d.n_layers < 1 || d.n_layers > bp::kMaxLayers) fail(BP_UNSUPPORTED, "objective: layer count outside 1..8");
-  if (d.widths[0] != d.ks + d.ka || d.widths[d.n_layers] != d.ks)
+  if (net) {
+    if (d.horizon != 1 || d.widths[0] != d.ka || d.widths[d.n_layers] != d.ks)
+      fail(BP_INVALID_ARGUMENT, "build_network_objective: one step, the network reads the box and outputs the value");
+  } else if (d.widths[0] != d.ks + d.ka || d.widths[d.n_layers] != d.ks) {
     fail(BP_INVALID_ARGUMENT, "build_objective: model input must take state plus action and output the state");
+  }
   if (d.relu_after[d.n_layers - 1]) fail(BP_INVALID_ARGUMENT, "objective: final layer must stay linear");
   if (d.n_ops > bp::kMaxOps) fail(BP_UNSUPPORTED, "objective: more than 32 cost ops");
   o.ks = d.ks;
@@ -368,6 +363,7 @@ Compiled compile(const bp_objective_desc& d) {
   o.kd = d.kd;
   o.H = d.horizon;
   o.rel = d.feature_mode == BP_FEATURE_RELATIVE ? 1 : 0;
+  o.net = net ? 1 : 0;
   o.L = d.n_layers;
   o.d = d.ka * d.horizon;
   c.d = o.d;
@@ -502,6 +498,9 @@ Compiled compile(const bp_objective_desc& d) {
       case BP_OP_HINGE:
         dim = 1;
         need[static_cast<size_t>(nv)] = 1;  // anchored on its own output
+        // watch set = args and selves of every ReLU, SquaredDistance and PenaltyHinge
+        // (objective.cpp:64-75): full CROWN encloses the hinge from its argument's bounds
+        need[static_cast<size_t>(s.src0)] = 1;
         require_finite(s.center, static_cast<size_t>(in), "penalty_hinge center");
         if (!std::isfinite(s.radius) || s.radius < 0.0) fail(BP_INVALID_ARGUMENT, "penalty_hinge: radius must be finite and nonnegative");
         if (!std::isfinite(s.penalty) || s.penalty < 0.0) fail(BP_INVALID_ARGUMENT, "penalty_hinge: penalty must be finite and nonnegative");
@@ -641,7 +640,7 @@ Compiled compile(const bp_objective_desc& d) {
     o.tc2 = 0;
     o.tc2_rw = 0;
     o.tc2_ring = 0;
-    if (ok2) {
+    if (ok2 && !net) {
       o.tc_kbmax = kbmax;
       o.tc_npadmax = npadmax;
       o.tc_S = std::max(col, d.ks) | 1;  // odd row stride: one row per thread, conflict-free
@@ -802,6 +801,7 @@ struct bp_ctx {
   }
   void rollout(const float* actions, float* costs, float* states, int* smin, int* smax, int* fail_flags,
                long long n_rows, int rows_per_sub) {
+    if (comp.o.net) fail(BP_UNSUPPORTED, "a bare network objective is bounded, not rolled out");
     bp::RolloutArgs a{actions, costs, states, smin, smax, fail_flags, n_rows, rows_per_sub, comp.kslab, nullptr};
     static const bool want_tl = std::getenv("BP_TC_TIMELINE") != nullptr;
     const int kern = kernel();
@@ -1043,7 +1043,6 @@ void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
     }
     return;
   }
-  if (mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
   const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
   std::vector<int> use(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) use[static_cast<size_t>(i)] = c->h_failed[static_cast<size_t>(i)] ? 0 : 1;
@@ -1052,8 +1051,32 @@ void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
   bp::BoundArgs a{c->lo_d.p, c->hi_d.p, c->stat_min.p, c->stat_max.p, du,
                   c->ivl_lo.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
                   c->ivl_hi.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
-                  c->lf.get(static_cast<size_t>(n)), mode, alpha};
+                  c->lf.get(static_cast<size_t>(n)), mode, alpha, -1, 0, 0, 0, 0};
   if (c->timing) ck(cudaEventRecord(c->ev0, c->stream), "event");
+  if (mode == BP_BOUND_FULL_CROWN) {
+    // crown_node_bounds (crown.cpp:379-412): a backward pass per recorded node in
+    // ascending graph order -- per step the MLP pre-activations by layer, x_t, u_t,
+    // p_t, then the cost-op values in op order -- one CTA per (subdomain, row), each
+    // node's bounds written before any later pass reads them; hinge outputs enclosed
+    // from their argument's bounds.  Then the output pass without a stop set.
+    for (int t = 0; t < cp.o.H; ++t)
+      for (size_t k = 0; k < cp.slot_kind.size(); ++k) {
+        bp::BoundArgs na = a;
+        const int kind = cp.slot_kind[k], idx = cp.slot_index[k];
+        na.start_t = t;
+        na.start_index = idx;
+        na.start_dim = cp.slot_dim[k];
+        na.start_slot = cp.slot_off[k];
+        na.start_kind = kind == 0 ? 0 : kind == 1 ? 1 : kind == 2 ? 2 : kind == 3 ? 3 : 4;
+        if (kind == 4 && cp.o.ops[idx].kind == BP_OP_HINGE) {
+          na.start_dim = n;
+          ck(bp::launch_hinge_bounds(c->dev(), na, t, idx, c->stream), "hinge bounds launch");
+        } else {
+          ck(bp::launch_bound(c->dev(), na, n, c->stream), "crown node pass launch");
+        }
+        ++c->launches;
+      }
+  }
   ck(bp::launch_bound(c->dev(), a, n, c->stream), "bound launch");
   if (c->timing) ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
@@ -1870,8 +1893,6 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
   return guard([&] {
     check_loaded(ctx);
     if (n_boxes <= 0) fail(BP_INVALID_ARGUMENT, "bp_bound_boxes: no boxes");
-    if (mode == BP_BOUND_FULL_CROWN && !ctx->comp.synth)
-      fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
     const int d = ctx->comp.d;
     const size_t nd = static_cast<size_t>(n_boxes) * d;
     for (size_t i = 0; i < nd; ++i)
@@ -1884,6 +1905,17 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
     ctx->h_failed.assign(static_cast<size_t>(n_boxes), 1);
     ctx->reports.clear();
     device_batch_bound(ctx, mode, alpha, lf);
+  });
+}
+
+bp_status bp_node_bounds(bp_ctx* ctx, double* lo, double* hi) {
+  return guard([&] {
+    check_loaded(ctx);
+    const size_t n = static_cast<size_t>(ctx->n) * ctx->comp.o.H * ctx->comp.o.SP;
+    if (n == 0) return;
+    ck(memcpy_counted(lo, ctx->ivl_lo.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(memcpy_counted(hi, ctx->ivl_hi.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
 

@@ -19,7 +19,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _capi
-from ._capi import (BP_FEATURE_ABSOLUTE, BP_FEATURE_RELATIVE, BP_OP_HINGE, BP_OP_LINEAR, BP_OP_RELU,
+from ._capi import (BP_FEATURE_ABSOLUTE, BP_FEATURE_NETWORK, BP_FEATURE_RELATIVE, BP_OP_HINGE, BP_OP_LINEAR, BP_OP_RELU,
                     BP_OP_SCALAR_AFFINE, BP_OP_SLICE, BP_OP_SQDIST, BP_OP_SUM, BP_STOP_CUSTOM,
                     BP_STOP_LAST_RELU, BP_VAL_OP0, BP_VAL_P, BP_VAL_U, BP_VAL_X)
 
@@ -171,6 +171,21 @@ def build_objective(model, s) -> ObjectiveSpec:
         W=list(model.W), b=list(model.b), relu=list(model.relu), x0=s.x0, p0=s.p0,
         u_lower=s.u_lower, u_upper=s.u_upper,
         step_weight=np.array([s.tracking_weight(t) for t in range(1, H + 1)]), ops=ops)
+
+
+def build_network_objective(model, lower, upper) -> ObjectiveSpec:
+    """build_network_objective (model.cpp:389-405): the bare network over an input box,
+    its scalar output the objective -- one step, the MLP reads the box only."""
+    if model.output_dim != 1:
+        raise ValueError("build_network_objective: network output must be scalar")
+    lo = np.asarray(lower, dtype=np.float64).reshape(-1)
+    hi = np.asarray(upper, dtype=np.float64).reshape(-1)
+    if lo.size != model.input_dim or hi.size != model.input_dim:
+        raise ValueError("lower_bound: box dim mismatch")
+    n = model.input_dim
+    return ObjectiveSpec(ks=1, ka=n, kd=n, horizon=1, feature_mode=BP_FEATURE_NETWORK,
+                         W=list(model.W), b=list(model.b), relu=list(model.relu), x0=np.zeros(1), p0=np.zeros(n),
+                         u_lower=lo, u_upper=hi, step_weight=np.ones(1), ops=[Op(BP_OP_SUM, X, dim=1, is_term=True)])
 
 
 def round_spec_to_f32(spec: ObjectiveSpec) -> ObjectiveSpec:
