@@ -227,6 +227,12 @@ bp_status bp_batch_bound(bp_ctx* ctx, int mode, int alpha, double* lf);
 bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const double* hi, int mode, int alpha,
                          double* lf);
 
+/* d objective / d actions for n_rows action sequences (Objective::gradient,
+ * objective.hpp:61-62: reverse mode over the unrolled graph, graph.cpp:403-564, or the
+ * synthetic objective's elementwise derivative, objective.cpp:100-107).  FP64 on the
+ * device, returned as FP32; drives the GD searcher (search.cpp:214-245). */
+bp_status bp_gradient(bp_ctx* ctx, int64_t n_rows, const float* actions, float* grad);
+
 /* The intermediate (node) bounds the last bound call used, in the stat layout
  * [n_boxes][H][per_step]: the interval pass (interval modes, failed searches) or the
  * full-CROWN node passes (crown_node_bounds, crown.cpp:379-412).  Diagnostic. */

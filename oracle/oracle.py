@@ -321,6 +321,12 @@ class Objective:
                                 vp(stats.h) if stats else None, ALPHAS[alpha], C.byref(out)))
         return out.value
 
+    def gradient(self, batch):
+        b = _d(np.atleast_2d(batch))
+        out = np.zeros_like(b)
+        ck(lib().or_objective_gradient(self.h, b.ctypes.data_as(dp), C.c_int(b.shape[0]), out.ctypes.data_as(dp)))
+        return out
+
     def crown_node_stats(self, lo, hi, ids, alpha="adaptive") -> Stats:
         """crown_node_bounds (crown.cpp:379-412) for the given nodes, as watch stats."""
         lo, hi = _d(lo), _d(hi)

@@ -416,6 +416,15 @@ int or_graph_evaluate(void* g, const double* batch, int rows, int cols, double* 
     std::copy(v.begin(), v.end(), out);
   });
 }
+// Objective::gradient (objective.hpp:61-62; graph.cpp:403-564 / objective.cpp:100-107).
+int or_objective_gradient(void* h, const double* batch, int rows, double* out) {
+  return guard([&] {
+    const int d = O->obj->dim();
+    const Mat m = O->obj->gradient(mat_of(batch, rows, d));
+    for (int i = 0; i < rows; ++i)
+      for (int j = 0; j < d; ++j) out[static_cast<size_t>(i) * d + j] = m(i, j);
+  });
+}
 int or_graph_gradient(void* g, const double* batch, int rows, int cols, double* out) {
   return guard([&] {
     const Mat m = gradient(*static_cast<CompGraph*>(g), mat_of(batch, rows, cols));

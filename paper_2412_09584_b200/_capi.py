@@ -89,7 +89,7 @@ class PoolMeta(C.Structure):
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
-    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds",
+    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds", "bp_gradient",
     "bp_load_objective", "bp_load_synthetic",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
@@ -128,6 +128,7 @@ def load() -> C.CDLL:
             "bp_set_rollout_path": (C.c_int, [vp, C.c_int, _ip]),
             "bp_rollout_info": (C.c_int, [vp, _ip, _ip, _ip, C.POINTER(C.c_int64)]),
             "bp_node_bounds": (C.c_int, [vp, _dp, _dp]),
+            "bp_gradient": (C.c_int, [vp, C.c_int64, _fp, _fp]),
             "bp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_load_objective": (C.c_int, [vp, C.POINTER(ObjectiveDesc)]),
             "bp_load_synthetic": (C.c_int, [vp, C.c_int]),

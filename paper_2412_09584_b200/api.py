@@ -158,6 +158,13 @@ class Device:
                                       _ALPHA[_config._parse_enum(_ALPHA, alpha, "alpha policy")], _capi.dptr(lf)))
         return lf
 
+    def gradient(self, actions: np.ndarray) -> np.ndarray:
+        """d objective / d actions per row (Objective::gradient), FP64 on the device."""
+        a = np.ascontiguousarray(np.atleast_2d(actions), dtype=np.float32)
+        g = np.zeros_like(a)
+        check(self.lib.bp_gradient(self.h, a.shape[0], _capi.fptr(a), _capi.fptr(g)))
+        return g
+
     def node_bounds(self, n_boxes: int):
         """The intermediate bounds of the last bound call, (n_boxes, H, per_step) lo / hi."""
         per, _ = self.stat_layout()

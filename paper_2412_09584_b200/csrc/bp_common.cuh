@@ -94,6 +94,45 @@ struct BoundArgs {
   int start_t, start_index, start_dim, start_slot;
 };
 
+// K3/K4/K5 launch arguments (search.cu; built by host.cu).
+struct SearchArgs {
+  int n, d, rows, n_samp;        // rows = n_samp + 1 (incumbent row); GD: rows = n_samp = starts
+  int method;                    // 0 CEM, 1 MPPI, 2 GD
+  int groups, per_group;         // CEM agents / MPPI instances, samples per group
+  int elites;
+  int top_cap;
+  int iter;
+  const unsigned long long* seeds;  // [n] derived per-box seeds
+  const float* lo;               // [n][d]
+  const float* hi;
+  const float* warm;             // [n][d] or null; NaN first coordinate = none
+  float* mu;                     // [n][groups][d]
+  float* var;                    // [n][groups][d] (CEM)
+  float* var_floor;              // [n][d] (CEM)
+  float* best;                   // [n][d]
+  float* uf;                     // [n]
+  float* actions;                // [n][rows][d]
+  const float* costs;            // [n][rows]
+  int* failed;                   // [n]
+  float* top_val[2];             // [n][top_cap]
+  int* top_seq[2];
+  float* top_act[2];             // [n][top_cap][d]
+  int* top_cnt;                  // [n]
+  int cur;                       // which top buffer holds the current list
+  // CEM
+  float jitter, init_sigma;
+  // MPPI
+  float noise_frac, temperature;
+  const float* noise_ratios;     // [n_noise]
+  const float* temp_ratios;      // [n_temp]
+  int n_noise;
+  // GD (search.cpp:214-245)
+  float gd_base_step;
+  const float* gd_ratios;        // [gd_n_ratios], assigned round-robin over the starts
+  int gd_n_ratios;
+  const float* grad;             // [n][rows][d]
+};
+
 // Order-preserving float <-> int encoding for atomicMin/atomicMax extrema.
 __device__ __forceinline__ int enc_f(float f) {
   int i = __float_as_int(f);

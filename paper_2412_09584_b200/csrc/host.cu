@@ -43,36 +43,7 @@ struct RolloutArgs {
   long long* timeline;
 };
 // BoundArgs: bp_common.cuh
-struct SearchArgs {
-  int n, d, rows, n_samp;
-  int method;
-  int groups, per_group;
-  int elites;
-  int top_cap;
-  int iter;
-  const unsigned long long* seeds;
-  const float* lo;
-  const float* hi;
-  const float* warm;
-  float* mu;
-  float* var;
-  float* var_floor;
-  float* best;
-  float* uf;
-  float* actions;
-  const float* costs;
-  int* failed;
-  float* top_val[2];
-  int* top_seq[2];
-  float* top_act[2];
-  int* top_cnt;
-  int cur;
-  float jitter, init_sigma;
-  float noise_frac, temperature;
-  const float* noise_ratios;
-  const float* temp_ratios;
-  int n_noise;
-};
+// SearchArgs: bp_common.cuh
 cudaError_t launch_rollout(const DevObjective& o, const RolloutArgs& a, int nq, bool stream, size_t smem, cudaStream_t st);
 cudaError_t launch_rollout_tc(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
 size_t rollout_tc_smem(const DevObjective& o);
@@ -90,6 +61,10 @@ size_t bound_smem_bytes();
 cudaError_t launch_search_init(const SearchArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const SearchArgs& a, int sms, cudaStream_t st);
 cudaError_t launch_search_update(const SearchArgs& a, cudaStream_t st);
+cudaError_t launch_gd_step(const SearchArgs& a, int sms, cudaStream_t st);
+cudaError_t launch_gradient(const DevObjective& o, const float* actions, float* grad, double* ckpt, long long n_rows,
+                            cudaStream_t st);
+cudaError_t launch_synthetic_gradient(const float* actions, float* grad, long long n, cudaStream_t st);
 size_t search_update_smem(const SearchArgs& a);
 }  // namespace bp
 
@@ -730,7 +705,8 @@ struct bp_ctx {
   int top_cap = 0;
   DBuf<unsigned long long> seeds;
   DBuf<float> lo_f, hi_f, warm_f, mu, var, var_floor, best, uf, actions, costs, top_val0, top_val1, top_act0, top_act1;
-  DBuf<float> ratios;
+  DBuf<float> ratios, grad;
+  DBuf<double> grad_ckpt;
   DBuf<int> failed, top_seq0, top_seq1, top_cnt, stat_min, stat_max, use_flags;
   DBuf<double> lo_d, hi_d, ivl_lo, ivl_hi, lf;
   DBuf<float> uf_hist;
@@ -858,13 +834,22 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   const int d = cp.d;
   if (cfg.iterations <= 0 || cfg.samples_per_iter <= 0)
     fail(BP_INVALID_ARGUMENT, "search: iterations and samples per iteration must be positive");
-  if (cfg.method == BP_SEARCH_GD) fail(BP_UNSUPPORTED, "gd search is not implemented on the device");
   bp::SearchArgs a{};
   a.n = n;
   a.d = d;
-  a.method = cfg.method == BP_SEARCH_MPPI ? 1 : 0;
+  a.method = cfg.method == BP_SEARCH_MPPI ? 1 : cfg.method == BP_SEARCH_GD ? 2 : 0;
   std::vector<float> ratios;
-  if (a.method == 0) {
+  if (a.method == 2) {  // run_gd (search.cpp:214-245): samples_per_iter starts, no incumbent row
+    a.groups = 1;
+    a.per_group = std::max(1, cfg.samples_per_iter);
+    a.elites = 1;
+    a.gd_base_step = static_cast<float>(cfg.gd_base_step);
+    if (cfg.gd_n_ratios > 0)
+      for (int i = 0; i < cfg.gd_n_ratios; ++i) ratios.push_back(static_cast<float>(cfg.gd_step_ratios[i]));
+    else
+      ratios.push_back(1.f);
+    a.gd_n_ratios = static_cast<int>(ratios.size());
+  } else if (a.method == 0) {
     a.groups = std::max(1, cfg.cem_agents);
     a.per_group = std::max(1, cfg.samples_per_iter / a.groups);
     a.elites = std::max(1, cfg.cem_elites);
@@ -880,7 +865,7 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   }
   if (a.groups > 32) fail(BP_UNSUPPORTED, "search: more than 32 agents / instances");
   a.n_samp = a.groups * a.per_group;
-  a.rows = a.n_samp + 1;
+  a.rows = a.method == 2 ? a.n_samp : a.n_samp + 1;
   a.top_cap = std::max(cfg.top_capacity, 1);
   a.jitter = static_cast<float>(cfg.cem_jitter);
   a.init_sigma = static_cast<float>(cfg.cem_init_sigma);
@@ -925,8 +910,12 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   if (!ratios.empty()) {
     float* r = c->ratios.get(ratios.size());
     ck(memcpy_counted(r, ratios.data(), ratios.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-    a.noise_ratios = r;
-    a.temp_ratios = r + a.n_noise;
+    if (a.method == 2) {
+      a.gd_ratios = r;
+    } else {
+      a.noise_ratios = r;
+      a.temp_ratios = r + a.n_noise;
+    }
   }
   a.mu = c->mu.get(static_cast<size_t>(n) * a.groups * d);
   a.var = c->var.get(static_cast<size_t>(n) * a.groups * d);
@@ -953,12 +942,28 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   ck(bp::launch_search_init(a, st), "search init");
   ++c->launches;
   a.cur = 0;
+  const long long n_rows = static_cast<long long>(n) * a.rows;
+  if (a.method == 2) a.grad = c->grad.get(static_cast<size_t>(n_rows) * d);
   for (int it = 0; it < cfg.iterations; ++it) {
     a.iter = it;
-    ck(bp::launch_sample(a, c->sms, st), "sample");
-    c->rollout(a.actions, const_cast<float*>(a.costs), nullptr, smin, smax, a.failed,
-               static_cast<long long>(n) * a.rows, a.rows);
+    if (a.method != 2 || it == 0) ck(bp::launch_sample(a, c->sms, st), "sample");
+    c->rollout(a.actions, const_cast<float*>(a.costs), nullptr, smin, smax, a.failed, n_rows, a.rows);
     ck(bp::launch_search_update(a, st), "search update");
+    if (a.method == 2 && it + 1 < cfg.iterations) {  // gradient of the consumed points, projected step
+      float* g = const_cast<float*>(a.grad);
+      if (cp.synth) {
+        ck(bp::launch_synthetic_gradient(a.actions, g, n_rows * d, st), "gradient launch");
+      } else {
+        const long long per = static_cast<long long>(cp.o.H) * cp.o.ks;
+        const long long chunk = std::max<long long>(1024, std::min<long long>(n_rows, (256ll << 20) / (8 * per)));
+        double* ckpt = c->grad_ckpt.get(static_cast<size_t>(chunk * per));
+        for (long long r0 = 0; r0 < n_rows; r0 += chunk)
+          ck(bp::launch_gradient(c->dev(), a.actions + r0 * d, g + r0 * d, ckpt, std::min(chunk, n_rows - r0), st),
+             "gradient launch");
+      }
+      ck(bp::launch_gd_step(a, c->sms, st), "gd step");
+      c->launches += 2;
+    }
     ck(memcpy_counted(ufh + static_cast<size_t>(it) * n, a.uf, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st), "D2D");
     c->launches += 2;
     a.cur ^= 1;
@@ -1905,6 +1910,34 @@ bp_status bp_bound_boxes(bp_ctx* ctx, int n_boxes, const double* lo, const doubl
     ctx->h_failed.assign(static_cast<size_t>(n_boxes), 1);
     ctx->reports.clear();
     device_batch_bound(ctx, mode, alpha, lf);
+  });
+}
+
+bp_status bp_gradient(bp_ctx* ctx, int64_t n_rows, const float* actions, float* grad) {
+  return guard([&] {
+    check_loaded(ctx);
+    const Compiled& cp = ctx->comp;
+    if (cp.o.net) fail(BP_UNSUPPORTED, "a bare network objective is bounded, not differentiated");
+    if (n_rows <= 0) return;
+    const size_t nd = static_cast<size_t>(n_rows) * cp.d;
+    for (size_t i = 0; i < nd; ++i)
+      if (!std::isfinite(actions[i])) fail(BP_INVALID_ARGUMENT, "gradient batch: non-finite values");
+    cudaStream_t st = ctx->stream;
+    float* da = ctx->r_actions.get(nd);
+    float* dg = ctx->grad.get(nd);
+    ck(memcpy_counted(da, actions, nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+    if (cp.synth) {
+      ck(bp::launch_synthetic_gradient(da, dg, static_cast<long long>(nd), st), "gradient launch");
+    } else {
+      const long long per = static_cast<long long>(cp.o.H) * cp.o.ks;
+      const long long chunk = std::max<long long>(1024, std::min<long long>(n_rows, (256ll << 20) / (8 * per)));
+      double* ckpt = ctx->grad_ckpt.get(static_cast<size_t>(chunk * per));
+      for (long long r0 = 0; r0 < n_rows; r0 += chunk)
+        ck(bp::launch_gradient(ctx->dev(), da + r0 * cp.d, dg + r0 * cp.d, ckpt, std::min<long long>(chunk, n_rows - r0), st),
+           "gradient launch");
+    }
+    ck(memcpy_counted(grad, dg, nd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 

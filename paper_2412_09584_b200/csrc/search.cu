@@ -19,38 +19,7 @@
 
 namespace bp {
 
-struct SearchArgs {
-  int n, d, rows, n_samp;        // rows = n_samp + 1 (incumbent row)
-  int method;                    // 0 CEM, 1 MPPI
-  int groups, per_group;         // CEM agents / MPPI instances, samples per group
-  int elites;
-  int top_cap;
-  int iter;
-  const unsigned long long* seeds;  // [n] derived per-box seeds
-  const float* lo;               // [n][d]
-  const float* hi;
-  const float* warm;             // [n][d] or null; NaN first coordinate = none
-  float* mu;                     // [n][groups][d]
-  float* var;                    // [n][groups][d] (CEM)
-  float* var_floor;              // [n][d] (CEM)
-  float* best;                   // [n][d]
-  float* uf;                     // [n]
-  float* actions;                // [n][rows][d]
-  const float* costs;            // [n][rows]
-  int* failed;                   // [n]
-  float* top_val[2];             // [n][top_cap]
-  int* top_seq[2];
-  float* top_act[2];             // [n][top_cap][d]
-  int* top_cnt;                  // [n]
-  int cur;                       // which top buffer holds the current list
-  // CEM
-  float jitter, init_sigma;
-  // MPPI
-  float noise_frac, temperature;
-  const float* noise_ratios;     // [n_noise]
-  const float* temp_ratios;      // [n_temp]
-  int n_noise;
-};
+// SearchArgs: bp_common.cuh
 
 namespace {
 
@@ -108,6 +77,19 @@ __global__ void sample_kernel(const SearchArgs a) {
     float* out = a.actions + (static_cast<size_t>(s) * a.rows + row) * a.d;
     const float* lo = a.lo + static_cast<size_t>(s) * a.d;
     const float* hi = a.hi + static_cast<size_t>(s) * a.d;
+    if (a.method == 2) {  // GD starts (search.cpp:226-229): row 0 the clamped warm start or centre, others U[box]
+      const uint4 r = Philox::gen(make_uint4(0xFFFFFFFEu, static_cast<uint32_t>(row), static_cast<uint32_t>(q), 3u),
+                                  key_of(a.seeds[s]));
+      const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+      for (int c = 0; c < 4; ++c) {
+        const int j = q * 4 + c;
+        if (j >= a.d) break;
+        out[j] = row == 0 ? a.best[static_cast<size_t>(s) * a.d + j]
+                          : fminf(fmaxf(lo[j] + (hi[j] - lo[j]) * (static_cast<float>(rr[c] >> 8) * (1.0f / 16777216.0f)),
+                                        lo[j]), hi[j]);
+      }
+      continue;
+    }
     if (row == a.n_samp) {  // incumbent re-injected as the last row
       for (int c = 0; c < 4; ++c) {
         const int j = q * 4 + c;
@@ -263,7 +245,8 @@ __global__ void __launch_bounds__(kThreads) search_update_kernel(const SearchArg
   }
   if (tid == 0) a.top_cnt[s] = ncnt;
 
-  // 3. refit
+  // 3. refit (GD keeps its iterates: the step kernel moves them)
+  if (a.method == 2) return;
   if (a.method == 0) {
     // CEM elites per agent: first n_el of the agent's rows in (value, row)
     // order (search.cpp:131-149); agent 0 also owns the incumbent row.
@@ -323,7 +306,33 @@ __global__ void __launch_bounds__(kThreads) search_update_kernel(const SearchArg
   }
 }
 
+// Projected gradient step of every start (search.cpp:232-239): x <- clamp(x - step_i *
+// width_j * g_j) with step_i = base_step * ratio[i mod n_ratios].
+__global__ void gd_step_kernel(const SearchArgs a) {
+  const long long total = static_cast<long long>(a.n) * a.rows * a.d;
+  for (long long w = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(w % a.d);
+    const long long sr = w / a.d;
+    const int row = static_cast<int>(sr % a.rows);
+    const int s = static_cast<int>(sr / a.rows);
+    if (a.failed[s]) continue;
+    const float lo = a.lo[static_cast<size_t>(s) * a.d + j], hi = a.hi[static_cast<size_t>(s) * a.d + j];
+    const double step = static_cast<double>(a.gd_base_step) * a.gd_ratios[row % a.gd_n_ratios];
+    const double x = static_cast<double>(a.actions[w]) - step * (static_cast<double>(hi) - lo) * a.grad[w];
+    a.actions[w] = static_cast<float>(fmin(fmax(x, static_cast<double>(lo)), static_cast<double>(hi)));
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_gd_step(const SearchArgs& a, int sms, cudaStream_t st) {
+  const long long total = static_cast<long long>(a.n) * a.rows * a.d;
+  if (total <= 0) return cudaSuccess;
+  const long long want = (total + 255) / 256;
+  gd_step_kernel<<<static_cast<unsigned>(want < 8LL * sms ? want : 8LL * sms), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_search_init(const SearchArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
