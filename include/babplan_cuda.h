@@ -166,13 +166,22 @@ bp_status bp_init(int device, bp_ctx** out);
 bp_status bp_destroy(bp_ctx* ctx);
 /* Thread-local message of the last failing call (empty when none). */
 size_t bp_get_last_error(char* buf, size_t cap);
-/* Subdomain sharding across ranks (one process per GPU).  With world > 1 the
- * planner assigns child k of every BaB iteration to rank k % world, searches
- * and bounds its own children on the device, and calls fn to allgather the
- * packed reports: fn(user, send, bytes, recv) must fill recv (world * bytes)
- * with every rank's send buffer in rank order and return 0.  The runtime's
- * hook is torch.distributed.all_gather_into_tensor over NCCL (NVLink). */
+/* Subdomain sharding across ranks (one process per GPU, replacing the
+ * reference's std::thread fan-out of batch_search, proj/src/search.cpp:262-282, and
+ * the serial bound loop, bab.cpp:392-403).  Every rank keeps the pool's heads (id,
+ * bounds, volume, width, owner) and replays pick_out / prune identically; the full
+ * records live on their owners.  With world > 1 child k of every BaB iteration is
+ * searched and bounded on rank k % world: the parent's owner splits it and ships the
+ * child record with the all-to-all hook, and the children's heads are shared with
+ * the allgather hook.  fn(user, send, bytes, recv) must fill recv (world * bytes)
+ * with every rank's send buffer in rank order; a2a(user, send, send_bytes[world],
+ * recv, recv_bytes[world]) must deliver rank r's send segment for this rank in rank
+ * order (an all-to-all-v of bytes).  Both return 0 on success.  The runtime's hooks are
+ * torch.distributed all_gather_into_tensor / all_to_all_single over NCCL (NVLink). */
 typedef int (*bp_exchange_fn)(void* user, const void* send, size_t bytes, void* recv);
+typedef int (*bp_alltoallv_fn)(void* user, const void* send, const int64_t* send_bytes, void* recv,
+                               const int64_t* recv_bytes);
+bp_status bp_set_alltoall(bp_ctx* ctx, bp_alltoallv_fn a2a);
 bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, void* user);
 
 /* Launch the context's work on an external stream (NULL = its own stream),

@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <unordered_map>
 #include <memory>
 #include <numeric>
 #include <random>
@@ -718,6 +720,7 @@ struct bp_ctx {
   // sharding: rank / world and the allgather hook (host buffers)
   int rank = 0, world = 1;
   bp_exchange_fn exchange = nullptr;
+  bp_alltoallv_fn alltoallv = nullptr;
   void* exchange_user = nullptr;
   // scratch for bp_rollout
   DBuf<float> r_actions, r_costs, r_states;
@@ -1322,122 +1325,126 @@ void merge_report(Rec& rec, Report&& rep, int top_capacity, int d) {  // bab.cpp
   }
 }
 
-// One child's search result as exchanged between ranks (fixed size).
-struct PackedReport {
-  static size_t bytes(int d, int K) { return sizeof(double) * (6 + static_cast<size_t>(d)) + sizeof(float) * static_cast<size_t>(K) * (1 + d); }
-  static void pack(unsigned char* p, int64_t index, const Report& r, double lf, int d, int K) {
-    double* h = reinterpret_cast<double*>(p);
-    const int nt = static_cast<int>(r.top_val.size());
-    h[0] = static_cast<double>(index);
-    h[1] = r.ok ? 1.0 : 0.0;
-    h[2] = static_cast<double>(r.samples);
-    h[3] = r.uf;
-    h[4] = lf;
-    h[5] = nt;
-    for (int j = 0; j < d; ++j) h[6 + j] = r.best.empty() ? std::nan("") : r.best[static_cast<size_t>(j)];
-    float* f = reinterpret_cast<float*>(h + 6 + d);
-    std::copy(r.top_val.begin(), r.top_val.end(), f);
-    std::copy(r.top_act.begin(), r.top_act.end(), f + K);
-  }
-  static int64_t unpack(const unsigned char* p, Report& r, double& lf, int d, int K) {
-    const double* h = reinterpret_cast<const double*>(p);
-    const int64_t index = static_cast<int64_t>(h[0]);
-    if (index < 0) return -1;
-    r = Report();
-    r.ok = h[1] != 0.0;
-    if (!r.ok) r.error = "evaluate: non-finite objective value (malformed weights?)";
-    r.samples = static_cast<int64_t>(h[2]);
-    r.uf = h[3];
-    lf = h[4];
-    const int nt = static_cast<int>(h[5]);
-    if (r.ok) r.best.assign(h + 6, h + 6 + d);
-    const float* f = reinterpret_cast<const float*>(h + 6 + d);
-    r.top_val.assign(f, f + nt);
-    r.top_act.assign(f + K, f + K + static_cast<size_t>(nt) * d);
-    return index;
-  }
-};
-
-std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec>& boxes, const std::vector<const std::vector<double>*>& warms,
+// Search + bound of this rank's children on the device: boxes, warm starts and the
+// children's global indices (the sampler stream key, so results do not depend on the
+// rank a child runs on).
+std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec*>& boxes, const std::vector<int64_t>& index,
                                      const bp_search_config& scfg, int mode, int alpha, std::vector<double>* lfs) {
   const int d = c->comp.d;
-  const int n_all = static_cast<int>(boxes.size());
-  const bool shard = c->world > 1 && c->exchange != nullptr && n_all > 1;
-  // children of the global pick order go round-robin to the ranks; a child's
-  // sampler stream is keyed by its global index, so results do not depend on
-  // the number of ranks.
-  std::vector<int64_t> mine;
-  for (int i = 0; i < n_all; ++i)
-    if (!shard || i % c->world == c->rank) mine.push_back(i);
-  const int n = static_cast<int>(mine.size());
+  const int n = static_cast<int>(boxes.size());
   std::vector<double> lo(static_cast<size_t>(n) * d), hi(static_cast<size_t>(n) * d), warm(static_cast<size_t>(n) * d);
   bool any_warm = false;
   for (int k = 0; k < n; ++k) {
-    const size_t i = static_cast<size_t>(mine[static_cast<size_t>(k)]);
-    std::copy(boxes[i].lo.begin(), boxes[i].lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(k) * d);
-    std::copy(boxes[i].hi.begin(), boxes[i].hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(k) * d);
-    const std::vector<double>* w = warms[i];
-    if (w != nullptr && !w->empty()) {
+    const Rec& b = *boxes[static_cast<size_t>(k)];
+    std::copy(b.lo.begin(), b.lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(k) * d);
+    std::copy(b.hi.begin(), b.hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(k) * d);
+    if (!b.best.empty()) {
       any_warm = true;
-      std::copy(w->begin(), w->end(), warm.begin() + static_cast<std::ptrdiff_t>(k) * d);
+      std::copy(b.best.begin(), b.best.end(), warm.begin() + static_cast<std::ptrdiff_t>(k) * d);
     } else {
       std::fill(warm.begin() + static_cast<std::ptrdiff_t>(k) * d, warm.begin() + static_cast<std::ptrdiff_t>(k + 1) * d,
                 std::numeric_limits<double>::quiet_NaN());
     }
   }
   std::vector<Report> reps;
-  std::vector<double> my_lf(static_cast<size_t>(n), 0.0);
+  lfs->assign(static_cast<size_t>(n), 0.0);
   const auto t0 = std::chrono::steady_clock::now();
   if (n > 0) {
-    device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps, mine.data());
-    device_batch_bound(c, mode, alpha, my_lf.data());
+    device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps, index.data());
+    device_batch_bound(c, mode, alpha, lfs->data());
   }
   c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   c->harvest_roll_events();
-  if (!shard) {
-    *lfs = std::move(my_lf);
-    return reps;
-  }
-  // allgather of the packed reports (every rank then replays the same host logic)
-  const int K = std::max(scfg.top_capacity, 1);
-  const size_t rb = PackedReport::bytes(d, K);
-  const int per_rank = (n_all + c->world - 1) / c->world;
-  std::vector<unsigned char> send(rb * static_cast<size_t>(per_rank), 0), recv(send.size() * static_cast<size_t>(c->world), 0);
-  for (int k = 0; k < per_rank; ++k) {
-    unsigned char* p = send.data() + rb * static_cast<size_t>(k);
-    if (k < n)
-      PackedReport::pack(p, mine[static_cast<size_t>(k)], reps[static_cast<size_t>(k)], my_lf[static_cast<size_t>(k)], d, K);
-    else
-      reinterpret_cast<double*>(p)[0] = -1.0;
-  }
-  if (c->exchange(c->exchange_user, send.data(), send.size(), recv.data()) != 0)
-    fail(BP_NCCL, "exchange: allgather of child reports failed");
-  std::vector<Report> all(static_cast<size_t>(n_all));
-  lfs->assign(static_cast<size_t>(n_all), 0.0);
-  std::vector<char> seen(static_cast<size_t>(n_all), 0);
-  for (size_t k = 0; k < static_cast<size_t>(per_rank) * c->world; ++k) {
-    Report r;
-    double lf = 0.0;
-    const int64_t idx = PackedReport::unpack(recv.data() + rb * k, r, lf, d, K);
-    if (idx < 0) continue;
-    if (idx >= n_all || seen[static_cast<size_t>(idx)]) fail(BP_NCCL, "exchange: inconsistent child reports");
-    seen[static_cast<size_t>(idx)] = 1;
-    all[static_cast<size_t>(idx)] = std::move(r);
-    (*lfs)[static_cast<size_t>(idx)] = lf;
-  }
-  if (std::find(seen.begin(), seen.end(), 0) != seen.end()) fail(BP_NCCL, "exchange: missing child reports");
-  return all;
+  return reps;
 }
+
+// A pool record as every rank sees it: what pick_out, the retirement
+// test, prune and the trace read.  The full record (box, best, top samples) lives only
+// on its owner rank.
+struct Head {
+  int64_t id;
+  double lf, uf, log_vol, max_width;
+  int owner;
+};
+
+// Fixed-size wire forms (doubles, then floats) of a full record (owner -> search rank)
+// and of a searched child's head + incumbent candidate (allgather).
+struct Wire {
+  static size_t rec_bytes(int d, int K) {
+    return sizeof(double) * (10 + 3 * static_cast<size_t>(d)) + sizeof(float) * static_cast<size_t>(K) * (1 + d);
+  }
+  static void put_rec(unsigned char* p, int64_t k, const Rec& r, int d, int K) {
+    double* h = reinterpret_cast<double*>(p);
+    const int nt = static_cast<int>(r.top_val.size());
+    h[0] = static_cast<double>(k);
+    h[1] = static_cast<double>(r.id);
+    h[2] = static_cast<double>(r.parent);
+    h[3] = r.depth;
+    h[4] = r.log_vol;
+    h[5] = r.lf;
+    h[6] = r.uf;
+    h[7] = static_cast<double>(r.samples);
+    h[8] = nt;
+    h[9] = r.best.empty() ? 0.0 : 1.0;
+    std::copy(r.lo.begin(), r.lo.end(), h + 10);
+    std::copy(r.hi.begin(), r.hi.end(), h + 10 + d);
+    if (!r.best.empty()) std::copy(r.best.begin(), r.best.end(), h + 10 + 2 * d);
+    float* f = reinterpret_cast<float*>(h + 10 + 3 * d);
+    std::copy(r.top_val.begin(), r.top_val.end(), f);
+    std::copy(r.top_act.begin(), r.top_act.end(), f + K);
+  }
+  static int64_t get_rec(const unsigned char* p, Rec& r, int d, int K) {
+    const double* h = reinterpret_cast<const double*>(p);
+    r = Rec();
+    r.id = static_cast<int64_t>(h[1]);
+    r.parent = static_cast<int64_t>(h[2]);
+    r.depth = static_cast<int>(h[3]);
+    r.log_vol = h[4];
+    r.lf = h[5];
+    r.uf = h[6];
+    r.samples = static_cast<int64_t>(h[7]);
+    const int nt = static_cast<int>(h[8]);
+    r.lo.assign(h + 10, h + 10 + d);
+    r.hi.assign(h + 10 + d, h + 10 + 2 * d);
+    if (h[9] != 0.0) r.best.assign(h + 10 + 2 * d, h + 10 + 3 * d);
+    const float* f = reinterpret_cast<const float*>(h + 10 + 3 * d);
+    r.top_val.assign(f, f + nt);
+    r.top_act.assign(f + K, f + K + static_cast<size_t>(nt) * d);
+    return static_cast<int64_t>(h[0]);
+  }
+  static size_t head_bytes(int d) { return sizeof(double) * (9 + static_cast<size_t>(d)); }
+  static void put_head(double* h, int64_t k, const Rec& r, int64_t rep_samples, bool ok, int d) {
+    h[0] = static_cast<double>(k);
+    h[1] = static_cast<double>(r.id);
+    h[2] = r.lf;
+    h[3] = r.uf;
+    h[4] = r.log_vol;
+    h[5] = r.max_width();
+    h[6] = static_cast<double>(rep_samples);
+    h[7] = ok ? 1.0 : 0.0;
+    h[8] = r.best.empty() ? 0.0 : 1.0;
+    for (int j = 0; j < d; ++j) h[9 + j] = r.best.empty() ? 0.0 : r.best[static_cast<size_t>(j)];
+  }
+};
 
 // plan() (bab.cpp:266-415) as a steppable object: the constructor runs the
 // root search + bound, step() one pick -> split -> search -> bound -> merge ->
 // prune iteration, finish() the result fields.
+//
+// Sharded over ranks: every rank holds the pool's heads in the same
+// order and replays pick_out / retirement / prune / trace on them identically (the
+// pick stream is the shared mt19937_64(mix_seed(seed, 1))).  Child k of an iteration
+// (global pick order) is searched on rank k % world; the owner of its parent splits
+// the parent and ships the child record there (fixed-size all-to-all); after search,
+// bound and merge only the children's heads (+ their best actions, the incumbent
+// candidates) are all-gathered.  One rank runs the same code with no exchange.
 struct Planner {
   bp_ctx* c;
   bp_planner_config cfg;
   int d;
   std::chrono::steady_clock::time_point t0;
-  std::vector<Rec> pool;
+  std::vector<Head> pool;                    // heads, pool order, identical on every rank
+  std::unordered_map<int64_t, Rec> own;      // full records owned by this rank
   bp_rng pick_rng;
   int64_t next_id = 1;
   double pruned_cum = 0.0;
@@ -1448,6 +1455,9 @@ struct Planner {
   bool done = false;
   int64_t children_bounded = 0;  // subdomains searched + bounded so far (root included)
   int last_children = 0;
+
+  int world() const { return c->world > 1 && c->exchange != nullptr ? c->world : 1; }
+  int rank() const { return world() > 1 ? c->rank : 0; }
 
   double elapsed_ms() const {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1471,49 +1481,139 @@ struct Planner {
   }
   double prune() {  // bab.cpp:225-241
     double removed = 0.0;
-    std::vector<Rec> keep;
+    std::vector<Head> keep;
     keep.reserve(pool.size());
     for (auto& r : pool) {
-      if (r.lf > result.uf)
+      if (r.lf > result.uf) {
         removed += std::exp(r.log_vol);
-      else
-        keep.push_back(std::move(r));
+        own.erase(r.id);
+      } else {
+        keep.push_back(r);
+      }
     }
     pool = std::move(keep);
     return removed;
   }
 
+  // Search, bound and merge the children of one iteration (global order; child k runs on
+  // rank k % world).  `local` holds this rank's child records (by k); afterwards every
+  // rank appends all children's heads in order and updates the incumbent as the
+  // reference's sequential loop does (bab.cpp:388-403).
+  void run_children(int n_all, std::map<int64_t, Rec>& local, uint64_t seed) {
+    const int W = world(), R = rank();
+    std::vector<Rec*> boxes;
+    std::vector<int64_t> index;
+    for (auto& kv : local) {
+      boxes.push_back(&kv.second);
+      index.push_back(kv.first);
+    }
+    bp_search_config scfg = cfg.search;
+    scfg.seed = seed;
+    std::vector<double> lfs;
+    std::vector<Report> reps = search_and_bound(c, boxes, index, scfg, cfg.bound_mode, cfg.alpha, &lfs);
+    std::vector<int64_t> rep_samples(boxes.size());
+    std::vector<char> rep_ok(boxes.size());
+    parallel_for(static_cast<int>(boxes.size()), [&](int i) {
+      rep_samples[static_cast<size_t>(i)] = reps[static_cast<size_t>(i)].samples;
+      rep_ok[static_cast<size_t>(i)] = reps[static_cast<size_t>(i)].ok ? 1 : 0;
+      boxes[static_cast<size_t>(i)]->lf = lfs[static_cast<size_t>(i)];
+      merge_report(*boxes[static_cast<size_t>(i)], std::move(reps[static_cast<size_t>(i)]), cfg.search.top_capacity, d);
+    });
+    // heads of every child, in global order
+    const size_t hb = Wire::head_bytes(d) / sizeof(double);
+    std::vector<double> heads(static_cast<size_t>(n_all) * hb, 0.0);
+    if (W == 1) {
+      for (size_t i = 0; i < boxes.size(); ++i)
+        Wire::put_head(heads.data() + static_cast<size_t>(index[i]) * hb, index[i], *boxes[i], rep_samples[i], rep_ok[i], d);
+    } else {
+      const int per_rank = (n_all + W - 1) / W;
+      std::vector<double> send(static_cast<size_t>(per_rank) * hb, -1.0), recv(send.size() * static_cast<size_t>(W));
+      for (size_t i = 0; i < boxes.size(); ++i)
+        Wire::put_head(send.data() + i * hb, index[i], *boxes[i], rep_samples[i], rep_ok[i], d);
+      if (c->exchange(c->exchange_user, send.data(), send.size() * sizeof(double), recv.data()) != 0)
+        fail(BP_NCCL, "exchange: allgather of child heads failed");
+      std::vector<char> seen(static_cast<size_t>(n_all), 0);
+      for (size_t q = 0; q < static_cast<size_t>(per_rank) * W; ++q) {
+        const double* h = recv.data() + q * hb;
+        if (h[0] < 0.0) continue;
+        const int64_t k = static_cast<int64_t>(h[0]);
+        if (k >= n_all || seen[static_cast<size_t>(k)]) fail(BP_NCCL, "exchange: inconsistent child heads");
+        seen[static_cast<size_t>(k)] = 1;
+        std::copy(h, h + hb, heads.data() + static_cast<size_t>(k) * hb);
+      }
+      if (std::find(seen.begin(), seen.end(), 0) != seen.end()) fail(BP_NCCL, "exchange: missing child heads");
+    }
+    for (int k = 0; k < n_all; ++k) {
+      const double* h = heads.data() + static_cast<size_t>(k) * hb;
+      Head hd{static_cast<int64_t>(h[1]), h[2], h[3], h[4], h[5], k % W};
+      result.samples += static_cast<int64_t>(h[6]);
+      if (hd.uf < result.uf) {
+        result.uf = hd.uf;
+        result.best.assign(h + 9, h + 9 + d);
+      }
+      pool.push_back(hd);
+    }
+    for (auto& kv : local) {
+      const int64_t id = kv.second.id;
+      own.emplace(id, std::move(kv.second));
+    }
+    children_bounded += n_all;
+  }
+
   Planner(bp_ctx* ctx, const bp_planner_config& config, const double* warm_start)
       : c(ctx), cfg(config), d(ctx->comp.d), t0(std::chrono::steady_clock::now()), pick_rng(mix_seed(config.seed, 1)) {
     if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
-    if (cfg.bound_mode == BP_BOUND_FULL_CROWN) fail(BP_UNSUPPORTED, "full-crown bounds are not implemented on the device");
-    Rec root;
-    root.lo.resize(static_cast<size_t>(d));
-    root.hi.resize(static_cast<size_t>(d));
-    for (int t = 0; t < c->comp.o.H; ++t)
-      for (int j = 0; j < c->comp.o.ka; ++j) {
-        root.lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
-        root.hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
-      }
-    std::vector<double> w;
-    if (warm_start) w.assign(warm_start, warm_start + d);
-    bp_search_config scfg = cfg.search;
-    scfg.seed = mix_seed(cfg.seed, 0);
-    std::vector<double> lfs;
-    std::vector<Report> reps = search_and_bound(c, {root}, {warm_start ? &w : nullptr}, scfg, cfg.bound_mode, cfg.alpha, &lfs);
-    if (!reps[0].ok) fail(BP_RUNTIME, "plan: root search failed: " + reps[0].error);
-    root.id = 0;
-    root.log_vol = 0.0;
-    root.lf = lfs[0];
-    merge_report(root, std::move(reps[0]), cfg.search.top_capacity, d);
-    result.uf = root.uf;
-    result.best = root.best;
-    result.samples = root.samples;
-    pool.push_back(std::move(root));
-    children_bounded = 1;
+    std::map<int64_t, Rec> local;
+    int64_t samples = 0;
+    if (rank() == 0) {  // the root is child 0 of the root search: rank 0 searches it
+      Rec root;
+      root.lo.resize(static_cast<size_t>(d));
+      root.hi.resize(static_cast<size_t>(d));
+      for (int t = 0; t < c->comp.o.H; ++t)
+        for (int j = 0; j < c->comp.o.ka; ++j) {
+          root.lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
+          root.hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
+        }
+      if (warm_start) root.best.assign(warm_start, warm_start + d);  // search warm start only
+      bp_search_config scfg = cfg.search;
+      scfg.seed = mix_seed(cfg.seed, 0);
+      std::vector<double> lfs;
+      std::vector<Rec*> boxes{&root};
+      std::vector<Report> reps = search_and_bound(c, boxes, {0}, scfg, cfg.bound_mode, cfg.alpha, &lfs);
+      if (!reps[0].ok) fail(BP_RUNTIME, "plan: root search failed: " + reps[0].error);
+      root.best.clear();
+      root.id = 0;
+      root.log_vol = 0.0;
+      root.lf = lfs[0];
+      samples = reps[0].samples;
+      merge_report(root, std::move(reps[0]), cfg.search.top_capacity, d);
+      local.emplace(0, std::move(root));
+    }
+    root_heads(local, samples);
     last_children = 1;
     pruned_cum += prune();
     push_trace(0, 1.0);
+  }
+
+  // The root's head (and incumbent) from rank 0 to every rank.
+  void root_heads(std::map<int64_t, Rec>& local, int64_t samples) {
+    const int W = world();
+    const size_t hb = Wire::head_bytes(d) / sizeof(double);
+    std::vector<double> h(hb, -1.0);
+    if (rank() == 0) Wire::put_head(h.data(), 0, local.begin()->second, samples, true, d);
+    if (W > 1) {
+      std::vector<double> recv(hb * static_cast<size_t>(W));
+      if (c->exchange(c->exchange_user, h.data(), hb * sizeof(double), recv.data()) != 0)
+        fail(BP_NCCL, "exchange: allgather of the root head failed");
+      std::copy(recv.begin(), recv.begin() + static_cast<std::ptrdiff_t>(hb), h.begin());  // rank 0's
+    }
+    Head hd{static_cast<int64_t>(h[1]), h[2], h[3], h[4], h[5], 0};
+    result.uf = hd.uf;
+    result.best.assign(h.begin() + 9, h.begin() + 9 + d);
+    result.samples = static_cast<int64_t>(h[6]);
+    pool.push_back(hd);
+    if (rank() == 0) own.emplace(0, std::move(local.begin()->second));
+    children_bounded = 1;
   }
 
   // One BaB iteration; returns false (and records the stop reason) when the
@@ -1529,63 +1629,111 @@ struct Planner {
       return false;
     }
     ++iter;
+    const int W = world(), R = rank();
     std::vector<bp_pool_meta> meta(pool.size());
     for (size_t i = 0; i < pool.size(); ++i) meta[i] = {pool[i].lf, pool[i].uf, pool[i].id, pool[i].log_vol};
     const std::vector<int> chosen = pick_indices(meta.data(), static_cast<int>(pool.size()), cfg.batch, cfg.eta, cfg.temperature, pick_rng);
     std::vector<char> taken(pool.size(), 0);
-    std::vector<Rec> picked;
+    std::vector<Head> picked;
     for (int idx : chosen) {
       taken[static_cast<size_t>(idx)] = 1;
-      picked.push_back(std::move(pool[static_cast<size_t>(idx)]));
+      picked.push_back(pool[static_cast<size_t>(idx)]);
     }
     {
-      std::vector<Rec> keep;
+      std::vector<Head> keep;
       for (size_t i = 0; i < pool.size(); ++i)
-        if (!taken[i]) keep.push_back(std::move(pool[i]));
+        if (!taken[i]) keep.push_back(pool[i]);
       pool = std::move(keep);
     }
     double selected_vol = 0.0;
     for (const auto& r : picked) selected_vol += std::exp(r.log_vol);
-    std::vector<Rec*> to_split;
-    for (Rec& rec : picked) {
-      if (rec.max_width() <= cfg.min_width) {
-        retired_min_lf = std::min(retired_min_lf, rec.lf);
+    std::vector<Head> to_split;
+    for (const Head& h : picked) {
+      if (h.max_width <= cfg.min_width) {
+        retired_min_lf = std::min(retired_min_lf, h.lf);
+        own.erase(h.id);
         continue;
       }
-      to_split.push_back(&rec);
+      to_split.push_back(h);
     }
-    std::vector<Rec> children(2 * to_split.size());
-    parallel_for(static_cast<int>(to_split.size()), [&](int i) {  // ids by pick order, as the serial loop
-      split_rec(*to_split[static_cast<size_t>(i)], d, cfg.top_percent, cfg.min_width, next_id + 2 * i, cfg.split_rule,
-                children[2 * static_cast<size_t>(i)], children[2 * static_cast<size_t>(i) + 1]);
+    const int n_all = 2 * static_cast<int>(to_split.size());
+    // the owners split their picked parents; child k goes to rank k % W
+    std::vector<int> mine_par;
+    for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
+      if (to_split[static_cast<size_t>(i)].owner == R) mine_par.push_back(i);
+    std::vector<Rec> kids(2 * mine_par.size());
+    parallel_for(static_cast<int>(mine_par.size()), [&](int q) {  // ids by pick order, as the serial loop
+      const int i = mine_par[static_cast<size_t>(q)];
+      const Rec& par = own.at(to_split[static_cast<size_t>(i)].id);
+      split_rec(par, d, cfg.top_percent, cfg.min_width, next_id + 2 * i, cfg.split_rule, kids[2 * static_cast<size_t>(q)],
+                kids[2 * static_cast<size_t>(q) + 1]);
     });
-    next_id += 2 * static_cast<int64_t>(to_split.size());
-    last_children = static_cast<int>(children.size());
-    if (!children.empty()) {
-      std::vector<const std::vector<double>*> warms;
-      for (const auto& ch : children) warms.push_back(ch.best.empty() ? nullptr : &ch.best);
-      bp_search_config scfg = cfg.search;
-      scfg.seed = mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1);
-      std::vector<double> lfs;
-      std::vector<Report> reps = search_and_bound(c, children, warms, scfg, cfg.bound_mode, cfg.alpha, &lfs);
-      parallel_for(static_cast<int>(children.size()), [&](int i) {
-        children[static_cast<size_t>(i)].lf = lfs[static_cast<size_t>(i)];
-        merge_report(children[static_cast<size_t>(i)], std::move(reps[static_cast<size_t>(i)]), cfg.search.top_capacity, d);
-      });
-      for (size_t i = 0; i < children.size(); ++i) {
-        Rec& ch = children[i];
-        result.samples += reps[i].samples;
-        if (ch.uf < result.uf) {
-          result.uf = ch.uf;
-          result.best = ch.best;
-        }
-        pool.push_back(std::move(ch));
+    for (int i : mine_par) own.erase(to_split[static_cast<size_t>(i)].id);
+    next_id += n_all;
+    last_children = n_all;
+    std::map<int64_t, Rec> local;  // this rank's children, by global index
+    if (W == 1) {
+      for (size_t q = 0; q < mine_par.size(); ++q) {
+        local.emplace(2 * static_cast<int64_t>(mine_par[q]), std::move(kids[2 * q]));
+        local.emplace(2 * static_cast<int64_t>(mine_par[q]) + 1, std::move(kids[2 * q + 1]));
       }
-      children_bounded += static_cast<int64_t>(children.size());
+    } else if (n_all > 0) {
+      ship_children(to_split, mine_par, kids, local);
     }
+    if (n_all > 0) run_children(n_all, local, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1));
     pruned_cum += prune();
     push_trace(iter, selected_vol);
     return true;
+  }
+
+  // Child records from their parent's owner to their search rank: a fixed-size
+  // all-to-all whose counts every rank derives from the replicated heads.
+  void ship_children(const std::vector<Head>& to_split, const std::vector<int>& mine_par, std::vector<Rec>& kids,
+                     std::map<int64_t, Rec>& local) {
+    const int W = world(), R = rank();
+    const int K = std::max(cfg.search.top_capacity, 1);
+    const size_t rb = Wire::rec_bytes(d, K);
+    std::vector<std::vector<int64_t>> out(static_cast<size_t>(W));  // child indices this rank sends to r
+    std::vector<int64_t> in_count(static_cast<size_t>(W), 0);      // records this rank receives from r
+    for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
+      for (int b = 0; b < 2; ++b) {
+        const int64_t k = 2 * static_cast<int64_t>(i) + b;
+        const int dst = static_cast<int>(k % W), src = to_split[static_cast<size_t>(i)].owner;
+        if (src == R && dst != R) out[static_cast<size_t>(dst)].push_back(k);
+        if (dst == R && src != R) ++in_count[static_cast<size_t>(src)];
+      }
+    std::map<int64_t, Rec*> by_k;
+    for (size_t q = 0; q < mine_par.size(); ++q) {
+      by_k[2 * static_cast<int64_t>(mine_par[q])] = &kids[2 * q];
+      by_k[2 * static_cast<int64_t>(mine_par[q]) + 1] = &kids[2 * q + 1];
+    }
+    std::vector<int64_t> sb(static_cast<size_t>(W)), rbts(static_cast<size_t>(W));
+    size_t s_total = 0, r_total = 0;
+    for (int r = 0; r < W; ++r) {
+      sb[static_cast<size_t>(r)] = static_cast<int64_t>(out[static_cast<size_t>(r)].size() * rb);
+      rbts[static_cast<size_t>(r)] = static_cast<int64_t>(in_count[static_cast<size_t>(r)] * static_cast<int64_t>(rb));
+      s_total += static_cast<size_t>(sb[static_cast<size_t>(r)]);
+      r_total += static_cast<size_t>(rbts[static_cast<size_t>(r)]);
+    }
+    std::vector<unsigned char> send(std::max<size_t>(s_total, 1)), recv(std::max<size_t>(r_total, 1));
+    {
+      size_t off = 0;
+      for (int r = 0; r < W; ++r)
+        for (int64_t k : out[static_cast<size_t>(r)]) {
+          Wire::put_rec(send.data() + off, k, *by_k.at(k), d, K);
+          off += rb;
+        }
+    }
+    if (c->alltoallv == nullptr) fail(BP_NCCL, "exchange: no all-to-all hook for the sharded pool");
+    if (c->alltoallv(c->exchange_user, send.data(), sb.data(), recv.data(), rbts.data()) != 0)
+      fail(BP_NCCL, "exchange: all-to-all of child records failed");
+    for (size_t off = 0; off + rb <= r_total; off += rb) {
+      Rec r;
+      const int64_t k = Wire::get_rec(recv.data() + off, r, d, K);
+      local.emplace(k, std::move(r));
+    }
+    for (auto& kv : by_k)
+      if (kv.first % W == R) local.emplace(kv.first, std::move(*kv.second));
   }
 
   void finish() {
@@ -1686,6 +1834,13 @@ bp_status bp_destroy(bp_ctx* ctx) {
       cudaSetDevice(ctx->device);
       delete ctx;
     }
+  });
+}
+
+bp_status bp_set_alltoall(bp_ctx* ctx, bp_alltoallv_fn fn) {
+  return guard([&] {
+    check_ctx(ctx);
+    ctx->alltoallv = fn;
   });
 }
 

@@ -1,12 +1,14 @@
 """Multi-GPU runtime: one process per GPU, torch.distributed as the plumbing.
 
 The planner shards every BaB iteration's children round-robin over the ranks
-(child k -> rank k % world) and exchanges the packed per-child reports once
-per iteration with an allgather (bp_set_exchange in include/babplan_cuda.h).
-Every rank then replays the identical host pick / split / merge / prune on
-the same data, so the picks are bit-exact to the single-GPU order; each
-child's sampler stream is keyed by its global index, so the whole run is
-independent of the number of GPUs.
+(child k -> rank k % world).  Every rank keeps the pool's heads
+(id, bounds, volume, width, owner) and replays pick_out / prune identically, so
+the picks are bit-exact to the single-GPU order; full records (box, best, top
+samples) live on their owner.  Per iteration: the owner of each picked parent
+splits it and ships the child records to their search ranks (all-to-all), then
+the children's heads are all-gathered (bp_set_exchange / bp_set_alltoall in
+include/babplan_cuda.h).  Each child's sampler stream is keyed by its global
+index, so the whole run is independent of the number of GPUs.
 
 The exchange goes over NCCL (NVLink 5 / NVSwitch) when the process group is
 NCCL, or gloo for the CPU / same-GPU tests.
@@ -36,6 +38,7 @@ class Exchange:
         self.bytes_sent = 0
         self.calls = 0
         self.c_fn = _capi.EXCHANGE_FN(self._call)
+        self.c_a2a = _capi.ALLTOALL_FN(self._a2a)
 
     def allgather(self, send: np.ndarray) -> np.ndarray:
         torch = self.torch
@@ -43,6 +46,28 @@ class Exchange:
         out = torch.empty(self.world * t.numel(), dtype=torch.uint8, device=self.device)
         self.dist.all_gather_into_tensor(out, t, group=self.group)
         return out.cpu().numpy()
+
+    def alltoallv(self, send: np.ndarray, send_bytes, recv_bytes) -> np.ndarray:
+        torch = self.torch
+        t = torch.from_numpy(np.ascontiguousarray(send, dtype=np.uint8)).to(self.device)
+        out = torch.empty(int(sum(recv_bytes)), dtype=torch.uint8, device=self.device)
+        self.dist.all_to_all_single(out, t, [int(x) for x in recv_bytes], [int(x) for x in send_bytes], group=self.group)
+        return out.cpu().numpy()
+
+    def _a2a(self, user, send_ptr, send_bytes_ptr, recv_ptr, recv_bytes_ptr) -> int:
+        try:
+            sb = [send_bytes_ptr[i] for i in range(self.world)]
+            rb = [recv_bytes_ptr[i] for i in range(self.world)]
+            total = int(sum(sb))
+            send = np.ctypeslib.as_array((C.c_ubyte * max(total, 1)).from_address(send_ptr))[:total]
+            got = self.alltoallv(send, sb, rb)
+            if got.nbytes:
+                C.memmove(recv_ptr, got.ctypes.data, got.nbytes)
+            self.bytes_sent += total
+            self.calls += 1
+            return 0
+        except Exception:  # never raise through the C-ABI
+            return 1
 
     def _call(self, user, send_ptr, nbytes, recv_ptr) -> int:
         try:
@@ -69,5 +94,6 @@ def attach(dev, group=None) -> Optional[Exchange]:
         return None
     ex = Exchange(group)
     _capi.check(dev.lib.bp_set_exchange(dev.h, ex.rank, ex.world, ex.c_fn, None))
+    _capi.check(dev.lib.bp_set_alltoall(dev.h, ex.c_a2a))
     dev._exchange = ex  # keep the callback alive as long as the device
     return ex

@@ -167,3 +167,21 @@ def test_network_lower_bound_rejects_bad_inputs():
         bp.network_lower_bound(m, np.zeros(2), np.ones(2))  # box dim mismatch
     with pytest.raises(ValueError):
         bp.network_lower_bound(m, np.ones(3), np.zeros(3))  # inverted box
+
+
+def test_plan_with_full_crown_is_certified(device):
+    """plan() in the sound full-CROWN mode: a certified bracket (bab.cpp:410, crown.cpp:326)."""
+    import json
+    from paper_2412_09584_b200.config import from_json
+    spec = spec_of("c1")
+    dev = device.load(spec)
+    cfg = json.loads(bp.default_config())
+    cfg["bound_mode"] = "full-crown"
+    cfg["batch"] = 4
+    cfg["termination"]["max_iterations"] = 3
+    cfg["search"]["samples_per_iter"] = 64
+    cfg["search"]["iterations"] = 3
+    res = dev.plan(from_json(json.dumps(cfg)))
+    assert res["certified"] and res["lower_bound"] <= res["objective"] + 1e-9
+    lo, hi = spec.box()
+    assert res["lower_bound"] >= orc.Objective(spec).lower_bound(lo, hi, mode="full-crown") - 1e-9

@@ -1,6 +1,8 @@
-"""Sharded planner on the GPU: two ranks (processes) on one B200 exchanging the
-per-child reports over gloo must reproduce the single-process plan exactly
-(children keyed by global index, identical host decisions on every rank)."""
+"""Sharded planner on the GPU: two and three ranks (processes) on one B200 over
+gloo -- replicated pool heads, child records shipped from their parent's owner
+to their search rank (all-to-all), children's heads all-gathered -- must
+reproduce the single-process plan exactly (children keyed by global index,
+identical host decisions on every rank)."""
 import os
 import socket
 
@@ -24,7 +26,7 @@ def _cfg():
     wl = workloads.c1()
     cfg = wl.planner_config()
     cfg["batch"] = 8
-    cfg["termination"]["max_iterations"] = 4
+    cfg["termination"]["max_iterations"] = 5
     cfg["search"]["samples_per_iter"] = 128
     cfg["search"]["iterations"] = 4
     return wl, cfg
@@ -50,7 +52,8 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(300)
-def test_two_ranks_reproduce_single_process_plan():
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_reproduce_single_process_plan(world):
     import paper_2412_09584_b200 as bp
 
     wl, cfg = _cfg()
@@ -58,14 +61,14 @@ def test_two_ranks_reproduce_single_process_plan():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = sorted(q.get(timeout=250) for _ in ps)
     for p in ps:
         p.join(timeout=60)
     for rank, obj, act, uf, mlf, pool, samples, calls in res:
-        assert calls == 4  # one exchange per BaB iteration
+        assert calls == 1 + 2 * 5  # root head; per iteration one all-to-all and one allgather
         assert obj == single["objective"] and np.array_equal(act, single["action"])
         assert uf == single["trace"]["uf"] and mlf == single["trace"]["min_lf"]
         assert pool == single["trace"]["pool_size"] and samples == single["samples"]

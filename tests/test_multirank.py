@@ -37,7 +37,16 @@ def _worker(rank, world, port, q):
         got = ex.allgather(np.array(mine + [255] * (6 - len(mine)), dtype=np.uint8))
         covered = sorted(int(x) for x in got if x != 255)
         ok2 = covered == list(range(11))
-        q.put((rank, bool(ok1), bool(ok2)))
+        # all-to-all-v through the ctypes callback: rank r sends (r+1)*10 + dst, dst+1 bytes to dst
+        sb = np.array([dst + 1 for dst in range(world)], dtype=np.int64)
+        send = np.concatenate([np.full(dst + 1, (rank + 1) * 10 + dst, dtype=np.uint8) for dst in range(world)])
+        rb = np.array([rank + 1] * world, dtype=np.int64)
+        recv = np.zeros(int(rb.sum()), dtype=np.uint8)
+        rc = ex.c_a2a(None, send.ctypes.data, sb.ctypes.data_as(C.POINTER(C.c_int64)), recv.ctypes.data,
+                      rb.ctypes.data_as(C.POINTER(C.c_int64)))
+        want = np.concatenate([np.full(rank + 1, (src + 1) * 10 + rank, dtype=np.uint8) for src in range(world)])
+        ok3 = rc == 0 and np.array_equal(recv, want)
+        q.put((rank, bool(ok1), bool(ok2 and ok3)))
     finally:
         dist.destroy_process_group()
 
