@@ -277,15 +277,9 @@ __device__ __forceinline__ void warp_chunk_extrema(const RolloutArgs& a, const f
 // tensor core reads its top 19 bits), lo = x - trunc(x) into the row's 128-byte
 // line of the SW128 K-block in shared memory.
 __device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_blk, int row, float (&v)[32]) {
-#ifndef BP_EXP_NOTMEM
   tmem_st32(t_hi, v);
-#endif
 #pragma unroll
-#ifdef BP_EXP_NOLO
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(__float_as_uint(v[j]) & 0x80001fffu);
-#else
   for (int j = 0; j < 32; ++j) v[j] = v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
-#endif
   float4* line = reinterpret_cast<float4*>(lo_blk + row * 128);
 #pragma unroll
   for (int q = 0; q < 8; ++q) line[q ^ (row & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -389,12 +383,6 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
                   const int s = it % kSlots;
                   lo_b[s] = at;
                   hi_b[s] = at + bytes;
-#ifdef BP_EXP_NOSTREAM
-                  if (it >= 2 * kSlots) {
-                    mbar_arrive(m.full + s);
-                    continue;
-                  }
-#endif
                   mbar_expect_tx(m.full + s, bytes);
                   bulk_g2s(m.w + at, src + part * nr * 32, bytes, m.full + s);
                 }
@@ -617,16 +605,10 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
           const int N = o.widths[l + 1];
           for (int c = h; c < nch; c += WPQ) {
             float v[32];
-#ifdef BP_EXP_NOTMEM
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.001f * (j + c);
-#else
             if (npad - c * 32 >= 32)
               tmem_ld32(tl + dcol + 32 * c, v);
             else
               tmem_ld16(tl + dcol + 32 * c, v);
-#endif
-#ifndef BP_EXP_NOBIAS
             const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -636,7 +618,6 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
               v[4 * q + 2] += bb.z;
               v[4 * q + 3] += bb.w;
             }
-#endif
             {  // A of layer l+1 first (in place), so its MMAs start before the extrema work
               float w[32];
 #pragma unroll

@@ -15,9 +15,9 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
   return d;
 }
 
-__device__ __forceinline__ uint32_t idesc(int fmt, int n) {  // fmt 2: tf32 (kind::tf32), 1: bf16 (kind::f16)
+__device__ __forceinline__ uint32_t idesc(int fmt, int n, int m = 128) {  // fmt 2: tf32 (kind::tf32), 1: bf16 (kind::f16)
   return (1u << 4) | (static_cast<uint32_t>(fmt) << 7) | (static_cast<uint32_t>(fmt) << 10) |
-         (static_cast<uint32_t>(n >> 3) << 17) | ((128u >> 4) << 24);
+         (static_cast<uint32_t>(n >> 3) << 17) | ((static_cast<uint32_t>(m) >> 4) << 24);
 }
 
 template <int V>
@@ -292,11 +292,46 @@ __global__ void rate(int n_mma, long long* out) {
       stop = 1;
     }
   } else if (V < 19 && threadIdx.x == 0) {
-    const uint32_t id = idesc(V == 2 ? 1 : 2, N);  // V 3..6: tf32
+    const uint32_t id = (V >= 40 && V < 50) ? idesc(2, N, 64) : idesc(V == 2 ? 1 : 2, N);  // V 3..6: tf32
     const uint64_t da = sw128(su32(sm)), db = sw128(su32(sm + 32768));
     const long long t0 = clock64();
     for (int i = 0; i < n_mma; ++i) {
-      if constexpr (V >= 7) {
+      if constexpr (V >= 60 && V < 70) {
+        // v2 kernel pattern per 12: q=0..3 {TS(Ahi_q,Bhi_q), SS(Alo_q,Bhi_q)}, q=0..3 TS(Ahi_q,Blo_q)
+        // 61: lo-run reads other A columns; 62: SS uses another B than its TS partner; 63: lo-run reversed;
+        // 64: pairs reordered SS first; 65: B blocks advance every 12 (fresh per group)
+        const int j = i % 12, g = (i / 12) & 7;
+        const uint64_t bbase = db + (V == 65 ? 512 * g : 0);
+        int q;
+        bool ss;
+        uint64_t b;
+        uint32_t acol;
+        if (j < 8) {
+          q = j >> 1;
+          const bool second = (j & 1) != 0;
+          ss = (V == 64) ? !second : second;
+          b = bbase + 2 * q + ((V == 62 && ss) ? 256 : 0);
+          acol = 8 * q;
+        } else {
+          q = V == 63 ? 11 - j : j - 8;
+          ss = false;
+          b = bbase + 256 * 2 + 2 * q;
+          acol = (V == 61 ? 64 : 0) + 8 * q;
+        }
+        if (ss) issue<1>(tm, tm + 256, da + 2 * q, b, id); else issue<0>(tm, tm + 256 + acol, da, b, id);
+      } else if constexpr (V >= 50 && V < 60) {  // runs: (2^(V-50)*8) TS then half as many SS
+        const int run = 8 << (V - 50), per = run + run / 2;
+        const int j = i % per;
+        const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
+        if (j >= run) issue<1>(tm, tm + 256, da + 2 * (i & 3), b, id); else issue<0>(tm, tm + 256 + 8 * (i & 3), da, b, id);
+      } else if constexpr (V >= 40) {
+        const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
+        const uint32_t dl = (V == 42 && (i & 1)) ? (16u << 16) : 0u;  // second tile: lanes +16 per quadrant
+        if (V == 41)
+          issue<1>(tm + dl, tm + 256, da + 2 * (i & 3), b, id);
+        else
+          issue<0>(tm + dl, tm + 256 + dl, da, b, id);
+      } else if constexpr (V >= 7) {
         const uint64_t b = db + 2 * (i & 3) + 256 * ((i >> 2) & 7);
         const uint64_t aa = da + 2 * (i & 3) + 256 * ((i >> 2) & 3);
         if (i & 1) issue<1>(tm, tm + 256, aa, b, id); else issue<0>(tm, tm + 256, aa, b, id);
@@ -389,7 +424,11 @@ void run(const char* name, int grid) {
 }
 
 int main() {
-  run<33, 128, 0>("4xTF32 alternating", 148);
-  run<33, 256, 0>("4xTF32 alternating N256", 148);
+  run<60, 128, 0>("kernel pattern", 148);
+  run<61, 128, 0>("lo-run other A", 148);
+  run<62, 128, 0>("SS other B", 148);
+  run<63, 128, 0>("lo-run reversed", 148);
+  run<64, 128, 0>("pairs SS first", 148);
+  run<65, 128, 0>("fresh B per group", 148);
   return 0;
 }
