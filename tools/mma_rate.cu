@@ -239,6 +239,69 @@ __global__ void rate(int n_mma, long long* out) {
         }
         continue;
       }
+      if (V >= 80 && V < 90) {
+        // per 12-MMA group (issued at j == 0): 80 one asm block for all 12 (one elect);
+        // 81 per k-step {TS hi.Bhi, SS lo.Bhi, TS hi.Blo} (mma3 style, 4 asm blocks);
+        // 82/83 as 80/81 plus commit + wait after the group
+        const int j = i % 12;
+        if (j != 0) continue;
+        if (V == 80 || V == 82) {
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], %7, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %8, %7, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %10, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %11, %10, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %13, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %14, %13, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], %15, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], %16, %5, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%12], %17, %5, p;\n\t}"
+              ::"r"(tm), "r"(tm + 256), "l"(da), "l"(db), "l"(db + 512), "r"(id),
+              "r"(tm + 264), "l"(db + 2), "l"(da + 2), "r"(tm + 272), "l"(db + 4), "l"(da + 4),
+              "r"(tm + 280), "l"(db + 6), "l"(da + 6), "l"(db + 514), "l"(db + 516), "l"(db + 518));
+        } else {
+          for (int q = 0; q < 4; ++q)
+            asm volatile(
+                "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, p;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, p;\n\t}"
+                ::"r"(tm), "r"(tm + 256 + 8 * q), "l"(da + 2 * q), "l"(db + 2 * q), "l"(db + 512 + 2 * q), "r"(id));
+        }
+        if (V >= 82) {
+          asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+          asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t@!P1 bra WAIT_%=;\n\t}"
+                       ::"r"(su32(&ybar)), "r"(1u), "r"(0x989680u) : "memory");
+        }
+        continue;
+      }
+      if (V >= 70 && V < 80) {  // v2 MMA warp: 4 elected pairs (TS,SS), [commit+wait], 4 elected TS, [commit+wait]
+        // 70: commits + waits; 71: no commit/wait; 72: commit only; 73: wait only; 74: lo TS as elected pairs of 2
+        const int j = i % 12;
+        const int q = j < 8 ? (j >> 1) : j - 8;
+        const uint64_t b = db + 2 * q + (j >= 8 ? 512 : 0);
+        const bool ss = j < 8 && (j & 1);
+        if (ss)
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm), "l"(da + 2 * q), "l"(b), "r"(id));
+        else
+          asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm), "r"(tm + 256 + 8 * q), "l"(b), "r"(id));
+        if (j == 7 || j == 11) {
+          if (V == 70 || V == 72)
+            asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&xbar)));
+          if (V == 70 || V == 73)
+            asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t@!P1 bra WAIT_%=;\n\t}"
+                         ::"r"(su32(&ybar)), "r"(1u), "r"(0x989680u) : "memory");
+        }
+        continue;
+      }
       if (V >= 21) {  // elected lane inside the asm, the whole warp converged (v1 style)
         if (i & 1)
           asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\t"
@@ -424,11 +487,10 @@ void run(const char* name, int grid) {
 }
 
 int main() {
-  run<60, 128, 0>("kernel pattern", 148);
-  run<61, 128, 0>("lo-run other A", 148);
-  run<62, 128, 0>("SS other B", 148);
-  run<63, 128, 0>("lo-run reversed", 148);
-  run<64, 128, 0>("pairs SS first", 148);
-  run<65, 128, 0>("fresh B per group", 148);
+  run<71, 128, 0>("per-MMA elect", 148);
+  run<80, 128, 0>("12 in one asm", 148);
+  run<81, 128, 0>("mma3 per kstep", 148);
+  run<82, 128, 0>("12 in one asm +c/w", 148);
+  run<83, 128, 0>("mma3 per kstep +c/w", 148);
   return 0;
 }
