@@ -28,14 +28,16 @@
 // alternate TS/SS, then the A_hi.B_lo run; a 4xTF32 order with strict alternation runs
 // each MMA faster but costs more in total (measured on C3: 142 vs 159 TFLOP/s).
 //
-// Warps (W = 16 epilogue warps; warp w can reach TMEM lanes 32*(w%4)..+31):
-//   0-15   epilogue.  NT=2: tile w/8, chunks c = (w%8)/4 (mod 2);  NT=1: chunks
-//          c = w/4 (mod 4).  Row = 32*(w%4) + lane of its tile.
-//   17     MMA issuer (sub-partition 1), one elected lane issues.
-//   16, (18)  cost warps, one per tile, four rows per thread: the cost program,
-//          the states output and the extrema of the recorded scratch columns
-//          (x_t, u_t, p_t, cost-op values).
-//   last   producer: cp.async.bulk of the weight blocks into the byte ring.
+// Warps (template <NT, RW, EPI, CW>; warp w can reach TMEM lanes 32*(w%4)..+31):
+//   0..EPI-1  epilogue, EPI/NT per tile, chunks c = ((w % (EPI/NT)) / 4) mod WPQ.
+//             Row = 32*(w%4) + lane of its tile.
+//   EPI+1     MMA issuer (sub-partition 1), whole warp, elect.sync inside the asm.
+//   EPI, EPI+2, ...  cost warps, CW per tile, 4/CW rows per thread: the cost program,
+//             the states output and the extrema of the recorded scratch columns
+//             (x_t, u_t, p_t, cost-op values).
+//   last      producer: cp.async.bulk of the weight blocks into the byte ring.
+// Instances: <2,128,16,1> two ping-pong tiles; <1,128,8,4> one tile whose cost program
+// is heavy (C4: 4 cost warps, one row per thread); <1,256,16,1> one 256-wide tile (C3).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -49,7 +51,6 @@ namespace {
 
 using namespace tc;
 
-constexpr int kEpiWarps = 16;
 
 // Debug timeline (compiled in with -DBP_TC_TIMELINE, tools/tc_timeline.py): clock64 marks of
 // CTA 0 at step 3.  Slots: 0 step start (epilogue warp 0); 100+20l+10i+{0,1,2} MMA layer l of
@@ -72,17 +73,20 @@ constexpr int kSlots = 8;  // weight blocks in flight at most (mbarrier pairs)
 // __nanosleep backoff (ns) of the long waits: producer / cost warp / epilogue
 constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
 
-template <int NT, int RW_>
+template <int NT, int RW_, int EPI_, int CW_>
 struct Tc2 {
   static constexpr int RW = RW_;                  // TMEM region width >= widest padded layer
   static constexpr int KBMAX = RW / 32;           // A operand K-blocks of 32 per tile
-  static constexpr int WPQ = kEpiWarps / (4 * NT);  // epilogue warps per TMEM quadrant per tile
-  static constexpr int kWarps = kEpiWarps + 2 + NT;  // <= 5 warps per sub-partition: 96 registers
+  static constexpr int EPI = EPI_;                // epilogue warps (warps 0 .. EPI-1)
+  static constexpr int WPQ = EPI / (4 * NT);      // epilogue warps per TMEM quadrant per tile
+  static constexpr int CW = CW_;                  // cost warps per tile
+  static constexpr int NR = 4 / CW;               // rows per cost-warp thread (128 rows per tile)
+  static constexpr int kWarps = EPI + 2 + NT * CW;
   static constexpr int kThreads = 32 * kWarps;
-  static constexpr int kMmaWarp = 17;
+  static constexpr int kMmaWarp = EPI + 1;        // sub-partition 1 (EPI is a multiple of 4)
   static constexpr int kProducerWarp = kWarps - 1;
-  // tile of cost warp w (warps 16 and, for NT = 2, 18)
-  __device__ static int cost_tile(int w) { return w == 16 ? 0 : 1; }
+  // index (0 .. NT*CW-1) of cost warp w: warps EPI, EPI+2, EPI+3, ...
+  __device__ static int cost_index(int w) { return w == EPI ? 0 : w - EPI - 1; }
 };
 
 struct Tc2Smem {
@@ -298,10 +302,11 @@ __device__ __forceinline__ void publish_chunk(uint64_t* bar) {
 __device__ __forceinline__ int n_halves(int npad) { return npad > 128 ? 2 : 1; }
 __device__ __forceinline__ int half_rows(int npad, int h) { return npad > 128 ? (h == 0 ? 128 : npad - 128) : npad; }
 
-template <int NT, int RW_>
-__global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
-  using C = Tc2<NT, RW_>;
-  constexpr int RW = C::RW, KBMAX = C::KBMAX, WPQ = C::WPQ;
+template <int NT, int RW_, int EPI_, int CW_>
+__global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
+    rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
+  using C = Tc2<NT, RW_, EPI_, CW_>;
+  constexpr int RW = C::RW, KBMAX = C::KBMAX, WPQ = C::WPQ, CW = C::CW, NR = C::NR;
   constexpr uint32_t kTmemCols = 2 * NT * RW;  // a power of two >= 32
   extern __shared__ unsigned char smraw[];
   const uint32_t s0 = smem_u32(smraw);
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
       mbar_init(m.d_full + 2 * i + 1, 1);
       for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_chunk + i * KBMAX + c, 4);
       mbar_init(m.x_full + i, 4 * WPQ);
-      mbar_init(m.x_empty + i, 1);
+      mbar_init(m.x_empty + i, CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -454,10 +459,11 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
           mark2(a, t, 102 + 20 * l + 10 * i);
           put2(a, t, 300 + 20 * l + 10 * i, wfull + (1ll << 40));
         }
-  } else if (warp >= kEpiWarps) {
-    // ------------------------------------------------ cost warp: four rows per thread
-    // (rows lane + 32q); p_t lives in the scratch row (its pcol columns)
-    const int ti = C::cost_tile(warp);
+  } else if (warp >= C::EPI) {
+    // ------------------------------------------------ cost warps: CW per tile, NR rows per
+    // thread (rows 32 (cw NR + q) + lane); p_t lives in the scratch row (its pcol columns)
+    const int ci = C::cost_index(warp);
+    const int ti = ci / CW, cw = ci % CW;
     const long long row0 = cta_row0 + ti * 128;
     const long long rem = a.n_rows - row0;
     const int nvalid = static_cast<int>(rem < 0 ? 0 : rem < 128 ? rem : 128);
@@ -465,22 +471,33 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
     const long long SPH = static_cast<long long>(o.SP) * H;
     const bool rec_any = a.stat_min != nullptr;
     float* sct = m.sc + ti * 128 * S;
-    float* const rows[4] = {sct + lane * S, sct + (lane + 32) * S, sct + (lane + 64) * S, sct + (lane + 96) * S};
-    float cost[4] = {0.f, 0.f, 0.f, 0.f};
+    int rr[NR];
+    float* rows[NR];
+    float cost[NR];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < NR; ++q) {
+      rr[q] = 32 * (cw * NR + q) + lane;
+      rows[q] = sct + rr[q] * S;
+      cost[q] = 0.f;
       for (int e = 0; e < kd; ++e) rows[q][o.pcol + e] = o.f[o.p0 + e];
+    }
     const int* segl = m.segl + ti * 128;
     const int k_first = o.x_stat >= 0 ? ks : 0;  // the x_t columns' extrema come from the epilogue
     const long long b1 = (seg0 + 1) * rps - row0;
     const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
     const bool two = nvalid == 0 || (row0 + nvalid - 1) / rps - seg0 <= 1;
+    auto tile_sync = [&]() {  // the tile's cost warps (named barrier 1 + tile)
+      if constexpr (CW == 1)
+        __syncwarp();
+      else
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + ti), "r"(32 * CW) : "memory");
+    };
     for (int t = 0; t < H; ++t) {
       mbar_wait(m.x_full + ti, static_cast<uint32_t>(t & 1), kSleepCost);  // x_t of the tile's rows in the scratch
       mark2(a, t, 400 + 10 * ti);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = lane + 32 * q;
+      for (int q = 0; q < NR; ++q) {
+        const int r = rr[q];
         const float* ur = a.actions + (row0 + r) * d + t * ka;
         for (int j = 0; j < ka; ++j) {
           const float u = r < nvalid ? __ldg(ur + j) : 0.f;
@@ -488,35 +505,35 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
           if (j < kd) rows[q][o.pcol + j] += u;
         }
       }
-      cost_program_n<4>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
+      cost_program_n<NR>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
       mark2(a, t, 403 + 10 * ti);
       if (a.states != nullptr)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (lane + 32 * q < nvalid)
-            for (int j = 0; j < ks; ++j) a.states[((row0 + lane + 32 * q) * H + t) * ks + j] = rows[q][j];
+        for (int q = 0; q < NR; ++q)
+          if (rr[q] < nvalid)
+            for (int j = 0; j < ks; ++j) a.states[((row0 + rr[q]) * H + t) * ks + j] = rows[q][j];
       if (rec_any) {
-        __syncwarp();
-        for (int k = k_first + lane; k < o.n_sc; k += 32)
+        tile_sync();  // every row of the tile written
+        for (int k = k_first + 32 * cw + lane; k < o.n_sc; k += 32 * CW)
           scratch_column_extrema(a, sct + m.pairs[2 * k], S, two, bnd, nvalid, segl, seg0, SPH,
                                  t * o.SP + m.pairs[2 * k + 1]);
       }
-      mark2(a, t, 402 + 10 * ti);
       mark2(a, t, 401 + 10 * ti);
-      mbar_arrive_warp(m.x_empty + ti);  // scratch of step t consumed
+      mbar_arrive_warp(m.x_empty + ti);  // this warp's part of the scratch of step t consumed
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (lane + 32 * q < nvalid) {
-        const long long r = row0 + lane + 32 * q;
+    for (int q = 0; q < NR; ++q)
+      if (rr[q] < nvalid) {
+        const long long r = row0 + rr[q];
         a.costs[r] = cost[q];
         if (a.failed != nullptr && !isfinite(cost[q])) atomicOr(a.failed + r / rps, 1);
       }
   } else {
     // ------------------------------------------------ epilogue warps: layer to layer
-    const int ti = NT == 2 ? warp >> 3 : 0;
+    constexpr int per_tile = C::EPI / NT;  // epilogue warps per tile
+    const int ti = warp / per_tile;
     const int g = warp & 3;
-    const int h = NT == 2 ? (warp >> 2) & 1 : warp >> 2;
+    const int h = (warp % per_tile) >> 2;
     const int row = 32 * g + lane;
     const long long row0 = cta_row0 + ti * 128;
     const long long grow = row0 + row;
@@ -581,7 +598,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_>::kThreads, 1) rollout_tc2_kernel(
       publish_chunk(m.a_chunk + ti * KBMAX + c);
     }
     int li = 0;
-    const bool lead = (warp & 7) == 0;  // first epilogue warp of its tile (timeline)
+    const bool lead = warp % per_tile == 0;  // first epilogue warp of its tile (timeline)
     for (int t = 0; t < H; ++t) {
       if (warp == 0) mark2(a, t, 0);
 #pragma unroll
@@ -703,12 +720,15 @@ cudaError_t launch_rollout_tc2(const DevObjective& o, const RolloutArgs& a, cuda
     return cudaSuccess;
   };
   cudaError_t e;
+  // (tiles, region width, epilogue warps, cost warps per tile): two ping-pong tiles; one
+  // 128-wide tile with a heavy cost program (C4: 8 epilogue warps, 4 cost warps); one
+  // 256-wide tile
   if (nt == 2 && o.tc2_rw == 128)
-    e = go(rollout_tc2_kernel<2, 128>, Tc2<2, 128>::kThreads);
+    e = go(rollout_tc2_kernel<2, 128, 16, 1>, Tc2<2, 128, 16, 1>::kThreads);
   else if (nt == 1 && o.tc2_rw == 128)
-    e = go(rollout_tc2_kernel<1, 128>, Tc2<1, 128>::kThreads);
+    e = go(rollout_tc2_kernel<1, 128, 8, 4>, Tc2<1, 128, 8, 4>::kThreads);
   else if (nt == 1 && o.tc2_rw == 256)
-    e = go(rollout_tc2_kernel<1, 256>, Tc2<1, 256>::kThreads);
+    e = go(rollout_tc2_kernel<1, 256, 16, 1>, Tc2<1, 256, 16, 1>::kThreads);
   else
     return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
