@@ -613,6 +613,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       for (int j = 0; j < ks; ++j) m.xbuf[(128 + row) * o.tc_xs + j] = o.f[o.x0 + j];
     }
     const int us = ustride(o);
+    // early features: the input layer is one K-block and the output layer's x_t one chunk
+    // (so the chunk-0 warps of the output epilogue hold all of x_t)
+    const bool early = o.tc_kb[0] == 1 && o.tc_npad[L - 1] <= 32 && ks + ka <= 32;
     asm volatile("bar.sync 2, 256;" ::: "memory");
     int layer_it = 0;
     uint32_t stg_used = 0, stg_par = 0;  // bit cb: chunk staged before / parity of its last use
@@ -620,10 +623,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       if (warp == 0) mark(a, t, 0);
       const float* xprev = m.xbuf + (((t + 1) & 1) * 128 + row) * o.tc_xs;  // x_{t-1}
       const float* ucur = m.ubuf + ((t & 1) * 128 + row) * us;               // u_t
-      mbar_wait(m.u_full + (t & 1), static_cast<uint32_t>((t >> 1) & 1));  // written a step ago
+      if (!early || t == 0) mbar_wait(m.u_full + (t & 1), static_cast<uint32_t>((t >> 1) & 1));  // written a step ago
       if (warp == 0) mark(a, t, 407);
-      // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded
-      for (int kb = h; kb < o.tc_kb[0]; kb += 2) {
+      // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded (from
+      // step 1 on, the early path wrote them in the previous step's output epilogue)
+      for (int kb = h; kb < o.tc_kb[0] && (!early || t == 0); kb += 2) {
         // every load is issued unconditionally from a clamped address (no predicated
         // loads, no branches), so they pipeline; the selects come after
         float v[32];
@@ -730,8 +734,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           if (!hidden) {
             float* xo = m.xbuf + ((t & 1) * 128 + row) * o.tc_xs;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (cb * 32 + j < ks) xo[cb * 32 + j] = relu ? fmaxf(v[j], 0.f) : v[j];
+            for (int j = 0; j < 32; ++j) {
+              if (relu) v[j] = fmaxf(v[j], 0.f);
+              if (cb * 32 + j < ks) xo[cb * 32 + j] = v[j];
+            }
+            if (early && t + 1 < H) {
+              // step t+1's features straight from x_t (this chunk holds all of it):
+              // concat(x_t [- tile(p_t)], u_{t+1}) into A K-block 0, whose MMAs (this
+              // output layer's) have retired
+              mbar_wait(m.u_full + ((t + 1) & 1), static_cast<uint32_t>(((t + 1) >> 1) & 1));
+              const float* unext = m.ubuf + (((t + 1) & 1) * 128 + row) * us;
+              float f[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) f[j] = j < ks ? v[j] : unext[min(max(j - ks, 0), ka - 1)];
+              if (o.rel) {
+                float pa[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) pa[e] = prow[e];  // p_t
+                int km = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  float pv = pa[0];
+#pragma unroll
+                  for (int e = 1; e < 8; ++e) pv = km == e ? pa[e] : pv;
+                  if (j < ks) f[j] -= pv;
+                  km = km + 1 == kd ? 0 : km + 1;
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) f[j] = j < ks + ka ? f[j] : 0.f;
+              store_operand_tmem(tlane, 0, f);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+              fence_before();
+              mbar_arrive_warp(m.a_chunk + 0);
+            }
           }
         }
         if (warp == 0) mark(a, t, 201 + 10 * l);
