@@ -21,7 +21,8 @@
  *   bp_batch_bound      CrownBounder::lower        src/bab.cpp:25-28
  *                       -> lower_bound             src/crown.cpp:440-469
  *   bp_plan             plan / sample_only_plan    src/bab.cpp:266-454
- *   bp_pick_out/split/prune   pick_out/split/prune src/bab.cpp:85-241
+ *   bp_pick_out         pick_out                   src/bab.cpp:85-153
+ *   bp_pool_split/merge split / merge_report       src/bab.cpp:155-262
  */
 #ifndef BABPLAN_CUDA_H_
 #define BABPLAN_CUDA_H_
@@ -297,12 +298,28 @@ bp_status bp_rng_fill(bp_rng* r, int kind, int64_t n, double* out);
 uint64_t bp_mix_seed(uint64_t master, uint64_t salt);
 bp_status bp_pick_out(const bp_pool_meta* pool, int n_pool, int n, double eta, double temperature,
                       bp_rng* rng, int* picked, int* n_picked);
-/* split(): box lo/hi (d), top list (n_top values + n_top x d actions,
- * ascending), samples; returns axis, mid and the routing of each top sample
- * (0 = lo child, 1 = hi child). */
-bp_status bp_split_axis(int d, const double* lo, const double* hi, int n_top, const double* top_u,
-                        int64_t samples, double top_percent, double min_width, int split_rule,
-                        int* axis, double* mid, unsigned char* route);
+/* Device pool operations (pool.cu; what plan() runs every iteration).
+ * bp_pool_split: split() (src/bab.cpp:155-223) of n parents -- boxes lo/hi (n x d),
+ * top lists (n_top[i] <= K entries of top_val (n x K) / top_act (n x K x d),
+ * ascending), samples -- into 2n children (2i = lower half, 2i+1 = upper half):
+ * the axis per parent, child boxes (2n x d) and the routed top lists (child_n,
+ * child_val 2n x K, child_act 2n x K x d).  BP_INVALID_ARGUMENT when a parent has no
+ * axis above min_width. */
+bp_status bp_pool_split(bp_ctx* ctx, int n, int d, int K, const double* lo, const double* hi,
+                        const int* n_top, const float* top_val, const float* top_act,
+                        const int64_t* samples, double top_percent, double min_width, int split_rule,
+                        int* axis, double* child_lo, double* child_hi, int* child_n,
+                        float* child_val, float* child_act);
+/* bp_pool_merge: merge_report() (src/bab.cpp:245-262) of n records whose incumbent is
+ * their list's front -- record lists (a_n, a_val n x K, a_act n x K x d) with search
+ * reports (b_n, b_val, b_act, b_uf, b_best n x d, b_failed: a failed report merges
+ * nothing); capacity = top_capacity.  Outputs the merged lists, the incumbent value
+ * and action, has_best. */
+bp_status bp_pool_merge(bp_ctx* ctx, int n, int d, int K, int capacity, const int* a_n,
+                        const float* a_val, const float* a_act, const int* b_n, const float* b_val,
+                        const float* b_act, const float* b_uf, const float* b_best, const int* b_failed,
+                        int* out_n, float* out_val, float* out_act, float* out_uf, int* has_best,
+                        float* out_best);
 /* Generates a Glorot-uniform MLP exactly like generate_model (model.cpp:136-158). */
 bp_status bp_generate_model(uint64_t seed, int n_widths, const int* widths, double* params);
 

@@ -478,6 +478,25 @@ def split(lo, hi, top_values, top_u, samples, top_percent=1.0, min_width=1e-6, s
     return axis.value, mid.value, route[:len(top_values)]
 
 
+def merge_report(capacity, a_val, a_act, a_uf, a_best, b_val, b_act, b_uf, b_best):
+    """merge_report (bab.cpp:245-262): returns (values, actions, uf, best or None)."""
+    a_act, b_act = np.atleast_2d(a_act), np.atleast_2d(b_act)
+    d = a_act.shape[1] if a_act.size else b_act.shape[1]
+    na, nb = len(a_val), len(b_val)
+    n = C.c_int()
+    out_v = np.zeros(max(1, na + nb))
+    out_a = np.zeros((max(1, na + nb), d))
+    uf, has = C.c_double(), C.c_int()
+    best = np.zeros(d)
+    opt = lambda x: _d(x).ctypes.data_as(dp) if x is not None else None
+    ck(lib().or_merge_report(C.c_int(d), C.c_int(capacity), C.c_int(na), opt(np.asarray(a_val) if na else np.zeros(1)),
+                             opt(a_act if na else np.zeros((1, d))), C.c_double(a_uf), opt(a_best),
+                             C.c_int(nb), opt(np.asarray(b_val) if nb else np.zeros(1)), opt(b_act if nb else np.zeros((1, d))),
+                             C.c_double(b_uf), opt(b_best), C.byref(n), out_v.ctypes.data_as(dp),
+                             out_a.ctypes.data_as(dp), C.byref(uf), C.byref(has), best.ctypes.data_as(dp)))
+    return out_v[:n.value], out_a[:n.value], uf.value, (best if has.value else None)
+
+
 def prune(meta, incumbent):
     arr = (_capi.PoolMeta * max(1, len(meta)))(*[_capi.PoolMeta(*m) for m in meta])
     keep = np.zeros(max(1, len(meta)), dtype=np.int32)

@@ -602,6 +602,32 @@ int or_split(int d, const double* lo, const double* hi, int n_top, const double*
     for (int i = 0; i < n_top; ++i) route[i] = top_u[static_cast<size_t>(i) * d + s.axis] <= *mid ? 0 : 1;
   });
 }
+// merge_report (bab.cpp:245-262) on one record: (a_*) the record's list / incumbent,
+// (b_*) the search report's.  Outputs the merged list and incumbent.
+int or_merge_report(int d, int capacity, int na, const double* a_val, const double* a_act, double a_uf,
+                    const double* a_best, int nb, const double* b_val, const double* b_act, double b_uf,
+                    const double* b_best, int* n_out, double* out_val, double* out_act, double* out_uf,
+                    int* has_best, double* out_best) {
+  return guard([&] {
+    SubdomainRecord r;
+    r.uf = a_uf;
+    if (a_best) r.best = vec_of(a_best, d);
+    for (int i = 0; i < na; ++i) r.top.push_back({a_val[i], vec_of(a_act + static_cast<size_t>(i) * d, d)});
+    SearchReport rep;
+    rep.uf = b_uf;
+    if (b_best) rep.best = vec_of(b_best, d);
+    for (int i = 0; i < nb; ++i) rep.top.push_back({b_val[i], vec_of(b_act + static_cast<size_t>(i) * d, d)});
+    merge_report(r, std::move(rep), capacity);
+    *n_out = static_cast<int>(r.top.size());
+    for (size_t i = 0; i < r.top.size(); ++i) {
+      out_val[i] = r.top[i].value;
+      std::copy(r.top[i].u.begin(), r.top[i].u.end(), out_act + i * static_cast<size_t>(d));
+    }
+    *out_uf = r.uf;
+    *has_best = r.best.empty() ? 0 : 1;
+    if (!r.best.empty()) std::copy(r.best.begin(), r.best.end(), out_best);
+  });
+}
 int or_prune(const bp_pool_meta* meta, int n_pool, double incumbent, int* keep, int* n_keep, double* removed) {
   return guard([&] {
     DomainPool pool;

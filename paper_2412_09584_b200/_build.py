@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libbabplan_cuda.so")
-SOURCES = ["rollout.cu", "rollout_tc.cu", "rollout_tc2.cu", "bound.cu", "search.cu", "synthetic.cu", "gradient.cu", "host.cu", "diag.cu"]
+SOURCES = ["rollout.cu", "rollout_tc.cu", "rollout_tc2.cu", "bound.cu", "search.cu", "synthetic.cu", "gradient.cu", "pool.cu", "host.cu", "diag.cu"]
 HEADERS = ["bp_common.cuh", "rollout_common.cuh", "tc_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

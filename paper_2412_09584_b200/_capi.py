@@ -97,7 +97,7 @@ EXPORTS = [
     "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
     "bp_result_trace", "bp_result_free", "bp_timing", "bp_rng_new", "bp_rng_free",
     "bp_rng_uniform", "bp_rng_normal", "bp_rng_bits", "bp_rng_fill", "bp_mix_seed", "bp_pick_out",
-    "bp_split_axis", "bp_generate_model", "bp_measure_fp32_peak", "bp_measure_tf32_peak",
+    "bp_pool_split", "bp_pool_merge", "bp_generate_model", "bp_measure_fp32_peak", "bp_measure_tf32_peak",
 ]
 
 _lib = None
@@ -162,8 +162,11 @@ def load() -> C.CDLL:
             "bp_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
             "bp_pick_out": (C.c_int, [C.POINTER(PoolMeta), C.c_int, C.c_int, C.c_double,
                                       C.c_double, vp, _ip, _ip]),
-            "bp_split_axis": (C.c_int, [C.c_int, _dp, _dp, C.c_int, _dp, C.c_int64, C.c_double,
-                                        C.c_double, C.c_int, _ip, _dp, C.POINTER(C.c_ubyte)]),
+            "bp_pool_split": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, _fp, _fp,
+                                        C.POINTER(C.c_int64), C.c_double, C.c_double, C.c_int, _ip, _dp, _dp,
+                                        _ip, _fp, _fp]),
+            "bp_pool_merge": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _fp, _fp, _ip, _fp, _fp,
+                                        _fp, _fp, _ip, _ip, _fp, _fp, _fp, _ip, _fp]),
             "bp_generate_model": (C.c_int, [C.c_uint64, C.c_int, _ip, _dp]),
             "bp_measure_fp32_peak": (C.c_int, [C.c_int, _dp, _dp]),
             "bp_measure_tf32_peak": (C.c_int, [C.c_int, _dp, _dp]),

@@ -173,6 +173,49 @@ class Device:
         check(self.lib.bp_node_bounds(self.h, _capi.dptr(lo), _capi.dptr(hi)))
         return lo, hi
 
+    # ---------------------------------------------------------- pool operations
+    def pool_split(self, lo, hi, top_val, top_act, n_top, samples, top_percent=1.0, min_width=1e-6, split_rule=0):
+        """split() (bab.cpp:155-223) of n parents on the device (pool.cu split_kernel).
+
+        lo / hi (n, d); top_val (n, K) and top_act (n, K, d) hold n_top[i] ascending
+        entries each.  Returns (axis (n,), child_lo / child_hi (2n, d), child_n (2n,),
+        child_val (2n, K), child_act (2n, K, d)); child 2i is the lower half."""
+        lo, hi = np.ascontiguousarray(lo, np.float64), np.ascontiguousarray(hi, np.float64)
+        n, d = lo.shape
+        tv = np.ascontiguousarray(top_val, np.float32)
+        K = tv.shape[1]
+        ta = np.ascontiguousarray(top_act, np.float32).reshape(n, K, d)
+        nt = np.ascontiguousarray(n_top, np.int32)
+        sm = np.ascontiguousarray(samples, np.int64)
+        axis = np.zeros(n, np.int32)
+        clo, chi = np.zeros((2 * n, d)), np.zeros((2 * n, d))
+        cn = np.zeros(2 * n, np.int32)
+        cv, ca = np.zeros((2 * n, K), np.float32), np.zeros((2 * n, K, d), np.float32)
+        check(self.lib.bp_pool_split(self.h, n, d, K, _capi.dptr(lo), _capi.dptr(hi), _capi.iptr(nt), _capi.fptr(tv),
+                                     _capi.fptr(ta), sm.ctypes.data_as(C.POINTER(C.c_int64)), float(top_percent),
+                                     float(min_width), int(split_rule), _capi.iptr(axis), _capi.dptr(clo),
+                                     _capi.dptr(chi), _capi.iptr(cn), _capi.fptr(cv), _capi.fptr(ca)))
+        return axis, clo, chi, cn, cv, ca
+
+    def pool_merge(self, capacity, a_n, a_val, a_act, b_n, b_val, b_act, b_uf, b_best, b_failed):
+        """merge_report() (bab.cpp:245-262) of n records on the device (pool.cu merge_kernel);
+        the record's incumbent is its list's front.  Returns (n, val, act, uf, has_best, best)."""
+        a_val = np.ascontiguousarray(a_val, np.float32)
+        n, K = a_val.shape
+        a_act = np.ascontiguousarray(a_act, np.float32)
+        d = a_act.shape[2]
+        f = lambda x: np.ascontiguousarray(x, np.float32)
+        i32 = lambda x: np.ascontiguousarray(x, np.int32)
+        on, ov, oa = np.zeros(n, np.int32), np.zeros((n, K), np.float32), np.zeros((n, K, d), np.float32)
+        ou, oh, ob = np.zeros(n, np.float32), np.zeros(n, np.int32), np.zeros((n, d), np.float32)
+        an, bn, bf = i32(a_n), i32(b_n), i32(b_failed)
+        bv, ba, bu, bb = f(b_val), f(b_act), f(b_uf), f(b_best)
+        check(self.lib.bp_pool_merge(self.h, n, d, K, int(capacity), _capi.iptr(an), _capi.fptr(a_val),
+                                     _capi.fptr(a_act), _capi.iptr(bn), _capi.fptr(bv), _capi.fptr(ba),
+                                     _capi.fptr(bu), _capi.fptr(bb), _capi.iptr(bf), _capi.iptr(on), _capi.fptr(ov),
+                                     _capi.fptr(oa), _capi.fptr(ou), _capi.iptr(oh), _capi.fptr(ob)))
+        return on, ov, oa, ou, oh, ob
+
     # --------------------------------------------------------------------- plan
     def plan(self, cfg: dict, warm: Optional[np.ndarray] = None, method: str = "babnd") -> dict:
         packed = _config.PackedConfig(cfg, method)

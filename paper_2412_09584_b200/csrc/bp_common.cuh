@@ -73,6 +73,70 @@ struct DevObjective {
   const int* iv;
 };
 
+// Device-resident subdomain pool (pool.cu; SubdomainRecord payload, bab.hpp:18-28):
+// per slot the box, the incumbent action and the top-sample list.  The head fields
+// (id, lf, uf, depth, log_vol, samples) stay with the host planner, which replays
+// pick_out / prune on them.  Slots live in fixed-size chunks (2^shift slots each, one
+// allocation per chunk, never moved), found through a chunk table; within a chunk
+// each field is a dense array at a fixed byte offset.
+struct PoolArgs {
+  int d, K;                       // dimension, top-list capacity
+  int shift;                      // log2(slots per chunk)
+  unsigned char* const* chunk;    // chunk table (device pointer in kernels, host array on the host)
+  size_t o_lo, o_hi, o_best, o_val, o_act, o_n, o_has;  // byte offsets of the fields in a chunk
+};
+__host__ __device__ inline size_t pool_in_chunk(const PoolArgs& P, int s) {
+  return static_cast<size_t>(s & ((1 << P.shift) - 1));
+}
+__host__ __device__ inline unsigned char* pool_chunk(const PoolArgs& P, int s) { return P.chunk[s >> P.shift]; }
+__host__ __device__ inline double* pool_lo(const PoolArgs& P, int s) {  // [d]
+  return reinterpret_cast<double*>(pool_chunk(P, s) + P.o_lo) + pool_in_chunk(P, s) * P.d;
+}
+__host__ __device__ inline double* pool_hi(const PoolArgs& P, int s) {  // [d]
+  return reinterpret_cast<double*>(pool_chunk(P, s) + P.o_hi) + pool_in_chunk(P, s) * P.d;
+}
+__host__ __device__ inline float* pool_best(const PoolArgs& P, int s) {  // [d]
+  return reinterpret_cast<float*>(pool_chunk(P, s) + P.o_best) + pool_in_chunk(P, s) * P.d;
+}
+__host__ __device__ inline float* pool_val(const PoolArgs& P, int s) {  // [K], ascending
+  return reinterpret_cast<float*>(pool_chunk(P, s) + P.o_val) + pool_in_chunk(P, s) * P.K;
+}
+__host__ __device__ inline float* pool_act(const PoolArgs& P, int s) {  // [K][d]
+  return reinterpret_cast<float*>(pool_chunk(P, s) + P.o_act) + pool_in_chunk(P, s) * P.K * P.d;
+}
+__host__ __device__ inline int* pool_n(const PoolArgs& P, int s) {
+  return reinterpret_cast<int*>(pool_chunk(P, s) + P.o_n) + pool_in_chunk(P, s);
+}
+__host__ __device__ inline int* pool_has(const PoolArgs& P, int s) {
+  return reinterpret_cast<int*>(pool_chunk(P, s) + P.o_has) + pool_in_chunk(P, s);
+}
+// One iteration's children by local index i: the search inputs the split writes and the
+// top samples routed from the parent (merged with the search's list afterwards).
+struct StageArgs {
+  float* lo_f;       // [n][d]
+  float* hi_f;
+  float* warm_f;     // [n][d]; NaN first coordinate = no warm start
+  double* lo_d;
+  double* hi_d;
+  float* val;        // [n][K]
+  float* act;        // [n][K][d]
+  int* n;            // [n]
+};
+// One parent split (bab.cpp:155-223).  k_round: -2 width rule (k = 0), -1 no samples
+// yet (k = n_top), else llround(top_percent / 100 * samples) before the [1, n_top] clamp.
+struct SplitTask {
+  int parent;        // parent slot
+  int slot[2];       // child slots of local children, else -1
+  int dst[2];        // child local index, else -1
+  int pack[2];       // shipped record index, else -1
+  long long key[2];  // the children's global indices (shipped record header)
+  long long k_round;
+};
+// Shipped child record: doubles {key, n, lo[d], hi[d]}, then floats {val[K], act[K][d]}.
+__host__ __device__ inline size_t pool_record_bytes(int d, int K) {
+  return sizeof(double) * (2 + 2 * static_cast<size_t>(d)) + sizeof(float) * static_cast<size_t>(K) * (1 + d);
+}
+
 // K7 launch arguments (bound.cu; built by host.cu).
 struct BoundArgs {
   const double* lo;       // [n][d] boxes

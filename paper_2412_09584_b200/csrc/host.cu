@@ -2,10 +2,12 @@
 // compilation, device batch search / bound, and the host planner loop.
 //
 // The planner is the reference's plan() (proj/src/bab.cpp:266-415) with its
-// search and bound calls replaced by the device kernels: pick_out, split,
-// merge_report and prune stay host C++ restated bit-for-bit (they are
-// O(pool) bookkeeping; every rank of a multi-GPU run replays them on the same
-// exchanged data, so decisions are identical on every rank).
+// search, bound, split and merge_report on the device (the pool's boxes,
+// incumbents and top lists live in a device slab, pool.cu); pick_out, the
+// retirement test and prune stay host C++ restated bit-for-bit over the pool's
+// heads (O(pool) bookkeeping; pick_out's softmax needs the reference's exp();
+// every rank of a multi-GPU run replays them on the same exchanged heads, so
+// decisions are identical on every rank).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -68,6 +70,13 @@ cudaError_t launch_gradient(const DevObjective& o, const float* actions, float* 
                             cudaStream_t st);
 cudaError_t launch_synthetic_gradient(const float* actions, float* grad, long long n, cudaStream_t st);
 size_t search_update_smem(const SearchArgs& a);
+cudaError_t launch_pool_split(const PoolArgs& P, const SplitTask* tasks, int n_tasks, const StageArgs& S,
+                              unsigned char* pack, double min_width, int* axis_out, cudaStream_t st);
+cudaError_t launch_pool_unpack(const PoolArgs& P, const StageArgs& S, const unsigned char* recv, const int* dst,
+                               const int* slot, int n, cudaStream_t st);
+cudaError_t launch_pool_merge(const PoolArgs& P, const StageArgs& S, const int* slots, int n, const float* s_val,
+                              const float* s_act, const int* s_cnt, const float* s_uf, const float* s_best,
+                              const int* failed, int capacity, float* out_uf, double* out_maxw, cudaStream_t st);
 }  // namespace bp
 
 namespace {
@@ -714,7 +723,16 @@ struct bp_ctx {
   DBuf<float> uf_hist;
   HBuf<float> h_uf, h_best, h_hist, h_tv, h_ta;  // pinned report staging
   HBuf<int> h_cnt;
-  std::vector<double> h_lo, h_hi;
+  bp::SearchArgs last{};  // the last search's arguments (the pool merge reads its outputs)
+  // routed top samples of the iteration's children (pool.cu), by local index
+  DBuf<float> st_val, st_act;
+  DBuf<int> st_n;
+  // slab chunks (pool.cu) kept between plans, for pools of this geometry
+  int slab_d = 0, slab_K = 0;
+  std::vector<unsigned char*> slab_spare;
+  // search / bound buffers are sized for at least this many boxes (a planner's children
+  // per step), so the ramp-up iterations do not reallocate them
+  int reserve_boxes = 0;
   std::vector<int> h_failed;
   std::vector<Report> reports;
   // sharding: rank / world and the allgather hook (host buffers)
@@ -745,6 +763,7 @@ struct bp_ctx {
   }
 
   ~bp_ctx() {
+    for (unsigned char* p : slab_spare) cudaFree(p);
     for (auto& e : roll_events) {
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);
@@ -830,9 +849,11 @@ void check_loaded(bp_ctx* c) {
   if (!c->loaded) fail(BP_LOGIC, "no objective loaded");
 }
 
-// Device batch search (batch_search, search.cpp:262-282, with run_cem / run_mppi).
-void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm,
-                         const bp_search_config& cfg, std::vector<Report>* out, const int64_t* seed_index = nullptr) {
+// Device batch search (batch_search, search.cpp:262-282, with run_cem / run_mppi / run_gd),
+// in three parts: search_setup (configuration, per-box seeds, state buffers; the boxes
+// and warm starts must already be in c->lo_f / hi_f / lo_d / hi_d / warm_f), search_run
+// (init + the iterations), search_harvest (host reports for the C-ABI's report calls).
+bp::SearchArgs search_setup(bp_ctx* c, int n, const bp_search_config& cfg, const int64_t* seed_index, bool warm) {
   const Compiled& cp = c->comp;
   const int d = cp.d;
   if (cfg.iterations <= 0 || cfg.samples_per_iter <= 0)
@@ -878,38 +899,19 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   c->rows = a.rows;
   c->top_cap = a.top_cap;
   c->iters = cfg.iterations;
-  c->h_lo.assign(lo, lo + static_cast<size_t>(n) * d);
-  c->h_hi.assign(hi, hi + static_cast<size_t>(n) * d);
-  for (size_t i = 0; i < c->h_lo.size(); ++i)
-    if (!(c->h_lo[i] <= c->h_hi[i]) || !std::isfinite(c->h_lo[i]) || !std::isfinite(c->h_hi[i]))
-      fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
   cudaStream_t st = c->stream;
-  const size_t nd = static_cast<size_t>(n) * d;
-  std::vector<float> lf32(nd), hf32(nd);
-  for (size_t i = 0; i < nd; ++i) {
-    lf32[i] = static_cast<float>(lo[i]);
-    hf32[i] = static_cast<float>(hi[i]);
-  }
+  // buffers sized for at least c->reserve_boxes boxes (no reallocation while a plan ramps up)
+  const size_t nb = static_cast<size_t>(std::max(n, c->reserve_boxes));
+  const size_t nd = nb * d;
   std::vector<unsigned long long> seeds(static_cast<size_t>(n));
   // derive_seed(seed, i) (rng.hpp:37-39) with i the box's index in the caller's batch
   for (int i = 0; i < n; ++i)
     seeds[static_cast<size_t>(i)] = cfg.seed ^ static_cast<unsigned long long>(seed_index ? seed_index[i] : i);
-  a.seeds = c->seeds.get(static_cast<size_t>(n));
+  a.seeds = c->seeds.get(nb);
+  ck(memcpy_counted(const_cast<unsigned long long*>(a.seeds), seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
   a.lo = c->lo_f.get(nd);
   a.hi = c->hi_f.get(nd);
-  ck(memcpy_counted(const_cast<unsigned long long*>(a.seeds), seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(const_cast<float*>(a.lo), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(const_cast<float*>(a.hi), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
-  a.warm = nullptr;
-  std::vector<float> w32;
-  if (warm != nullptr) {
-    w32.resize(nd);
-    for (size_t i = 0; i < nd; ++i) w32[i] = static_cast<float>(warm[i]);
-    a.warm = c->warm_f.get(nd);
-    ck(memcpy_counted(const_cast<float*>(a.warm), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  }
+  a.warm = warm ? c->warm_f.get(nd) : nullptr;
   if (!ratios.empty()) {
     float* r = c->ratios.get(ratios.size());
     ck(memcpy_counted(r, ratios.data(), ratios.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
@@ -920,33 +922,65 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
       a.temp_ratios = r + a.n_noise;
     }
   }
-  a.mu = c->mu.get(static_cast<size_t>(n) * a.groups * d);
-  a.var = c->var.get(static_cast<size_t>(n) * a.groups * d);
+  a.mu = c->mu.get(nb * a.groups * d);
+  a.var = c->var.get(nb * a.groups * d);
   a.var_floor = c->var_floor.get(nd);
   a.best = c->best.get(nd);
-  a.uf = c->uf.get(static_cast<size_t>(n));
-  a.actions = c->actions.get(static_cast<size_t>(n) * a.rows * d);
-  a.costs = c->costs.get(static_cast<size_t>(n) * a.rows);
-  a.failed = c->failed.get(static_cast<size_t>(n));
-  const size_t tk = static_cast<size_t>(n) * a.top_cap;
+  a.uf = c->uf.get(nb);
+  a.actions = c->actions.get(nb * a.rows * d);
+  a.costs = c->costs.get(nb * a.rows);
+  a.failed = c->failed.get(nb);
+  const size_t tk = nb * a.top_cap;
   a.top_val[0] = c->top_val0.get(tk);
   a.top_val[1] = c->top_val1.get(tk);
   a.top_seq[0] = c->top_seq0.get(tk);
   a.top_seq[1] = c->top_seq1.get(tk);
   a.top_act[0] = c->top_act0.get(tk * d);
   a.top_act[1] = c->top_act1.get(tk * d);
-  a.top_cnt = c->top_cnt.get(static_cast<size_t>(n));
+  a.top_cnt = c->top_cnt.get(nb);
+  return a;
+}
+
+// Host boxes / warm starts into the search inputs (the C-ABI's bp_batch_search path).
+void place_host_boxes(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm) {
+  const int d = c->comp.d;
+  const size_t nd = static_cast<size_t>(n) * d;
+  for (size_t i = 0; i < nd; ++i)
+    if (!(lo[i] <= hi[i]) || !std::isfinite(lo[i]) || !std::isfinite(hi[i]))
+      fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
+  cudaStream_t st = c->stream;
+  std::vector<float> lf32(nd), hf32(nd);
+  for (size_t i = 0; i < nd; ++i) {
+    lf32[i] = static_cast<float>(lo[i]);
+    hf32[i] = static_cast<float>(hi[i]);
+  }
+  ck(memcpy_counted(c->lo_f.get(nd), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->hi_f.get(nd), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  if (warm != nullptr) {
+    std::vector<float> w32(nd);
+    for (size_t i = 0; i < nd; ++i) w32[i] = static_cast<float>(warm[i]);
+    ck(memcpy_counted(c->warm_f.get(nd), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  }
+}
+
+void search_run(bp_ctx* c, bp::SearchArgs& a, const bp_search_config& cfg) {
+  const Compiled& cp = c->comp;
+  const int n = a.n, d = a.d;
+  cudaStream_t st = c->stream;
   const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
-  int* smin = c->stat_min.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
-  int* smax = c->stat_max.get(static_cast<size_t>(std::max<long long>(nstat, 1)));
+  const long long nstat_cap = static_cast<long long>(std::max(n, c->reserve_boxes)) * cp.o.H * cp.o.SP;
+  int* smin = c->stat_min.get(static_cast<size_t>(std::max<long long>(nstat_cap, 1)));
+  int* smax = c->stat_max.get(static_cast<size_t>(std::max<long long>(nstat_cap, 1)));
   fill_int(smin, nstat, bp::enc_f_host(INFINITY), st);
   fill_int(smax, nstat, bp::enc_f_host(-INFINITY), st);
-  float* ufh = c->uf_hist.get(static_cast<size_t>(n) * cfg.iterations);
+  float* ufh = c->uf_hist.get(static_cast<size_t>(std::max(n, c->reserve_boxes)) * cfg.iterations);
   ck(bp::launch_search_init(a, st), "search init");
   ++c->launches;
   a.cur = 0;
   const long long n_rows = static_cast<long long>(n) * a.rows;
-  if (a.method == 2) a.grad = c->grad.get(static_cast<size_t>(n_rows) * d);
+  if (a.method == 2) a.grad = c->grad.get(static_cast<size_t>(std::max(n, c->reserve_boxes)) * a.rows * d);
   for (int it = 0; it < cfg.iterations; ++it) {
     a.iter = it;
     if (a.method != 2 || it == 0) ck(bp::launch_sample(a, c->sms, st), "sample");
@@ -973,13 +1007,16 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   }
   c->cur = a.cur;
   c->searched = true;
+  c->last = a;
   c->h_failed.assign(static_cast<size_t>(n), 0);
   ck(memcpy_counted(c->h_failed.data(), a.failed, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  if (out == nullptr) {
-    ck(cudaStreamSynchronize(st), "sync");
-    return;
-  }
-  // harvest reports
+}
+
+void search_harvest(bp_ctx* c, const bp::SearchArgs& a, const bp_search_config& cfg, std::vector<Report>* out) {
+  const int n = a.n, d = a.d;
+  const size_t nd = static_cast<size_t>(n) * d;
+  cudaStream_t st = c->stream;
+  float* ufh = c->uf_hist.p;
   float* uf = c->h_uf.get(static_cast<size_t>(n));
   float* best = c->h_best.get(nd);
   float* hist = c->h_hist.get(static_cast<size_t>(n) * cfg.iterations);
@@ -990,6 +1027,7 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   ck(memcpy_counted(hist, ufh, static_cast<size_t>(n) * cfg.iterations * 4, cudaMemcpyDeviceToHost, st), "D2H");
   // only the filled part of each top list crosses: counts first, then per-box extents
   ck(cudaStreamSynchronize(st), "sync");
+  const size_t tk = static_cast<size_t>(n) * a.top_cap;
   float* tv = c->h_tv.get(tk);
   float* ta = c->h_ta.get(tk * d);
   {
@@ -1031,12 +1069,24 @@ void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, c
   });
 }
 
+void device_batch_search(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm,
+                         const bp_search_config& cfg, std::vector<Report>* out, const int64_t* seed_index = nullptr) {
+  place_host_boxes(c, n, lo, hi, warm);
+  bp::SearchArgs a = search_setup(c, n, cfg, seed_index, warm != nullptr);
+  search_run(c, a, cfg);
+  if (out == nullptr) {
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return;
+  }
+  search_harvest(c, a, cfg, out);
+}
+
 void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
   if (!c->searched) fail(BP_LOGIC, "bound: no batch searched");
   const Compiled& cp = c->comp;
   const int n = c->n;
   if (cp.synth) {  // SeparableBounder (bab.cpp:70-83): exact, needs no search statistics
-    double* lf = c->lf.get(static_cast<size_t>(n));
+    double* lf = c->lf.get(static_cast<size_t>(std::max(n, c->reserve_boxes)));
     if (c->timing) ck(cudaEventRecord(c->ev0, c->stream), "event");
     ck(bp::launch_separable_bound(c->lo_d.p, c->hi_d.p, n, cp.d, c->d_da.p, static_cast<int>(cp.da.size()), nullptr,
                                   lf, c->stream), "separable bound launch");
@@ -1051,15 +1101,15 @@ void device_batch_bound(bp_ctx* c, int mode, int alpha, double* lf_out) {
     }
     return;
   }
-  const long long nstat = static_cast<long long>(n) * cp.o.H * cp.o.SP;
+  const long long nstat_cap = static_cast<long long>(std::max(n, c->reserve_boxes)) * cp.o.H * cp.o.SP;
   std::vector<int> use(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) use[static_cast<size_t>(i)] = c->h_failed[static_cast<size_t>(i)] ? 0 : 1;
-  int* du = c->use_flags.get(static_cast<size_t>(n));
+  int* du = c->use_flags.get(static_cast<size_t>(std::max(n, c->reserve_boxes)));
   ck(memcpy_counted(du, use.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
   bp::BoundArgs a{c->lo_d.p, c->hi_d.p, c->stat_min.p, c->stat_max.p, du,
-                  c->ivl_lo.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
-                  c->ivl_hi.get(static_cast<size_t>(std::max<long long>(nstat, 1))),
-                  c->lf.get(static_cast<size_t>(n)), mode, alpha, -1, 0, 0, 0, 0};
+                  c->ivl_lo.get(static_cast<size_t>(std::max<long long>(nstat_cap, 1))),
+                  c->ivl_hi.get(static_cast<size_t>(std::max<long long>(nstat_cap, 1))),
+                  c->lf.get(static_cast<size_t>(std::max(n, c->reserve_boxes))), mode, alpha, -1, 0, 0, 0, 0};
   if (c->timing) ck(cudaEventRecord(c->ev0, c->stream), "event");
   if (mode == BP_BOUND_FULL_CROWN) {
     // crown_node_bounds (crown.cpp:379-412): a backward pass per recorded node in
@@ -1149,25 +1199,6 @@ struct bp_result {
 
 namespace {
 
-// SubdomainRecord (bab.hpp:18-28) with the top list in the device's float form.
-struct Rec {
-  std::vector<double> lo, hi;
-  double lf = -std::numeric_limits<double>::infinity();
-  double uf = std::numeric_limits<double>::infinity();
-  std::vector<double> best;
-  std::vector<float> top_val;  // ascending
-  std::vector<float> top_act;  // n_top x d
-  int64_t samples = 0;
-  int depth = 0;
-  int64_t id = 0, parent = -1;
-  double log_vol = 0.0;
-  double max_width() const {
-    double w = 0.0;
-    for (size_t j = 0; j < lo.size(); ++j) w = std::max(w, hi[j] - lo[j]);
-    return w;
-  }
-};
-
 // pick_out (bab.cpp:85-153) over pool metadata; returns pool indices in pick order.
 std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double eta, double temperature, bp_rng& rng) {
   n = std::min(n, total);
@@ -1219,232 +1250,121 @@ std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double
   return chosen;
 }
 
-// Axis choice of split (bab.cpp:155-195); top_u is n_top x d, ascending by value.
-int split_axis(int d, const double* lo, const double* hi, int n_top, const float* top_u, int64_t samples,
-               double top_percent, double min_width, int split_rule) {
-  int k = 0;
-  if (n_top > 0 && split_rule == BP_SPLIT_SAMPLES) {
-    const int64_t stored = n_top;
-    k = samples > 0 ? static_cast<int>(std::clamp<int64_t>(std::llround(top_percent / 100.0 * static_cast<double>(samples)), 1, stored))
-                    : static_cast<int>(stored);
+// Device pool slab (pool.cu): the payload of every record this rank owns -- box,
+// incumbent action, top-sample list -- one slot per record, with a host free list.
+// Slots come in fixed-size chunks (>= 32 MB or 4096 slots each) that are never moved
+// or freed while the planner runs, so the pool grows without copies or device-wide
+// synchronisation; the chunks go back to the context when the planner ends and the
+// next plan with the same geometry reuses them.
+struct DevPool {
+  static constexpr int kMaxChunks = 1 << 16;
+  bp_ctx* ctx;  // chunk cache (null: chunks are freed)
+  int d, K, shift = 4;
+  size_t o_lo = 0, o_hi = 0, o_best = 0, o_val = 0, o_act = 0, o_n = 0, o_has = 0, chunk_bytes = 0;
+  std::vector<unsigned char*> chunks;
+  DBuf<unsigned char*> table;
+  int used = 0;
+  std::vector<int> free_slots;
+  DevPool(bp_ctx* c, int d_, int K_) : ctx(c), d(d_), K(K_) {
+    const size_t sd = static_cast<size_t>(d), sk = static_cast<size_t>(K);
+    const size_t slot_bytes = 20 * sd + 4 * sk + 4 * sk * sd + 8;
+    while (shift < 12 && (slot_bytes << shift) < (32u << 20)) ++shift;
+    const size_t per = size_t{1} << shift;
+    auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
+    o_hi = o_lo + al(per * sd * 8);
+    o_best = o_hi + al(per * sd * 8);
+    o_val = o_best + al(per * sd * 4);
+    o_act = o_val + al(per * sk * 4);
+    o_n = o_act + al(per * sk * sd * 4);
+    o_has = o_n + al(per * 4);
+    chunk_bytes = o_has + al(per * 4);
+    table.get(kMaxChunks);
   }
-  auto best_axis = [&](bool use_samples) {
-    int axis = -1;
-    double best = -1.0;
-    for (int j = 0; j < d; ++j) {
-      const double wj = hi[j] - lo[j];
-      if (wj <= min_width) continue;
-      double score = wj;
-      if (use_samples) {
-        const double mid = 0.5 * (lo[j] + hi[j]);
-        int n_lo = 0;
-        for (int i = 0; i < k; ++i)
-          if (static_cast<double>(top_u[static_cast<size_t>(i) * d + j]) <= mid) ++n_lo;
-        score = wj * std::abs(2 * n_lo - k);
-      }
-      if (score > best) {
-        best = score;
-        axis = j;
-      }
+  DevPool(const DevPool&) = delete;
+  DevPool& operator=(const DevPool&) = delete;
+  ~DevPool() {
+    if (ctx != nullptr && (ctx->slab_d != d || ctx->slab_K != K)) {
+      for (unsigned char* p : ctx->slab_spare) cudaFree(p);
+      ctx->slab_spare.clear();
+      ctx->slab_d = d;
+      ctx->slab_K = K;
     }
-    return std::pair<int, double>{axis, best};
-  };
-  auto [axis, score] = k > 0 ? best_axis(true) : best_axis(false);
-  if (k > 0 && axis >= 0 && score == 0.0) axis = best_axis(false).first;
-  if (axis < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
-  return axis;
-}
-
-void split_rec(const Rec& rec, int d, double top_percent, double min_width, int64_t next_id, int split_rule, Rec& lo_c,
-               Rec& hi_c) {  // bab.cpp:155-223
-  const int n_top = static_cast<int>(rec.top_val.size());
-  const int axis = split_axis(d, rec.lo.data(), rec.hi.data(), n_top, rec.top_act.data(), rec.samples, top_percent,
-                              min_width, split_rule);
-  const double mid = 0.5 * (rec.lo[static_cast<size_t>(axis)] + rec.hi[static_cast<size_t>(axis)]);
-  lo_c = Rec();
-  hi_c = Rec();
-  lo_c.lo = rec.lo;
-  lo_c.hi = rec.hi;
-  lo_c.hi[static_cast<size_t>(axis)] = mid;
-  hi_c.lo = rec.lo;
-  hi_c.hi = rec.hi;
-  hi_c.lo[static_cast<size_t>(axis)] = mid;
-  for (Rec* c : {&lo_c, &hi_c}) {
-    c->depth = rec.depth + 1;
-    c->parent = rec.id;
-    c->log_vol = rec.log_vol + std::log(0.5);
-  }
-  lo_c.id = next_id;
-  hi_c.id = next_id + 1;
-  for (int i = 0; i < n_top; ++i) {
-    const float* u = rec.top_act.data() + static_cast<size_t>(i) * d;
-    Rec& c = static_cast<double>(u[axis]) <= mid ? lo_c : hi_c;
-    c.top_val.push_back(rec.top_val[static_cast<size_t>(i)]);
-    c.top_act.insert(c.top_act.end(), u, u + d);
-  }
-  for (Rec* c : {&lo_c, &hi_c})
-    if (!c->top_val.empty()) {
-      c->uf = c->top_val.front();
-      c->best.assign(c->top_act.begin(), c->top_act.begin() + d);
+    for (unsigned char* p : chunks) {
+      if (ctx != nullptr) ctx->slab_spare.push_back(p);
+      else cudaFree(p);
     }
-}
-
-void merge_report(Rec& rec, Report&& rep, int top_capacity, int d) {  // bab.cpp:245-262
-  rec.samples += rep.samples;
-  if (rep.uf < rec.uf) {
-    rec.uf = rep.uf;
-    rec.best = rep.best;
   }
-  if (rec.top_val.empty()) {
-    rec.top_val = std::move(rep.top_val);
-    rec.top_act = std::move(rep.top_act);
-  } else if (!rep.top_val.empty()) {
-    // std::merge: stable, ties keep the record's own samples first
-    std::vector<float> mv, ma;
-    const size_t na = rec.top_val.size(), nb = rep.top_val.size();
-    const size_t keep = std::min<size_t>(na + nb, static_cast<size_t>(top_capacity));
-    mv.reserve(keep);
-    ma.reserve(keep * d);
-    size_t i = 0, j = 0;
-    while (mv.size() < keep) {
-      const bool take_b = j < nb && (i >= na || rep.top_val[j] < rec.top_val[i]);
-      if (take_b) {
-        mv.push_back(rep.top_val[j]);
-        ma.insert(ma.end(), rep.top_act.begin() + static_cast<std::ptrdiff_t>(j * d),
-                  rep.top_act.begin() + static_cast<std::ptrdiff_t>((j + 1) * d));
-        ++j;
-      } else {
-        mv.push_back(rec.top_val[i]);
-        ma.insert(ma.end(), rec.top_act.begin() + static_cast<std::ptrdiff_t>(i * d),
-                  rec.top_act.begin() + static_cast<std::ptrdiff_t>((i + 1) * d));
-        ++i;
-      }
-    }
-    rec.top_val = std::move(mv);
-    rec.top_act = std::move(ma);
-  }
-}
-
-// Search + bound of this rank's children on the device: boxes, warm starts and the
-// children's global indices (the sampler stream key, so results do not depend on the
-// rank a child runs on).
-std::vector<Report> search_and_bound(bp_ctx* c, const std::vector<Rec*>& boxes, const std::vector<int64_t>& index,
-                                     const bp_search_config& scfg, int mode, int alpha, std::vector<double>* lfs) {
-  const int d = c->comp.d;
-  const int n = static_cast<int>(boxes.size());
-  std::vector<double> lo(static_cast<size_t>(n) * d), hi(static_cast<size_t>(n) * d), warm(static_cast<size_t>(n) * d);
-  bool any_warm = false;
-  for (int k = 0; k < n; ++k) {
-    const Rec& b = *boxes[static_cast<size_t>(k)];
-    std::copy(b.lo.begin(), b.lo.end(), lo.begin() + static_cast<std::ptrdiff_t>(k) * d);
-    std::copy(b.hi.begin(), b.hi.end(), hi.begin() + static_cast<std::ptrdiff_t>(k) * d);
-    if (!b.best.empty()) {
-      any_warm = true;
-      std::copy(b.best.begin(), b.best.end(), warm.begin() + static_cast<std::ptrdiff_t>(k) * d);
+  bp::PoolArgs args() const { return {d, K, shift, table.p, o_lo, o_hi, o_best, o_val, o_act, o_n, o_has}; }
+  bp::PoolArgs host_args() const { return {d, K, shift, chunks.data(), o_lo, o_hi, o_best, o_val, o_act, o_n, o_has}; }
+  void add_chunk(cudaStream_t st) {
+    if (static_cast<int>(chunks.size()) == kMaxChunks) fail(BP_UNSUPPORTED, "subdomain pool: too many records");
+    unsigned char* p = nullptr;
+    if (ctx != nullptr && ctx->slab_d == d && ctx->slab_K == K && !ctx->slab_spare.empty()) {
+      p = ctx->slab_spare.back();
+      ctx->slab_spare.pop_back();
     } else {
-      std::fill(warm.begin() + static_cast<std::ptrdiff_t>(k) * d, warm.begin() + static_cast<std::ptrdiff_t>(k + 1) * d,
-                std::numeric_limits<double>::quiet_NaN());
+      ck(cudaMalloc(&p, chunk_bytes), "cudaMalloc (subdomain pool chunk)");
     }
+    chunks.push_back(p);
+    ck(memcpy_counted(table.p + chunks.size() - 1, &chunks.back(), sizeof(p), cudaMemcpyHostToDevice, st), "H2D");
   }
-  std::vector<Report> reps;
-  lfs->assign(static_cast<size_t>(n), 0.0);
-  const auto t0 = std::chrono::steady_clock::now();
-  if (n > 0) {
-    device_batch_search(c, n, lo.data(), hi.data(), any_warm ? warm.data() : nullptr, scfg, &reps, index.data());
-    device_batch_bound(c, mode, alpha, lfs->data());
+  int alloc(cudaStream_t st) {
+    if (!free_slots.empty()) {
+      const int s = free_slots.back();
+      free_slots.pop_back();
+      return s;
+    }
+    if (static_cast<size_t>(used) == (chunks.size() << shift)) add_chunk(st);
+    return used++;
   }
-  c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  c->harvest_roll_events();
-  return reps;
+  void release(int s) {
+    if (s >= 0) free_slots.push_back(s);
+  }
+};
+
+// The iteration's per-child search inputs and routed top lists (local index order).
+bp::StageArgs stage_buffers(bp_ctx* c, int n, int K) {
+  const size_t nb = static_cast<size_t>(std::max({n, c->reserve_boxes, 1}));
+  const size_t nd = nb * c->comp.d, nk = nb * K;
+  return {c->lo_f.get(nd), c->hi_f.get(nd), c->warm_f.get(nd), c->lo_d.get(nd), c->hi_d.get(nd),
+          c->st_val.get(nk), c->st_act.get(nk * c->comp.d), c->st_n.get(nb)};
 }
 
 // A pool record as every rank sees it: what pick_out, the retirement
-// test, prune and the trace read.  The full record (box, best, top samples) lives only
-// on its owner rank.
+// test, split's sample count, prune and the trace read.  The payload lives in the
+// owner rank's device slab (slot).
 struct Head {
   int64_t id;
   double lf, uf, log_vol, max_width;
   int owner;
+  int depth;
+  int64_t samples;
+  int slot;  // the owner's slab slot
 };
 
-// Fixed-size wire forms (doubles, then floats) of a full record (owner -> search rank)
-// and of a searched child's head + incumbent candidate (allgather).
-struct Wire {
-  static size_t rec_bytes(int d, int K) {
-    return sizeof(double) * (10 + 3 * static_cast<size_t>(d)) + sizeof(float) * static_cast<size_t>(K) * (1 + d);
-  }
-  static void put_rec(unsigned char* p, int64_t k, const Rec& r, int d, int K) {
-    double* h = reinterpret_cast<double*>(p);
-    const int nt = static_cast<int>(r.top_val.size());
-    h[0] = static_cast<double>(k);
-    h[1] = static_cast<double>(r.id);
-    h[2] = static_cast<double>(r.parent);
-    h[3] = r.depth;
-    h[4] = r.log_vol;
-    h[5] = r.lf;
-    h[6] = r.uf;
-    h[7] = static_cast<double>(r.samples);
-    h[8] = nt;
-    h[9] = r.best.empty() ? 0.0 : 1.0;
-    std::copy(r.lo.begin(), r.lo.end(), h + 10);
-    std::copy(r.hi.begin(), r.hi.end(), h + 10 + d);
-    if (!r.best.empty()) std::copy(r.best.begin(), r.best.end(), h + 10 + 2 * d);
-    float* f = reinterpret_cast<float*>(h + 10 + 3 * d);
-    std::copy(r.top_val.begin(), r.top_val.end(), f);
-    std::copy(r.top_act.begin(), r.top_act.end(), f + K);
-  }
-  static int64_t get_rec(const unsigned char* p, Rec& r, int d, int K) {
-    const double* h = reinterpret_cast<const double*>(p);
-    r = Rec();
-    r.id = static_cast<int64_t>(h[1]);
-    r.parent = static_cast<int64_t>(h[2]);
-    r.depth = static_cast<int>(h[3]);
-    r.log_vol = h[4];
-    r.lf = h[5];
-    r.uf = h[6];
-    r.samples = static_cast<int64_t>(h[7]);
-    const int nt = static_cast<int>(h[8]);
-    r.lo.assign(h + 10, h + 10 + d);
-    r.hi.assign(h + 10 + d, h + 10 + 2 * d);
-    if (h[9] != 0.0) r.best.assign(h + 10 + 2 * d, h + 10 + 3 * d);
-    const float* f = reinterpret_cast<const float*>(h + 10 + 3 * d);
-    r.top_val.assign(f, f + nt);
-    r.top_act.assign(f + K, f + K + static_cast<size_t>(nt) * d);
-    return static_cast<int64_t>(h[0]);
-  }
-  static size_t head_bytes(int d) { return sizeof(double) * (9 + static_cast<size_t>(d)); }
-  static void put_head(double* h, int64_t k, const Rec& r, int64_t rep_samples, bool ok, int d) {
-    h[0] = static_cast<double>(k);
-    h[1] = static_cast<double>(r.id);
-    h[2] = r.lf;
-    h[3] = r.uf;
-    h[4] = r.log_vol;
-    h[5] = r.max_width();
-    h[6] = static_cast<double>(rep_samples);
-    h[7] = ok ? 1.0 : 0.0;
-    h[8] = r.best.empty() ? 0.0 : 1.0;
-    for (int j = 0; j < d; ++j) h[9 + j] = r.best.empty() ? 0.0 : r.best[static_cast<size_t>(j)];
-  }
-};
-
-// plan() (bab.cpp:266-415) as a steppable object: the constructor runs the
-// root search + bound, step() one pick -> split -> search -> bound -> merge ->
-// prune iteration, finish() the result fields.
+// plan() (bab.cpp:266-415) as a steppable object: the constructor runs the root
+// search + bound, step() one pick -> split -> search -> bound -> merge -> prune
+// iteration, finish() the result fields.  pick_out, the retirement test and prune run
+// on the host over the heads (pick_out's softmax must use the reference's exp() to
+// pick the same records); split and merge_report run on the device over the slab
+// (pool.cu), so no top list crosses PCIe.
 //
 // Sharded over ranks: every rank holds the pool's heads in the same
 // order and replays pick_out / retirement / prune / trace on them identically (the
 // pick stream is the shared mt19937_64(mix_seed(seed, 1))).  Child k of an iteration
-// (global pick order) is searched on rank k % world; the owner of its parent splits
-// the parent and ships the child record there (fixed-size all-to-all); after search,
-// bound and merge only the children's heads (+ their best actions, the incumbent
-// candidates) are all-gathered.  One rank runs the same code with no exchange.
+// (global pick order) is searched on rank k % world and owned there; the owner of its
+// parent splits the parent and ships the child record there (fixed-size all-to-all);
+// after search, bound and merge the children's heads and each rank's incumbent
+// candidate are all-gathered.  One rank runs the same code with no exchange.
 struct Planner {
+  static constexpr int kHeadWords = 8;  // k, id, lf, uf, log_vol, max_width, samples, depth
   bp_ctx* c;
   bp_planner_config cfg;
-  int d;
+  int d, K;
   std::chrono::steady_clock::time_point t0;
-  std::vector<Head> pool;                    // heads, pool order, identical on every rank
-  std::unordered_map<int64_t, Rec> own;      // full records owned by this rank
+  std::vector<Head> pool;  // heads, pool order, identical on every rank
+  DevPool slab;
+  bp::StageArgs S{};
   bp_rng pick_rng;
   int64_t next_id = 1;
   double pruned_cum = 0.0;
@@ -1455,6 +1375,16 @@ struct Planner {
   bool done = false;
   int64_t children_bounded = 0;  // subdomains searched + bounded so far (root included)
   int last_children = 0;
+  // per-iteration scratch
+  DBuf<bp::SplitTask> d_tasks;
+  DBuf<int> d_axis, d_slots, d_unpack_dst, d_unpack_slot;
+  DBuf<unsigned char> d_pack, d_recv;
+  DBuf<float> d_uf;
+  DBuf<double> d_maxw;
+  HBuf<int> h_axis;
+  HBuf<float> h_uf, h_best;
+  HBuf<double> h_maxw;
+  HBuf<unsigned char> h_pack;
 
   int world() const { return c->world > 1 && c->exchange != nullptr ? c->world : 1; }
   int rank() const { return world() > 1 ? c->rank : 0; }
@@ -1486,7 +1416,7 @@ struct Planner {
     for (auto& r : pool) {
       if (r.lf > result.uf) {
         removed += std::exp(r.log_vol);
-        own.erase(r.id);
+        if (r.owner == rank()) slab.release(r.slot);
       } else {
         keep.push_back(r);
       }
@@ -1495,125 +1425,122 @@ struct Planner {
     return removed;
   }
 
-  // Search, bound and merge the children of one iteration (global order; child k runs on
-  // rank k % world).  `local` holds this rank's child records (by k); afterwards every
-  // rank appends all children's heads in order and updates the incumbent as the
-  // reference's sequential loop does (bab.cpp:388-403).
-  void run_children(int n_all, std::map<int64_t, Rec>& local, uint64_t seed) {
-    const int W = world(), R = rank();
-    std::vector<Rec*> boxes;
-    std::vector<int64_t> index;
-    for (auto& kv : local) {
-      boxes.push_back(&kv.second);
-      index.push_back(kv.first);
-    }
+  // Search, bound and merge_report of this rank's n staged children (keys = global
+  // indices, the sampler stream key, so results do not depend on the rank a child runs
+  // on); per child the bound, the merged incumbent value, the box's max width and the
+  // samples taken.
+  struct Out {
+    std::vector<double> lf, maxw;
+    std::vector<float> uf;
+    std::vector<int64_t> samples;
+  };
+  Out search_bound_merge(const std::vector<int64_t>& keys, const std::vector<int>& slots, uint64_t seed) {
+    const int n = static_cast<int>(keys.size());
+    Out o;
+    o.lf.assign(static_cast<size_t>(n), 0.0);
+    o.maxw.assign(static_cast<size_t>(n), 0.0);
+    o.uf.assign(static_cast<size_t>(n), INFINITY);
+    o.samples.assign(static_cast<size_t>(n), 0);
+    if (n == 0) return o;
+    const auto ts = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
     bp_search_config scfg = cfg.search;
     scfg.seed = seed;
-    std::vector<double> lfs;
-    std::vector<Report> reps = search_and_bound(c, boxes, index, scfg, cfg.bound_mode, cfg.alpha, &lfs);
-    std::vector<int64_t> rep_samples(boxes.size());
-    std::vector<char> rep_ok(boxes.size());
-    parallel_for(static_cast<int>(boxes.size()), [&](int i) {
-      rep_samples[static_cast<size_t>(i)] = reps[static_cast<size_t>(i)].samples;
-      rep_ok[static_cast<size_t>(i)] = reps[static_cast<size_t>(i)].ok ? 1 : 0;
-      boxes[static_cast<size_t>(i)]->lf = lfs[static_cast<size_t>(i)];
-      merge_report(*boxes[static_cast<size_t>(i)], std::move(reps[static_cast<size_t>(i)]), cfg.search.top_capacity, d);
-    });
-    // heads of every child, in global order
-    const size_t hb = Wire::head_bytes(d) / sizeof(double);
-    std::vector<double> heads(static_cast<size_t>(n_all) * hb, 0.0);
-    if (W == 1) {
-      for (size_t i = 0; i < boxes.size(); ++i)
-        Wire::put_head(heads.data() + static_cast<size_t>(index[i]) * hb, index[i], *boxes[i], rep_samples[i], rep_ok[i], d);
-    } else {
-      const int per_rank = (n_all + W - 1) / W;
-      std::vector<double> send(static_cast<size_t>(per_rank) * hb, -1.0), recv(send.size() * static_cast<size_t>(W));
-      for (size_t i = 0; i < boxes.size(); ++i)
-        Wire::put_head(send.data() + i * hb, index[i], *boxes[i], rep_samples[i], rep_ok[i], d);
-      if (c->exchange(c->exchange_user, send.data(), send.size() * sizeof(double), recv.data()) != 0)
-        fail(BP_NCCL, "exchange: allgather of child heads failed");
-      std::vector<char> seen(static_cast<size_t>(n_all), 0);
-      for (size_t q = 0; q < static_cast<size_t>(per_rank) * W; ++q) {
-        const double* h = recv.data() + q * hb;
-        if (h[0] < 0.0) continue;
-        const int64_t k = static_cast<int64_t>(h[0]);
-        if (k >= n_all || seen[static_cast<size_t>(k)]) fail(BP_NCCL, "exchange: inconsistent child heads");
-        seen[static_cast<size_t>(k)] = 1;
-        std::copy(h, h + hb, heads.data() + static_cast<size_t>(k) * hb);
-      }
-      if (std::find(seen.begin(), seen.end(), 0) != seen.end()) fail(BP_NCCL, "exchange: missing child heads");
+    bp::SearchArgs a = search_setup(c, n, scfg, keys.data(), true);
+    search_run(c, a, scfg);
+    const size_t nb = static_cast<size_t>(std::max(n, c->reserve_boxes));  // no reallocation while ramping up
+    int* ds = d_slots.get(nb);
+    ck(memcpy_counted(ds, slots.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    float* du = d_uf.get(nb);
+    double* dm = d_maxw.get(nb);
+    ck(bp::launch_pool_merge(slab.args(), S, ds, n, a.top_val[a.cur], a.top_act[a.cur], a.top_cnt, a.uf, a.best, a.failed,
+                             cfg.search.top_capacity, du, dm, st), "pool merge launch");
+    ++c->launches;
+    float* hu = h_uf.get(nb);
+    double* hm = h_maxw.get(nb);
+    ck(memcpy_counted(hu, du, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(memcpy_counted(hm, dm, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    device_batch_bound(c, cfg.bound_mode, cfg.alpha, o.lf.data());  // synchronises the stream
+    for (int i = 0; i < n; ++i) {
+      o.uf[static_cast<size_t>(i)] = hu[i];
+      o.maxw[static_cast<size_t>(i)] = hm[i];
+      o.samples[static_cast<size_t>(i)] =
+          c->h_failed[static_cast<size_t>(i)] ? 0 : static_cast<int64_t>(scfg.iterations) * a.rows;
     }
-    for (int k = 0; k < n_all; ++k) {
-      const double* h = heads.data() + static_cast<size_t>(k) * hb;
-      Head hd{static_cast<int64_t>(h[1]), h[2], h[3], h[4], h[5], k % W};
-      result.samples += static_cast<int64_t>(h[6]);
-      if (hd.uf < result.uf) {
-        result.uf = hd.uf;
-        result.best.assign(h + 9, h + 9 + d);
-      }
-      pool.push_back(hd);
-    }
-    for (auto& kv : local) {
-      const int64_t id = kv.second.id;
-      own.emplace(id, std::move(kv.second));
-    }
-    children_bounded += n_all;
+    c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count();
+    c->harvest_roll_events();
+    return o;
+  }
+
+  // The incumbent action of one owned record (FP32 on the device, FP64 in the result).
+  std::vector<double> fetch_best(int slot) {
+    float* hb = h_best.get(static_cast<size_t>(d));
+    ck(memcpy_counted(hb, bp::pool_best(slab.host_args(), slot), static_cast<size_t>(d) * 4, cudaMemcpyDeviceToHost,
+                      c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return std::vector<double>(hb, hb + d);
   }
 
   Planner(bp_ctx* ctx, const bp_planner_config& config, const double* warm_start)
-      : c(ctx), cfg(config), d(ctx->comp.d), t0(std::chrono::steady_clock::now()), pick_rng(mix_seed(config.seed, 1)) {
+      : c(ctx), cfg(config), d(ctx->comp.d), K(std::max(config.search.top_capacity, 1)),
+        t0(std::chrono::steady_clock::now()), slab(ctx, ctx->comp.d, std::max(config.search.top_capacity, 1)),
+        pick_rng(mix_seed(config.seed, 1)) {
     if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
-    std::map<int64_t, Rec> local;
-    int64_t samples = 0;
-    if (rank() == 0) {  // the root is child 0 of the root search: rank 0 searches it
-      Rec root;
-      root.lo.resize(static_cast<size_t>(d));
-      root.hi.resize(static_cast<size_t>(d));
+    const int W = world();
+    // at most 2 * batch children per step, ceil(2 * batch / W) of them on this rank
+    c->reserve_boxes = std::max(c->reserve_boxes, (2 * cfg.batch + W - 1) / W);
+    std::vector<double> h(static_cast<size_t>(kHeadWords + 2 + d), 0.0);  // the root's head + incumbent
+    int root_slot = -1;
+    if (rank() == 0) {  // the root is child 0 of the root search: rank 0 searches and owns it
+      std::vector<double> lo(static_cast<size_t>(d)), hi(static_cast<size_t>(d));
       for (int t = 0; t < c->comp.o.H; ++t)
         for (int j = 0; j < c->comp.o.ka; ++j) {
-          root.lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
-          root.hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
+          lo[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.ulo[static_cast<size_t>(j)];
+          hi[static_cast<size_t>(t * c->comp.o.ka + j)] = c->comp.uhi[static_cast<size_t>(j)];
         }
-      if (warm_start) root.best.assign(warm_start, warm_start + d);  // search warm start only
-      bp_search_config scfg = cfg.search;
-      scfg.seed = mix_seed(cfg.seed, 0);
-      std::vector<double> lfs;
-      std::vector<Rec*> boxes{&root};
-      std::vector<Report> reps = search_and_bound(c, boxes, {0}, scfg, cfg.bound_mode, cfg.alpha, &lfs);
-      if (!reps[0].ok) fail(BP_RUNTIME, "plan: root search failed: " + reps[0].error);
-      root.best.clear();
-      root.id = 0;
-      root.log_vol = 0.0;
-      root.lf = lfs[0];
-      samples = reps[0].samples;
-      merge_report(root, std::move(reps[0]), cfg.search.top_capacity, d);
-      local.emplace(0, std::move(root));
+      cudaStream_t st = c->stream;
+      root_slot = slab.alloc(st);
+      S = stage_buffers(c, 1, K);
+      place_host_boxes(c, 1, lo.data(), hi.data(), warm_start);  // the warm start seeds the root search only
+      if (warm_start == nullptr) {
+        const std::vector<float> nan(static_cast<size_t>(d), std::numeric_limits<float>::quiet_NaN());
+        ck(memcpy_counted(S.warm_f, nan.data(), static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, st), "H2D");
+      }
+      ck(cudaMemsetAsync(S.n, 0, sizeof(int), st), "memset");
+      ck(cudaMemcpyAsync(bp::pool_lo(slab.host_args(), root_slot), S.lo_d, static_cast<size_t>(d) * 8,
+                         cudaMemcpyDeviceToDevice, st), "D2D");
+      ck(cudaMemcpyAsync(bp::pool_hi(slab.host_args(), root_slot), S.hi_d, static_cast<size_t>(d) * 8,
+                         cudaMemcpyDeviceToDevice, st), "D2D");
+      Out o = search_bound_merge({0}, {root_slot}, mix_seed(cfg.seed, 0));
+      if (c->h_failed[0]) fail(BP_RUNTIME, "plan: root search failed: evaluate: non-finite objective value (malformed weights?)");
+      h[0] = 0.0;
+      h[1] = 0.0;
+      h[2] = o.lf[0];
+      h[3] = o.uf[0];
+      h[4] = 0.0;
+      h[5] = o.maxw[0];
+      h[6] = static_cast<double>(o.samples[0]);
+      h[7] = 0.0;
+      h[8] = o.uf[0];
+      if (std::isfinite(o.uf[0])) {
+        const std::vector<double> b = fetch_best(root_slot);
+        std::copy(b.begin(), b.end(), h.begin() + kHeadWords + 2);
+      }
     }
-    root_heads(local, samples);
+    if (W > 1) {  // the root's head from rank 0 to every rank
+      std::vector<double> recv(h.size() * static_cast<size_t>(W));
+      if (c->exchange(c->exchange_user, h.data(), h.size() * sizeof(double), recv.data()) != 0)
+        fail(BP_NCCL, "exchange: allgather of the root head failed");
+      std::copy(recv.begin(), recv.begin() + static_cast<std::ptrdiff_t>(h.size()), h.begin());  // rank 0's
+    }
+    pool.push_back(Head{0, h[2], h[3], 0.0, h[5], 0, 0, static_cast<int64_t>(h[6]), root_slot});
+    result.uf = h[3];
+    result.best.assign(h.begin() + kHeadWords + 2, h.end());
+    result.samples = static_cast<int64_t>(h[6]);
+    children_bounded = 1;
     last_children = 1;
     pruned_cum += prune();
     push_trace(0, 1.0);
-  }
-
-  // The root's head (and incumbent) from rank 0 to every rank.
-  void root_heads(std::map<int64_t, Rec>& local, int64_t samples) {
-    const int W = world();
-    const size_t hb = Wire::head_bytes(d) / sizeof(double);
-    std::vector<double> h(hb, -1.0);
-    if (rank() == 0) Wire::put_head(h.data(), 0, local.begin()->second, samples, true, d);
-    if (W > 1) {
-      std::vector<double> recv(hb * static_cast<size_t>(W));
-      if (c->exchange(c->exchange_user, h.data(), hb * sizeof(double), recv.data()) != 0)
-        fail(BP_NCCL, "exchange: allgather of the root head failed");
-      std::copy(recv.begin(), recv.begin() + static_cast<std::ptrdiff_t>(hb), h.begin());  // rank 0's
-    }
-    Head hd{static_cast<int64_t>(h[1]), h[2], h[3], h[4], h[5], 0};
-    result.uf = hd.uf;
-    result.best.assign(h.begin() + 9, h.begin() + 9 + d);
-    result.samples = static_cast<int64_t>(h[6]);
-    pool.push_back(hd);
-    if (rank() == 0) own.emplace(0, std::move(local.begin()->second));
-    children_bounded = 1;
   }
 
   // One BaB iteration; returns false (and records the stop reason) when the
@@ -1630,6 +1557,7 @@ struct Planner {
     }
     ++iter;
     const int W = world(), R = rank();
+    cudaStream_t st = c->stream;
     std::vector<bp_pool_meta> meta(pool.size());
     for (size_t i = 0; i < pool.size(); ++i) meta[i] = {pool[i].lf, pool[i].uf, pool[i].id, pool[i].log_vol};
     const std::vector<int> chosen = pick_indices(meta.data(), static_cast<int>(pool.size()), cfg.batch, cfg.eta, cfg.temperature, pick_rng);
@@ -1649,38 +1577,84 @@ struct Planner {
     for (const auto& r : picked) selected_vol += std::exp(r.log_vol);
     std::vector<Head> to_split;
     for (const Head& h : picked) {
-      if (h.max_width <= cfg.min_width) {
+      if (h.max_width <= cfg.min_width) {  // retired: too narrow to split
         retired_min_lf = std::min(retired_min_lf, h.lf);
-        own.erase(h.id);
+        if (h.owner == R) slab.release(h.slot);
         continue;
       }
       to_split.push_back(h);
     }
     const int n_all = 2 * static_cast<int>(to_split.size());
-    // the owners split their picked parents; child k goes to rank k % W
-    std::vector<int> mine_par;
-    for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
-      if (to_split[static_cast<size_t>(i)].owner == R) mine_par.push_back(i);
-    std::vector<Rec> kids(2 * mine_par.size());
-    parallel_for(static_cast<int>(mine_par.size()), [&](int q) {  // ids by pick order, as the serial loop
-      const int i = mine_par[static_cast<size_t>(q)];
-      const Rec& par = own.at(to_split[static_cast<size_t>(i)].id);
-      split_rec(par, d, cfg.top_percent, cfg.min_width, next_id + 2 * i, cfg.split_rule, kids[2 * static_cast<size_t>(q)],
-                kids[2 * static_cast<size_t>(q) + 1]);
-    });
-    for (int i : mine_par) own.erase(to_split[static_cast<size_t>(i)].id);
+    const int64_t base_id = next_id;  // child k gets id base_id + k (ids by pick order, as the serial loop)
     next_id += n_all;
     last_children = n_all;
-    std::map<int64_t, Rec> local;  // this rank's children, by global index
-    if (W == 1) {
-      for (size_t q = 0; q < mine_par.size(); ++q) {
-        local.emplace(2 * static_cast<int64_t>(mine_par[q]), std::move(kids[2 * q]));
-        local.emplace(2 * static_cast<int64_t>(mine_par[q]) + 1, std::move(kids[2 * q + 1]));
+    // this rank's children (k % W == R) in global order, with their slab slots
+    std::vector<int64_t> keys;
+    std::vector<int> li_of(static_cast<size_t>(n_all), -1);
+    for (int k = 0; k < n_all; ++k)
+      if (k % W == R) {
+        li_of[static_cast<size_t>(k)] = static_cast<int>(keys.size());
+        keys.push_back(k);
       }
-    } else if (n_all > 0) {
-      ship_children(to_split, mine_par, kids, local);
+    const int n_loc = static_cast<int>(keys.size());
+    std::vector<int> slots(static_cast<size_t>(n_loc));
+    for (int& s : slots) s = slab.alloc(st);
+    S = stage_buffers(c, n_loc, K);
+    // split this rank's parents (one CTA each); shipped children packed by destination rank
+    std::vector<std::vector<int64_t>> out_k(static_cast<size_t>(W));
+    for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
+      if (to_split[static_cast<size_t>(i)].owner == R)
+        for (int b = 0; b < 2; ++b) {
+          const int64_t k = 2 * static_cast<int64_t>(i) + b;
+          if (k % W != R) out_k[static_cast<size_t>(k % W)].push_back(k);
+        }
+    std::vector<int> pack_of(static_cast<size_t>(n_all), -1);
+    int n_pack = 0;
+    for (int r = 0; r < W; ++r)
+      for (int64_t k : out_k[static_cast<size_t>(r)]) pack_of[static_cast<size_t>(k)] = n_pack++;
+    std::vector<bp::SplitTask> tasks;
+    for (int i = 0; i < static_cast<int>(to_split.size()); ++i) {
+      const Head& p = to_split[static_cast<size_t>(i)];
+      if (p.owner != R) continue;
+      bp::SplitTask t{};
+      t.parent = p.slot;
+      for (int b = 0; b < 2; ++b) {
+        const int64_t k = 2 * static_cast<int64_t>(i) + b;
+        const int li = li_of[static_cast<size_t>(k)];
+        t.key[b] = k;
+        t.dst[b] = li;
+        t.slot[b] = li >= 0 ? slots[static_cast<size_t>(li)] : -1;
+        t.pack[b] = pack_of[static_cast<size_t>(k)];
+      }
+      // split's k (bab.cpp:160-165) before the clamp to the stored list
+      t.k_round = cfg.split_rule != BP_SPLIT_SAMPLES ? -2
+                  : p.samples > 0 ? static_cast<long long>(std::llround(cfg.top_percent / 100.0 * static_cast<double>(p.samples)))
+                                  : -1;
+      tasks.push_back(t);
     }
-    if (n_all > 0) run_children(n_all, local, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1));
+    const size_t rb = bp::pool_record_bytes(d, K);
+    unsigned char* dpack = n_pack > 0 ? d_pack.get(static_cast<size_t>(n_pack) * rb) : nullptr;
+    if (!tasks.empty()) {
+      const size_t tb = std::max<size_t>(tasks.size(), static_cast<size_t>(cfg.batch));
+      bp::SplitTask* dt = d_tasks.get(tb);
+      ck(memcpy_counted(dt, tasks.data(), tasks.size() * sizeof(bp::SplitTask), cudaMemcpyHostToDevice, st), "H2D");
+      int* da = d_axis.get(tb);
+      ck(bp::launch_pool_split(slab.args(), dt, static_cast<int>(tasks.size()), S, dpack, cfg.min_width, da, st),
+         "pool split launch");
+      ++c->launches;
+      int* ha = h_axis.get(tb);
+      ck(memcpy_counted(ha, da, tasks.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      for (size_t q = 0; q < tasks.size(); ++q)
+        if (ha[q] < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
+    }
+    for (const Head& p : to_split)  // the parents' payload has been read by the split
+      if (p.owner == R) slab.release(p.slot);
+    if (W > 1 && n_all > 0) ship_children(to_split, n_pack, li_of, slots);
+    if (n_all > 0) {
+      Out o = search_bound_merge(keys, slots, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1));
+      gather_children(to_split, base_id, keys, slots, o);
+    }
     pruned_cum += prune();
     push_trace(iter, selected_vol);
     return true;
@@ -1688,52 +1662,126 @@ struct Planner {
 
   // Child records from their parent's owner to their search rank: a fixed-size
   // all-to-all whose counts every rank derives from the replicated heads.
-  void ship_children(const std::vector<Head>& to_split, const std::vector<int>& mine_par, std::vector<Rec>& kids,
-                     std::map<int64_t, Rec>& local) {
+  void ship_children(const std::vector<Head>& to_split, int n_pack, const std::vector<int>& li_of,
+                     const std::vector<int>& slots) {
     const int W = world(), R = rank();
-    const int K = std::max(cfg.search.top_capacity, 1);
-    const size_t rb = Wire::rec_bytes(d, K);
-    std::vector<std::vector<int64_t>> out(static_cast<size_t>(W));  // child indices this rank sends to r
-    std::vector<int64_t> in_count(static_cast<size_t>(W), 0);      // records this rank receives from r
+    cudaStream_t st = c->stream;
+    const size_t rb = bp::pool_record_bytes(d, K);
+    std::vector<int64_t> sb(static_cast<size_t>(W), 0), rbts(static_cast<size_t>(W), 0);
     for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
       for (int b = 0; b < 2; ++b) {
         const int64_t k = 2 * static_cast<int64_t>(i) + b;
         const int dst = static_cast<int>(k % W), src = to_split[static_cast<size_t>(i)].owner;
-        if (src == R && dst != R) out[static_cast<size_t>(dst)].push_back(k);
-        if (dst == R && src != R) ++in_count[static_cast<size_t>(src)];
+        if (src == R && dst != R) sb[static_cast<size_t>(dst)] += static_cast<int64_t>(rb);
+        if (dst == R && src != R) rbts[static_cast<size_t>(src)] += static_cast<int64_t>(rb);
       }
-    std::map<int64_t, Rec*> by_k;
-    for (size_t q = 0; q < mine_par.size(); ++q) {
-      by_k[2 * static_cast<int64_t>(mine_par[q])] = &kids[2 * q];
-      by_k[2 * static_cast<int64_t>(mine_par[q]) + 1] = &kids[2 * q + 1];
+    size_t r_total = 0;
+    for (int r = 0; r < W; ++r) r_total += static_cast<size_t>(rbts[static_cast<size_t>(r)]);
+    unsigned char* send = h_pack.get(std::max<size_t>(static_cast<size_t>(n_pack) * rb, 1));
+    if (n_pack > 0) {
+      ck(memcpy_counted(send, d_pack.p, static_cast<size_t>(n_pack) * rb, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
     }
-    std::vector<int64_t> sb(static_cast<size_t>(W)), rbts(static_cast<size_t>(W));
-    size_t s_total = 0, r_total = 0;
-    for (int r = 0; r < W; ++r) {
-      sb[static_cast<size_t>(r)] = static_cast<int64_t>(out[static_cast<size_t>(r)].size() * rb);
-      rbts[static_cast<size_t>(r)] = static_cast<int64_t>(in_count[static_cast<size_t>(r)] * static_cast<int64_t>(rb));
-      s_total += static_cast<size_t>(sb[static_cast<size_t>(r)]);
-      r_total += static_cast<size_t>(rbts[static_cast<size_t>(r)]);
-    }
-    std::vector<unsigned char> send(std::max<size_t>(s_total, 1)), recv(std::max<size_t>(r_total, 1));
-    {
-      size_t off = 0;
-      for (int r = 0; r < W; ++r)
-        for (int64_t k : out[static_cast<size_t>(r)]) {
-          Wire::put_rec(send.data() + off, k, *by_k.at(k), d, K);
-          off += rb;
-        }
-    }
+    std::vector<unsigned char> recv(std::max<size_t>(r_total, 1));
     if (c->alltoallv == nullptr) fail(BP_NCCL, "exchange: no all-to-all hook for the sharded pool");
-    if (c->alltoallv(c->exchange_user, send.data(), sb.data(), recv.data(), rbts.data()) != 0)
+    if (c->alltoallv(c->exchange_user, send, sb.data(), recv.data(), rbts.data()) != 0)
       fail(BP_NCCL, "exchange: all-to-all of child records failed");
-    for (size_t off = 0; off + rb <= r_total; off += rb) {
-      Rec r;
-      const int64_t k = Wire::get_rec(recv.data() + off, r, d, K);
-      local.emplace(k, std::move(r));
+    const int n_in = static_cast<int>(r_total / rb);
+    if (n_in == 0) return;
+    std::vector<int> dst(static_cast<size_t>(n_in)), slot(static_cast<size_t>(n_in));
+    for (int q = 0; q < n_in; ++q) {
+      double key;
+      std::memcpy(&key, recv.data() + static_cast<size_t>(q) * rb, sizeof(double));
+      const int64_t k = static_cast<int64_t>(key);
+      if (k < 0 || k >= static_cast<int64_t>(li_of.size()) || li_of[static_cast<size_t>(k)] < 0)
+        fail(BP_NCCL, "exchange: child record for another rank");
+      dst[static_cast<size_t>(q)] = li_of[static_cast<size_t>(k)];
+      slot[static_cast<size_t>(q)] = slots[static_cast<size_t>(li_of[static_cast<size_t>(k)])];
     }
-    for (auto& kv : by_k)
-      if (kv.first % W == R) local.emplace(kv.first, std::move(*kv.second));
+    unsigned char* dr = d_recv.get(r_total);
+    ck(memcpy_counted(dr, recv.data(), r_total, cudaMemcpyHostToDevice, st), "H2D");
+    int* dd = d_unpack_dst.get(static_cast<size_t>(n_in));
+    int* ds = d_unpack_slot.get(static_cast<size_t>(n_in));
+    ck(memcpy_counted(dd, dst.data(), static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(ds, slot.data(), static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(bp::launch_pool_unpack(slab.args(), S, dr, dd, ds, n_in, st), "pool unpack launch");
+    ++c->launches;
+  }
+
+  // Every child's head in global order (all-gathered across ranks) appended to the
+  // pool; the incumbent updated as the reference's sequential loop does
+  // (bab.cpp:388-403): the first child holding the iteration's lowest value, if lower.
+  void gather_children(const std::vector<Head>& to_split, int64_t base_id, const std::vector<int64_t>& keys,
+                       const std::vector<int>& slots, const Out& o) {
+    const int W = world(), R = rank();
+    const int n_all = 2 * static_cast<int>(to_split.size());
+    const int n_loc = static_cast<int>(keys.size());
+    int cand = -1;  // this rank's lowest child (first in global order on ties)
+    for (int i = 0; i < n_loc; ++i)
+      if (std::isfinite(o.uf[static_cast<size_t>(i)]) && (cand < 0 || o.uf[static_cast<size_t>(i)] < o.uf[static_cast<size_t>(cand)]))
+        cand = i;
+    const int per_rank = (n_all + W - 1) / W;
+    const size_t words = static_cast<size_t>(per_rank) * kHeadWords + 2 + static_cast<size_t>(d);
+    std::vector<double> send(words, -1.0);
+    for (int i = 0; i < n_loc; ++i) {
+      double* h = send.data() + static_cast<size_t>(i) * kHeadWords;
+      const Head& p = to_split[static_cast<size_t>(keys[static_cast<size_t>(i)] / 2)];
+      h[0] = static_cast<double>(keys[static_cast<size_t>(i)]);
+      h[1] = static_cast<double>(base_id + keys[static_cast<size_t>(i)]);
+      h[2] = o.lf[static_cast<size_t>(i)];
+      h[3] = o.uf[static_cast<size_t>(i)];
+      h[4] = p.log_vol + std::log(0.5);
+      h[5] = o.maxw[static_cast<size_t>(i)];
+      h[6] = static_cast<double>(o.samples[static_cast<size_t>(i)]);
+      h[7] = p.depth + 1;
+    }
+    double* cd = send.data() + static_cast<size_t>(per_rank) * kHeadWords;
+    cd[0] = cand >= 0 ? o.uf[static_cast<size_t>(cand)] : INFINITY;
+    cd[1] = cand >= 0 ? static_cast<double>(keys[static_cast<size_t>(cand)]) : -1.0;
+    if (cand >= 0) {
+      const std::vector<double> b = fetch_best(slots[static_cast<size_t>(cand)]);
+      std::copy(b.begin(), b.end(), cd + 2);
+    }
+    std::vector<double> recv;
+    if (W == 1) {
+      recv = std::move(send);
+    } else {
+      recv.resize(words * static_cast<size_t>(W));
+      if (c->exchange(c->exchange_user, send.data(), words * sizeof(double), recv.data()) != 0)
+        fail(BP_NCCL, "exchange: allgather of child heads failed");
+    }
+    std::vector<const double*> by_k(static_cast<size_t>(n_all), nullptr);
+    const double* best_cd = nullptr;
+    for (int r = 0; r < W; ++r) {
+      const double* blk = recv.data() + static_cast<size_t>(r) * words;
+      for (int q = 0; q < per_rank; ++q) {
+        const double* h = blk + static_cast<size_t>(q) * kHeadWords;
+        if (h[0] < 0.0) continue;
+        const int64_t k = static_cast<int64_t>(h[0]);
+        if (k >= n_all || by_k[static_cast<size_t>(k)] != nullptr) fail(BP_NCCL, "exchange: inconsistent child heads");
+        by_k[static_cast<size_t>(k)] = h;
+      }
+      const double* cr = blk + static_cast<size_t>(per_rank) * kHeadWords;
+      if (cr[1] >= 0.0 && (best_cd == nullptr || cr[0] < best_cd[0] || (cr[0] == best_cd[0] && cr[1] < best_cd[1])))
+        best_cd = cr;
+    }
+    for (int k = 0; k < n_all; ++k) {
+      const double* h = by_k[static_cast<size_t>(k)];
+      if (h == nullptr) fail(BP_NCCL, "exchange: missing child heads");
+      const int owner = k % W;
+      const int slot = owner == R ? slots[static_cast<size_t>(li_of_local(keys, k))] : -1;
+      pool.push_back(Head{static_cast<int64_t>(h[1]), h[2], h[3], h[4], h[5], owner, static_cast<int>(h[7]),
+                          static_cast<int64_t>(h[6]), slot});
+      result.samples += static_cast<int64_t>(h[6]);
+    }
+    if (best_cd != nullptr && best_cd[0] < result.uf) {
+      result.uf = best_cd[0];
+      result.best.assign(best_cd + 2, best_cd + 2 + d);
+    }
+    children_bounded += n_all;
+  }
+  static int li_of_local(const std::vector<int64_t>& keys, int64_t k) {  // keys ascending
+    return static_cast<int>(std::lower_bound(keys.begin(), keys.end(), k) - keys.begin());
   }
 
   void finish() {
@@ -2244,15 +2292,115 @@ bp_status bp_pick_out(const bp_pool_meta* pool, int n_pool, int n, double eta, d
   });
 }
 
-bp_status bp_split_axis(int d, const double* lo, const double* hi, int n_top, const double* top_u, int64_t samples,
-                        double top_percent, double min_width, int split_rule, int* axis, double* mid,
-                        unsigned char* route) {
-  return guard([&] {
-    std::vector<float> u(static_cast<size_t>(n_top) * d);
-    for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<float>(top_u[i]);
-    *axis = split_axis(d, lo, hi, n_top, u.data(), samples, top_percent, min_width, split_rule);
-    *mid = 0.5 * (lo[*axis] + hi[*axis]);
-    for (int i = 0; i < n_top; ++i) route[i] = static_cast<double>(u[static_cast<size_t>(i) * d + *axis]) <= *mid ? 0 : 1;
+bp_status bp_pool_split(bp_ctx* ctx, int n, int d, int K, const double* lo, const double* hi, const int* n_top,
+                        const float* top_val, const float* top_act, const int64_t* samples, double top_percent,
+                        double min_width, int split_rule, int* axis, double* child_lo, double* child_hi, int* child_n,
+                        float* child_val, float* child_act) {
+  return guard([&] {  // split (bab.cpp:155-223) of n parents through pool.cu's split_kernel
+    check_ctx(ctx);
+    if (n <= 0 || d <= 0 || K <= 0) fail(BP_INVALID_ARGUMENT, "pool_split: n, d and K must be positive");
+    for (int i = 0; i < n; ++i)
+      if (n_top[i] < 0 || n_top[i] > K) fail(BP_INVALID_ARGUMENT, "pool_split: top list longer than K");
+    cudaStream_t st = ctx->stream;
+    const size_t nd = static_cast<size_t>(n) * d, nk = static_cast<size_t>(n) * K;
+    DevPool slab(nullptr, d, K);
+    for (int i = 0; i < 3 * n; ++i) slab.alloc(st);  // parents 0..n-1, children n..3n-1
+    const bp::PoolArgs H = slab.host_args();
+    const size_t sd = static_cast<size_t>(d), sk = static_cast<size_t>(K);
+    for (int i = 0; i < n; ++i) {
+      ck(memcpy_counted(bp::pool_lo(H, i), lo + i * sd, sd * 8, cudaMemcpyHostToDevice, st), "H2D");
+      ck(memcpy_counted(bp::pool_hi(H, i), hi + i * sd, sd * 8, cudaMemcpyHostToDevice, st), "H2D");
+      ck(memcpy_counted(bp::pool_n(H, i), n_top + i, 4, cudaMemcpyHostToDevice, st), "H2D");
+      ck(memcpy_counted(bp::pool_val(H, i), top_val + i * sk, sk * 4, cudaMemcpyHostToDevice, st), "H2D");
+      ck(memcpy_counted(bp::pool_act(H, i), top_act + i * sk * sd, sk * sd * 4, cudaMemcpyHostToDevice, st), "H2D");
+    }
+    DBuf<float> lo_f, hi_f, warm_f, sv, sa;
+    DBuf<double> lo_d, hi_d;
+    DBuf<int> sn, da;
+    DBuf<bp::SplitTask> dt;
+    const size_t cn = 2 * static_cast<size_t>(n);
+    bp::StageArgs S{lo_f.get(cn * d), hi_f.get(cn * d), warm_f.get(cn * d), lo_d.get(cn * d), hi_d.get(cn * d),
+                    sv.get(cn * K), sa.get(cn * K * d), sn.get(cn)};
+    std::vector<bp::SplitTask> tasks(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      bp::SplitTask& t = tasks[static_cast<size_t>(i)];
+      t.parent = i;
+      for (int b = 0; b < 2; ++b) {
+        t.slot[b] = n + 2 * i + b;
+        t.dst[b] = 2 * i + b;
+        t.pack[b] = -1;
+        t.key[b] = 2 * i + b;
+      }
+      t.k_round = split_rule != BP_SPLIT_SAMPLES ? -2
+                  : samples[i] > 0 ? static_cast<long long>(std::llround(top_percent / 100.0 * static_cast<double>(samples[i])))
+                                   : -1;
+    }
+    ck(memcpy_counted(dt.get(tasks.size()), tasks.data(), tasks.size() * sizeof(bp::SplitTask), cudaMemcpyHostToDevice, st), "H2D");
+    ck(bp::launch_pool_split(slab.args(), dt.p, n, S, nullptr, min_width, da.get(static_cast<size_t>(n)), st), "pool split launch");
+    ck(memcpy_counted(axis, da.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    for (int i = 0; i < n; ++i)
+      if (axis[i] < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
+    for (size_t q = 0; q < cn; ++q) {
+      ck(memcpy_counted(child_lo + q * sd, bp::pool_lo(H, n + static_cast<int>(q)), sd * 8, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(child_hi + q * sd, bp::pool_hi(H, n + static_cast<int>(q)), sd * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    ck(memcpy_counted(child_n, sn.p, cn * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(memcpy_counted(child_val, sv.p, cn * K * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(memcpy_counted(child_act, sa.p, cn * K * d * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+bp_status bp_pool_merge(bp_ctx* ctx, int n, int d, int K, int capacity, const int* a_n, const float* a_val,
+                        const float* a_act, const int* b_n, const float* b_val, const float* b_act, const float* b_uf,
+                        const float* b_best, const int* b_failed, int* out_n, float* out_val, float* out_act,
+                        float* out_uf, int* has_best, float* out_best) {
+  return guard([&] {  // merge_report (bab.cpp:245-262) of n records through pool.cu's merge_kernel
+    check_ctx(ctx);
+    if (n <= 0 || d <= 0 || K <= 0) fail(BP_INVALID_ARGUMENT, "pool_merge: n, d and K must be positive");
+    for (int i = 0; i < n; ++i)
+      if (a_n[i] < 0 || a_n[i] > K || b_n[i] < 0 || b_n[i] > K) fail(BP_INVALID_ARGUMENT, "pool_merge: list longer than K");
+    cudaStream_t st = ctx->stream;
+    const size_t nd = static_cast<size_t>(n) * d, nk = static_cast<size_t>(n) * K;
+    DevPool slab(nullptr, d, K);
+    for (int i = 0; i < n; ++i) slab.alloc(st);
+    const bp::PoolArgs H = slab.host_args();
+    const size_t sd = static_cast<size_t>(d), sk = static_cast<size_t>(K);
+    for (int i = 0; i < n; ++i) {
+      ck(cudaMemsetAsync(bp::pool_lo(H, i), 0, sd * 8, st), "memset");
+      ck(cudaMemsetAsync(bp::pool_hi(H, i), 0, sd * 8, st), "memset");
+    }
+    DBuf<float> sv, sa, bv, ba, bu, bb, du;
+    DBuf<int> sn, bn, bf, ds;
+    DBuf<double> dm;
+    bp::StageArgs S{};
+    S.val = sv.get(nk);
+    S.act = sa.get(nk * d);
+    S.n = sn.get(static_cast<size_t>(n));
+    ck(memcpy_counted(S.val, a_val, nk * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(S.act, a_act, nk * d * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(S.n, a_n, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(bv.get(nk), b_val, nk * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(ba.get(nk * d), b_act, nk * d * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(bn.get(static_cast<size_t>(n)), b_n, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(bu.get(static_cast<size_t>(n)), b_uf, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(bb.get(nd), b_best, nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(bf.get(static_cast<size_t>(n)), b_failed, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    std::vector<int> slots(static_cast<size_t>(n));
+    std::iota(slots.begin(), slots.end(), 0);
+    ck(memcpy_counted(ds.get(static_cast<size_t>(n)), slots.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(bp::launch_pool_merge(slab.args(), S, ds.p, n, bv.p, ba.p, bn.p, bu.p, bb.p, bf.p, capacity,
+                             du.get(static_cast<size_t>(n)), dm.get(static_cast<size_t>(n)), st), "pool merge launch");
+    ck(memcpy_counted(out_uf, du.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    for (int i = 0; i < n; ++i) {
+      ck(memcpy_counted(out_n + i, bp::pool_n(H, i), 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(out_val + i * sk, bp::pool_val(H, i), sk * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(out_act + i * sk * sd, bp::pool_act(H, i), sk * sd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(has_best + i, bp::pool_has(H, i), 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(memcpy_counted(out_best + i * sd, bp::pool_best(H, i), sd * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 

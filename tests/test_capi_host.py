@@ -1,6 +1,7 @@
 """CPU checks of the C-ABI library: it loads, exports every symbol the header
 declares, and its host-side restatements (Rng stream, generate_model,
-pick_out, split) agree bit-for-bit with the oracle.  No GPU compute."""
+pick_out) agrees bit-for-bit with the oracle (split / merge_report run on the
+device: tests/test_gpu_pool.py).  No GPU compute."""
 import ctypes as C
 import json
 import math
@@ -91,32 +92,6 @@ def test_pick_out_bit_exact_vs_oracle():
         meta = [(float(lf[i]), float(uf[i]), i, -0.7 * i) for i in range(n_pool)]
         for n, eta, T in ((4, 0.75, 0.05), (10, 0.0, 0.5), (n_pool + 3, 0.5, 1e-13)):
             assert product_pick(meta, n, eta, T, 99 + trial) == orc.pick_out(meta, n, eta, T, orc.Rng(99 + trial))
-
-
-def test_split_axis_bit_exact_vs_oracle():
-    lib = _capi.load()
-    rng = np.random.default_rng(8)
-    for trial in range(60):
-        d = int(rng.integers(1, 9))
-        lo = rng.uniform(-2, 0, d)
-        hi = lo + rng.uniform(0, 2, d)
-        if trial % 7 == 0:
-            hi[0] = lo[0]  # degenerate axis
-        n_top = int(rng.integers(0, 30))
-        top = rng.uniform(lo, hi, (n_top, d)).astype(np.float32).astype(np.float64)
-        samples = int(rng.integers(0, 3000))
-        rule = trial % 2
-        axis, mid = C.c_int(), C.c_double()
-        route = (C.c_ubyte * max(1, n_top))()
-        st = lib.bp_split_axis(d, _capi.dptr(lo), _capi.dptr(hi), n_top, _capi.dptr(np.ascontiguousarray(top)),
-                               samples, 1.0, 1e-6, rule, C.byref(axis), C.byref(mid), route)
-        try:
-            ref = orc.split(lo, hi, np.zeros(n_top), top, samples, 1.0, 1e-6, rule)
-        except ValueError:
-            assert st == _capi.BP_INVALID_ARGUMENT
-            continue
-        assert st == 0 and (axis.value, mid.value) == (ref[0], ref[1])
-        assert list(route[:n_top]) == list(ref[2])
 
 
 def test_config_defaults_and_round_trip():
