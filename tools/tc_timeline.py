@@ -11,6 +11,8 @@ import paper_2412_09584_b200 as bp
 from paper_2412_09584_b200 import workloads
 wl = workloads.ALL[sys.argv[1] if len(sys.argv) > 1 else "c2"]()
 dev = bp.Device(0).load(wl.spec)
+if len(sys.argv) > 2:
+    dev.rollout_path(sys.argv[2])
 lo, hi = wl.spec.box()
 acts = np.random.default_rng(0).uniform(lo, hi, size=(512, 1025, wl.spec.d)).astype(np.float32)
 for _ in range(2):
