@@ -945,6 +945,9 @@ bp::SearchArgs search_setup(bp_ctx* c, int n, const bp_search_config& cfg, const
 void place_host_boxes(bp_ctx* c, int n, const double* lo, const double* hi, const double* warm) {
   const int d = c->comp.d;
   const size_t nd = static_cast<size_t>(n) * d;
+  // the same capacities search_setup asks for (a smaller request here and a larger one
+  // there would reallocate and drop the uploaded boxes)
+  const size_t cap = static_cast<size_t>(std::max(n, c->reserve_boxes)) * d;
   for (size_t i = 0; i < nd; ++i)
     if (!(lo[i] <= hi[i]) || !std::isfinite(lo[i]) || !std::isfinite(hi[i]))
       fail(BP_INVALID_ARGUMENT, "BoxDomain: invalid bounds");
@@ -954,14 +957,14 @@ void place_host_boxes(bp_ctx* c, int n, const double* lo, const double* hi, cons
     lf32[i] = static_cast<float>(lo[i]);
     hf32[i] = static_cast<float>(hi[i]);
   }
-  ck(memcpy_counted(c->lo_f.get(nd), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(c->hi_f.get(nd), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(c->lo_d.get(nd), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
-  ck(memcpy_counted(c->hi_d.get(nd), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->lo_f.get(cap), lf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->hi_f.get(cap), hf32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->lo_d.get(cap), lo, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
+  ck(memcpy_counted(c->hi_d.get(cap), hi, nd * 8, cudaMemcpyHostToDevice, st), "H2D");
   if (warm != nullptr) {
     std::vector<float> w32(nd);
     for (size_t i = 0; i < nd; ++i) w32[i] = static_cast<float>(warm[i]);
-    ck(memcpy_counted(c->warm_f.get(nd), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(memcpy_counted(c->warm_f.get(cap), w32.data(), nd * 4, cudaMemcpyHostToDevice, st), "H2D");
   }
 }
 

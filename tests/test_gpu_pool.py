@@ -111,3 +111,25 @@ def test_merge_matches_oracle(device, d, K, cap, tied):
         assert oh[i] == (best is not None), i
         if best is not None:
             assert np.array_equal(ob[i], best.astype(np.float32)), i
+
+
+def test_search_after_plan_sees_its_own_boxes():
+    """A plan sizes the context's search buffers for its children per step; a later
+    batch_search on the same context (fewer boxes, a warm start) must give exactly what
+    a fresh context gives (regression: buffers reallocated between upload and use)."""
+    import paper_2412_09584_b200 as bp
+    from paper_2412_09584_b200 import workloads
+
+    wl = workloads.c1(glorot=True)
+    cfg = wl.planner_config()
+    cfg["batch"] = 64
+    cfg["termination"]["max_iterations"] = 2
+    cfg["search"]["samples_per_iter"] = 128
+    cfg["search"]["iterations"] = 3
+    lo, hi = wl.spec.box()
+    warm = np.random.default_rng(3).uniform(lo, hi).astype(np.float32).astype(np.float64)
+    used = bp.Device(0).load(wl.spec)
+    used.plan(cfg)
+    a = used.batch_search(lo[None], hi[None], warm[None], cfg, seed=11)
+    b = bp.Device(0).load(wl.spec).batch_search(lo[None], hi[None], warm[None], cfg, seed=11)
+    assert a["uf"][0] == b["uf"][0] and np.array_equal(a["best"], b["best"])
