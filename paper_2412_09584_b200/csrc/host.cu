@@ -667,7 +667,9 @@ Compiled compile(const bp_objective_desc& d) {
       }
       // two ping-pong tiles when the widths allow it and both tiles' scratch rows fit,
       // else one tile; the weight ring takes the rest (>= three 128-row blocks)
-      const size_t min_ring = 3 * 128 * 128;
+      // the MMA warp holds a K-block's weight blocks at once (hi, lo per N half: four 16 KB
+      // blocks at width 256), and the producer needs one more in flight
+      const size_t min_ring_narrow = 3 * 128 * 128, min_ring_wide = 5 * 128 * 128;
       const bool narrow = npadmax <= 128 && kbmax <= 4;
       const int plans[3][2] = {{2, 128}, {1, 128}, {1, 256}};
       for (const auto& pl : plans) {
@@ -675,6 +677,7 @@ Compiled compile(const bp_objective_desc& d) {
         o.tc2 = pl[0];
         o.tc2_rw = pl[1];
         const size_t fixed = bp::rollout_tc2_fixed_smem(o);
+        const size_t min_ring = pl[1] == 256 ? min_ring_wide : min_ring_narrow;
         if (fixed + min_ring <= cap) {
           o.tc2_ring = static_cast<int>((cap - fixed) & ~static_cast<size_t>(1023));
           break;

@@ -18,8 +18,14 @@
 //    registers by a transposing warp butterfly (lane j ends with column j over
 //    the warp's 32 rows) and go straight to the global record with one atomic
 //    pair per column and warp -- no staging buffer, no extrema warps.
-//  * Weight blocks stream as separate hi and lo entries ([rows][128 B] each), so
-//    more of them are in flight in a smaller ring.
+//  * Weight blocks stream as separate hi and lo entries ([rows][128 B] each).  The MMA
+//    warp walks K-blocks outermost (N halves inside): it waits for all of a K-block's
+//    weight blocks, then issues the K-block's 12 (24 at width 256) MMAs in one burst
+//    from one elected asm per N half, and commits one barrier per K-block (a_free) that
+//    frees both its ring bytes and its A_lo slot.  A_lo keeps only ALO K-block slots
+//    (2 at width 256: K-block c waits until K-block c-2's MMAs retired), which leaves
+//    the weight ring room for two K-blocks' weights (C3: 162.9 -> 178 TFLOP/s; the
+//    timeline shows the 64 KB weight stream per K-block now pacing the 24-MMA bursts).
 //
 // Precision (as v1): 3xTF32, D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, hi read as the top
 // 19 bits of the FP32 value, lo = x - trunc(x) exact; ~2^-21 relative per product.  The
@@ -73,10 +79,18 @@ constexpr int kSlots = 8;  // weight blocks in flight at most (mbarrier pairs)
 // __nanosleep backoff (ns) of the long waits: producer / cost warp / epilogue
 constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
 
+#ifndef BP_ALO_WIDE
+#define BP_ALO_WIDE 2
+#endif
+__host__ __device__ constexpr int tc2_alo_slots(int rw) { return rw >= 256 ? BP_ALO_WIDE : rw / 32 < 4 ? rw / 32 : 4; }
+
 template <int NT, int RW_, int EPI_, int CW_>
 struct Tc2 {
   static constexpr int RW = RW_;                  // TMEM region width >= widest padded layer
   static constexpr int KBMAX = RW / 32;           // A operand K-blocks of 32 per tile
+  // shared-memory slots of A_lo K-blocks per tile: two at width 256 (the rest of shared
+  // memory goes to the weight ring, which then holds two K-blocks' weights), else up to 4
+  static constexpr int ALO = tc2_alo_slots(RW);
   static constexpr int EPI = EPI_;                // epilogue warps (warps 0 .. EPI-1)
   static constexpr int WPQ = EPI / (4 * NT);      // epilogue warps per TMEM quadrant per tile
   static constexpr int CW = CW_;                  // cost warps per tile
@@ -90,7 +104,7 @@ struct Tc2 {
 };
 
 struct Tc2Smem {
-  unsigned char* alo;  // [NT][KBMAX] K-blocks of 128 rows x 128 B (A lo part, SW128 K-major)
+  unsigned char* alo;  // [NT][ALO] slots of A lo K-blocks, 128 rows x 128 B (SW128 K-major); K-block c in slot c % ALO
   unsigned char* w;    // weight byte ring
   float* sc;           // [NT][128][tc_S] per-row scratch of the cost warps (x_t written by the epilogue)
   float* bias;         // [L][RW]
@@ -99,18 +113,18 @@ struct Tc2Smem {
   int* segl;           // [NT][128] tile-local subdomain of each row (-1 past the last)
   int* pairs;          // [n_sc][2] recorded scratch columns (column, record offset)
   uint64_t* full;      // [kSlots] weight block landed
-  uint64_t* empty;     // [kSlots] weight block consumed by the MMAs
   uint64_t* d_full;    // [NT][2] accumulator region ready for the epilogue
   uint64_t* a_chunk;   // [NT][KBMAX] A operand K-block written (4 quadrant warps)
   uint64_t* x_full;    // [NT] x_t of every row in the scratch (all epilogue warps of the tile)
   uint64_t* x_empty;   // [NT] step's scratch rows consumed (the tile's cost warp)
+  uint64_t* a_free;    // [NT][KBMAX] A operand K-block read by its MMAs (commit): its A_lo slot is free
   uint32_t* tmem_slot;
-  uint32_t* ring;      // [2][kSlots] producer bookkeeping
+  uint32_t* ring;      // [3][kSlots] producer bookkeeping
   size_t bytes;
 };
 
 __host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* base) {
-  const int NT = o.tc2, RW = o.tc2_rw, KBMAX = RW / 32;
+  const int NT = o.tc2, RW = o.tc2_rw, KBMAX = RW / 32, ALO = tc2_alo_slots(RW);
   Tc2Smem m;
   size_t off = 0;
   auto take = [&](size_t n, size_t align) {
@@ -119,7 +133,7 @@ __host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* 
     off += n;
     return p;
   };
-  m.alo = take(static_cast<size_t>(NT) * KBMAX * 16384, 1024);
+  m.alo = take(static_cast<size_t>(NT) * ALO * 16384, 1024);
   m.w = take(static_cast<size_t>(o.tc2_ring), 1024);
   m.sc = reinterpret_cast<float*>(take(sizeof(float) * NT * 128 * o.tc_S, 16));
   m.bias = reinterpret_cast<float*>(take(sizeof(float) * o.L * RW, 16));
@@ -127,15 +141,15 @@ __host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* 
   m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops, 16));
   m.segl = reinterpret_cast<int*>(take(sizeof(int) * NT * 128, 16));
   m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc, 16));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kSlots + NT * (2 + KBMAX + 2)), 16));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (kSlots + NT * (2 + KBMAX + 2 + KBMAX)), 16));
   m.full = bars;
-  m.empty = m.full + kSlots;
-  m.d_full = m.empty + kSlots;
+  m.d_full = m.full + kSlots;
   m.a_chunk = m.d_full + 2 * NT;
   m.x_full = m.a_chunk + NT * KBMAX;
   m.x_empty = m.x_full + NT;
+  m.a_free = m.x_empty + NT;
   m.tmem_slot = reinterpret_cast<uint32_t*>(take(16, 16));
-  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2 * kSlots, 16));
+  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 3 * kSlots, 16));
   m.bytes = off;
   return m;
 }
@@ -306,7 +320,7 @@ template <int NT, int RW_, int EPI_, int CW_>
 __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
     rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
   using C = Tc2<NT, RW_, EPI_, CW_>;
-  constexpr int RW = C::RW, KBMAX = C::KBMAX, WPQ = C::WPQ, CW = C::CW, NR = C::NR;
+  constexpr int RW = C::RW, KBMAX = C::KBMAX, ALO = C::ALO, WPQ = C::WPQ, CW = C::CW, NR = C::NR;
   constexpr uint32_t kTmemCols = 2 * NT * RW;  // a power of two >= 32
   extern __shared__ unsigned char smraw[];
   const uint32_t s0 = smem_u32(smraw);
@@ -339,7 +353,6 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(m.full + s, 1);
-      mbar_init(m.empty + s, 1);
     }
     for (int i = 0; i < NT; ++i) {
       mbar_init(m.d_full + 2 * i, 1);
@@ -347,6 +360,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
       for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_chunk + i * KBMAX + c, 4);
       mbar_init(m.x_full + i, 4 * WPQ);
       mbar_init(m.x_empty + i, CW);
+      for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_free + i * KBMAX + c, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -363,17 +377,23 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
 
   if (warp == C::kProducerWarp) {
     // ------------------------------------------------ producer: weight blocks, hi then lo
+    // A block's ring bytes are free once the MMAs of its K-block retired: the MMA warp
+    // commits one barrier per K-block (a_free), so the producer waits on that, with the
+    // completion's parity recorded when the block was placed.
     if (lane == 0) {
       uint32_t pos = 0;
       uint32_t* lo_b = m.ring;  // byte ranges of the in-flight blocks, oldest first
       uint32_t* hi_b = m.ring + kSlots;
+      uint32_t* fr_b = m.ring + 2 * kSlots;  // a_free barrier index << 1 | parity of the completion
+      uint32_t ppar = 0;  // bit i*KBMAX+kb: parity of a_free[i][kb]'s next completion
       int it = 0, head = 0;
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l)
           for (int i = 0; i < NT; ++i) {
             const int npad = o.tc_npad[l], nh = n_halves(npad);
-            for (int h = 0; h < nh; ++h)  // N half outer: one accumulator address per pass
-              for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
+            for (int kb = 0; kb < o.tc_kb[l]; ++kb) {  // K-block outer: its A_lo slot is freed after it
+              const int bit = i * KBMAX + kb;
+              for (int h = 0; h < nh; ++h) {
                 const int nr = half_rows(npad, h);
                 const float* src = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32 + (h ? 2 * 128 * 32 : 0);
                 const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
@@ -382,16 +402,19 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
                   while (head < it) {
                     const int hs = head % kSlots;
                     if (it - head < kSlots && (hi_b[hs] <= at || lo_b[hs] >= at + bytes)) break;
-                    mbar_wait(m.empty + hs, static_cast<uint32_t>((head / kSlots) & 1), kSleepProducer);
+                    mbar_wait(m.a_free + (fr_b[hs] >> 1), fr_b[hs] & 1u, kSleepProducer);
                     ++head;
                   }
                   const int s = it % kSlots;
                   lo_b[s] = at;
                   hi_b[s] = at + bytes;
+                  fr_b[s] = (static_cast<uint32_t>(bit) << 1) | ((ppar >> bit) & 1u);
                   mbar_expect_tx(m.full + s, bytes);
                   bulk_g2s(m.w + at, src + part * nr * 32, bytes, m.full + s);
                 }
               }
+            }
+            ppar ^= ((1u << o.tc_kb[l]) - 1u) << (i * KBMAX);  // one completion per K-block of this operand
           }
     }
   } else if (warp == C::kMmaWarp) {
@@ -409,55 +432,57 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
           const int npad = o.tc_npad[l], nh = n_halves(npad), ksteps = o.tc_ksteps[l];
           const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
           const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
-          long long wfull = 0;  // timeline: cycles waiting for weight blocks
-          for (int h = 0; h < nh; ++h) {  // N half outer: the accumulator address stays put
-            const int nr = half_rows(npad, h);
-            const uint32_t idesc = tf32_idesc(nr);
-            const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
-            const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
-            for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
-              const int bit = i * KBMAX + kb;
-              if (h == 0) {  // first pass: this K-block of A written by the epilogue
-                if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
-                mbar_wait_warp(m.a_chunk + bit, (a_par >> bit) & 1u);
-                if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
-                a_par ^= 1u << bit;
-                fence_after();
-              }
-              const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(bit) * 16384u);
-              const int nq = min(4, ksteps - kb * 4);
-              const uint32_t a0 = areg + 32 * kb;
-              // hi block: A_hi.B_hi and A_lo.B_hi as strictly alternating TS/SS pairs
-              {
-                const uint32_t at = ring_place(pos, bytes, ring_bytes);
-                const int s = it % kSlots;
-                const long long w0 = tl_clock();
-                mbar_wait_warp(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
-                wfull += tl_clock() - w0;
-                if (l == 1 && i == 0) mark2(a, t, 600 + 2 * (h * 8 + kb));
-                const uint64_t bd = sw128_desc(wbase + at);
+          long long wfull = 0, awt = 0;  // timeline: cycles waiting for weight blocks / A K-blocks
+          // K-block outer, N half inner: K-block kb's A_lo slot is free for the epilogue's
+          // next K-block in that slot once both halves' MMAs have read it
+          for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
+            const int bit = i * KBMAX + kb;
+            if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
+            const long long aw0 = tl_clock();
+            mbar_wait_warp(m.a_chunk + bit, (a_par >> bit) & 1u);  // this K-block of A written by the epilogue
+            awt += tl_clock() - aw0;
+            if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
+            a_par ^= 1u << bit;
+            fence_after();
+            const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(i * ALO + kb % ALO) * 16384u);
+            const int nq = min(4, ksteps - kb * 4);
+            const uint32_t a0 = areg + 32 * kb;
+            // every weight block of the K-block (hi, lo per N half: consecutive ring entries)
+            // first, then all its MMAs back to back: one burst per K-block keeps the tensor
+            // pipe fed (the waits and commits between bursts are the issuer's overhead)
+            uint32_t at[4];
+            int sl[4];
+            const int nblk = 2 * nh;
+            const long long w0 = tl_clock();
+            for (int b = 0; b < nblk; ++b) {
+              at[b] = ring_place(pos, static_cast<uint32_t>(half_rows(npad, b >> 1)) * 128u, ring_bytes);
+              sl[b] = (it + b) % kSlots;
+              mbar_wait_warp(m.full + sl[b], static_cast<uint32_t>(((it + b) / kSlots) & 1));
+            }
+            wfull += tl_clock() - w0;
+            if (l == 1 && i == 0) mark2(a, t, 600 + 2 * kb);
+            for (int h = 0; h < nh; ++h) {
+              const uint32_t idesc = tf32_idesc(half_rows(npad, h));
+              const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
+              const uint64_t bh = sw128_desc(wbase + at[2 * h]), bl = sw128_desc(wbase + at[2 * h + 1]);
+              if (nq == 4) {
+                mma_kblock_elect(dcol, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
+              } else {
+                // hi block: A_hi.B_hi and A_lo.B_hi as strictly alternating TS/SS pairs
                 for (int q = 0; q < nq; ++q)
-                  mma_pair_elect(dcol, a0 + 8 * q, alo_d + 2 * q, bd + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
-                mma_commit_elect(m.empty + s);
-                ++it;
-              }
-              // lo block: A_hi.B_lo
-              {
-                const uint32_t at = ring_place(pos, bytes, ring_bytes);
-                const int s = it % kSlots;
-                const long long w0 = tl_clock();
-                mbar_wait_warp(m.full + s, static_cast<uint32_t>((it / kSlots) & 1));
-                wfull += tl_clock() - w0;
-                const uint64_t bd = sw128_desc(wbase + at);
-                for (int q = 0; q < nq; ++q) mma_ts(dcol, a0 + 8 * q, bd + 2 * q, idesc, 1u);
-                mma_commit_elect(m.empty + s);
-                ++it;
+                  mma_pair_elect(dcol, a0 + 8 * q, alo_d + 2 * q, bh + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
+                // lo block: A_hi.B_lo
+                for (int q = 0; q < nq; ++q) mma_ts(dcol, a0 + 8 * q, bl + 2 * q, idesc, 1u);
               }
             }
+            if (l == 1 && i == 0) mark2(a, t, 601 + 2 * kb);
+            it += nblk;  // the blocks are free once these MMAs retire: the a_free commit below
+            mma_commit_elect(m.a_free + bit);
           }
           mma_commit_elect(m.d_full + 2 * i + (li & 1));  // accumulator region complete
           mark2(a, t, 102 + 20 * l + 10 * i);
           put2(a, t, 300 + 20 * l + 10 * i, wfull + (1ll << 40));
+          if (NT == 1) put2(a, t, 310 + 20 * l, awt + (1ll << 40));
         }
   } else if (warp >= C::EPI) {
     // ------------------------------------------------ cost warps: CW per tile, NR rows per
@@ -539,7 +564,16 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
     const long long grow = row0 + row;
     const bool row_ok = grow < a.n_rows;
     const uint32_t tl = tmem + (static_cast<uint32_t>(32 * g) << 16) + static_cast<uint32_t>(ti * 2 * RW);
-    unsigned char* alo = m.alo + ti * KBMAX * 16384;
+    unsigned char* alo = m.alo + ti * ALO * 16384;
+    // A_lo slots: K-block c of an A operand goes to slot c % ALO.  K-block c >= ALO waits
+    // until the MMAs read K-block c - ALO of the same operand (a_free, one completion per
+    // operand; bit k of fpar = its parity); the slot's uses by earlier operands were read
+    // before this operand's writer started (it waited for the accumulator).
+    uint32_t fpar = 0;
+    auto slot_wait = [&](int c) {
+      if (c >= ALO) mbar_wait(m.a_free + ti * KBMAX + (c - ALO), (fpar >> (c - ALO)) & 1u, kSleepEpi);
+    };
+    auto a_done = [&](int kb) { fpar ^= (1u << kb) - 1u; };  // an operand of kb K-blocks was consumed
     float* scrow = m.sc + (ti * 128 + row) * S;
     const float* urow = row_ok ? a.actions + grow * d : nullptr;
     // warp's subdomain span (uniform): the common case is one subdomain, all rows valid
@@ -594,9 +628,10 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
         const int k = c * 32 + j;
         v[j] = k < ks ? o.f[o.x0 + min(k, ks - 1)] : 0.f;
       }
-      features_store(c, v, tl + RW + 32 * c, alo + c * 16384);
+      features_store(c, v, tl + RW + 32 * c, alo + (c % ALO) * 16384);  // no earlier use of the slots
       publish_chunk(m.a_chunk + ti * KBMAX + c);
     }
+    a_done(o.tc_kb[0]);
     int li = 0;
     const bool lead = warp % per_tile == 0;  // first epilogue warp of its tile (timeline)
     for (int t = 0; t < H; ++t) {
@@ -639,7 +674,8 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
               float w[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) w[j] = relu ? fmaxf(v[j], 0.f) : v[j];
-              store_operand(tl + dcol + 32 * c, alo + c * 16384, row, w);
+              slot_wait(c);
+              store_operand(tl + dcol + 32 * c, alo + (c % ALO) * 16384, row, w);
               publish_chunk(m.a_chunk + ti * KBMAX + c);
             }
             if (rec) {
@@ -648,6 +684,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
                                  static_cast<long long>(t) * o.SP + stat + col, col, N);
             }
           }
+          a_done(nch);
         } else {
           // output layer: x_t -> the cost warps' scratch; features of step t+1 -> A in place
           const int nf = t + 1 < H ? o.tc_kb[0] : 0;
@@ -683,10 +720,12 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (c * 32 + j >= ks) v[j] = 0.f;
-              features_store(c, v, tl + dcol + 32 * c, alo + c * 16384);
+              slot_wait(c);
+              features_store(c, v, tl + dcol + 32 * c, alo + (c % ALO) * 16384);
               publish_chunk(m.a_chunk + ti * KBMAX + c);
             }
           }
+          if (nf > 0) a_done(nf);
           mbar_arrive_warp(m.x_full + ti);  // this warp's x_t columns written
         }
         if (lead) mark2(a, t, 201 + 20 * l + 10 * ti);

@@ -162,6 +162,38 @@ __device__ __forceinline__ void mma_quad_elect(uint32_t d, uint32_t a_hi, uint64
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %5, one;\n\t}\n" ::"r"(d),
       "r"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accum));
 }
+// One 32-wide K-block of 3xTF32 (4 k-steps, 12 MMAs) in one elected asm, in the order
+// the pipe runs at full rate: the hi block as strict TS/SS pairs A_hi.B_hi, A_lo.B_hi
+// over the 4 k-steps, then the lo block's 4 TS MMAs A_hi.B_lo (the order of the
+// per-k-step form, so results are identical).  a_hi: TMEM column of k-step 0 (+8 per
+// k-step); a_lo, b_hi, b_lo: descriptors of k-step 0 (+2 = 32 B per k-step inside the
+// 128B swizzle atom).  accum = 0 starts the accumulator.
+__device__ __forceinline__ void mma_kblock_elect(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                                 uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r, a1, a2, a3;\n\t"
+      ".reg .b64 l1, l2, l3, h1, h2, h3, o1, o2, o3;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 l1, %2, 2;\n\tadd.u64 l2, %2, 4;\n\tadd.u64 l3, %2, 6;\n\t"
+      "add.u64 h1, %3, 2;\n\tadd.u64 h2, %3, 4;\n\tadd.u64 h3, %3, 6;\n\t"
+      "add.u64 o1, %4, 2;\n\tadd.u64 o2, %4, 4;\n\tadd.u64 o3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], h1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], l1, h1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], h2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], l2, h2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], h3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], l3, h3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], o1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], o2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], o3, %5, one;\n\t}\n" ::"r"(d),
+      "r"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accum));
+}
 // Whole-warp wait in one asm loop (no per-iteration bookkeeping).
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
   asm volatile(
