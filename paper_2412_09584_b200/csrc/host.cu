@@ -680,6 +680,9 @@ Compiled compile(const bp_objective_desc& d) {
         const size_t min_ring = pl[1] == 256 ? min_ring_wide : min_ring_narrow;
         if (fixed + min_ring <= cap) {
           o.tc2_ring = static_cast<int>((cap - fixed) & ~static_cast<size_t>(1023));
+          if (std::getenv("BP_DEBUG_TC2"))
+            std::fprintf(stderr, "[tc2] tiles %d width %d: fixed %zu B (S=%d), ring %d B\n", o.tc2, o.tc2_rw, fixed,
+                         o.tc_S, o.tc2_ring);
           break;
         }
         o.tc2 = 0;
