@@ -450,21 +450,20 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
             // every weight block of the K-block (hi, lo per N half: consecutive ring entries)
             // first, then all its MMAs back to back: one burst per K-block keeps the tensor
             // pipe fed (the waits and commits between bursts are the issuer's overhead)
-            uint32_t at[4];
-            int sl[4];
             const int nblk = 2 * nh;
-            const long long w0 = tl_clock();
-            for (int b = 0; b < nblk; ++b) {
-              at[b] = ring_place(pos, static_cast<uint32_t>(half_rows(npad, b >> 1)) * 128u, ring_bytes);
-              sl[b] = (it + b) % kSlots;
-              mbar_wait_warp(m.full + sl[b], static_cast<uint32_t>(((it + b) / kSlots) & 1));
-            }
-            wfull += tl_clock() - w0;
             if (l == 1 && i == 0) mark2(a, t, 600 + 2 * kb);
             for (int h = 0; h < nh; ++h) {
+              // this half's hi and lo blocks (the other half's keep landing under this burst)
+              const uint32_t bytes = static_cast<uint32_t>(half_rows(npad, h)) * 128u;
+              const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+              const int b0 = it + 2 * h;
+              const long long w0 = tl_clock();
+              mbar_wait_warp(m.full + b0 % kSlots, static_cast<uint32_t>((b0 / kSlots) & 1));
+              mbar_wait_warp(m.full + (b0 + 1) % kSlots, static_cast<uint32_t>(((b0 + 1) / kSlots) & 1));
+              wfull += tl_clock() - w0;
               const uint32_t idesc = tf32_idesc(half_rows(npad, h));
               const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
-              const uint64_t bh = sw128_desc(wbase + at[2 * h]), bl = sw128_desc(wbase + at[2 * h + 1]);
+              const uint64_t bh = sw128_desc(wbase + at_h), bl = sw128_desc(wbase + at_l);
               if (nq == 4) {
                 mma_kblock_elect(dcol, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
               } else {
