@@ -63,6 +63,7 @@ struct DevObjective {
   // weight ring bytes.  The tc_w images of layers wider than 128 hold per K-block two N halves
   // [kb][half][hi|lo][rows x 32] (half 0 = 128 rows); narrower layers are the v1 layout.
   int tc2, tc2_rw, tc2_ring;  // tc2_rw: TMEM region width (128 or 256 columns)
+  int tc2_pair;               // width 256 as a CTA pair (cta_group::2): every layer 256 wide or <= 128 in 32s
   int sc_list, n_sc;
   int cost_f0, cost_f1;  // float arena range holding every cost-op constant (copied to smem by the tcgen05 kernel)  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
   // constants

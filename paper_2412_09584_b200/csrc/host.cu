@@ -626,6 +626,7 @@ Compiled compile(const bp_objective_desc& d) {
     o.tc2 = 0;
     o.tc2_rw = 0;
     o.tc2_ring = 0;
+    o.tc2_pair = 0;
     if (ok2 && !net) {
       o.tc_kbmax = kbmax;
       o.tc_npadmax = npadmax;
@@ -676,13 +677,27 @@ Compiled compile(const bp_objective_desc& d) {
         if (pl[1] == 128 && !narrow) continue;
         o.tc2 = pl[0];
         o.tc2_rw = pl[1];
+        // CTA pair (rollout_tc2.cu, cta_group::2) at width 256 when each layer's N splits
+        // evenly between the two CTAs (256, or a multiple of 32 up to 128).  Opt-in
+        // (BP_TC2_PAIR=1): correct, but epilogue-bound and slower than one CTA on C3
+        // (168.5 vs 178.5 TFLOP/s).  The ring is planned for its layout.
+        o.tc2_pair = 0;
+        if (pl[1] == 256) {
+          const char* e = std::getenv("BP_TC2_PAIR");
+          bool ok = e != nullptr && std::string(e) == "1";
+          for (int l = 0; l < d.n_layers; ++l) {
+            const int np = o.tc_npad[l];
+            ok = ok && (np == 256 || (np <= 128 && np % 32 == 0));
+          }
+          o.tc2_pair = ok ? 1 : 0;
+        }
         const size_t fixed = bp::rollout_tc2_fixed_smem(o);
         const size_t min_ring = pl[1] == 256 ? min_ring_wide : min_ring_narrow;
         if (fixed + min_ring <= cap) {
           o.tc2_ring = static_cast<int>((cap - fixed) & ~static_cast<size_t>(1023));
           if (std::getenv("BP_DEBUG_TC2"))
-            std::fprintf(stderr, "[tc2] tiles %d width %d: fixed %zu B (S=%d), ring %d B\n", o.tc2, o.tc2_rw, fixed,
-                         o.tc_S, o.tc2_ring);
+            std::fprintf(stderr, "[tc2] tiles %d width %d pair %d: fixed %zu B (S=%d), ring %d B\n", o.tc2, o.tc2_rw,
+                         o.tc2_pair, fixed, o.tc_S, o.tc2_ring);
           break;
         }
         o.tc2 = 0;

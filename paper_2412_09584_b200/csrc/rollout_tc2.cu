@@ -79,18 +79,18 @@ constexpr int kSlots = 8;  // weight blocks in flight at most (mbarrier pairs)
 // __nanosleep backoff (ns) of the long waits: producer / cost warp / epilogue
 constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
 
-#ifndef BP_ALO_WIDE
-#define BP_ALO_WIDE 2
-#endif
-__host__ __device__ constexpr int tc2_alo_slots(int rw) { return rw >= 256 ? BP_ALO_WIDE : rw / 32 < 4 ? rw / 32 : 4; }
+// A_lo K-block slots per tile: two at width 256 (the rest of shared memory goes to the
+// weight ring, which then holds two K-blocks' weights), four for a CTA pair (its weight
+// blocks are half as large; its epilogue, not the ring, is the constraint), else up to 4.
+__host__ __device__ constexpr int tc2_alo_slots(int rw, bool pair) {
+  return rw >= 256 ? (pair ? 4 : 2) : rw / 32 < 4 ? rw / 32 : 4;
+}
 
-template <int NT, int RW_, int EPI_, int CW_>
+template <int NT, int RW_, int EPI_, int CW_, bool PAIR_ = false>  // PAIR_: CTA pair (cluster of 2, cta_group::2, M = 256)
 struct Tc2 {
   static constexpr int RW = RW_;                  // TMEM region width >= widest padded layer
   static constexpr int KBMAX = RW / 32;           // A operand K-blocks of 32 per tile
-  // shared-memory slots of A_lo K-blocks per tile: two at width 256 (the rest of shared
-  // memory goes to the weight ring, which then holds two K-blocks' weights), else up to 4
-  static constexpr int ALO = tc2_alo_slots(RW);
+  static constexpr int ALO = tc2_alo_slots(RW, PAIR_);  // A_lo K-block slots per tile
   static constexpr int EPI = EPI_;                // epilogue warps (warps 0 .. EPI-1)
   static constexpr int WPQ = EPI / (4 * NT);      // epilogue warps per TMEM quadrant per tile
   static constexpr int CW = CW_;                  // cost warps per tile
@@ -113,6 +113,7 @@ struct Tc2Smem {
   int* segl;           // [NT][128] tile-local subdomain of each row (-1 past the last)
   int* pairs;          // [n_sc][2] recorded scratch columns (column, record offset)
   uint64_t* full;      // [kSlots] weight block landed
+  uint64_t* peer_full; // [kSlots] CTA pair, rank 0: the peer's copy of the block landed (relayed)
   uint64_t* d_full;    // [NT][2] accumulator region ready for the epilogue
   uint64_t* a_chunk;   // [NT][KBMAX] A operand K-block written (4 quadrant warps)
   uint64_t* x_full;    // [NT] x_t of every row in the scratch (all epilogue warps of the tile)
@@ -124,7 +125,7 @@ struct Tc2Smem {
 };
 
 __host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* base) {
-  const int NT = o.tc2, RW = o.tc2_rw, KBMAX = RW / 32, ALO = tc2_alo_slots(RW);
+  const int NT = o.tc2, RW = o.tc2_rw, KBMAX = RW / 32, ALO = tc2_alo_slots(RW, o.tc2_pair != 0);
   Tc2Smem m;
   size_t off = 0;
   auto take = [&](size_t n, size_t align) {
@@ -141,9 +142,10 @@ __host__ __device__ inline Tc2Smem carve2(const DevObjective& o, unsigned char* 
   m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops, 16));
   m.segl = reinterpret_cast<int*>(take(sizeof(int) * NT * 128, 16));
   m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc, 16));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (kSlots + NT * (2 + KBMAX + 2 + KBMAX)), 16));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kSlots + NT * (2 + KBMAX + 2 + KBMAX)), 16));
   m.full = bars;
-  m.d_full = m.full + kSlots;
+  m.peer_full = m.full + kSlots;
+  m.d_full = m.peer_full + kSlots;
   m.a_chunk = m.d_full + 2 * NT;
   m.x_full = m.a_chunk + NT * KBMAX;
   m.x_empty = m.x_full + NT;
@@ -304,22 +306,28 @@ __device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_b
 }
 
 // Publish a written K-block: TMEM stores complete, shared stores visible to the
-// async proxy, then one arrival per warp.
-__device__ __forceinline__ void publish_chunk(uint64_t* bar) {
+// async proxy, then one arrival per warp -- on rank 0's barrier for a CTA pair (rank 0
+// issues the MMAs that read both CTAs' operands).
+__device__ __forceinline__ void publish_chunk(uint64_t* bar, bool to_rank0 = false) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   fence_proxy_async();
   fence_before();
-  mbar_arrive_warp(bar);
+  if (to_rank0) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_cta(bar, 0);
+  } else {
+    mbar_arrive_warp(bar);
+  }
 }
 
 // Number of N halves of layer l (<= 128 columns per MMA) and the rows of half h.
 __device__ __forceinline__ int n_halves(int npad) { return npad > 128 ? 2 : 1; }
 __device__ __forceinline__ int half_rows(int npad, int h) { return npad > 128 ? (h == 0 ? 128 : npad - 128) : npad; }
 
-template <int NT, int RW_, int EPI_, int CW_>
-__global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
+template <int NT, int RW_, int EPI_, int CW_, bool PAIR>
+__global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
     rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
-  using C = Tc2<NT, RW_, EPI_, CW_>;
+  using C = Tc2<NT, RW_, EPI_, CW_, PAIR>;
   constexpr int RW = C::RW, KBMAX = C::KBMAX, ALO = C::ALO, WPQ = C::WPQ, CW = C::CW, NR = C::NR;
   constexpr uint32_t kTmemCols = 2 * NT * RW;  // a power of two >= 32
   extern __shared__ unsigned char smraw[];
@@ -329,11 +337,16 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
   const long long cta_row0 = static_cast<long long>(blockIdx.x) * (128 * NT);
   const int ks = o.ks, ka = o.ka, kd = o.kd, d = o.d, S = o.tc_S, L = o.L, H = o.H;
   const long long rps = a.rows_per_sub;
+  // CTA pair: rank 0 issues every MMA for both CTAs' rows (M = 256); both stream their
+  // half of each weight block and run their own epilogue and cost warps
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
 
-  if (a.failed != nullptr) {  // skip CTAs whose subdomains all failed already
-    const long long last = min(a.n_rows, cta_row0 + 128 * NT) - 1;
-    bool all_failed = true;
-    for (long long s = cta_row0 / rps; s <= last / rps; ++s) all_failed = all_failed && a.failed[s] != 0;
+  if (a.failed != nullptr) {  // skip CTAs (pairs) whose subdomains all failed already
+    const long long g0 = PAIR ? cta_row0 - static_cast<long long>(rank) * 128 : cta_row0;
+    const long long g1 = PAIR ? g0 + 256 : cta_row0 + 128 * NT;
+    const long long last = min(a.n_rows, g1) - 1;
+    bool all_failed = last >= g0;
+    for (long long s = g0 / rps; s <= last / rps && all_failed; ++s) all_failed = a.failed[s] != 0;
     if (all_failed) return;
   }
 
@@ -353,11 +366,12 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(m.full + s, 1);
+      mbar_init(m.peer_full + s, 1);
     }
     for (int i = 0; i < NT; ++i) {
       mbar_init(m.d_full + 2 * i, 1);
       mbar_init(m.d_full + 2 * i + 1, 1);
-      for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_chunk + i * KBMAX + c, 4);
+      for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_chunk + i * KBMAX + c, PAIR ? 8 : 4);  // quadrant warps (of both CTAs)
       mbar_init(m.x_full + i, 4 * WPQ);
       mbar_init(m.x_empty + i, CW);
       for (int c = 0; c < KBMAX; ++c) mbar_init(m.a_free + i * KBMAX + c, 1);
@@ -365,12 +379,19 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
   fence_after();
   const uint32_t tmem = *m.tmem_slot;
   const uint32_t ring_bytes = static_cast<uint32_t>(o.tc2_ring);
@@ -393,11 +414,16 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
             const int npad = o.tc_npad[l], nh = n_halves(npad);
             for (int kb = 0; kb < o.tc_kb[l]; ++kb) {  // K-block outer: its A_lo slot is freed after it
               const int bit = i * KBMAX + kb;
-              for (int h = 0; h < nh; ++h) {
-                const int nr = half_rows(npad, h);
-                const float* src = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32 + (h ? 2 * 128 * 32 : 0);
+              for (int h = 0; h < (PAIR ? 1 : nh); ++h) {
+                // one N half per block; a CTA of a pair streams its half of the N rows
+                // (256 wide: image half `rank`; <= 128 wide: rows [rank n/2, (rank+1) n/2))
+                const int nr = PAIR ? (npad > 128 ? 128 : npad / 2) : half_rows(npad, h);
+                const float* kbase = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32;
                 const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
                 for (int part = 0; part < 2; ++part, ++it) {
+                  const float* src = !PAIR ? kbase + (h ? 2 * 128 * 32 : 0) + part * nr * 32
+                                     : npad > 128 ? kbase + (rank ? 2 * 128 * 32 : 0) + part * nr * 32
+                                                  : kbase + part * npad * 32 + rank * nr * 32;
                   const uint32_t at = ring_place(pos, bytes, ring_bytes);
                   while (head < it) {
                     const int hs = head % kSlots;
@@ -410,13 +436,78 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
                   hi_b[s] = at + bytes;
                   fr_b[s] = (static_cast<uint32_t>(bit) << 1) | ((ppar >> bit) & 1u);
                   mbar_expect_tx(m.full + s, bytes);
-                  bulk_g2s(m.w + at, src + part * nr * 32, bytes, m.full + s);
+                  bulk_g2s(m.w + at, src, bytes, m.full + s);
                 }
               }
             }
             ppar ^= ((1u << o.tc_kb[l]) - 1u) << (i * KBMAX);  // one completion per K-block of this operand
           }
     }
+  } else if (warp == C::kMmaWarp && PAIR && rank == 1) {
+    // ------------------------------------------------ CTA pair, rank 1: relay "my half of
+    // the block landed" to rank 0, which issues the MMAs over both halves
+    int it = 0;
+    for (int t = 0; t < H; ++t)
+      for (int l = 0; l < L; ++l)
+        for (int kb = 0; kb < o.tc_kb[l]; ++kb)
+          for (int part = 0; part < 2; ++part, ++it) {
+            mbar_wait(m.full + it % kSlots, static_cast<uint32_t>((it / kSlots) & 1));
+            if (lane == 0) mbar_arrive_cta(m.peer_full + it % kSlots, 0);
+            __syncwarp();
+          }
+  } else if (warp == C::kMmaWarp && PAIR) {
+    // ------------------------------------------------ CTA pair, rank 0: MMA issuer for both
+    // CTAs (M = 256: each CTA's 128 rows of A from its TMEM / shared memory, B's N rows
+    // half in each CTA); commits arrive in both CTAs
+    int it = 0, li = 0;
+    uint32_t pos = 0;
+    uint32_t a_par = 0;
+    const uint32_t wbase = smem_u32(m.w);
+    const uint32_t abase = smem_u32(m.alo);
+    for (int t = 0; t < H; ++t)
+      for (int l = 0; l < L; ++l, ++li) {
+        const int npad = o.tc_npad[l], ksteps = o.tc_ksteps[l];
+        const uint32_t dreg = tmem + static_cast<uint32_t>((li & 1) * RW);
+        const uint32_t areg = tmem + static_cast<uint32_t>(((li + 1) & 1) * RW);
+        const uint32_t idesc = tf32_idesc_mn(256, npad);
+        const uint32_t bytes = static_cast<uint32_t>(npad > 128 ? 128 : npad / 2) * 128u;
+        long long wfull = 0, awt = 0;
+        for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
+          if (kb == 0) mark2(a, t, 100 + 20 * l);
+          const long long aw0 = tl_clock();
+          mbar_wait_cluster(m.a_chunk + kb, (a_par >> kb) & 1u);  // both CTAs wrote this K-block of A
+          awt += tl_clock() - aw0;
+          if (kb == 0) mark2(a, t, 101 + 20 * l);
+          a_par ^= 1u << kb;
+          const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(kb % ALO) * 16384u);
+          const int nq = min(4, ksteps - kb * 4);
+          const uint32_t a0 = areg + 32 * kb;
+          const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+          const long long w0 = tl_clock();
+          for (int b = 0; b < 2; ++b) {
+            mbar_wait_warp(m.full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
+            mbar_wait_cluster(m.peer_full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
+          }
+          wfull += tl_clock() - w0;
+          fence_after();
+          if (l == 1) mark2(a, t, 600 + 2 * kb);
+          const uint64_t bh = sw128_desc(wbase + at_h), bl = sw128_desc(wbase + at_l);
+          if (nq == 4) {
+            mma_kblock_pair_elect(dreg, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
+          } else {
+            for (int q = 0; q < nq; ++q)
+              mma_pair2_elect(dreg, a0 + 8 * q, alo_d + 2 * q, bh + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
+            for (int q = 0; q < nq; ++q) mma_ts2(dreg, a0 + 8 * q, bl + 2 * q, idesc, 1u);
+          }
+          if (l == 1) mark2(a, t, 601 + 2 * kb);
+          it += 2;
+          commit_pair_elect(m.a_free + kb);  // ring bytes and A_lo slot free in both CTAs
+        }
+        commit_pair_elect(m.d_full + (li & 1));  // accumulator complete in both CTAs
+        mark2(a, t, 102 + 20 * l);
+        put2(a, t, 300 + 20 * l, wfull + (1ll << 40));
+        put2(a, t, 310 + 20 * l, awt + (1ll << 40));
+      }
   } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------ MMA issuer: the whole warp runs the
     // uniform loop and waits; elect.sync inside the asm picks the issuing lane
@@ -628,7 +719,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
         v[j] = k < ks ? o.f[o.x0 + min(k, ks - 1)] : 0.f;
       }
       features_store(c, v, tl + RW + 32 * c, alo + (c % ALO) * 16384);  // no earlier use of the slots
-      publish_chunk(m.a_chunk + ti * KBMAX + c);
+      publish_chunk(m.a_chunk + ti * KBMAX + c, PAIR);
     }
     a_done(o.tc_kb[0]);
     int li = 0;
@@ -675,7 +766,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
               for (int j = 0; j < 32; ++j) w[j] = relu ? fmaxf(v[j], 0.f) : v[j];
               slot_wait(c);
               store_operand(tl + dcol + 32 * c, alo + (c % ALO) * 16384, row, w);
-              publish_chunk(m.a_chunk + ti * KBMAX + c);
+              publish_chunk(m.a_chunk + ti * KBMAX + c, PAIR);
             }
             if (rec) {
               const int col = c * 32 + lane;
@@ -721,7 +812,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
                 if (c * 32 + j >= ks) v[j] = 0.f;
               slot_wait(c);
               features_store(c, v, tl + dcol + 32 * c, alo + (c % ALO) * 16384);
-              publish_chunk(m.a_chunk + ti * KBMAX + c);
+              publish_chunk(m.a_chunk + ti * KBMAX + c, PAIR);
             }
           }
           if (nf > 0) a_done(nf);
@@ -734,9 +825,13 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_>::kThreads, 1)
 
   fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM
   if (warp == 0) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -757,16 +852,35 @@ cudaError_t launch_rollout_tc2(const DevObjective& o, const RolloutArgs& a, cuda
     kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(o, a);
     return cudaSuccess;
   };
+  auto go_pair = [&](auto kern, int threads) {  // clusters of 2 CTAs (an even grid)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>((grid + 1) & ~1LL));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, o, a);
+  };
   cudaError_t e;
-  // (tiles, region width, epilogue warps, cost warps per tile): two ping-pong tiles; one
-  // 128-wide tile with a heavy cost program (C4: 8 epilogue warps, 4 cost warps); one
-  // 256-wide tile
+  // (tiles, region width, epilogue warps, cost warps per tile[, CTA pair]): two ping-pong
+  // tiles; one 128-wide tile with a heavy cost program (C4: 8 epilogue warps, 4 cost
+  // warps); one 256-wide tile, as a CTA pair when every layer splits evenly (C3)
   if (nt == 2 && o.tc2_rw == 128)
-    e = go(rollout_tc2_kernel<2, 128, 16, 1>, Tc2<2, 128, 16, 1>::kThreads);
+    e = go(rollout_tc2_kernel<2, 128, 16, 1, false>, Tc2<2, 128, 16, 1>::kThreads);
   else if (nt == 1 && o.tc2_rw == 128)
-    e = go(rollout_tc2_kernel<1, 128, 8, 4>, Tc2<1, 128, 8, 4>::kThreads);
+    e = go(rollout_tc2_kernel<1, 128, 8, 4, false>, Tc2<1, 128, 8, 4>::kThreads);
+  else if (nt == 1 && o.tc2_rw == 256 && o.tc2_pair)
+    e = go_pair(rollout_tc2_kernel<1, 256, 16, 1, true>, Tc2<1, 256, 16, 1, true>::kThreads);
   else if (nt == 1 && o.tc2_rw == 256)
-    e = go(rollout_tc2_kernel<1, 256, 16, 1>, Tc2<1, 256, 16, 1>::kThreads);
+    e = go(rollout_tc2_kernel<1, 256, 16, 1, false>, Tc2<1, 256, 16, 1>::kThreads);
   else
     return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;

@@ -194,6 +194,101 @@ __device__ __forceinline__ void mma_kblock_elect(uint32_t d, uint32_t a_hi, uint
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], o3, %5, one;\n\t}\n" ::"r"(d),
       "r"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accum));
 }
+// ---- CTA pair (cta_group::2; tools/cta2_probe.cu checks the operand split): M = 256
+// rows across the two CTAs of a cluster (128 in each CTA's TMEM / shared memory), B's N
+// rows split between the CTAs' shared memory at the same offset (N/2 each), D = each
+// CTA's 128 rows x N in its own TMEM.  Only rank 0 issues; commits multicast to both.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive (release at cluster scope) on the mbarrier at the same offset in CTA `rank`.
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+// Whole-warp wait with cluster-scope acquire (arrivals from the peer CTA), trap on a
+// lost arrival.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  for (long long spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase), "r"(0x989680u)
+        : "memory");
+    if (ok) return;
+    if (spin > (1ll << 24)) asm volatile("trap;");
+  }
+}
+__device__ __forceinline__ void commit_pair_elect(uint64_t* bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+// mma_kblock_elect for the CTA pair (idesc with M = 256).
+__device__ __forceinline__ void mma_kblock_pair_elect(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                                      uint64_t b_lo, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r, a1, a2, a3;\n\t"
+      ".reg .b64 l1, l2, l3, h1, h2, h3, o1, o2, o3;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 l1, %2, 2;\n\tadd.u64 l2, %2, 4;\n\tadd.u64 l3, %2, 6;\n\t"
+      "add.u64 h1, %3, 2;\n\tadd.u64 h2, %3, 4;\n\tadd.u64 h3, %3, 6;\n\t"
+      "add.u64 o1, %4, 2;\n\tadd.u64 o2, %4, 4;\n\tadd.u64 o3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %2, %3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a1], h1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], l1, h1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a2], h2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], l2, h2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a3], h3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], l3, h3, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %4, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a1], o1, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a2], o2, %5, one;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [a3], o3, %5, one;\n\t}\n" ::"r"(d),
+      "r"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accum));
+}
+// Partial K-blocks of the pair: A_hi.B_hi (TS) + A_lo.B_hi (SS) pairs, then A_hi.B_lo (TS).
+__device__ __forceinline__ void mma_pair2_elect(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 one, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %3, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %2, %3, %4, one;\n\t}\n" ::"r"(d),
+      "r"(a_hi), "l"(a_lo), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_ts2(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+// Instruction descriptor: D f32, A/B tf32, K-major, M, N.
+__device__ __forceinline__ uint32_t tf32_idesc_mn(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
 // Whole-warp wait in one asm loop (no per-iteration bookkeeping).
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
   asm volatile(

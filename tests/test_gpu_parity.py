@@ -127,6 +127,28 @@ def test_tcgen05_v2_matches_oracle(device, name, tiles, shape):
     assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
 
 
+@pytest.mark.parametrize("shape", [(3, 37), (1, 300), (3, 130)])
+def test_tcgen05_v2_cta_pair_matches_one_cta(device, shape, monkeypatch):
+    """The CTA-pair form of the 256-wide v2 kernel (BP_TC2_PAIR=1: clusters of two CTAs,
+    cta_group::2 MMAs with M = 256, B's rows split between the CTAs) computes the same
+    rollouts as the one-CTA form -- bit for bit (the same MMA terms in the same order per
+    row) -- and matches the oracle; odd tile counts leave a CTA of the last pair empty."""
+    spec = small_spec("c3")
+    lo, hi = spec.box()
+    n_sub, rows = shape
+    acts = np.random.default_rng(5).uniform(lo, hi, size=(n_sub, rows, spec.d)).astype(np.float32)
+    one = device.load(spec).rollout(acts, want_states=True)
+    monkeypatch.setenv("BP_TC2_PAIR", "1")
+    dev = device.load(spec)
+    assert dev.rollout_kernel() == "tc2"
+    pair = dev.rollout(acts, want_states=True)
+    for x, y in zip(one, pair):
+        assert np.array_equal(x, y)
+    ob = orc.Objective(spec)
+    ref = ob.evaluate(acts[0].astype(np.float64))
+    assert rel_err(pair[0][0], ref) < RTOL_TC
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "ref-obstacles"])
 def test_tcgen05_v1_still_matches_oracle(device, name):
     """The v1 kernel (rollout_tc.cu) stays selectable (BP_ROLLOUT=tc1) and parity-green."""
