@@ -43,7 +43,11 @@
 //             (x_t, u_t, p_t, cost-op values).
 //   last      producer: cp.async.bulk of the weight blocks into the byte ring.
 // Instances: <2,128,16,1> two ping-pong tiles; <1,128,8,4> one tile whose cost program
-// is heavy (C4: 4 cost warps, one row per thread); <1,256,16,1> one 256-wide tile (C3).
+// is heavy (C4: 4 cost warps, one row per thread); <1,256,16,1> one 256-wide tile (C3);
+// <1,256,16,1,PAIR> the same tile as a CTA pair (opt-in, BP_TC2_PAIR=1): clusters of two
+// CTAs, rank 0 issues cta_group::2 MMAs with M = 256 over both CTAs' rows, each CTA
+// streams half of every weight block's N rows, commits multicast to both, the peer's
+// epilogue arrives on rank 0's A barriers and its MMA warp relays its weight arrivals.
 #include <cuda_runtime.h>
 
 #include <cstdint>
