@@ -1236,7 +1236,12 @@ std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double
   std::vector<int> chosen(order.begin(), order.begin() + n1);
   std::vector<int> rem(order.begin() + n1, order.end());
   const double temp = std::max(temperature, 1e-12);
+  // The weights depend on a record's lf and on (lo, hi) over the remaining records only,
+  // so they are recomputed (exp per record) only when a pick moved lo or hi; the sum is
+  // re-accumulated in pool order every pick, exactly as the reference does.
   std::vector<double> w;
+  double w_lo = std::numeric_limits<double>::quiet_NaN(), w_hi = w_lo;
+  bool w_deg = false;
   for (int need = n - n1; need > 0; --need) {
     double lo = std::numeric_limits<double>::infinity(), hi = -lo;
     for (int idx : rem) {
@@ -1247,17 +1252,22 @@ std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double
       }
     }
     const bool degenerate = !(hi > lo);
-    w.assign(rem.size(), 0.0);
-    double sum = 0.0;
-    for (size_t i = 0; i < rem.size(); ++i) {
-      double scaled = 0.5;
-      if (!degenerate) {
-        const double lf = recs[rem[i]].lf;
-        scaled = std::isfinite(lf) ? (lf - lo) / (hi - lo) : (lf < 0.0 ? 0.0 : 1.0);
+    if (w.empty() || degenerate != w_deg || (!degenerate && (lo != w_lo || hi != w_hi))) {  // w, rem kept in step
+      w.assign(rem.size(), 0.0);
+      for (size_t i = 0; i < rem.size(); ++i) {
+        double scaled = 0.5;
+        if (!degenerate) {
+          const double lf = recs[rem[i]].lf;
+          scaled = std::isfinite(lf) ? (lf - lo) / (hi - lo) : (lf < 0.0 ? 0.0 : 1.0);
+        }
+        w[i] = degenerate ? 1.0 : std::exp(-scaled / temp);
       }
-      w[i] = degenerate ? 1.0 : std::exp(-scaled / temp);
-      sum += w[i];
+      w_lo = lo;
+      w_hi = hi;
+      w_deg = degenerate;
     }
+    double sum = 0.0;
+    for (size_t i = 0; i < rem.size(); ++i) sum += w[i];
     const double u = rng.uniform() * sum;
     double acc = 0.0;
     size_t sel = rem.size() - 1;
@@ -1270,6 +1280,7 @@ std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double
     }
     chosen.push_back(rem[sel]);
     rem.erase(rem.begin() + static_cast<std::ptrdiff_t>(sel));
+    w.erase(w.begin() + static_cast<std::ptrdiff_t>(sel));  // the other records' weights stand unless lo / hi move
   }
   return chosen;
 }
@@ -1412,6 +1423,20 @@ struct Planner {
 
   int world() const { return c->world > 1 && c->exchange != nullptr ? c->world : 1; }
   int rank() const { return world() > 1 ? c->rank : 0; }
+  // BP_STEP_PROFILE: host wall time per phase of step(), printed per iteration (dev aid)
+  std::chrono::steady_clock::time_point ph_t;
+  std::string ph_line;
+  void phase(const char* name) {
+    static const bool on = std::getenv("BP_STEP_PROFILE") != nullptr;
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    if (name != nullptr) {
+      char buf[64];
+      std::snprintf(buf, sizeof(buf), " %s=%.2f", name, std::chrono::duration<double, std::milli>(now - ph_t).count());
+      ph_line += buf;
+    }
+    ph_t = now;
+  }
 
   double elapsed_ms() const {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1471,7 +1496,9 @@ struct Planner {
     bp_search_config scfg = cfg.search;
     scfg.seed = seed;
     bp::SearchArgs a = search_setup(c, n, scfg, keys.data(), true);
+    phase("setup");
     search_run(c, a, scfg);
+    phase("search");
     const size_t nb = static_cast<size_t>(std::max(n, c->reserve_boxes));  // no reallocation while ramping up
     int* ds = d_slots.get(nb);
     ck(memcpy_counted(ds, slots.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
@@ -1582,6 +1609,8 @@ struct Planner {
     ++iter;
     const int W = world(), R = rank();
     cudaStream_t st = c->stream;
+    ph_line.clear();
+    phase(nullptr);
     std::vector<bp_pool_meta> meta(pool.size());
     for (size_t i = 0; i < pool.size(); ++i) meta[i] = {pool[i].lf, pool[i].uf, pool[i].id, pool[i].log_vol};
     const std::vector<int> chosen = pick_indices(meta.data(), static_cast<int>(pool.size()), cfg.batch, cfg.eta, cfg.temperature, pick_rng);
@@ -1599,6 +1628,7 @@ struct Planner {
     }
     double selected_vol = 0.0;
     for (const auto& r : picked) selected_vol += std::exp(r.log_vol);
+    phase("pick");
     std::vector<Head> to_split;
     for (const Head& h : picked) {
       if (h.max_width <= cfg.min_width) {  // retired: too narrow to split
@@ -1672,15 +1702,20 @@ struct Planner {
       for (size_t q = 0; q < tasks.size(); ++q)
         if (ha[q] < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
     }
+    phase("split");
     for (const Head& p : to_split)  // the parents' payload has been read by the split
       if (p.owner == R) slab.release(p.slot);
     if (W > 1 && n_all > 0) ship_children(to_split, n_pack, li_of, slots);
     if (n_all > 0) {
       Out o = search_bound_merge(keys, slots, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1));
+      phase("merge+bound");
       gather_children(to_split, base_id, keys, slots, o);
+      phase("gather");
     }
     pruned_cum += prune();
     push_trace(iter, selected_vol);
+    phase("prune");
+    if (!ph_line.empty()) std::fprintf(stderr, "[step %d]%s\n", iter, ph_line.c_str());
     return true;
   }
 

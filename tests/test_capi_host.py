@@ -161,3 +161,16 @@ def test_objective_program_matches_oracle_graph_order():
     assert sn["ops"] == [11, 12, 13, 14, 15, 16]
     # kLastRelu: the final step's last ReLU (22) plus every hinge (objective.cpp:45-63)
     assert ob.stop_set() == [13, 15, 16, 22, 27, 29, 30]
+
+
+def test_pick_out_bit_exact_on_large_pools():
+    """Pools of a throughput run's size (the weights are reused between softmax picks
+    unless a pick moves the lf range; picks of the extreme records force recomputes)."""
+    rng = np.random.default_rng(12)
+    for trial, n_pool in enumerate((700, 2500)):
+        lf = rng.normal(size=n_pool) * 5
+        lf[rng.random(n_pool) < 0.05] = -math.inf
+        uf = lf + rng.exponential(size=n_pool)
+        meta = [(float(lf[i]), float(uf[i]), i, -0.1 * i) for i in range(n_pool)]
+        for n, eta, T in ((256, 0.75, 0.05), (120, 0.0, 5.0), (64, 0.0, 1e-4)):
+            assert product_pick(meta, n, eta, T, 7 + trial) == orc.pick_out(meta, n, eta, T, orc.Rng(7 + trial))
