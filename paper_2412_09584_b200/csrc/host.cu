@@ -308,6 +308,11 @@ Compiled compile_synthetic(int dim) {
   return c;
 }
 
+float bit_float(int32_t x) {
+  float f;
+  std::memcpy(&f, &x, 4);
+  return f;
+}
 int push_f(std::vector<float>& a, const double* p, size_t n) {
   while (a.size() % 4) a.push_back(0.f);
   const int off = static_cast<int>(a.size());
@@ -447,6 +452,33 @@ Compiled compile(const bp_objective_desc& d) {
         p.b = push_f(c.fa, s.b, static_cast<size_t>(dim));
         p.wd = push_d(c.da, s.W, static_cast<size_t>(dim) * in);
         p.bd = push_d(c.da, s.b, static_cast<size_t>(dim));
+        {
+          // A weight matrix at most a quarter full (C4's [I; -I]) also gets a CSR copy for the
+          // rollouts' forward pass: the same fma chain over the nonzeros in column order (the
+          // dense chain adds exact zeros; only the sign of an exactly-zero sum can differ)
+          size_t nnz = 0;
+          for (size_t k = 0; k < static_cast<size_t>(dim) * in; ++k) nnz += static_cast<float>(s.W[k]) != 0.f ? 1 : 0;
+          if (static_cast<size_t>(dim) * in >= 64 && 4 * nnz <= static_cast<size_t>(dim) * in) {
+            std::vector<int32_t> rp(static_cast<size_t>(dim) + 1, 0), ci;
+            std::vector<float> val;
+            for (int r = 0; r < dim; ++r) {
+              for (int j = 0; j < in; ++j) {
+                const float w = static_cast<float>(s.W[static_cast<size_t>(r) * in + j]);
+                if (w != 0.f) {
+                  ci.push_back(j);
+                  val.push_back(w);
+                }
+              }
+              rp[static_cast<size_t>(r) + 1] = static_cast<int32_t>(ci.size());
+            }
+            while (c.fa.size() % 4) c.fa.push_back(0.f);
+            p.tgt = static_cast<int>(c.fa.size());  // [rowptr dim+1][cols nnz] as int bits, then [values nnz]
+            for (int32_t x : rp) c.fa.push_back(bit_float(x));
+            for (int32_t x : ci) c.fa.push_back(bit_float(x));
+            for (float v : val) c.fa.push_back(v);
+            p.ctr = 1;
+          }
+        }
         break;
       case BP_OP_RELU:
         dim = in;

@@ -134,6 +134,27 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
       case 0: {  // LINEAR
         const float* W = cf + op.w;
         const float* b = cf + op.b;
+        if (op.ctr) {  // CSR of a sparse weight matrix (host compile): the fma chain over the nonzeros
+          const int* rp = reinterpret_cast<const int*>(cf + op.tgt);
+          const int* ci = rp + dim + 1;
+          const float* val = reinterpret_cast<const float*>(ci + rp[dim]);
+          for (int r = 0; r < dim; ++r) {
+            float s[NR];
+#pragma unroll
+            for (int q = 0; q < NR; ++q) s[q] = 0.f;
+            for (int k = rp[r]; k < rp[r + 1]; ++k) {
+              const float w = val[k];
+              const int j = ci[k];
+#pragma unroll
+              for (int q = 0; q < NR; ++q) s[q] = fmaf(w, row[q][c0 + j], s[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < NR; ++q) row[q][oc + r] = s[q] + b[r];
+          }
+#pragma unroll
+          for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
+          break;
+        }
         for (int r = 0; r < dim; ++r) {
           float s[NR];
 #pragma unroll
