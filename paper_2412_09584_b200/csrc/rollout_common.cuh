@@ -138,10 +138,12 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
           const int* rp = reinterpret_cast<const int*>(cf + op.tgt);
           const int* ci = rp + dim + 1;
           const float* val = reinterpret_cast<const float*>(ci + rp[dim]);
+#pragma unroll 4
           for (int r = 0; r < dim; ++r) {
             float s[NR];
 #pragma unroll
             for (int q = 0; q < NR; ++q) s[q] = 0.f;
+#pragma unroll 4
             for (int k = rp[r]; k < rp[r + 1]; ++k) {
               const float w = val[k];
               const int j = ci[k];
@@ -155,10 +157,12 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
           for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
           break;
         }
+#pragma unroll 4
         for (int r = 0; r < dim; ++r) {
           float s[NR];
 #pragma unroll
           for (int q = 0; q < NR; ++q) s[q] = 0.f;
+#pragma unroll 4
           for (int j = 0; j < in; ++j) {
             const float w = W[r * in + j];
 #pragma unroll
@@ -172,6 +176,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         break;
       }
       case 1:  // RELU
+#pragma unroll 4
         for (int j = 0; j < dim; ++j)
 #pragma unroll
           for (int q = 0; q < NR; ++q) row[q][oc + j] = fmaxf(row[q][c0 + j], 0.f);
@@ -179,6 +184,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
         break;
       case 2:  // SUM
+#pragma unroll 4
         for (int j = 0; j < dim; ++j)
 #pragma unroll
           for (int q = 0; q < NR; ++q) row[q][oc + j] = c1 >= 0 ? row[q][c0 + j] + row[q][c1 + j] : row[q][c0 + j];
@@ -187,6 +193,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         break;
       case 3: {  // SCALAR_AFFINE
         const float sc = op.scale, of = op.offset;
+#pragma unroll 4
         for (int j = 0; j < dim; ++j)
 #pragma unroll
           for (int q = 0; q < NR; ++q) row[q][oc + j] = sc * row[q][c0 + j] + of;
@@ -200,6 +207,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         float acc[NR];
 #pragma unroll
         for (int q = 0; q < NR; ++q) acc[q] = 0.f;
+#pragma unroll 4
         for (int j = 0; j < in; ++j) {
           const float g = tg[j], w = wt[j];
 #pragma unroll
@@ -217,6 +225,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         float acc[NR];
 #pragma unroll
         for (int q = 0; q < NR; ++q) acc[q] = 0.f;
+#pragma unroll 4
         for (int j = 0; j < in; ++j) {
           const float g = c[j];
 #pragma unroll
@@ -235,6 +244,7 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
       }
       default: {  // SLICE
         const int b0 = c0 + op.begin;
+#pragma unroll 4
         for (int j = 0; j < dim; ++j)
 #pragma unroll
           for (int q = 0; q < NR; ++q) row[q][oc + j] = row[q][b0 + j];
