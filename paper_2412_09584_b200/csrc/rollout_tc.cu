@@ -51,9 +51,14 @@ namespace bp {
 
 namespace {
 
-constexpr int kTcThreads = 448;  // 8 epilogue warps + 4 aux warps + producer warp + MMA warp
-constexpr int kProducerWarp = 9, kMmaWarp = 13;  // aux warps: 8, 10, 11, 12
-__device__ __forceinline__ int aux_index(int warp) { return warp == 8 ? 0 : warp - 9; }  // warps 8, 10, 11, 12
+#ifndef BP_V1_EPI
+#define BP_V1_EPI 8
+#endif
+constexpr int kEpiWarps = BP_V1_EPI;              // epilogue warps: 4 TMEM quadrants x kEpiWarps/4 chunk groups
+constexpr int kChunkGroups = kEpiWarps / 4;
+constexpr int kTcThreads = 32 * (kEpiWarps + 6);  // + 4 aux warps + producer warp + MMA warp
+constexpr int kProducerWarp = kEpiWarps + 1, kMmaWarp = kEpiWarps + 5;  // aux warps: E, E+2, E+3, E+4
+__device__ __forceinline__ int aux_index(int warp) { return warp == kEpiWarps ? 0 : warp - kEpiWarps - 1; }
 constexpr int kStgStride = 36;  // staging row stride (floats): 16B rows, conflict-free column reads
 constexpr int kStages = 3;   // weight ring capacity, in K-blocks of the widest layer
 constexpr int kSlots = 8;    // K-blocks in flight in the ring at most (mbarrier pairs)
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       mbar_init(m.stg_empty + c, 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(m.x_full + b, 8);
+      mbar_init(m.x_full + b, kEpiWarps);
       mbar_init(m.x_empty + b, 2);  // the two cost warps
       mbar_init(m.sc_full + b, 2);
       mbar_init(m.sc_empty + b, 2);  // the two extrema warps
@@ -482,7 +487,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         mma_commit_elect(m.d_full + (layer_it & 1));  // accumulator complete
         mark(a, t, 101 + 10 * l);
       }
-  } else if (warp >= 8) {
+  } else if (warp >= kEpiWarps) {
     const int ai = aux_index(warp);
     const long long b1 = (seg0 + 1) * a.rows_per_sub - row0;
     const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     }
   } else {
     // ------------------------------------------------ epilogue warps: layer to layer
-    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column-chunk parity
+    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column-chunk group
     const int row = 32 * g + lane;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(32 * g) << 16);
     const bool row_ok = row < nvalid;
@@ -616,7 +621,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
     // early features: the input layer is one K-block and the output layer's x_t one chunk
     // (so the chunk-0 warps of the output epilogue hold all of x_t)
     const bool early = o.tc_kb[0] == 1 && o.tc_npad[L - 1] <= 32 && ks + ka <= 32;
-    asm volatile("bar.sync 2, 256;" ::: "memory");
+    asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
     int layer_it = 0;
     uint32_t stg_used = 0, stg_par = 0;  // bit cb: chunk staged before / parity of its last use
     for (int t = 0; t < H; ++t) {
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       if (warp == 0) mark(a, t, 407);
       // features of layer 0 -> A: concat(x_{t-1} [- tile(p_{t-1})], u_t), zero padded (from
       // step 1 on, the early path wrote them in the previous step's output epilogue)
-      for (int kb = h; kb < o.tc_kb[0] && (!early || t == 0); kb += 2) {
+      for (int kb = h; kb < o.tc_kb[0] && (!early || t == 0); kb += kChunkGroups) {
         // every load is issued unconditionally from a clamped address (no predicated
         // loads, no branches), so they pipeline; the selects come after
         float v[32];
@@ -665,7 +670,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
       }
       if (warp == 0) mark(a, t, 403);
       // p_t and u_{t+1} for the next step's features
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // both groups read prow above
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");  // both groups read prow above
       if (h == 0)
         for (int j = 0; j < ka; ++j) prow[j] += ucur[j];
       for (int l = 0; l < L; ++l, ++layer_it) {
@@ -683,7 +688,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         const bool rec = relu && stat >= 0 && a.stat_min != nullptr && hidden;
         const float* bias = m.bias + l * bias_stride(o);
         const int nchunk = (npad + 31) / 32;
-        for (int cb = h; cb < nchunk; cb += 2) {
+        for (int cb = h; cb < nchunk; cb += kChunkGroups) {
           float v[32];
           float4 bb[8];  // bias loads issued first: their latency overlaps the TMEM load
           const float4* b4 = reinterpret_cast<const float4*>(bias + cb * 32);
@@ -774,7 +779,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
         if (!hidden) {  // x_t of every row written: hand it to the aux warps and to the next features
           fence_before();
           mbar_arrive_warp(m.x_full + (t & 1));
-          asm volatile("bar.sync 2, 256;" ::: "memory");
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
         }
       }
     }
