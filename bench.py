@@ -122,8 +122,11 @@ def run_reference(args, wl):
         "impl": "reference", "metric": "subdomains_bounded_per_s", "value": rate, "unit": "subdomains/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.name, "D_per_step": n, "M": wl.samples_per_iter, "H": wl.spec.horizon,
-                   "cem_iterations": 10},
+        # the same workload as this repo's arm (its config keys); each timed step is a bounded sample of it
+        "config": {"workload": f"{wl.name} (BASELINE.json configs[1])", "widths": wl.spec.widths, "H": wl.spec.horizon,
+                   "M": wl.samples_per_iter, "D_per_step": n, "cem_iterations": wl.planner_config()["search"]["iterations"],
+                   "batch": wl.planner_config()["batch"], "parallelism": "host threads",
+                   "sample": f"{n} pre-split boxes per step (the GPU arm bounds {2 * wl.planner_config()['batch']} per step)"},
         "cpu_baseline": {"value": rate, "unit": "subdomains/s", "cores": cores, "kind": "port",
                          "sample": f"{n} pre-split C2 boxes per step: batch_search (CEM, M=1024, 10 iters) + "
                                    "early-stop-empirical CROWN, FP64 oracle restatement (reference does not build "
