@@ -27,17 +27,18 @@ namespace bp {
 
 namespace {
 
-constexpr int kMaxW = 1024;
+constexpr int kMaxW = 1024;  // widest supported layer / scratch row (the kernel is instantiated at 128 .. 1024)
 
+template <int MW>
 struct Smem {
-  double a_lo[kMaxW], a_hi[kMaxW];   // interval pass: current layer in/out
-  double b_lo[kMaxW], b_hi[kMaxW];
-  double x_lo[kMaxW], x_hi[kMaxW];   // interval x_t (ks)
+  double a_lo[MW], a_hi[MW];   // interval pass: current layer in/out
+  double b_lo[MW], b_hi[MW];
+  double x_lo[MW], x_hi[MW];   // interval x_t (ks)
   double p_lo[16], p_hi[16];
-  double o_lo[kMaxW], o_hi[kMaxW];   // interval op values (by op col)
-  double lam[kMaxW], lam2[kMaxW];    // backward coefficients
-  double lx[kMaxW];                  // coefficient on x_t
-  double lops[kMaxW];                // coefficients on op values (by op col)
+  double o_lo[MW], o_hi[MW];   // interval op values (by op col)
+  double lam[MW], lam2[MW];    // backward coefficients
+  double lx[MW];                  // coefficient on x_t
+  double lops[MW];                // coefficients on op values (by op col)
   double lu[16], lp[16], lpt[16];
   double red[kThreads / 32];
 };
@@ -84,14 +85,16 @@ __device__ void interval_linear(const double* W, const double* b, int N, int K, 
   }
 }
 
-__device__ __forceinline__ const double* ival_lo(const DevObjective& o, Smem& sm, int id, int t, const BoundArgs& a,
+template <int MW>
+__device__ __forceinline__ const double* ival_lo(const DevObjective& o, Smem<MW>& sm, int id, int t, const BoundArgs& a,
                                                  long long boxoff) {
   if (id == 0) return sm.x_lo;
   if (id == 1) return a.lo + boxoff + t * o.ka;
   if (id == 2) return sm.p_lo;
   return sm.o_lo + o.ops[id - 3].col;
 }
-__device__ __forceinline__ const double* ival_hi(const DevObjective& o, Smem& sm, int id, int t, const BoundArgs& a,
+template <int MW>
+__device__ __forceinline__ const double* ival_hi(const DevObjective& o, Smem<MW>& sm, int id, int t, const BoundArgs& a,
                                                  long long boxoff) {
   if (id == 0) return sm.x_hi;
   if (id == 1) return a.hi + boxoff + t * o.ka;
@@ -100,7 +103,8 @@ __device__ __forceinline__ const double* ival_hi(const DevObjective& o, Smem& sm
 }
 
 // K6: interval_forward over the unrolled graph; records every watched slot.
-__device__ void interval_pass(const DevObjective& o, const BoundArgs& a, Smem& sm, int s) {
+template <int MW>
+__device__ void interval_pass(const DevObjective& o, const BoundArgs& a, Smem<MW>& sm, int s) {
   const int tid = threadIdx.x;
   const long long boxoff = static_cast<long long>(s) * o.d;
   const long long base = static_cast<long long>(s) * o.H * o.SP;
@@ -247,7 +251,8 @@ __device__ void interval_pass(const DevObjective& o, const BoundArgs& a, Smem& s
   }
 }
 
-__device__ __forceinline__ double* lam_of(const DevObjective& o, Smem& sm, int id) {
+template <int MW>
+__device__ __forceinline__ double* lam_of(const DevObjective& o, Smem<MW>& sm, int id) {
   if (id == 0) return sm.lx;
   if (id == 1) return sm.lu;
   if (id == 2) return sm.lpt;
@@ -265,7 +270,8 @@ __device__ __forceinline__ int stat_of(const DevObjective& o, int id) {
 // One backward sweep (backward_propagate's lower form, crown.cpp:92-292) of a scalar:
 // the objective's output (start_kind < 0) or `sign` times row `row` of a start node.
 // Returns the concretised lower bound (crown.cpp:296-319) on every thread.
-__device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem& sm, const Bounds& B, int s, int row,
+template <int MW>
+__device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem<MW>& sm, const Bounds& B, int s, int row,
                         double sign) {
   const int tid = threadIdx.x;
   const long long boxoff = static_cast<long long>(s) * o.d;
@@ -273,7 +279,7 @@ __device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem& sm, con
   const bool stops = a.mode != 0;  // full CROWN: no stop set (crown.cpp:463-464)
   const int t_top = node ? a.start_t : o.H - 1;
   double bacc = 0.0;  // this thread's share of the offset
-  for (int j = tid; j < kMaxW; j += kThreads) sm.lx[j] = 0.0;
+  for (int j = tid; j < MW; j += kThreads) sm.lx[j] = 0.0;
   for (int j = tid; j < 16; j += kThreads) sm.lp[j] = 0.0;
   __syncthreads();
 
@@ -282,7 +288,7 @@ __device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem& sm, con
     const bool top = t == t_top;
     // 1. cost program, reverse op order; terms enter with coefficient 1 (output pass),
     //    or the start row of a cost-op node with coefficient `sign`.
-    for (int j = tid; j < kMaxW; j += kThreads) sm.lops[j] = 0.0;
+    for (int j = tid; j < MW; j += kThreads) sm.lops[j] = 0.0;
     for (int j = tid; j < 16; j += kThreads) {
       sm.lu[j] = 0.0;
       sm.lpt[j] = j < o.kd ? sm.lp[j] : 0.0;  // from step t+1's relative features
@@ -460,9 +466,10 @@ __device__ double sweep(const DevObjective& o, const BoundArgs& a, Smem& sm, con
   return tot;
 }
 
+template <int MW>
 __global__ void __launch_bounds__(kThreads) bound_kernel(const DevObjective o, const BoundArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  Smem<MW>& sm = *reinterpret_cast<Smem<MW>*>(smraw);
   if (a.start_kind >= 0) {  // full-CROWN node pass: CTA = (subdomain, row)
     const int s = blockIdx.x / a.start_dim, row = blockIdx.x % a.start_dim;
     const Bounds B{o, a, static_cast<long long>(s) * o.H * o.SP, false};
@@ -511,16 +518,31 @@ __global__ void hinge_bounds_kernel(const DevObjective o, const BoundArgs a, int
 
 }  // namespace
 
-size_t bound_smem_bytes() { return sizeof(Smem); }
+// Scratch width the bound kernel needs: the widest layer and the per-row scratch (op values by column).
+int bound_width(const DevObjective& o) {
+  int w = o.S > o.ks ? o.S : o.ks;
+  for (int l = 0; l <= o.L; ++l) w = o.widths[l] > w ? o.widths[l] : w;
+  return w;
+}
+size_t bound_smem_bytes() { return sizeof(Smem<kMaxW>); }
 
+// Instantiated at the smallest width class that holds the objective: shared memory of
+// 12 x width doubles per CTA, so narrow objectives keep several CTAs per SM.
 cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  const size_t smem = sizeof(Smem);
-  cudaError_t e = cudaFuncSetAttribute(bound_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
   const long long grid = a.start_kind >= 0 ? static_cast<long long>(n) * a.start_dim : n;
-  bound_kernel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(o, a);
-  return cudaGetLastError();
+  auto go = [&](auto kern, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(o, a);
+    return cudaGetLastError();
+  };
+  const int w = bound_width(o);
+  if (w <= 128) return go(bound_kernel<128>, sizeof(Smem<128>));
+  if (w <= 256) return go(bound_kernel<256>, sizeof(Smem<256>));
+  if (w <= 512) return go(bound_kernel<512>, sizeof(Smem<512>));
+  if (w <= kMaxW) return go(bound_kernel<kMaxW>, sizeof(Smem<kMaxW>));
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_hinge_bounds(const DevObjective& o, const BoundArgs& a, int t, int op_index, cudaStream_t st) {
