@@ -412,9 +412,12 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
       uint32_t* fr_b = m.ring + 2 * kSlots;  // a_free barrier index << 1 | parity of the completion
       uint32_t ppar = 0;  // bit i*KBMAX+kb: parity of a_free[i][kb]'s next completion
       int it = 0, head = 0;
+      // two tiles (NT = 2) run each layer's K-blocks in lockstep on the same weight blocks:
+      // streamed once per layer and freed by the last tile's release
+      constexpr bool kLock = NT == 2;
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l)
-          for (int i = 0; i < NT; ++i) {
+          for (int i = kLock ? NT - 1 : 0; i < NT; ++i) {
             const int npad = o.tc_npad[l], nh = n_halves(npad);
             for (int kb = 0; kb < o.tc_kb[l]; ++kb) {  // K-block outer: its A_lo slot is freed after it
               const int bit = i * KBMAX + kb;
@@ -511,6 +514,57 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
         mark2(a, t, 102 + 20 * l);
         put2(a, t, 300 + 20 * l, wfull + (1ll << 40));
         put2(a, t, 310 + 20 * l, awt + (1ll << 40));
+      }
+  } else if (warp == C::kMmaWarp && NT == 2) {
+    // ------------------------------------------------ MMA issuer, two tiles in lockstep: per
+    // K-block one wait for its weight blocks, then tile 0's burst and tile 1's burst on them
+    // (each tile's A K-block waited just before its burst, its release committed after it)
+    int it = 0, li = 0;
+    uint32_t pos = 0;
+    uint32_t a_par = 0;
+    const uint32_t wbase = smem_u32(m.w);
+    const uint32_t abase = smem_u32(m.alo);
+    for (int t = 0; t < H; ++t)
+      for (int l = 0; l < L; ++l, ++li) {
+        const int npad = o.tc_npad[l], ksteps = o.tc_ksteps[l];
+        const uint32_t idesc = tf32_idesc(npad);
+        const uint32_t bytes = static_cast<uint32_t>(npad) * 128u;
+        for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
+          const int nq = min(4, ksteps - kb * 4);
+          const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+          bool weights = false;
+          for (int i = 0; i < NT; ++i) {
+            const int bit = i * KBMAX + kb;
+            if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
+            mbar_wait_warp(m.a_chunk + bit, (a_par >> bit) & 1u);
+            if (kb == 0) mark2(a, t, 101 + 20 * l + 10 * i);
+            a_par ^= 1u << bit;
+            if (!weights) {
+              mbar_wait_warp(m.full + it % kSlots, static_cast<uint32_t>((it / kSlots) & 1));
+              mbar_wait_warp(m.full + (it + 1) % kSlots, static_cast<uint32_t>(((it + 1) / kSlots) & 1));
+              weights = true;
+            }
+            fence_after();
+            const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
+            const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
+            const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(i * ALO + kb % ALO) * 16384u);
+            const uint32_t a0 = areg + 32 * kb;
+            const uint64_t bh = sw128_desc(wbase + at_h), bl = sw128_desc(wbase + at_l);
+            if (nq == 4) {
+              mma_kblock_elect(dreg, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
+            } else {
+              for (int q = 0; q < nq; ++q)
+                mma_pair_elect(dreg, a0 + 8 * q, alo_d + 2 * q, bh + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
+              for (int q = 0; q < nq; ++q) mma_ts(dreg, a0 + 8 * q, bl + 2 * q, idesc, 1u);
+            }
+            mma_commit_elect(m.a_free + bit);  // tile 1's also frees the weight blocks
+            if (kb + 1 == o.tc_kb[l]) {
+              mma_commit_elect(m.d_full + 2 * i + (li & 1));  // this tile's accumulator complete
+              mark2(a, t, 102 + 20 * l + 10 * i);
+            }
+          }
+          it += 2;
+        }
       }
   } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------ MMA issuer: the whole warp runs the
