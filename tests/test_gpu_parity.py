@@ -229,6 +229,25 @@ def test_interval_bound_matches_oracle(device, name):
     assert abs(lf[0] - ref) <= 1e-9 * max(1.0, abs(ref))
 
 
+@pytest.mark.parametrize("width", [100, 200, 300, 500])
+def test_bound_width_classes_match_oracle(device, width):
+    """The bound kernel is instantiated per width class (128 / 256 / 512 scratch doubles
+    for the widest layer or cost-scratch row); objectives in each class bound like the
+    oracle, full CROWN included."""
+    s = bp.Scenario()
+    s.x0, s.x_target, s.p0 = [0.4, -0.3, 0.1, 0.2], [0.0, 0.0, 0.1, 0.1], [0.0, 0.0]
+    s.horizon = 3
+    s.u_lower, s.u_upper = [-0.5, -0.5], [0.5, 0.5]
+    spec = objmod.round_spec_to_f32(objmod.build_objective(bp.generate_model(7, [6, width, 4]), s))
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    ob = orc.Objective(spec)
+    for mode in ("early-stop-interval", "full-crown"):
+        lf = dev.bound_boxes(lo[None], hi[None], mode)
+        ref = ob.lower_bound(lo, hi, mode)
+        assert abs(lf[0] - ref) <= 1e-8 * max(1.0, abs(ref)), (width, mode)
+
+
 def test_search_properties(device):
     spec = small_spec("c1")
     dev = device.load(spec)
