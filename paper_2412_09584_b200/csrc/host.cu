@@ -1319,7 +1319,7 @@ std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double
 
 // Device pool slab (pool.cu): the payload of every record this rank owns -- box,
 // incumbent action, top-sample list -- one slot per record, with a host free list.
-// Slots come in fixed-size chunks (>= 32 MB or 4096 slots each) that are never moved
+// Slots come in fixed-size chunks (>= 256 MB or 4096 slots each) that are never moved
 // or freed while the planner runs, so the pool grows without copies or device-wide
 // synchronisation; the chunks go back to the context when the planner ends and the
 // next plan with the same geometry reuses them.
@@ -1335,7 +1335,7 @@ struct DevPool {
   DevPool(bp_ctx* c, int d_, int K_) : ctx(c), d(d_), K(K_) {
     const size_t sd = static_cast<size_t>(d), sk = static_cast<size_t>(K);
     const size_t slot_bytes = 20 * sd + 4 * sk + 4 * sk * sd + 8;
-    while (shift < 12 && (slot_bytes << shift) < (32u << 20)) ++shift;
+    while (shift < 12 && (slot_bytes << shift) < (size_t{256} << 20)) ++shift;  // >= 256 MB: few cudaMallocs per plan
     const size_t per = size_t{1} << shift;
     auto al = [](size_t x) { return (x + 255) & ~size_t{255}; };
     o_hi = o_lo + al(per * sd * 8);
