@@ -1,26 +1,36 @@
 #!/usr/bin/env python
 """BaB-ND hot-path benchmark on B200 (BASELINE.json metric: subdomains bounded/s
-and sample*steps/s).
+and sample*steps/s; best objective vs the CPU planner at equal iterations).
 
-A step is one steady-state BaB iteration of the C2 workload (BASELINE.json
-configs[1]: MLP [12,128,128,128,10], H=20, M=1024 samples per CEM iteration,
-10 CEM iterations, D=512 children = 2 x batch 256): pick_out, split, device
-search (Philox sampling -> fused rollout + extrema -> incumbent / top-K / CEM
-refit), device early-stop CROWN bound, merge, prune.  Timed with CUDA events on
-the launching stream, L2 flushed between steps, max over ranks.
+Default workload: C3-wide (BASELINE.json configs[2]: MLP [36,256,256,256,32],
+H=30, M=4096 samples per CEM iteration, 10 CEM iterations, D=2048 children =
+2 x batch 1024 per BaB iteration) -- the largest configuration whose planner
+step fits one GPU and the width-256 configuration the >= 50 % tensor-pipe
+target names.  A step is one steady-state BaB iteration: pick_out, split,
+device search (Philox sampling -> fused rollout + extrema -> incumbent / top-K /
+CEM refit), device early-stop CROWN bound, merge, prune.  `--config c1|c2|c4`
+select the other planner configs; `--config c5 [--d D]` is SURVEY 8(d)'s sweep
+step: one search (10 CEM iterations) + one bound pass over D pre-split boxes.
+Timed with CUDA events on the launching stream, L2 flushed between steps, max
+over ranks.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c3] [--impl reference]
 
 Multi-GPU (torchrun): one planner sharded over the ranks -- every iteration's
-children go round-robin to the GPUs and their reports are allgathered over
-NCCL (paper_2412_09584_b200.parallel); the batch grows with the GPU count so
-each GPU keeps D=512 children per step (weak scaling).
+children go round-robin to the GPUs and their heads are all-gathered
+(paper_2412_09584_b200.parallel); the batch grows with the GPU count so each GPU
+keeps D=2048 children per step (weak scaling).
+
+--impl reference times the reference algorithm on the host cores: the FP64
+oracle restatement (oracle/, all host threads; the reference itself does not
+build here -- DESIGN.md 3) on a bounded sample of the same workload per step.
+That arm never loads this repo's CUDA library (fixtures come from the pure-
+Python reference Rng in workloads.py).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -33,8 +43,12 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-
 TF32_DENSE_TFLOPS = 1100.0  # /opt/skills/guides/B200_PROFILING.md, dense (non-sparse) TF32
+CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+# full CPU searches are affordable per step only for the small configs; above that the CPU arm
+# times a fixed slice of each box's search (1 of the 10 CEM iterations: every iteration does the
+# same work) and reports the full-search equivalent (SURVEY 8(d) "time a fixed slice")
+CPU_CEM_SLICE = {"c1": None, "c2": None, "c3": 1, "c4": 1, "c5": 1}
 
 
 def parse():
@@ -43,10 +57,22 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c3", choices=sorted(CONFIG_INDEX))
+    p.add_argument("--d", type=int, default=1024, help="C5 sweep: pre-split boxes per GPU")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-objective", action="store_true", help="skip the best-objective comparison")
     return p.parse_args()
+
+
+def workload(args):
+    from paper_2412_09584_b200 import workloads
+
+    return workloads.c5(D=args.d) if args.config == "c5" else workloads.ALL[args.config]()
+
+
+def label(args, wl) -> str:
+    return f"{wl.name} (BASELINE.json configs[{CONFIG_INDEX[args.config]}])"
 
 
 class ClockSampler:
@@ -90,24 +116,34 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_children_per_s(wl, n_children: int, steps: int = 1, warmup: int = 0):
-    """The oracle (FP64 CPU restatement of the reference path) on n_children boxes:
-    batch_search + CrownBounder::lower, all host threads (parallel_chunks over boxes)."""
+# ------------------------------------------------------------------ CPU (oracle) legs
+def cpu_children_per_s(cfg_name, wl, n_children: int, steps: int = 1, warmup: int = 0):
+    """The oracle (FP64 CPU restatement of the reference path) on n_children pre-split boxes:
+    batch_search + CrownBounder::lower, all host threads (parallel_chunks over boxes).  Configs
+    in CPU_CEM_SLICE run k of the CEM iterations per step; the rate is per full-search
+    equivalent (search time x iterations / k + bound time)."""
     from oracle import oracle as orc
     from paper_2412_09584_b200 import workloads
 
     ob = orc.Objective(wl.spec)
     los, his = workloads.presplit_boxes(wl.spec, n_children)
     cfg = wl.planner_config()
+    full_iters = cfg["search"]["iterations"]
+    k = CPU_CEM_SLICE[cfg_name] or full_iters
+    cfg["search"]["iterations"] = k
     times = []
     for i in range(warmup + steps):
         t0 = time.perf_counter()
         reps = ob.batch_search(los, his, None, cfg, seed=1000 + i)
+        t1 = time.perf_counter()
         reps.bound_all()
-        dt = time.perf_counter() - t0
+        t2 = time.perf_counter()
         if i >= warmup:
-            times.append(dt)
-    return n_children / (sum(times) / len(times)), times, orc.thread_count()
+            times.append((t1 - t0) * full_iters / k + (t2 - t1))
+    sample = (f"{n_children} pre-split {wl.name} boxes per step: batch_search (CEM M={wl.samples_per_iter}, "
+              + (f"{k} of {full_iters} iterations timed, scaled to the full search" if k != full_iters
+                 else f"{full_iters} iterations") + ") + early-stop-empirical CROWN, FP64 oracle restatement")
+    return n_children / (sum(times) / len(times)), times, orc.thread_count(), sample
 
 
 def run_reference(args, wl):
@@ -117,30 +153,96 @@ def run_reference(args, wl):
     from oracle import oracle as orc
 
     n = max(8, orc.thread_count())
-    rate, times, cores = cpu_children_per_s(wl, n, steps=args.steps, warmup=args.warmup)
+    rate, times, cores, sample = cpu_children_per_s(args.config, wl, n, steps=args.steps, warmup=args.warmup)
     line = {
         "impl": "reference", "metric": "subdomains_bounded_per_s", "value": rate, "unit": "subdomains/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        # the same workload as this repo's arm (its config keys); each timed step is a bounded sample of it
-        "config": {"workload": f"{wl.name} (BASELINE.json configs[1])", "widths": wl.spec.widths, "H": wl.spec.horizon,
-                   "M": wl.samples_per_iter, "D_per_step": n, "cem_iterations": wl.planner_config()["search"]["iterations"],
-                   "batch": wl.planner_config()["batch"], "parallelism": "host threads",
-                   "sample": f"{n} pre-split boxes per step (the GPU arm bounds {2 * wl.planner_config()['batch']} per step)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded He-init weights, x0/goal/obstacles from the reference Rng)",
+        "config": {"workload": label(args, wl), "widths": wl.spec.widths, "H": wl.spec.horizon,
+                   "M": wl.samples_per_iter, "cem_iterations": wl.planner_config()["search"]["iterations"],
+                   "D_per_step": n, "parallelism": f"{cores} host threads", "sample": sample},
         "cpu_baseline": {"value": rate, "unit": "subdomains/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} pre-split C2 boxes per step: batch_search (CEM, M=1024, 10 iters) + "
-                                   "early-stop-empirical CROWN, FP64 oracle restatement (reference does not build "
-                                   "here: Eigen/vendor headers absent)"},
+                         "sample": sample + " (the reference does not build here: Eigen / vendor headers absent)"},
         "e2e": {"value": rate, "unit": "subdomains/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse()
+def best_objective_vs_cpu():
+    """Best objective of the device planner and the CPU reference planner (oracle) at equal BaB
+    iteration counts, same fixtures and planner seed (the samplers differ: Philox vs mt19937_64, so
+    this is a statistical comparison).  C1 at its full 20 iterations; C2 with batch 4 for 4
+    iterations (the CPU planner needs ~14 s per C2 child)."""
+    import paper_2412_09584_b200 as bp
+    from oracle import oracle as orc
     from paper_2412_09584_b200 import workloads
 
-    wl = workloads.ALL[args.config]()
+    out = {}
+    for name, over, iters in (("c1", {}, None), ("c2", {"batch": 4}, 4)):
+        wl = workloads.ALL[name]()
+        cfg = wl.planner_config(**over)
+        if iters is not None:
+            cfg["termination"]["max_iterations"] = iters
+        dev = bp.Device(int(os.environ.get("LOCAL_RANK", "0"))).load(wl.spec)
+        g = dev.plan(cfg)
+        dev.close()
+        t0 = time.perf_counter()
+        c = orc.Objective(wl.spec).plan(cfg)
+        out[wl.name] = {"iterations": cfg["termination"]["max_iterations"], "batch": cfg["batch"],
+                        "gpu": g["objective"], "cpu": c["objective"],
+                        "gpu_le_cpu": bool(g["objective"] <= c["objective"]),
+                        "rel_gap": (g["objective"] - c["objective"]) / max(abs(c["objective"]), 1e-12),
+                        "gpu_lower_bound": g["lower_bound"], "cpu_lower_bound": c["lower_bound"],
+                        "cpu_s": time.perf_counter() - t0}
+    return out
+
+
+# ------------------------------------------------------------------ GPU arm
+def roofline(dev, wl, args, tm, rows_per_launch_total, peak_tf32, peak_fp32):
+    """Roofline of the dominant kernel (the rollout): algorithmic FLOPs / device time of its launches."""
+    path = dev.rollout_path()
+    kern = dev.rollout_kernel()
+    info = dev.rollout_info()
+    flop = rows_per_launch_total * wl.spec.horizon * wl.flops_per_sample_step
+    achieved = flop / (tm["rollout_ms"] / 1e3) / 1e12 if tm["rollout_ms"] > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"r02_{args.config}_ncu_summary.json")
+    if os.path.exists(tp):
+        j = json.load(open(tp))
+        if j.get("kernel_key") == kern:
+            traffic = j.get("dram_bytes_per_launch")
+    kname = {"tc1": "rollout_tc_kernel (K1 v1, rollout_tc.cu: tcgen05 kind::tf32, 3xTF32, one 128-row tile per CTA)",
+             "tc2": f"rollout_tc2_kernel (K1 v2, rollout_tc2.cu: tcgen05 kind::tf32, 3xTF32, in-place TMEM regions, "
+                    f"{info['tiles_per_cta']} tile(s) per CTA)",
+             "tc3": "rollout_tc3_kernel (K1 v3, rollout_tc3.cu: tcgen05 kind::tf32, 3xTF32, N-split CTA pair)",
+             "simt": "rollout_kernel (K1, rollout.cu: SIMT FFMA)"}.get(kern, kern)
+    if path == "tcgen05":
+        # 3xTF32: three dense kind::tf32 MMAs per FP32 product, so the ceiling for the algorithmic
+        # (FP32) FLOP rate is the TF32 tensor peak / 3.
+        roof = {"bound": "tensor", "achieved": achieved, "peak": TF32_DENSE_TFLOPS / 3.0, "unit": "TFLOP/s",
+                "kernel": kname,
+                "peak_source": "B200_PROFILING.md fallback: dense TF32 1100 TFLOP/s (MEASURED_PEAKS.json has no TF32 "
+                               "entry) / 3 MMAs per FP32 product",
+                "peak_measured_live": (peak_tf32 / 3.0) if peak_tf32 else None,
+                "tensor_tflops_executed": 3.0 * achieved if achieved else None}
+    else:
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s", "kernel": kname,
+                "peak_source": "bp_measure_fp32_peak: FFMA microbenchmark run live in this process "
+                               "(MEASURED_PEAKS.json has no FP32 SIMT entry)"}
+    roof["frac"] = (roof["achieved"] / roof["peak"]) if (roof["achieved"] and roof["peak"]) else None
+    roof["traffic"] = traffic
+    roof["traffic_source"] = (f"profiles/r02_{args.config}_ncu_summary.json (ncu --set full, "
+                              "dram__bytes_read.sum + dram__bytes_write.sum per launch)") if traffic else None
+    roof.update({"flop_per_sample_step": wl.flops_per_sample_step, "rollout_ms": tm["rollout_ms"],
+                 "rollout_launches": tm["rollout_launches"],
+                 "algorithmic": "2 * sum(in*out) FLOP per sample-step x rows x H per launch (SURVEY 8(d))"})
+    return roof, path
+
+
+def main():
+    args = parse()
+    wl = workload(args)
     if args.impl == "reference":
         run_reference(args, wl)
         return
@@ -155,6 +257,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2412_09584_b200 as bp
+    from paper_2412_09584_b200 import parallel, workloads
 
     peak_fp32 = peak_tf32 = None
     if rank == 0:
@@ -166,28 +269,49 @@ def main():
         _capi.check(_capi.load().bp_measure_tf32_peak(local, C.byref(t), C.byref(ms)))
         peak_tf32 = t.value
 
-    from paper_2412_09584_b200 import parallel
-
     dev = bp.Device(local).load(wl.spec)
-    path = dev.rollout_path()  # "tcgen05" (3xTF32 tensor cores) or "simt" (FP32 FFMA)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
-    parallel.attach(dev)
     cfg = wl.planner_config()
-    cfg["batch"] = cfg["batch"] * world
-    cfg["termination"]["max_iterations"] = 10**6
-    planner = dev.planner(cfg)
-    batch = cfg["batch"]
-    setup = 0
-    while True:  # grow the pool to the steady-state batch (2*batch children per step)
-        ok, ch, pool = planner.step()
-        setup += 1
-        if pool >= batch or setup >= 16:
-            break
-    for _ in range(args.warmup):
-        planner.step()
+    iters = cfg["search"]["iterations"]
+    rows = wl.rows_per_search_iter
+    H = wl.spec.horizon
+    sweep = args.config == "c5"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    if sweep:
+        # one search (10 CEM iterations) + one bound pass over D pre-split boxes per GPU;
+        # the boxes are this rank's slice of the global D*world leaves (weak scaling, no exchange)
+        los, his = workloads.presplit_boxes(wl.spec, args.d * world)
+        los, his = los[rank::world], his[rank::world]
+        n_box = los.shape[0]
+
+        def step():
+            dev.batch_search(los, his, None, cfg, seed=7)
+            dev.batch_bound(n_box)
+            return n_box
+        setup = 0
+    else:
+        parallel.attach(dev)
+        cfg["batch"] = cfg["batch"] * world
+        cfg["termination"]["max_iterations"] = 10**6
+        planner = dev.planner(cfg)
+        batch = cfg["batch"]
+        setup = 0
+        while True:  # grow the pool to the steady-state batch (2*batch children per step)
+            _, _, pool = planner.step()
+            setup += 1
+            if pool >= batch or setup >= 16:
+                break
+
+        def step():
+            _, ch, _ = planner.step()
+            return ch
+
+    for _ in range(args.warmup):
+        step()
     dev.timing()
+    dev.search_counters()
     bp.Device.io_bytes()
     step_ms, children = [], 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -198,112 +322,106 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             ev0.record(stream)
-            ok, ch, pool = planner.step()
+            ch = step()
             ev1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
             children += ch
     tm = dev.timing()
+    cnt = dev.search_counters()
     total_ms = sum(step_ms)
-    stats = torch.tensor([total_ms, float(children), tm["rollout_ms"], float(tm["launches"])], device="cuda",
-                         dtype=torch.float64)
+    stats = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
     if world > 1:
-        mx = stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        total_ms_max = mx[0].item()
-    else:
-        total_ms_max = total_ms
-    children_all = float(children)  # the planner's global child count (identical on every rank)
-    rows = wl.rows_per_search_iter
-    H = wl.spec.horizon
-    iters = cfg["search"]["iterations"]
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    total_ms_max = stats[0].item()
+    # planner: the global child count (identical on every rank); sweep: this rank's boxes x world
+    children_all = float(children) * (world if sweep else 1)
     value = children_all / (total_ms_max / 1e3)
     sample_steps = children_all * rows * iters * H / (total_ms_max / 1e3)
-    # roofline of the dominant kernel (rollout): algorithmic FLOPs / device time of its launches
-    flop = children / world * rows * iters * H * wl.flops_per_sample_step  # this rank's share
-    achieved = flop / (tm["rollout_ms"] / 1e3) / 1e12 if tm["rollout_ms"] > 0 else None
-    traffic = None
-    kern = dev.rollout_kernel()  # "tc1" (rollout_tc.cu), "tc2" (rollout_tc2.cu) or "simt" (rollout.cu)
-    info = dev.rollout_info()
-    # DRAM bytes per launch from the committed ncu --set full capture of this kernel on this workload
-    tp = os.path.join(ROOT, "profiles", {"tc1": "rollout_tc_ncu_summary.json", "simt": "rollout_ncu_summary.json",
-                                         "tc2": f"rollout_tc2_{args.config}_ncu_summary.json"}[kern])
-    if os.path.exists(tp) and (kern == "tc2" or args.config == "c2"):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    kname = {"tc1": "rollout_tc_kernel (K1 v1, rollout_tc.cu: tcgen05 kind::tf32, 3xTF32, one 128-row tile per CTA)",
-             "tc2": f"rollout_tc2_kernel<{info['tiles_per_cta']},{256 if info['tiles_per_cta'] == 1 and max(wl.spec.widths) > 128 else 128}> "
-                    "(K1 v2, rollout_tc2.cu: tcgen05 kind::tf32, 3xTF32, in-place TMEM regions)",
-             "simt": "rollout_kernel (K1, rollout.cu: SIMT FFMA)"}[kern]
-    if path == "tcgen05":
-        # 3xTF32: three dense kind::tf32 MMAs per FP32 product, so the ceiling for the
-        # algorithmic (FP32) FLOP rate is the TF32 tensor peak / 3.
-        roof = {"bound": "tensor", "achieved": achieved, "peak": TF32_DENSE_TFLOPS / 3.0, "unit": "TFLOP/s",
-                "kernel": kname,
-                "peak_source": "B200_PROFILING.md fallback: dense TF32 1100 TFLOP/s (MEASURED_PEAKS.json has no TF32 "
-                               "entry) / 3 MMAs per FP32 product",
-                "peak_measured_live": (peak_tf32 / 3.0) if peak_tf32 else None,
-                "tensor_tflops_executed": 3.0 * achieved if achieved else None}
-    else:
-        roof = {"bound": "fp32", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
-                "kernel": kname,
-                "peak_source": "bp_measure_fp32_peak: FFMA microbenchmark run live in this process "
-                               "(MEASURED_PEAKS.json has no FP32 SIMT entry)"}
-    roof["frac"] = (roof["achieved"] / roof["peak"]) if (roof["achieved"] and roof["peak"]) else None
-    roof["traffic"] = traffic
-    roof.update({"flop_per_sample_step": wl.flops_per_sample_step, "rollout_ms": tm["rollout_ms"],
-                 "rollout_launches": tm["rollout_launches"]})
+    my_rows = (children if sweep else children / world) * rows * iters  # this rank's rolled-out rows
+    roof, path = roofline(dev, wl, args, tm, my_rows, peak_tf32, peak_fp32)
 
     e2e = None
     if not args.no_e2e:
-        # end to end through the public API: objective upload, plan() from the root for the same number
-        # of iterations, host buffers in and the result dict out, wall clock around the whole call.
         dev2 = bp.Device(local)
-        parallel.attach(dev2)
-        cfg2 = wl.planner_config()
-        cfg2["batch"] = cfg2["batch"] * world
-        n_it = setup + args.warmup + args.steps
-        cfg2["termination"]["max_iterations"] = n_it
         bp.Device.io_bytes()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dev2.load(wl.spec)
-        res = dev2.plan(cfg2)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        h2d, d2h = bp.Device.io_bytes()
-        # every searched box (root and children) evaluates rows x iters samples
-        bounded = res["samples"] / (rows * iters)
-        e2e = {"value": bounded / wall, "unit": "subdomains/s", "h2d_bytes_per_step": int(h2d / max(1, n_it)),
-               "d2h_bytes_per_step": int(d2h / max(1, n_it)), "iterations": n_it,
-               "note": "plan() from the root incl. ramp-up iterations with fewer children; objective upload inside"}
+        if sweep:
+            # the public batch_search / batch_bound calls with host boxes in and reports / bounds out
+            dev2.load(wl.spec)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                dev2.batch_search(los, his, None, cfg, seed=7)
+                dev2.batch_bound(n_box)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            h2d, d2h = bp.Device.io_bytes()
+            e2e = {"value": n_box * world * args.steps / wall, "unit": "subdomains/s",
+                   "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
+                   "note": "batch_search + batch_bound through the public API, host boxes in, bounds and reports out"}
+        else:
+            # plan() from the root through the public API: objective upload, setup + timed iterations,
+            # host buffers in and the result dict out, wall clock around the whole call.
+            parallel.attach(dev2)
+            cfg2 = wl.planner_config()
+            cfg2["batch"] = cfg2["batch"] * world
+            n_it = setup + args.steps
+            cfg2["termination"]["max_iterations"] = n_it
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev2.load(wl.spec)
+            res = dev2.plan(cfg2)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            h2d, d2h = bp.Device.io_bytes()
+            bounded = res["samples"] / (rows * iters)  # every searched box evaluates rows x iters samples
+            e2e = {"value": bounded / wall, "unit": "subdomains/s", "h2d_bytes_per_step": int(h2d / max(1, n_it)),
+                   "d2h_bytes_per_step": int(d2h / max(1, n_it)), "iterations": n_it,
+                   "note": "plan() from the root incl. the ramp-up iterations with fewer children; objective "
+                           "upload inside"}
         dev2.close()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import oracle as orc
-            n = max(8, orc.thread_count())
-            rate, times, cores = cpu_children_per_s(wl, n, steps=1)
-            cpu = {"value": rate, "unit": "subdomains/s", "cores": cores, "kind": "port",
-                   "sample": f"{n} pre-split {wl.name} boxes: batch_search (CEM M={wl.samples_per_iter}, "
-                             f"{iters} iters) + early-stop-empirical CROWN in the FP64 oracle, {times[0]:.1f} s"}
-        except Exception as e:  # the checker is optional on the box
-            cpu = {"value": None, "unit": "subdomains/s", "cores": None, "kind": "port", "sample": f"unavailable: {e}"}
+    objective = None
+    if rank == 0 and world == 1:
+        if not args.no_cpu_baseline:
+            try:
+                from oracle import oracle as orc
+                n = max(8, orc.thread_count())
+                rate, times, cores, sample = cpu_children_per_s(args.config, wl, n, steps=1)
+                cpu = {"value": rate, "unit": "subdomains/s", "cores": cores, "kind": "port",
+                       "sample": sample + f" ({times[0]:.1f} s)"}
+            except Exception as e:  # the checker is optional on the box
+                cpu = {"value": None, "unit": "subdomains/s", "cores": None, "kind": "port", "sample": f"unavailable: {e}"}
+        if not args.no_objective:
+            try:
+                objective = best_objective_vs_cpu()
+            except Exception as e:
+                objective = {"unavailable": str(e)}
 
     if rank == 0:
         clk = clocks.summary()
+        conf = {"workload": label(args, wl), "widths": wl.spec.widths, "H": H, "M": wl.samples_per_iter,
+                "cem_iterations": iters, "D_per_step": children_all / args.steps,
+                "D_per_gpu": children_all / args.steps / world,
+                "l2": "flushed (256 MB write) between timed steps",
+                "parallelism": f"subdomain-sharded x{world}" if world > 1 else "1 GPU"}
+        if sweep:
+            conf["step"] = "one search (10 CEM iterations) + one early-stop-empirical bound pass over D pre-split boxes"
+        else:
+            conf.update({"batch": cfg["batch"], "setup_iterations": setup})
         line = {
             "metric": "subdomains_bounded_per_s", "value": value, "unit": "subdomains/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if path == "simt" else "tf32x3",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if path == "simt" else "tf32x3",
             "data": "synthetic (seeded He-init weights, x0/goal/obstacles from the reference Rng)",
-            "config": {"workload": f"{wl.name} (BASELINE.json configs[1])", "widths": wl.spec.widths,
-                       "H": H, "M": wl.samples_per_iter, "D_per_step": children / args.steps, "D_per_gpu": children / args.steps / world,
-                       "cem_iterations": iters, "batch": batch, "setup_iterations": setup,
-                       "l2": "flushed (256 MB write) between timed steps", "parallelism": f"subdomain-sharded x{world}" if world > 1 else "1 GPU"},
+            "config": conf,
             "sample_steps_per_s": sample_steps,
+            "failed_boxes": {"timed": cnt["failed"], "searched": cnt["boxes"]},
             "roofline": roof,
             "e2e": e2e, "gpu_launches": int(tm["launches"]), "clocks": clk, "cpu_baseline": cpu,
+            "best_objective_vs_cpu": objective,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

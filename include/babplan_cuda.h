@@ -230,6 +230,20 @@ bp_status bp_report_summary(bp_ctx* ctx, double* uf, double* best, int64_t* samp
 bp_status bp_report_top(bp_ctx* ctx, int box, double* values, double* actions, int cap);
 bp_status bp_report_stats(bp_ctx* ctx, int box, float* emp_lo, float* emp_hi);
 
+/* One sampler update of run_cem / run_mppi on caller-provided rows and costs
+ * (parity entry: the sampler and the rollout are bypassed).  It is the device step
+ * that batch_search runs after each rollout: SampleSink::consume's incumbent and top-K
+ * update (src/search.cpp:41-74) and the CEM elite refit (search.cpp:131-149) or the MPPI
+ * weighted mean (search.cpp:192-205), for n_boxes boxes at CEM/MPPI iteration `iter`.
+ * rows [n][R][d] with R = agents*floor(M/agents) + 1 (the last row is the incumbent
+ * row), costs [n][R].  State in/out: mu, var [n][groups][d] (var: CEM only, may be
+ * null for MPPI), uf [n], best [n][d], top_n [n], top_val / top_seq [n][top_capacity],
+ * top_act [n][top_capacity][d] (ascending by (value, seq); seq = iter*R + row). */
+bp_status bp_search_update(bp_ctx* ctx, int n_boxes, const bp_search_config* cfg, const double* lo,
+                           const double* hi, int iter, const float* rows, const float* costs, float* mu,
+                           float* var, float* uf, float* best, int* top_n, float* top_val, int* top_seq,
+                           float* top_act);
+
 /* Lower bound of every searched box (mode/alpha as in lower_bound). */
 bp_status bp_batch_bound(bp_ctx* ctx, int mode, int alpha, double* lf);
 /* Lower bound of boxes without search statistics: lower_bound(obj, box, mode,
@@ -271,6 +285,11 @@ bp_status bp_result_free(bp_result* r);
  * kernel family; rollout is the dominant kernel). */
 bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms,
                     double* search_ms, int64_t* launches);
+
+/* Boxes searched since the previous call, and how many of them failed (a non-finite
+ * rollout value: SearchReport.ok = false, search.cpp:273-278; their rows are skipped by
+ * the rollout and they are bounded by interval propagation). */
+bp_status bp_search_counters(bp_ctx* ctx, int64_t* boxes, int64_t* failed);
 
 /* Diagnostics: sustained FP32 FMA throughput of the device (TFLOP/s), the
  * roofline denominator of the SIMT rollout kernel. */

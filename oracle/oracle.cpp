@@ -1233,8 +1233,16 @@ Vec clamp_to(const BoxDomain& box, Vec u) {
   return u;
 }
 
+thread_local const SearchHooks* g_hooks = nullptr;
+
 class SampleSink {  // search.cpp:37-82
  public:
+  const SearchReport& report() const { return report_; }
+  std::vector<TopSample> sorted_top() const {  // test hook view: the heap in value order
+    std::vector<TopSample> t = heap_;
+    std::sort(t.begin(), t.end(), [](const TopSample& a, const TopSample& b) { return a.value < b.value; });
+    return t;
+  }
   SampleSink(const Objective& f, int capacity) : f_(f), cap_(std::max(capacity, 1)) {}
   Vec consume(const Mat& batch) {
     Vec v = f_.evaluate(batch, &report_.stats);
@@ -1275,6 +1283,10 @@ class SampleSink {  // search.cpp:37-82
   SearchReport report_;
 };
 
+}  // namespace
+void set_search_hooks(const SearchHooks* hooks) { g_hooks = hooks; }
+namespace {
+
 SearchReport run_cem(const Objective& f, const BoxDomain& box, const SearcherConfig& cfg, const Vec* warm) {
   // search.cpp:87-155
   const int d = box.dim();
@@ -1313,6 +1325,7 @@ SearchReport run_cem(const Objective& f, const BoxDomain& box, const SearcherCon
       }
     }
     std::copy(incumbent.begin(), incumbent.end(), batch.row(agents * spi));
+    if (g_hooks && g_hooks->inject) g_hooks->inject(it, batch);
     const Vec vals = sink.consume(batch);
     for (int a = 0; a < agents; ++a) {
       std::vector<int> idx(static_cast<size_t>(spi));
@@ -1340,6 +1353,7 @@ SearchReport run_cem(const Objective& f, const BoxDomain& box, const SearcherCon
     }
     incumbent = sink.current_best();
     sink.mark_iteration();
+    if (g_hooks && g_hooks->after) g_hooks->after(it, batch, mu, var, sink.report(), sink.sorted_top());
   }
   return sink.finish();
 }
@@ -1372,6 +1386,7 @@ SearchReport run_mppi(const Objective& f, const BoxDomain& box, const SearcherCo
     }
     const Vec& inc = it == 0 ? init : sink.current_best();
     std::copy(inc.begin(), inc.end(), batch.row(instances * m));
+    if (g_hooks && g_hooks->inject) g_hooks->inject(it, batch);
     const Vec vals = sink.consume(batch);
     for (int inst = 0; inst < instances; ++inst) {
       const double tr = temps[static_cast<size_t>(inst) / noise.size()];
@@ -1389,6 +1404,7 @@ SearchReport run_mppi(const Objective& f, const BoxDomain& box, const SearcherCo
       mu[static_cast<size_t>(inst)] = clamp_to(box, acc);
     }
     sink.mark_iteration();
+    if (g_hooks && g_hooks->after) g_hooks->after(it, batch, mu, {}, sink.report(), sink.sorted_top());
   }
   return sink.finish();
 }

@@ -274,6 +274,16 @@ struct SearchReport {  // search.hpp:53-63
 };
 SearchReport search(const Objective& f, const BoxDomain& box, const SearcherConfig& cfg,
                     const Vec* warm_start = nullptr);
+
+// Test hooks (not in the reference): replace the sampled rows [0, n_samp) of iteration `it`
+// before they are consumed, and observe the sampler state after each iteration's refit.
+// Parity of the device update on identical samples (tests/test_gpu_search_update.py).
+struct SearchHooks {
+  std::function<void(int it, Mat& batch)> inject;
+  std::function<void(int it, const Mat& batch, const std::vector<Vec>& mu, const std::vector<Vec>& var,
+                     const SearchReport& so_far, const std::vector<TopSample>& top)> after;
+};
+void set_search_hooks(const SearchHooks* hooks);  // thread-local; null = none
 std::vector<SearchReport> batch_search(const Objective& f, const std::vector<BoxDomain>& boxes,
                                        const SearcherConfig& cfg,
                                        const std::vector<const Vec*>* warm_starts = nullptr);

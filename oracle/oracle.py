@@ -412,6 +412,33 @@ class Objective:
                           ("iter", "uf", "min_lf", "pruned_vol", "selected_vol", "pool_size", "samples", "wall_ms")}}
 
 
+def search_injected(lo, hi, warm, cfg: dict, rows, costs, method: str = "babnd") -> list:
+    """run_cem / run_mppi (search.cpp:87-209) on injected samples rows[it][n_samp][d] and values
+    costs[it][R] (R = n_samp + 1; the incumbent row is the searcher's own).  Per iteration the
+    state after the refit: batch, mu, var, uf, best, top values / actions (value order)."""
+    lo, hi = _d(lo), _d(hi)
+    d = lo.shape[0]
+    rows, costs = _d(rows), _d(costs)
+    T, n_samp = rows.shape[0], rows.shape[1]
+    R = n_samp + 1
+    packed = PackedConfig(cfg, method)
+    s = packed.cfg.search
+    G = s.cem_agents if s.method == 0 else max(1, s.mppi_n_noise) * max(1, s.mppi_n_temp)
+    K = max(1, s.top_capacity)
+    out = {"batch": np.zeros((T, R, d)), "mu": np.zeros((T, G, d)), "var": np.zeros((T, G, d)), "uf": np.zeros(T),
+           "best": np.zeros((T, d)), "top_n": np.zeros(T, dtype=np.int32), "top_val": np.zeros((T, K)),
+           "top_act": np.zeros((T, K, d))}
+    w = _d(warm)
+    ck(lib().or_search_injected(C.c_int(d), lo.ctypes.data_as(dp), hi.ctypes.data_as(dp),
+                                w.ctypes.data_as(dp) if w is not None else None, packed.search_ref(0), C.c_int(T),
+                                C.c_int(n_samp),
+                                rows.ctypes.data_as(dp), costs.ctypes.data_as(dp),
+                                *[out[k].ctypes.data_as(dp) for k in ("batch", "mu", "var", "uf", "best")],
+                                out["top_n"].ctypes.data_as(ip), out["top_val"].ctypes.data_as(dp),
+                                out["top_act"].ctypes.data_as(dp)))
+    return [{k: v[t] for k, v in out.items()} for t in range(T)]
+
+
 class Reports:
     def __init__(self, h, obj: Objective, lo, hi):
         self.h, self.obj, self.lo, self.hi = h, obj, lo, hi

@@ -519,6 +519,70 @@ int or_batch_search(void* h, int n, const double* los, const double* his, const 
     *out = r;
   });
 }
+// run_cem / run_mppi on injected samples and costs (test hooks): iteration `it` consumes
+// rows [0, n_samp) from inj_rows[it] (the incumbent row stays the searcher's own) and the
+// values inj_costs[it][R]; after each refit the state is written to the per-iteration outputs.
+namespace {
+struct TableObjective : Objective {
+  int d;
+  int R;
+  const double* costs;
+  mutable int calls = 0;
+  int dim() const override { return d; }
+  Vec evaluate(const Mat& batch, WatchStats*) const override {
+    if (batch.rows != R) throw std::logic_error("TableObjective: unexpected batch size");
+    Vec v(costs + static_cast<size_t>(calls) * R, costs + static_cast<size_t>(calls + 1) * R);
+    ++calls;
+    return v;
+  }
+};
+}  // namespace
+int or_search_injected(int d, const double* lo, const double* hi, const double* warm, const bp_search_config* cfg,
+                       int iterations, int n_samp, const double* inj_rows, const double* inj_costs, double* out_batch, double* out_mu,
+                       double* out_var, double* out_uf, double* out_best, int* out_top_n, double* out_top_val,
+                       double* out_top_act) {
+  return guard([&] {
+    SearcherConfig sc = search_cfg(*cfg);
+    sc.iterations = iterations;  // one table entry per iteration
+    const int R = n_samp + 1, K = std::max(1, sc.top_capacity);
+    TableObjective f;
+    f.d = d;
+    f.R = R;
+    f.costs = inj_costs;
+    SearchHooks hooks;
+    hooks.inject = [&](int it, Mat& batch) {
+      for (int r = 0; r < n_samp; ++r)
+        for (int j = 0; j < d; ++j) batch(r, j) = inj_rows[(static_cast<size_t>(it) * n_samp + r) * d + j];
+    };
+    hooks.after = [&](int it, const Mat& batch, const std::vector<Vec>& mu, const std::vector<Vec>& var,
+                      const SearchReport& so_far, const std::vector<TopSample>& top) {
+      std::copy(batch.a.begin(), batch.a.end(), out_batch + static_cast<size_t>(it) * R * d);
+      const size_t G = mu.size();
+      for (size_t g = 0; g < G; ++g) {
+        std::copy(mu[g].begin(), mu[g].end(), out_mu + (static_cast<size_t>(it) * G + g) * d);
+        if (!var.empty()) std::copy(var[g].begin(), var[g].end(), out_var + (static_cast<size_t>(it) * G + g) * d);
+      }
+      out_uf[it] = so_far.uf;
+      std::copy(so_far.best.begin(), so_far.best.end(), out_best + static_cast<size_t>(it) * d);
+      out_top_n[it] = static_cast<int>(top.size());
+      for (size_t k = 0; k < top.size(); ++k) {
+        out_top_val[static_cast<size_t>(it) * K + k] = top[k].value;
+        std::copy(top[k].u.begin(), top[k].u.end(), out_top_act + (static_cast<size_t>(it) * K + k) * d);
+      }
+    };
+    Vec w;
+    if (warm != nullptr) w = vec_of(warm, d);
+    set_search_hooks(&hooks);
+    try {
+      search(f, BoxDomain(vec_of(lo, d), vec_of(hi, d)), sc, warm != nullptr ? &w : nullptr);
+    } catch (...) {
+      set_search_hooks(nullptr);
+      throw;
+    }
+    set_search_hooks(nullptr);
+  });
+}
+
 void or_reports_free(void* r) { delete static_cast<Reports*>(r); }
 int or_report_get(void* rp, int i, double* uf, double* best, int64_t* samples, int* ok, int* n_top) {
   const SearchReport& r = static_cast<Reports*>(rp)->r.at(static_cast<size_t>(i));

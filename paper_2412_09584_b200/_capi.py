@@ -137,6 +137,8 @@ def load() -> C.CDLL:
             "bp_stat_layout": (C.c_int, [vp, _ip, _ip, _ip, _ip, _ip, _ip, C.c_int]),
             "bp_rollout": (C.c_int, [vp, C.c_int, C.c_int, _fp, _fp, _fp, _fp, _fp, _ip]),
             "bp_batch_search": (C.c_int, [vp, C.c_int, _dp, _dp, _dp, C.POINTER(SearchConfig)]),
+            "bp_search_update": (C.c_int, [vp, C.c_int, C.POINTER(SearchConfig), _dp, _dp, C.c_int, _fp, _fp, _fp,
+                                           _fp, _fp, _fp, _ip, _fp, _ip, _fp]),
             "bp_report_summary": (C.c_int, [vp, _dp, _dp, C.POINTER(C.c_int64), _ip, _ip]),
             "bp_report_top": (C.c_int, [vp, C.c_int, _dp, _dp, C.c_int]),
             "bp_report_stats": (C.c_int, [vp, C.c_int, _fp, _fp]),
@@ -152,6 +154,7 @@ def load() -> C.CDLL:
             "bp_result_best": (C.c_int, [vp, _dp]),
             "bp_result_trace": (C.c_int, [vp, C.POINTER(TraceRow), C.c_int]),
             "bp_result_free": (C.c_int, [vp]),
+            "bp_search_counters": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "bp_timing": (C.c_int, [vp, _dp, C.POINTER(C.c_int64), _dp, _dp, C.POINTER(C.c_int64)]),
             "bp_rng_new": (C.c_int, [C.c_uint64, C.POINTER(vp)]),
             "bp_rng_free": (C.c_int, [vp]),

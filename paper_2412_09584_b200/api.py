@@ -131,6 +131,26 @@ class Device:
                                          _capi.iptr(ntop)))
         return {"uf": uf, "best": best, "samples": samples, "ok": ok.astype(bool), "n_top": ntop}
 
+    def search_update(self, cfg: dict, lo: np.ndarray, hi: np.ndarray, it: int, rows: np.ndarray, costs: np.ndarray,
+                      state: dict, method: str = "babnd") -> dict:
+        """One device sampler update (bp_search_update) on given rows [n][R][d] and costs [n][R]:
+        incumbent + top-K + CEM refit / MPPI mean.  state (and the result): mu, var, uf, best,
+        top_n, top_val, top_seq, top_act as float32 / int32 arrays."""
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        n = lo.shape[0]
+        packed = _config.PackedConfig(cfg, method)
+        st = {k: np.ascontiguousarray(v, dtype=np.int32 if k in ("top_n", "top_seq") else np.float32).copy()
+              for k, v in state.items()}
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        costs = np.ascontiguousarray(costs, dtype=np.float32)
+        check(self.lib.bp_search_update(self.h, n, packed.search_ref(0), _capi.dptr(lo), _capi.dptr(hi), int(it),
+                                        _capi.fptr(rows), _capi.fptr(costs), _capi.fptr(st["mu"]),
+                                        _capi.fptr(st.get("var")), _capi.fptr(st["uf"]), _capi.fptr(st["best"]),
+                                        _capi.iptr(st["top_n"]), _capi.fptr(st["top_val"]), _capi.iptr(st["top_seq"]),
+                                        _capi.fptr(st["top_act"])))
+        return st
+
     def report_top(self, box: int, n_top: int):
         d = self.spec.d
         v = np.zeros(max(n_top, 1))
@@ -272,6 +292,13 @@ class Device:
         check(self.lib.bp_timing(self.h, C.byref(r), C.byref(rl), C.byref(b), C.byref(s), C.byref(l)))
         return {"rollout_ms": r.value, "rollout_launches": rl.value, "bound_ms": b.value, "search_ms": s.value,
                 "launches": l.value}
+
+
+    def search_counters(self) -> dict:
+        """Boxes searched and boxes whose search failed (non-finite rollout) since the previous call."""
+        b, f = C.c_int64(), C.c_int64()
+        check(self.lib.bp_search_counters(self.h, C.byref(b), C.byref(f)))
+        return {"boxes": b.value, "failed": f.value}
 
 
 def _result_dict(lib, res) -> dict:

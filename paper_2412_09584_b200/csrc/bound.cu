@@ -520,7 +520,7 @@ __global__ void hinge_bounds_kernel(const DevObjective o, const BoundArgs a, int
 
 // Scratch width the bound kernel needs: the widest layer and the per-row scratch (op values by column).
 int bound_width(const DevObjective& o) {
-  int w = o.S > o.ks ? o.S : o.ks;
+  int w = o.bw;  // compile(): max(widest layer, ks, end of the last op column) -- what Smem<MW> is indexed by
   for (int l = 0; l <= o.L; ++l) w = o.widths[l] > w ? o.widths[l] : w;
   return w;
 }

@@ -44,6 +44,7 @@ struct DevObjective {
   int wd[kMaxLayers], bd[kMaxLayers];
   // per-row scratch layout in the activation buffer
   int S;          // row stride (floats) of the activation buffer
+  int bw;         // bound-kernel scratch width: max(widest layer, ks, end of the last op column)
   int ucol, pcol; // columns holding u_t and p_t during the cost program
   int n_ops;
   DevOp ops[kMaxOps];
@@ -196,6 +197,9 @@ struct SearchArgs {
   const float* gd_ratios;        // [gd_n_ratios], assigned round-robin over the starts
   int gd_n_ratios;
   const float* grad;             // [n][rows][d]
+  // search_update sort keys in global memory ([n][P] 12-byte keys) when P keys do not fit the
+  // opt-in shared memory (large samples_per_iter + top_capacity); null = shared memory
+  void* sort_keys;
 };
 
 // Order-preserving float <-> int encoding for atomicMin/atomicMax extrema.

@@ -70,6 +70,7 @@ cudaError_t launch_gradient(const DevObjective& o, const float* actions, float* 
                             cudaStream_t st);
 cudaError_t launch_synthetic_gradient(const float* actions, float* grad, long long n, cudaStream_t st);
 size_t search_update_smem(const SearchArgs& a);
+size_t search_sort_key_bytes(const SearchArgs& a);
 cudaError_t launch_pool_split(const PoolArgs& P, const SplitTask* tasks, int n_tasks, const StageArgs& S,
                               unsigned char* pack, double min_width, int* axis_out, cudaStream_t st);
 cudaError_t launch_pool_unpack(const PoolArgs& P, const StageArgs& S, const unsigned char* recv, const int* dst,
@@ -551,6 +552,8 @@ Compiled compile(const bp_objective_desc& d) {
   }
   if (!any_term) fail(BP_INVALID_ARGUMENT, "objective: cost program has no terms");
   o.S = r8(std::max({maxK4, r4(maxw), col})) + 4;
+  o.bw = std::max({maxw, col, d.ks});
+  if (o.bw > 1024) fail(BP_UNSUPPORTED, "objective: cost scratch wider than 1024 columns");
 
   // stop set (objective.cpp:45-63)
   std::vector<int> xstop(static_cast<size_t>(d.horizon), 0);
@@ -780,6 +783,8 @@ struct bp_ctx {
   // routed top samples of the iteration's children (pool.cu), by local index
   DBuf<float> st_val, st_act;
   DBuf<int> st_n;
+  DBuf<unsigned char> sort_keys;  // search_update keys in global memory (large batches)
+  int smem_optin = 0;             // cudaDevAttrMaxSharedMemoryPerBlockOptin
   // slab chunks (pool.cu) kept between plans, for pools of this geometry
   int slab_d = 0, slab_K = 0;
   std::vector<unsigned char*> slab_spare;
@@ -787,6 +792,7 @@ struct bp_ctx {
   // per step), so the ramp-up iterations do not reallocate them
   int reserve_boxes = 0;
   std::vector<int> h_failed;
+  int64_t boxes_searched = 0, boxes_failed = 0;  // bp_search_counters
   std::vector<Report> reports;
   // sharding: rank / world and the allgather hook (host buffers)
   int rank = 0, world = 1;
@@ -991,6 +997,15 @@ bp::SearchArgs search_setup(bp_ctx* c, int n, const bp_search_config& cfg, const
   a.top_act[0] = c->top_act0.get(tk * d);
   a.top_act[1] = c->top_act1.get(tk * d);
   a.top_cnt = c->top_cnt.get(nb);
+  // search_update sorts top_capacity + rows keys per box: in shared memory when they fit the opt-in
+  // limit, else in a global scratch (no limit on samples_per_iter, like the reference's heap)
+  a.sort_keys = nullptr;
+  static const bool force_global = std::getenv("BP_SEARCH_SORT_GLOBAL") != nullptr;  // test aid
+  if (force_global || bp::search_update_smem(a) > static_cast<size_t>(c->smem_optin)) {
+    a.sort_keys = c->sort_keys.get(nb * bp::search_sort_key_bytes(a));
+    if (bp::search_update_smem(a) > static_cast<size_t>(c->smem_optin))
+      fail(BP_UNSUPPORTED, "search: agents x elites too large for the refit's shared memory");
+  }
   return a;
 }
 
@@ -1066,6 +1081,8 @@ void search_run(bp_ctx* c, bp::SearchArgs& a, const bp_search_config& cfg) {
   c->last = a;
   c->h_failed.assign(static_cast<size_t>(n), 0);
   ck(memcpy_counted(c->h_failed.data(), a.failed, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  c->boxes_searched += n;  // pageable D2H: the flags are on the host now
+  for (int i = 0; i < n; ++i) c->boxes_failed += c->h_failed[static_cast<size_t>(i)] != 0;
 }
 
 void search_harvest(bp_ctx* c, const bp::SearchArgs& a, const bp_search_config& cfg, std::vector<Report>* out) {
@@ -1360,6 +1377,12 @@ struct DevPool {
       if (ctx != nullptr) ctx->slab_spare.push_back(p);
       else cudaFree(p);
     }
+    // keep at most two spare chunks for the next plan: one large plan must not pin its peak pool
+    // footprint for the context's lifetime
+    while (ctx != nullptr && ctx->slab_spare.size() > 2) {
+      cudaFree(ctx->slab_spare.back());
+      ctx->slab_spare.pop_back();
+    }
   }
   bp::PoolArgs args() const { return {d, K, shift, table.p, o_lo, o_hi, o_best, o_val, o_act, o_n, o_has}; }
   bp::PoolArgs host_args() const { return {d, K, shift, chunks.data(), o_lo, o_hi, o_best, o_val, o_act, o_n, o_has}; }
@@ -1369,7 +1392,11 @@ struct DevPool {
     if (ctx != nullptr && ctx->slab_d == d && ctx->slab_K == K && !ctx->slab_spare.empty()) {
       p = ctx->slab_spare.back();
       ctx->slab_spare.pop_back();
-    } else {
+    } else if (cudaMalloc(&p, chunk_bytes) != cudaSuccess) {
+      cudaGetLastError();  // out of memory: release the cached spares of another geometry and retry once
+      if (ctx != nullptr)
+        for (unsigned char* q : ctx->slab_spare) cudaFree(q);
+      if (ctx != nullptr) ctx->slab_spare.clear();
       ck(cudaMalloc(&p, chunk_bytes), "cudaMalloc (subdomain pool chunk)");
     }
     chunks.push_back(p);
@@ -1453,6 +1480,46 @@ struct Planner {
   HBuf<double> h_maxw;
   HBuf<unsigned char> h_pack;
 
+  // Rank-local failures (a root search that failed on rank 0, a split on a parent's owner, a CUDA error in
+  // one rank's search) are held until the next collective, which carries a status word, so every rank
+  // raises the same error together instead of leaving its peers blocked in an all-gather / all-to-all.
+  bp_status err_code = BP_OK;
+  std::string err_msg;
+  template <typename F>
+  void local(F&& f) {
+    if (err_code != BP_OK) return;
+    try {
+      f();
+    } catch (const Failure& e) {
+      err_code = e.code;
+      err_msg = e.what();
+    } catch (const std::exception& e) {
+      err_code = BP_RUNTIME;
+      err_msg = e.what();
+    }
+  }
+  // status[r] = rank r's err_code (one entry for a single-source exchange: rank 0's)
+  void raise_agreed(const std::vector<double>& status) {
+    for (size_t r = 0; r < status.size(); ++r) {
+      const int code = static_cast<int>(status[r]);
+      if (code == BP_OK) continue;
+      if (static_cast<int>(r) == rank() && err_code != BP_OK) fail(err_code, err_msg);
+      fail(static_cast<bp_status>(code), "plan: rank " + std::to_string(r) + " failed (its error is reported there)");
+    }
+    if (err_code != BP_OK) fail(err_code, err_msg);
+  }
+  void agree_status() {  // a dedicated status all-gather (one word per rank); no collective with one rank
+    const int W = world();
+    if (W == 1) {
+      if (err_code != BP_OK) fail(err_code, err_msg);
+      return;
+    }
+    double mine = static_cast<double>(err_code);
+    std::vector<double> all(static_cast<size_t>(W));
+    if (c->exchange(c->exchange_user, &mine, sizeof(double), all.data()) != 0)
+      fail(BP_NCCL, "exchange: status all-gather failed");
+    raise_agreed(all);
+  }
   int world() const { return c->world > 1 && c->exchange != nullptr ? c->world : 1; }
   int rank() const { return world() > 1 ? c->rank : 0; }
   // BP_STEP_PROFILE: host wall time per phase of step(), printed per iteration (dev aid)
@@ -1572,9 +1639,10 @@ struct Planner {
     const int W = world();
     // at most 2 * batch children per step, ceil(2 * batch / W) of them on this rank
     c->reserve_boxes = std::max(c->reserve_boxes, (2 * cfg.batch + W - 1) / W);
-    std::vector<double> h(static_cast<size_t>(kHeadWords + 2 + d), 0.0);  // the root's head + incumbent
+    // the root's head + incumbent + status word (last)
+    std::vector<double> h(static_cast<size_t>(kHeadWords + 2 + d + 1), 0.0);
     int root_slot = -1;
-    if (rank() == 0) {  // the root is child 0 of the root search: rank 0 searches and owns it
+    if (rank() == 0) local([&] {  // the root is child 0 of the root search: rank 0 searches and owns it
       std::vector<double> lo(static_cast<size_t>(d)), hi(static_cast<size_t>(d));
       for (int t = 0; t < c->comp.o.H; ++t)
         for (int j = 0; j < c->comp.o.ka; ++j) {
@@ -1609,16 +1677,18 @@ struct Planner {
         const std::vector<double> b = fetch_best(root_slot);
         std::copy(b.begin(), b.end(), h.begin() + kHeadWords + 2);
       }
-    }
-    if (W > 1) {  // the root's head from rank 0 to every rank
+    });
+    h.back() = static_cast<double>(err_code);
+    if (W > 1) {  // the root's head (and rank 0's status) from rank 0 to every rank
       std::vector<double> recv(h.size() * static_cast<size_t>(W));
       if (c->exchange(c->exchange_user, h.data(), h.size() * sizeof(double), recv.data()) != 0)
         fail(BP_NCCL, "exchange: allgather of the root head failed");
       std::copy(recv.begin(), recv.begin() + static_cast<std::ptrdiff_t>(h.size()), h.begin());  // rank 0's
     }
+    raise_agreed({h.back()});
     pool.push_back(Head{0, h[2], h[3], 0.0, h[5], 0, 0, static_cast<int64_t>(h[6]), root_slot});
     result.uf = h[3];
-    result.best.assign(h.begin() + kHeadWords + 2, h.end());
+    result.best.assign(h.begin() + kHeadWords + 2, h.end() - 1);
     result.samples = static_cast<int64_t>(h[6]);
     children_bounded = 1;
     last_children = 1;
@@ -1683,9 +1753,11 @@ struct Planner {
         keys.push_back(k);
       }
     const int n_loc = static_cast<int>(keys.size());
-    std::vector<int> slots(static_cast<size_t>(n_loc));
-    for (int& s : slots) s = slab.alloc(st);
-    S = stage_buffers(c, n_loc, K);
+    std::vector<int> slots(static_cast<size_t>(n_loc), -1);
+    local([&] {
+      for (int& s : slots) s = slab.alloc(st);
+      S = stage_buffers(c, n_loc, K);
+    });
     // split this rank's parents (one CTA each); shipped children packed by destination rank
     std::vector<std::vector<int64_t>> out_k(static_cast<size_t>(W));
     for (int i = 0; i < static_cast<int>(to_split.size()); ++i)
@@ -1719,6 +1791,7 @@ struct Planner {
       tasks.push_back(t);
     }
     const size_t rb = bp::pool_record_bytes(d, K);
+    local([&] {
     unsigned char* dpack = n_pack > 0 ? d_pack.get(static_cast<size_t>(n_pack) * rb) : nullptr;
     if (!tasks.empty()) {
       const size_t tb = std::max<size_t>(tasks.size(), static_cast<size_t>(cfg.batch));
@@ -1734,14 +1807,17 @@ struct Planner {
       for (size_t q = 0; q < tasks.size(); ++q)
         if (ha[q] < 0) fail(BP_INVALID_ARGUMENT, "split: no axis above the width floor");
     }
+    });
     phase("split");
+    agree_status();  // a split failure on a parent's owner raises on every rank before the all-to-all
     for (const Head& p : to_split)  // the parents' payload has been read by the split
       if (p.owner == R) slab.release(p.slot);
     if (W > 1 && n_all > 0) ship_children(to_split, n_pack, li_of, slots);
     if (n_all > 0) {
-      Out o = search_bound_merge(keys, slots, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1));
+      Out o;
+      local([&] { o = search_bound_merge(keys, slots, mix_seed(cfg.seed, static_cast<uint64_t>(iter) + 1)); });
       phase("merge+bound");
-      gather_children(to_split, base_id, keys, slots, o);
+      gather_children(to_split, base_id, keys, slots, o);  // carries this rank's status
       phase("gather");
     }
     pruned_cum += prune();
@@ -1769,14 +1845,22 @@ struct Planner {
     size_t r_total = 0;
     for (int r = 0; r < W; ++r) r_total += static_cast<size_t>(rbts[static_cast<size_t>(r)]);
     unsigned char* send = h_pack.get(std::max<size_t>(static_cast<size_t>(n_pack) * rb, 1));
-    if (n_pack > 0) {
-      ck(memcpy_counted(send, d_pack.p, static_cast<size_t>(n_pack) * rb, cudaMemcpyDeviceToHost, st), "D2H");
-      ck(cudaStreamSynchronize(st), "sync");
-    }
+    local([&] {  // a failure here is carried to the heads all-gather; the all-to-all still runs
+      if (n_pack > 0) {
+        ck(memcpy_counted(send, d_pack.p, static_cast<size_t>(n_pack) * rb, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+      }
+    });
     std::vector<unsigned char> recv(std::max<size_t>(r_total, 1));
     if (c->alltoallv == nullptr) fail(BP_NCCL, "exchange: no all-to-all hook for the sharded pool");
     if (c->alltoallv(c->exchange_user, send, sb.data(), recv.data(), rbts.data()) != 0)
       fail(BP_NCCL, "exchange: all-to-all of child records failed");
+    local([&] { unpack_children(recv, r_total, li_of, slots); });
+  }
+  void unpack_children(const std::vector<unsigned char>& recv, size_t r_total, const std::vector<int>& li_of,
+                       const std::vector<int>& slots) {
+    cudaStream_t st = c->stream;
+    const size_t rb = bp::pool_record_bytes(d, K);
     const int n_in = static_cast<int>(r_total / rb);
     if (n_in == 0) return;
     std::vector<int> dst(static_cast<size_t>(n_in)), slot(static_cast<size_t>(n_in));
@@ -1808,12 +1892,14 @@ struct Planner {
     const int n_all = 2 * static_cast<int>(to_split.size());
     const int n_loc = static_cast<int>(keys.size());
     int cand = -1;  // this rank's lowest child (first in global order on ties)
-    for (int i = 0; i < n_loc; ++i)
+    for (int i = 0; err_code == BP_OK && i < n_loc; ++i)
       if (std::isfinite(o.uf[static_cast<size_t>(i)]) && (cand < 0 || o.uf[static_cast<size_t>(i)] < o.uf[static_cast<size_t>(cand)]))
         cand = i;
     const int per_rank = (n_all + W - 1) / W;
-    const size_t words = static_cast<size_t>(per_rank) * kHeadWords + 2 + static_cast<size_t>(d);
+    const size_t words = static_cast<size_t>(per_rank) * kHeadWords + 2 + static_cast<size_t>(d) + 1;  // + status
     std::vector<double> send(words, -1.0);
+    send.back() = static_cast<double>(err_code);
+    if (err_code == BP_OK) {
     for (int i = 0; i < n_loc; ++i) {
       double* h = send.data() + static_cast<size_t>(i) * kHeadWords;
       const Head& p = to_split[static_cast<size_t>(keys[static_cast<size_t>(i)] / 2)];
@@ -1829,9 +1915,11 @@ struct Planner {
     double* cd = send.data() + static_cast<size_t>(per_rank) * kHeadWords;
     cd[0] = cand >= 0 ? o.uf[static_cast<size_t>(cand)] : INFINITY;
     cd[1] = cand >= 0 ? static_cast<double>(keys[static_cast<size_t>(cand)]) : -1.0;
-    if (cand >= 0) {
+    if (cand >= 0) local([&] {
       const std::vector<double> b = fetch_best(slots[static_cast<size_t>(cand)]);
       std::copy(b.begin(), b.end(), cd + 2);
+    });
+    send.back() = static_cast<double>(err_code);
     }
     std::vector<double> recv;
     if (W == 1) {
@@ -1840,6 +1928,11 @@ struct Planner {
       recv.resize(words * static_cast<size_t>(W));
       if (c->exchange(c->exchange_user, send.data(), words * sizeof(double), recv.data()) != 0)
         fail(BP_NCCL, "exchange: allgather of child heads failed");
+    }
+    {
+      std::vector<double> status(static_cast<size_t>(W));
+      for (int r = 0; r < W; ++r) status[static_cast<size_t>(r)] = recv[static_cast<size_t>(r + 1) * words - 1];
+      raise_agreed(status);
     }
     std::vector<const double*> by_k(static_cast<size_t>(n_all), nullptr);
     const double* best_cd = nullptr;
@@ -1955,6 +2048,7 @@ bp_status bp_init(int device, bp_ctx** out) {
     ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major < 10) fail(BP_CUDA, "bp_init: device is not sm_100 class (B200 required)");
     c->sms = prop.multiProcessorCount;
+    c->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
     if (const char* env = std::getenv("BP_ROLLOUT")) {
       const std::string e(env);
       c->path_mode = e == "simt" ? 1 : e == "tc1" ? 2 : e == "tc2" ? 3 : 0;
@@ -2133,6 +2227,58 @@ bp_status bp_batch_search(bp_ctx* ctx, int n_boxes, const double* lo, const doub
     if (n_boxes <= 0) fail(BP_INVALID_ARGUMENT, "bp_batch_search: no boxes");
     device_batch_search(ctx, n_boxes, lo, hi, warm, *cfg, &ctx->reports);
     ctx->harvest_roll_events();
+  });
+}
+
+bp_status bp_search_update(bp_ctx* ctx, int n, const bp_search_config* cfg, const double* lo, const double* hi,
+                           int iter, const float* rows, const float* costs, float* mu, float* var, float* uf,
+                           float* best, int* top_n, float* top_val, int* top_seq, float* top_act) {
+  return guard([&] {
+    check_loaded(ctx);
+    ctx->use();
+    if (cfg == nullptr || n <= 0 || lo == nullptr || hi == nullptr || rows == nullptr || costs == nullptr || mu == nullptr ||
+        uf == nullptr || best == nullptr || top_n == nullptr || top_val == nullptr || top_seq == nullptr || top_act == nullptr)
+      fail(BP_INVALID_ARGUMENT, "search_update: null argument");
+    if (cfg->method == BP_SEARCH_GD) fail(BP_INVALID_ARGUMENT, "search_update: CEM or MPPI only");
+    if (cfg->method == BP_SEARCH_CEM && var == nullptr) fail(BP_INVALID_ARGUMENT, "search_update: CEM needs var");
+    bp_ctx* c = ctx;
+    place_host_boxes(c, n, lo, hi, nullptr);
+    bp::SearchArgs a = search_setup(c, n, *cfg, nullptr, false);
+    cudaStream_t st = c->stream;
+    ck(bp::launch_search_init(a, st), "search init");  // var floor (and placeholders overwritten below)
+    const int d = a.d, R = a.rows, G = a.groups, K = a.top_cap;
+    const size_t nd = static_cast<size_t>(n) * d, ng = nd * G, nk = static_cast<size_t>(n) * K;
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) ck(memcpy_counted(dst, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    };
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) ck(memcpy_counted(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    };
+    for (int i = 0; i < n; ++i)
+      if (top_n[i] < 0 || top_n[i] > K) fail(BP_INVALID_ARGUMENT, "search_update: top_n outside [0, top_capacity]");
+    h2d(a.mu, mu, ng * 4);
+    if (a.method == 0) h2d(a.var, var, ng * 4);
+    h2d(a.uf, uf, static_cast<size_t>(n) * 4);
+    h2d(a.best, best, nd * 4);
+    h2d(a.top_cnt, top_n, static_cast<size_t>(n) * 4);
+    h2d(a.top_val[0], top_val, nk * 4);
+    h2d(const_cast<int*>(a.top_seq[0]), top_seq, nk * 4);
+    h2d(a.top_act[0], top_act, nk * d * 4);
+    h2d(a.actions, rows, static_cast<size_t>(n) * R * d * 4);
+    h2d(const_cast<float*>(a.costs), costs, static_cast<size_t>(n) * R * 4);
+    a.iter = iter;
+    a.cur = 0;
+    ck(bp::launch_search_update(a, st), "search update");
+    c->launches += 2;
+    d2h(mu, a.mu, ng * 4);
+    if (a.method == 0) d2h(var, a.var, ng * 4);
+    d2h(uf, a.uf, static_cast<size_t>(n) * 4);
+    d2h(best, a.best, nd * 4);
+    d2h(top_n, a.top_cnt, static_cast<size_t>(n) * 4);
+    d2h(top_val, a.top_val[1], nk * 4);
+    d2h(top_seq, a.top_seq[1], nk * 4);
+    d2h(top_act, a.top_act[1], nk * d * 4);
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 
@@ -2333,6 +2479,15 @@ bp_status bp_result_trace(const bp_result* r, bp_trace_row* rows, int cap) {
 bp_status bp_result_free(bp_result* r) {
   delete r;
   return BP_OK;
+}
+
+bp_status bp_search_counters(bp_ctx* ctx, int64_t* boxes, int64_t* failed) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (boxes) *boxes = ctx->boxes_searched;
+    if (failed) *failed = ctx->boxes_failed;
+    ctx->boxes_searched = ctx->boxes_failed = 0;
+  });
 }
 
 bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms, double* search_ms,

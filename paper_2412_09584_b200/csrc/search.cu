@@ -140,8 +140,10 @@ __device__ __forceinline__ bool key_less(const Key& x, const Key& y) {
 // Per-box update after a rollout: incumbent, top-K merge, distribution refit.
 __global__ void __launch_bounds__(kThreads) search_update_kernel(const SearchArgs a, int P) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  Key* keys = reinterpret_cast<Key*>(smraw);                 // [P]
-  int* elite = reinterpret_cast<int*>(keys + P);             // [groups][elites]
+  const bool gkeys = a.sort_keys != nullptr;  // P keys above the shared-memory limit: sort in global memory
+  Key* keys = gkeys ? reinterpret_cast<Key*>(a.sort_keys) + static_cast<size_t>(blockIdx.x) * P
+                    : reinterpret_cast<Key*>(smraw);                      // [P]
+  int* elite = reinterpret_cast<int*>(gkeys ? smraw : smraw + static_cast<size_t>(P) * sizeof(Key));  // [groups][elites]
   __shared__ int s_nel[32];
   __shared__ float s_red_v[kThreads / 32];
   __shared__ int s_red_i[kThreads / 32];
@@ -355,9 +357,15 @@ int search_sort_size(int top_cap, int rows) {
   return P;
 }
 
+// Dynamic shared memory of search_update_kernel: the P sort keys (unless they are in global memory,
+// a.sort_keys) and the elite rows.
 size_t search_update_smem(const SearchArgs& a) {
   const int P = search_sort_size(a.top_cap, a.rows);
-  return static_cast<size_t>(P) * sizeof(Key) + static_cast<size_t>(a.groups) * a.elites * sizeof(int) + 16;
+  return (a.sort_keys != nullptr ? 0 : static_cast<size_t>(P) * sizeof(Key)) +
+         static_cast<size_t>(a.groups) * a.elites * sizeof(int) + 16;
+}
+size_t search_sort_key_bytes(const SearchArgs& a) {
+  return static_cast<size_t>(search_sort_size(a.top_cap, a.rows)) * sizeof(Key);
 }
 
 cudaError_t launch_search_update(const SearchArgs& a, cudaStream_t st) {

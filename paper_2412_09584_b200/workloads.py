@@ -11,42 +11,95 @@ SURVEY.md Appendix A.  `glorot=True` swaps in generate_model-style weights
 from __future__ import annotations
 
 import copy
-import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
 
-from . import _capi, config as _config
+from . import config as _config
 from ._capi import (BP_FEATURE_ABSOLUTE, BP_OP_LINEAR, BP_OP_RELU, BP_OP_SCALAR_AFFINE, BP_OP_SLICE,
                     BP_OP_SQDIST, BP_STOP_CUSTOM, BP_STOP_LAST_RELU)
 from .objective import ObjectiveSpec, Op, P, U, X, op_id
 
 
 class Rng:
-    """The reference Rng stream (rng.hpp:12-35) through the library's bp_rng."""
+    """The reference Rng stream (rng.hpp:12-35, rng.cpp:20-35) on the host, in Python.
+
+    std::mt19937_64 (the C++ standard's parameters; the twist is vectorised with numpy
+    uint64 arithmetic), uniform = (bits >> 11) * 2^-53, Box-Muller with a cached spare
+    using the C library's log / sqrt / sin / cos (Python's math module) so every draw is
+    the reference's bit for bit.  Fixture generation needs no GPU library: the bench's
+    reference arm builds its fixtures through this class without loading the CUDA .so.
+    """
+
+    _N, _M = 312, 156
+    _A = np.uint64(0xB5026F5AA96619E9)
+    _UM, _LM = np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
 
     def __init__(self, seed: int):
-        self.lib = _capi.load()
-        self.h = C.c_void_p()
-        _capi.check(self.lib.bp_rng_new(seed & (2**64 - 1), C.byref(self.h)))
+        mt = [seed & 0xFFFFFFFFFFFFFFFF]
+        for i in range(1, self._N):
+            prev = mt[-1]
+            mt.append((6364136223846793005 * (prev ^ (prev >> 62)) + i) & 0xFFFFFFFFFFFFFFFF)
+        self.mt = np.array(mt, dtype=np.uint64)
+        self.out = np.zeros(0, dtype=np.uint64)
+        self.pos = 0
+        self.spare = None
 
-    def __del__(self):
-        try:
-            self.lib.bp_rng_free(self.h)
-        except Exception:
-            pass
+    def _twist(self):
+        mt, N, M = self.mt, self._N, self._M
+        one = np.uint64(1)
 
-    def _fill(self, kind, n):
-        out = np.zeros(int(n))
-        if n:
-            _capi.check(self.lib.bp_rng_fill(self.h, kind, int(n), _capi.dptr(out)))
-        return out
+        def step(i0, i1, nxt, far):  # mt[i] = mt[i+M] ^ (y >> 1) ^ (y & 1) * A, y = hi(mt[i]) | lo(mt[i+1])
+            y = (mt[i0:i1] & self._UM) | (nxt & self._LM)
+            mt[i0:i1] = far ^ (y >> one) ^ ((y & one) * self._A)
+
+        step(0, N - M, mt[1:N - M + 1].copy(), mt[M:N].copy())      # mt[i + M]: not yet updated
+        step(N - M, N - 1, mt[N - M + 1:N].copy(), mt[0:M - 1].copy())  # mt[i + M - N]: updated above
+        step(N - 1, N, mt[0:1].copy(), mt[M - 1:M].copy())
+        y = mt.copy()
+        y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        y ^= y >> np.uint64(43)
+        self.out = y
+        self.pos = 0
+
+    def bits(self, n: int) -> np.ndarray:
+        parts = []
+        while n > 0:
+            if self.pos == self._N:
+                self._twist()
+            if self.out.size == 0:
+                self._twist()
+            take = min(n, self._N - self.pos)
+            parts.append(self.out[self.pos:self.pos + take])
+            self.pos += take
+            n -= take
+        return np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint64)
+
+    def _uniform01(self, n: int) -> np.ndarray:
+        return (self.bits(n) >> np.uint64(11)).astype(np.float64) * 2.0**-53
 
     def uniform(self, n, lo=0.0, hi=1.0):
-        return lo + (hi - lo) * self._fill(0, n)
+        return lo + (hi - lo) * self._uniform01(int(n))
 
     def normal(self, n):
-        return self._fill(1, n)
+        import math
+
+        out = np.empty(int(n))
+        for i in range(int(n)):
+            if self.spare is not None:
+                out[i], self.spare = self.spare, None
+                continue
+            u1 = self._uniform01(1)[0]
+            while u1 <= 0.0:
+                u1 = self._uniform01(1)[0]
+            u2 = self._uniform01(1)[0]
+            r = math.sqrt(-2.0 * math.log(u1))
+            a = 6.283185307179586476925286766559 * u2
+            self.spare = r * math.sin(a)
+            out[i] = r * math.cos(a)
+        return out
 
 
 def f32(a):

@@ -68,7 +68,49 @@ def test_ranks_reproduce_single_process_plan(world):
     for p in ps:
         p.join(timeout=60)
     for rank, obj, act, uf, mlf, pool, samples, calls in res:
-        assert calls == 1 + 2 * 5  # root head; per iteration one all-to-all and one allgather
+        assert calls == 1 + 3 * 5  # root head; per iteration a status word, one all-to-all and one allgather
         assert obj == single["objective"] and np.array_equal(act, single["action"])
         assert uf == single["trace"]["uf"] and mlf == single["trace"]["min_lf"]
         assert pool == single["trace"]["pool_size"] and samples == single["samples"]
+
+
+def _fail_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2412_09584_b200 as bp
+        from paper_2412_09584_b200 import objective as objmod
+        from paper_2412_09584_b200 import parallel
+
+        wl, cfg = _cfg()
+        spec = wl.spec
+        big = objmod.ObjectiveSpec(**{**spec.__dict__, "W": [spec.W[0] * 1e30] + list(spec.W[1:])})
+        dev = bp.Device(0).load(big)
+        parallel.attach(dev)
+        try:
+            dev.plan(cfg)
+            q.put((rank, "no error"))
+        except RuntimeError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_rank_local_failure_raises_on_every_rank():
+    """A failure on one rank (the root search on rank 0 overflows) reaches every rank through the
+    status word of the next collective: all ranks raise, none is left blocked in the exchange."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_fail_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=250) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert "root search failed" in res[0]
+    assert "rank 0 failed" in res[1]

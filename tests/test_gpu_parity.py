@@ -229,7 +229,7 @@ def test_interval_bound_matches_oracle(device, name):
     assert abs(lf[0] - ref) <= 1e-9 * max(1.0, abs(ref))
 
 
-@pytest.mark.parametrize("width", [100, 200, 300, 500])
+@pytest.mark.parametrize("width", [100, 128, 200, 256, 300, 500, 512, 1000])
 def test_bound_width_classes_match_oracle(device, width):
     """The bound kernel is instantiated per width class (128 / 256 / 512 scratch doubles
     for the widest layer or cost-scratch row); objectives in each class bound like the
@@ -267,6 +267,23 @@ def test_search_properties(device):
     # the device values of the kept samples are the oracle's objective at those points
     ref = ob.evaluate(a.astype(np.float32).astype(np.float64))
     assert rel_err(v, ref) < rtol_for(dev)
+
+
+def test_search_large_batch_sorts_in_global_memory(device):
+    """samples_per_iter + top_capacity above the shared-memory sort (P = 32768 keys, 384 KB):
+    search_update sorts in a global scratch instead of failing; the kept list is the oracle's
+    objective at the kept points, ascending, and the incumbent is its head."""
+    spec = small_spec("c1")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    cfg = from_json('{"search": {"samples_per_iter": 20000, "iterations": 2, "top_capacity": 512}}')
+    rep = dev.batch_search(np.stack([lo, lo]), np.stack([hi, hi]), None, cfg, seed=5)
+    ob = orc.Objective(spec)
+    for b in range(2):
+        assert rep["ok"][b] and rep["samples"][b] == 2 * 20001
+        v, a = dev.report_top(b, rep["n_top"][b])
+        assert len(v) == 512 and v[0] == rep["uf"][b] and np.all(np.diff(v) >= 0)
+        assert rel_err(v, ob.evaluate(a.astype(np.float32).astype(np.float64))) < rtol_for(dev)
 
 
 def test_search_is_seeded_per_box(device):

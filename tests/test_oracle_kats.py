@@ -423,3 +423,33 @@ def test_graph_objective_plan_properties():  # test_bab.cpp:274-295
     cfg["bound_mode"] = "full-crown"
     sound = obj.plan(cfg)
     assert sound["certified"] and sound["lower_bound"] <= sound["objective"] + 1e-9
+
+
+def test_search_injection_hooks_restate_the_sink_and_refit():
+    """The oracle's injection hooks (used by the device sampler-update parity tests) leave run_cem's
+    own logic in charge: after each iteration uf / best are the first minimum so far, the top list is
+    the K smallest values consumed, and agent g's mean is the mean of its n_el best rows in (value,
+    row) order (search.cpp:41-74, 131-149)."""
+    from paper_2412_09584_b200.config import from_json
+
+    cfg = from_json('{"search": {"samples_per_iter": 24, "top_capacity": 10, "cem": {"agents": 3, "elites": 4}}}')
+    d, T = 5, 3
+    rng = np.random.default_rng(1)
+    lo, hi = -np.ones(d), np.ones(d)
+    rows = rng.uniform(lo, hi, size=(T, 24, d))
+    costs = np.round(rng.normal(size=(T, 25)) * 4) / 8
+    ref = orc.search_injected(lo, hi, None, cfg, rows, costs)
+    seen = []
+    for t in range(T):
+        b = ref[t]["batch"]
+        assert np.array_equal(b[:24], rows[t])
+        seen += list(costs[t])
+        assert ref[t]["uf"] == min(seen)
+        assert np.array_equal(ref[t]["top_val"][:ref[t]["top_n"]], np.sort(seen)[:10])
+        for g in range(3):
+            idx = list(range(8 * g, 8 * g + 8)) + ([24] if g == 0 else [])
+            el = sorted(idx, key=lambda i: (costs[t][i], i))[:4]
+            m = np.zeros(d)
+            for i in el:
+                m += b[i]
+            assert np.array_equal(ref[t]["mu"][g], m / 4)
