@@ -92,7 +92,7 @@ class PoolMeta(C.Structure):
 EXPORTS = [
     "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_alltoall", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds", "bp_gradient",
     "bp_load_objective", "bp_load_synthetic",
-    "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_report_summary", "bp_report_top",
+    "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_search_update", "bp_search_counters", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
     "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
     "bp_result_trace", "bp_result_free", "bp_timing", "bp_rng_new", "bp_rng_free",

@@ -174,3 +174,27 @@ def test_pick_out_bit_exact_on_large_pools():
         meta = [(float(lf[i]), float(uf[i]), i, -0.1 * i) for i in range(n_pool)]
         for n, eta, T in ((256, 0.75, 0.05), (120, 0.0, 5.0), (64, 0.0, 1e-4)):
             assert product_pick(meta, n, eta, T, 7 + trial) == orc.pick_out(meta, n, eta, T, orc.Rng(7 + trial))
+
+
+def test_workloads_rng_is_the_reference_stream_without_the_cuda_library():
+    """workloads.Rng (pure Python mt19937_64 + Box-Muller) draws the reference Rng stream bit for
+    bit (rng.hpp:12-35, rng.cpp:20-35; std::mt19937_64 10000th-output KAT), so the bench's
+    reference arm builds its fixtures without loading libbabplan_cuda.so."""
+    import subprocess
+    import sys
+
+    from paper_2412_09584_b200 import workloads
+
+    assert workloads.Rng(5489).bits(10000)[-1] == np.uint64(9981545732273789042)
+    for seed in (0, 1, 2, 2**63 + 12345):
+        a, b = workloads.Rng(seed), orc.Rng(seed)
+        assert np.array_equal(a.bits(700), np.array([b.bits() for _ in range(700)], dtype=np.uint64))
+        assert np.array_equal(a.uniform(333, -1, 1), np.array([-1 + 2 * b.uniform() for _ in range(333)]))
+        assert np.array_equal(a.normal(501), np.array([b.normal() for _ in range(501)]))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2412_09584_b200 import workloads\n"
+            "from oracle import oracle as orc\n"
+            "w = workloads.c2(); orc.Objective(w.spec)\n"
+            "print('libbabplan_cuda' in open('/proc/self/maps').read())" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "False", r.stderr
