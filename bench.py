@@ -171,30 +171,36 @@ def run_reference(args, wl):
 
 def best_objective_vs_cpu():
     """Best objective of the device planner and the CPU reference planner (oracle) at equal BaB
-    iteration counts, same fixtures and planner seed (the samplers differ: Philox vs mt19937_64, so
-    this is a statistical comparison).  C1 at its full 20 iterations; C2 with batch 4 for 4
-    iterations (the CPU planner needs ~14 s per C2 child)."""
+    iteration counts, same fixtures, over several planner seeds (the samplers differ -- Philox
+    vs mt19937_64 -- so one seed is one draw; the comparison is the paired set).  C1 at its
+    full 20 iterations (6 seeds); C2 with batch 4 for 4 iterations (3 seeds; the CPU planner
+    needs ~14 s per C2 child)."""
     import paper_2412_09584_b200 as bp
     from oracle import oracle as orc
     from paper_2412_09584_b200 import workloads
 
     out = {}
-    for name, over, iters in (("c1", {}, None), ("c2", {"batch": 4}, 4)):
+    dev = bp.Device(int(os.environ.get("LOCAL_RANK", "0")))
+    for name, over, iters, seeds in (("c1", {}, None, (2, 3, 4, 5, 6, 7)), ("c2", {"batch": 4}, 4, (2, 3, 4))):
         wl = workloads.ALL[name]()
-        cfg = wl.planner_config(**over)
-        if iters is not None:
-            cfg["termination"]["max_iterations"] = iters
-        dev = bp.Device(int(os.environ.get("LOCAL_RANK", "0"))).load(wl.spec)
-        g = dev.plan(cfg)
-        dev.close()
+        dev.load(wl.spec)
+        ob = orc.Objective(wl.spec)
+        g, c = [], []
         t0 = time.perf_counter()
-        c = orc.Objective(wl.spec).plan(cfg)
+        for seed in seeds:
+            cfg = wl.planner_config(**over)
+            cfg["seed"] = seed
+            if iters is not None:
+                cfg["termination"]["max_iterations"] = iters
+            g.append(dev.plan(cfg)["objective"])
+            c.append(ob.plan(cfg)["objective"])
+        g, c = np.array(g), np.array(c)
         out[wl.name] = {"iterations": cfg["termination"]["max_iterations"], "batch": cfg["batch"],
-                        "gpu": g["objective"], "cpu": c["objective"],
-                        "gpu_le_cpu": bool(g["objective"] <= c["objective"]),
-                        "rel_gap": (g["objective"] - c["objective"]) / max(abs(c["objective"]), 1e-12),
-                        "gpu_lower_bound": g["lower_bound"], "cpu_lower_bound": c["lower_bound"],
-                        "cpu_s": time.perf_counter() - t0}
+                        "seeds": list(seeds), "gpu": g.tolist(), "cpu": c.tolist(),
+                        "gpu_le_cpu_seeds": int((g <= c).sum()),
+                        "median_rel_gap": float(np.median((g - c) / np.maximum(np.abs(c), 1e-12))),
+                        "gpu_best_le_cpu_best": bool(g.min() <= c.min()), "s": time.perf_counter() - t0}
+    dev.close()
     return out
 
 
@@ -390,7 +396,7 @@ def main():
                 n = max(8, orc.thread_count())
                 rate, times, cores, sample = cpu_children_per_s(args.config, wl, n, steps=1)
                 cpu = {"value": rate, "unit": "subdomains/s", "cores": cores, "kind": "port",
-                       "sample": sample + f" ({times[0]:.1f} s)"}
+                       "sample": sample + f" ({times[0]:.1f} s full-search equivalent per step)"}
             except Exception as e:  # the checker is optional on the box
                 cpu = {"value": None, "unit": "subdomains/s", "cores": None, "kind": "port", "sample": f"unavailable: {e}"}
         if not args.no_objective:

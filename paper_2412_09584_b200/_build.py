@@ -10,8 +10,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libbabplan_cuda.so")
-SOURCES = ["rollout.cu", "rollout_tc.cu", "rollout_tc2.cu", "bound.cu", "search.cu", "synthetic.cu", "gradient.cu", "pool.cu", "host.cu", "diag.cu"]
-HEADERS = ["bp_common.cuh", "rollout_common.cuh", "tc_common.cuh"]
+SOURCES = ["rollout.cu", "rollout_tc.cu", "rollout_tc2.cu", "rollout_tc3.cu", "bound.cu", "search.cu", "synthetic.cu", "gradient.cu", "pool.cu", "host.cu", "diag.cu"]
+HEADERS = ["bp_common.cuh", "rollout_common.cuh", "tc_common.cuh", "tc_epilogue.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

@@ -253,19 +253,19 @@ class Device:
         check(self.lib.bp_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
 
     def rollout_path(self, path: Optional[str] = None) -> str:
-        """Select ("auto" | "simt" | "tc1" | "tc2") and report ("tcgen05" | "simt") the rollout
-        kernel family; rollout_kernel() names the exact kernel."""
-        code = {None: -1, "auto": 0, "simt": 1, "tc1": 2, "tc2": 3}[path]
+        """Select ("auto" | "simt" | "tc1" | "tc2" | "tc3") and report ("tcgen05" | "simt") the
+        rollout kernel family; rollout_kernel() names the exact kernel."""
+        code = {None: -1, "auto": 0, "simt": 1, "tc1": 2, "tc2": 3, "tc3": 5}[path]
         active = C.c_int()
         check(self.lib.bp_set_rollout_path(self.h, code, C.byref(active)))
-        return "tcgen05" if active.value in (2, 3) else "simt"
+        return "tcgen05" if active.value in (2, 3, 5) else "simt"
 
     def rollout_kernel(self) -> str:
-        """The rollout kernel the loaded objective runs: "tc2" (tcgen05 v2, rollout_tc2.cu),
-        "tc1" (tcgen05 v1, rollout_tc.cu) or "simt" (FP32 FFMA, rollout.cu)."""
+        """The rollout kernel the loaded objective runs: "tc3" (tcgen05 v3, rollout_tc3.cu), "tc2"
+        (tcgen05 v2, rollout_tc2.cu), "tc1" (tcgen05 v1, rollout_tc.cu) or "simt" (FP32 FFMA, rollout.cu)."""
         active = C.c_int()
         check(self.lib.bp_set_rollout_path(self.h, -1, C.byref(active)))
-        return {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic"}[active.value]
+        return {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic", 5: "tc3"}[active.value]
 
     def rollout_info(self) -> dict:
         """Rollout kernel, 128-row tiles per CTA, rows per CTA and shared memory per CTA."""

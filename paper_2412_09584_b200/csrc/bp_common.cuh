@@ -65,6 +65,15 @@ struct DevObjective {
   // [kb][half][hi|lo][rows x 32] (half 0 = 128 rows); narrower layers are the v1 layout.
   int tc2, tc2_rw, tc2_ring;  // tc2_rw: TMEM region width (128 or 256 columns)
   int tc2_pair;               // width 256 as a CTA pair (cta_group::2): every layer 256 wide or <= 128 in 32s
+  // tcgen05 v3 (rollout_tc3.cu): three layers [K0 <= 32, N0 <= 512, N1 <= 512, N2 <= 32], relu after
+  // the hidden two; layer 1 in N chunks of <= 256 with layer 0 recomputed per chunk
+  int tc3;                   // eligible
+  int tc3_w[3];              // float arena: per layer the weight image (layer 0: [kb][hi|lo][32 x 32];
+                             // layer 1: [chunk][kb][hi|lo][cw x 32]; layer 2: [kb][hi|lo][np2 x 32])
+  int tc3_np[3];             // padded N of each layer (32, 32, 16 multiples)
+  int tc3_bias;              // float arena: b0 [np0] | b1 [np1] | b2 [np2]
+  int tc3_k0steps;           // k-steps of 8 of the features (layer-0 K)
+  int tc3_ring;              // weight ring bytes
   int sc_list, n_sc;
   int cost_f0, cost_f1;  // float arena range holding every cost-op constant (copied to smem by the tcgen05 kernel)  // int arena: n_sc pairs (scratch column, offset in the step record) of recorded scratch values
   // constants

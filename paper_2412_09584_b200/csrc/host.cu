@@ -57,6 +57,9 @@ cudaError_t launch_synthetic_eval(const float* actions, float* costs, int* faile
 cudaError_t launch_separable_bound(const double* lo, const double* hi, int n, int d, const double* crit, int ncrit,
                                    const int* use, double* lf, cudaStream_t st);
 size_t rollout_tc2_fixed_smem(const DevObjective& o);
+cudaError_t launch_rollout_tc3(const DevObjective& o, const RolloutArgs& a, cudaStream_t st);
+size_t rollout_tc3_fixed_smem(const DevObjective& o);
+size_t rollout_tc3_smem(const DevObjective& o);
 size_t rollout_tc2_smem(const DevObjective& o);
 int rollout_rows_per_tile(int nq);
 cudaError_t launch_bound(const DevObjective& o, const BoundArgs& a, int n, cudaStream_t st);
@@ -738,6 +741,55 @@ Compiled compile(const bp_objective_desc& d) {
         o.tc2 = 0;
       }
     }
+    // tcgen05 v3 (rollout_tc3.cu): [K0 <= 32, N0, N1 <= 512, N2 <= 32] with relu after the two
+    // hidden layers -- the 512-wide C5 shape, whose accumulators v1 / v2 cannot hold in TMEM
+    o.tc3 = 0;
+    if (!net && d.n_layers == 3 && d.widths[0] <= 32 && d.widths[1] <= 512 && d.widths[2] <= 512 && d.widths[3] <= 32 &&
+        d.relu_after[0] && d.relu_after[1] && !d.relu_after[2] && std::max(d.widths[1], d.widths[2]) > 256) {
+      const int np0 = (d.widths[1] + 31) & ~31, np1 = (d.widths[2] + 31) & ~31, np2 = std::max(16, r16(d.widths[3]));
+      o.tc3_np[0] = np0;
+      o.tc3_np[1] = np1;
+      o.tc3_np[2] = np2;
+      o.tc3_k0steps = (d.widths[0] + 7) / 8;
+      o.tc_S = std::max(col, d.ks) | 1;
+      // one K-block image of `rows` output rows x 32 K-columns of W (hi block then lo block), rows
+      // n0.., columns k0.., 128B-swizzled rows (as the v1 / v2 images)
+      auto block = [&](std::vector<double>& img, int l, int n0, int rows, int k0) {
+        const int K = d.widths[l], N = d.widths[l + 1];
+        const size_t base = img.size();
+        img.resize(base + static_cast<size_t>(2) * rows * 32, 0.0);
+        for (int n = 0; n < rows; ++n)
+          for (int cc = 0; cc < 32; ++cc) {
+            const int gn = n0 + n, k = k0 + cc;
+            const float w = (gn < N && k < K) ? static_cast<float>(d.W[l][static_cast<size_t>(gn) * K + k]) : 0.f;
+            const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
+            const size_t pos = static_cast<size_t>(n) * 32 + (((cc >> 2) ^ (n & 7)) << 2) + (cc & 3);
+            img[base + pos] = hi;
+            img[base + static_cast<size_t>(rows) * 32 + pos] = lo;
+          }
+      };
+      std::vector<double> i0, i1, i2;
+      for (int kb = 0; kb < np0 / 32; ++kb) block(i0, 0, 32 * kb, 32, 0);  // layer 0: N-block kb, K = features
+      for (int j = 0; j * 256 < np1; ++j)
+        for (int kb = 0; kb < np0 / 32; ++kb) block(i1, 1, 256 * j, std::min(256, np1 - 256 * j), 32 * kb);
+      for (int kb = 0; kb < np1 / 32; ++kb) block(i2, 2, 0, np2, 32 * kb);
+      o.tc3_w[0] = push_f(c.fa, i0.data(), i0.size());
+      o.tc3_w[1] = push_f(c.fa, i1.data(), i1.size());
+      o.tc3_w[2] = push_f(c.fa, i2.data(), i2.size());
+      std::vector<double> bb(static_cast<size_t>(np0 + np1 + np2), 0.0);
+      for (int n = 0; n < d.widths[1]; ++n) bb[static_cast<size_t>(n)] = d.b[0][n];
+      for (int n = 0; n < d.widths[2]; ++n) bb[static_cast<size_t>(np0 + n)] = d.b[1][n];
+      for (int n = 0; n < d.widths[3]; ++n) bb[static_cast<size_t>(np0 + np1 + n)] = d.b[2][n];
+      o.tc3_bias = push_f(c.fa, bb.data(), bb.size());
+      const size_t fixed = bp::rollout_tc3_fixed_smem(o);
+      const size_t min_ring = 3 * 256 * 128;  // a layer-1 K-block (hi + lo) and one more entry in flight
+      if (fixed + min_ring <= cap) {
+        o.tc3_ring = static_cast<int>((cap - fixed) & ~static_cast<size_t>(1023));
+        o.tc3 = 1;
+        if (std::getenv("BP_DEBUG_TC2"))
+          std::fprintf(stderr, "[tc3] fixed %zu B (S=%d), ring %d B\n", fixed, o.tc_S, o.tc3_ring);
+      }
+    }
   }
   return c;
 }
@@ -810,15 +862,16 @@ struct bp_ctx {
   double rollout_ms = 0, bound_ms = 0, search_ms = 0;
   int64_t rollout_launches = 0, launches = 0;
   bool timing = true;
-  int path_mode = 0;  // 0 auto, 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2 (BP_ROLLOUT or bp_set_rollout_path)
-  // rollout kernel for the loaded objective: 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2
+  int path_mode = 0;  // 0 auto, 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2, 5 tcgen05 v3 (BP_ROLLOUT or bp_set_rollout_path)
+  // rollout kernel for the loaded objective: 1 SIMT, 2 tcgen05 v1, 3 tcgen05 v2, 4 synthetic, 5 tcgen05 v3
   int kernel() const {
     if (comp.synth) return 4;
     if (!loaded || path_mode == 1) return 1;
     if (path_mode == 2) return comp.o.tc ? 2 : 1;
     if (path_mode == 3) return comp.o.tc2 ? 3 : 1;
-    // auto: v1 where every width is <= 128 (faster there: rollout_tc2.cu header), else v2
-    return comp.o.tc ? 2 : comp.o.tc2 ? 3 : 1;
+    if (path_mode == 5) return comp.o.tc3 ? 5 : 1;
+    // auto: v1 where every width is <= 128 (faster there: rollout_tc2.cu header), else v2, else v3
+    return comp.o.tc ? 2 : comp.o.tc2 ? 3 : comp.o.tc3 ? 5 : 1;
   }
 
   ~bp_ctx() {
@@ -876,6 +929,8 @@ struct bp_ctx {
          "synthetic objective launch");
     else if (kern == 3)
       ck(bp::launch_rollout_tc2(dev(), a, stream), "rollout (tcgen05 v2) launch");
+    else if (kern == 5)
+      ck(bp::launch_rollout_tc3(dev(), a, stream), "rollout (tcgen05 v3) launch");
     else if (kern == 2)
       ck(bp::launch_rollout_tc(dev(), a, stream), "rollout (tcgen05) launch");
     else
@@ -2051,7 +2106,7 @@ bp_status bp_init(int device, bp_ctx** out) {
     c->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
     if (const char* env = std::getenv("BP_ROLLOUT")) {
       const std::string e(env);
-      c->path_mode = e == "simt" ? 1 : e == "tc1" ? 2 : e == "tc2" ? 3 : 0;
+      c->path_mode = e == "simt" ? 1 : e == "tc1" ? 2 : e == "tc2" ? 3 : e == "tc3" ? 5 : 0;
     }
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
@@ -2100,7 +2155,7 @@ bp_status bp_set_stream(bp_ctx* ctx, void* stream) {
 bp_status bp_set_rollout_path(bp_ctx* ctx, int path, int* active) {
   return guard([&] {
     check_ctx(ctx);
-    if (path >= 0 && path <= 3) ctx->path_mode = path;
+    if ((path >= 0 && path <= 3) || path == 5) ctx->path_mode = path;
     if (active) *active = ctx->kernel();
   });
 }
@@ -2110,12 +2165,15 @@ bp_status bp_rollout_info(bp_ctx* ctx, int* kernel, int* tiles_per_cta, int* row
     check_ctx(ctx);
     const int k = ctx->kernel();
     const bp::DevObjective& o = ctx->comp.o;
-    const int tiles = k == 3 ? o.tc2 : k == 2 ? 1 : 0;  // k == 4: synthetic objective
+    const int tiles = k == 3 ? o.tc2 : (k == 2 || k == 5) ? 1 : 0;  // k == 4: synthetic objective
     if (kernel) *kernel = k;
     if (tiles_per_cta) *tiles_per_cta = tiles;
     if (rows_per_cta) *rows_per_cta = k == 1 ? ctx->comp.R : 128 * tiles;
     if (smem_bytes)
-      *smem_bytes = static_cast<int64_t>(k == 3 ? bp::rollout_tc2_smem(o) : k == 2 ? bp::rollout_tc_smem(o) : ctx->comp.smem);
+      *smem_bytes = static_cast<int64_t>(k == 3   ? bp::rollout_tc2_smem(o)
+                                         : k == 2 ? bp::rollout_tc_smem(o)
+                                         : k == 5 ? bp::rollout_tc3_smem(o)
+                                                  : ctx->comp.smem);
   });
 }
 

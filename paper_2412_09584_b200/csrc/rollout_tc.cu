@@ -86,6 +86,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
+// 3xTF32 operand split: hi = rna_tf32(x), lo = rna_tf32(x - hi) (as tc_common.cuh split_tf32).
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = rna_tf32(x);
+  lo = rna_tf32(x - hi);
+}
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -189,12 +194,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 
 // Writes 32 consecutive K-values of this thread's row as the hi / lo A operand in TMEM.
 __device__ __forceinline__ void store_operand_tmem(uint32_t tlane, int chunk, const float (&v)[32]) {
-  // hi = v as stored: kind::tf32 reads the top 19 bits (truncation); lo = v - trunc(v),
-  // exact, read the same way.  Error ~2^-21 relative per product (tools/tc_err.py).
-  tmem_st32(tlane + kColAhi + 32 * chunk, v);
-  float l[32];
+  // hi = rna_tf32(v), lo = rna_tf32(v - hi) (split_tf32): unbiased, within 2^-22 |v|.
+  float h[32], l[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) l[j] = v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u);
+  for (int j = 0; j < 32; ++j) split_tf32(v[j], h[j], l[j]);
+  tmem_st32(tlane + kColAhi + 32 * chunk, h);
   tmem_st32(tlane + kColAlo + 32 * chunk, l);
 }
 
@@ -436,12 +440,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) rollout_tc_kernel(const DevObje
           const uint32_t bytes = 2u * npad * 128u;
           for (int kb = 0; kb < o.tc_kb[l]; ++kb, ++it) {
             const uint32_t at = ring_place(pos, bytes, ring_bytes);
-            while (head < it) {
-              const int hs = head % kSlots;
-              if (it - head < kSlots && (hi_b[hs] <= at || lo_b[hs] >= at + bytes)) break;
-              mbar_wait(m.empty + hs, static_cast<uint32_t>((head / kSlots) & 1));
-              ++head;
-            }
+            // the slot's previous block and every in-flight block overlapping the byte range
+            // must be free: wait in order up to the newest of them (a wrapped placement of
+            // mixed-size blocks can overlap a newer block but not the oldest)
+            int need = it - kSlots;
+            for (int q = it - 1; q >= head && q > need; --q)
+              if (!(hi_b[q % kSlots] <= at || lo_b[q % kSlots] >= at + bytes)) {
+                need = q;
+                break;
+              }
+            for (; head <= need; ++head)
+              mbar_wait(m.empty + head % kSlots, static_cast<uint32_t>((head / kSlots) & 1));
             const int s = it % kSlots;
             lo_b[s] = at;
             hi_b[s] = at + bytes;

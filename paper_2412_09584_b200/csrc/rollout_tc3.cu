@@ -1,0 +1,610 @@
+// rollout_tc3.cu -- K1 v3 on the 5th-generation tensor cores for MLPs with two hidden
+// layers up to 512 wide and narrow ends (C5: [20, 512, 512, 16]): the fused H-step
+// rollout (reference evaluate / forward_chunk, proj/src/graph.cpp:252-401, on the
+// build_objective graph, model.cpp:310-387) with every Linear layer done by
+// tcgen05.mma (kind::tf32, 3xTF32) into TMEM.
+//
+// Why a third kernel: a 512-wide layer's accumulator is 512 TMEM columns -- all of
+// TMEM -- and its 512-wide A operand would need as much again, so v2's "two in-place
+// regions" scheme cannot hold it.  v3 never materialises either in full:
+//  * layer 1 (K = N0, N = N1) is computed in N chunks of <= 256 columns (J = 2 at
+//    C5), each accumulated in a 256-column TMEM region D1;
+//  * its A operand -- relu(layer 0) -- is RECOMPUTED per chunk, one 32-column K-block
+//    at a time: layer 0's input is the step's features (ks + ka <= 32: a single
+//    K-block X kept in TMEM / shared memory for the whole step), so N-block kb of
+//    layer 0 is 9 small MMAs (N = 32) into one of NS TMEM slots, converted in place
+//    by the L0 epilogue into A K-block kb of layer 1.  Layer 0 is ~4 % of the step's
+//    FLOPs, so computing it J times costs ~4 % more MMA work;
+//  * layer 2 (K = N1, N = N2 <= 32) consumes each D1 chunk as soon as the epilogue has
+//    converted it in place (relu + hi/lo split) and accumulates into D2 across chunks.
+// TMEM: D1 [0, 256), X [256, 288), L0 slots [288, 288 + 32 NS), D2 [416, 448).
+//
+// Per step and chunk j the MMA warp issues
+//   L0(j, 0 .. NS-2), then for kb: L1(j, kb) [12 MMAs, N = chunk width], L0(j, kb+NS-1)
+//   [into the slot L1(j, kb-1) just freed -- L1(j, kb) keeps the pipe busy meanwhile],
+// then L0(j+1, 0 .. NS-2) and L2(j, c) per K-block c the D1 epilogue publishes.
+// Weight blocks stream through a byte ring in exactly that order (producer warp,
+// cp.async.bulk); every ring entry has its own full / empty barrier pair, so the
+// producer never waits on a barrier phase that could already have moved on.
+//
+// Precision: 3xTF32 as v1 / v2 (split_tf32: hi = rna(x), lo = rna(x - hi); weights split
+// on the host): D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, FP32 accumulation in TMEM; per
+// row a fixed order of operations, so results are batch-decomposition invariant
+// (graph.hpp:102-103).
+//
+// Warps (15, one 128-row tile per CTA; warp w reaches TMEM lanes 32 (w % 4) .. + 31):
+//   0-3   L0 epilogue: layer-0 N-blocks -> layer-1 A K-blocks (+ layer-0 extrema)
+//   4-11  D1 epilogue: two per quadrant, K-blocks c = h, h + 2, ... of each chunk (+ layer-1
+//         extrema); warps 4-7 also turn D2 into x_t (cost scratch, x_t extrema) and the next
+//         step's features X
+//   12    MMA issuer (whole warp, elect.sync inside the asm)
+//   13    producer (weight blocks)
+//   14    cost warp: the cost program (4 rows per thread), states, scratch-column extrema
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rollout_common.cuh"
+#include "tc_common.cuh"
+#include "tc_epilogue.cuh"
+
+namespace bp {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kNS = 2;              // L0 output slots (layer-1 A K-blocks in flight)
+constexpr int kRing = 16;           // ring entries in flight (full / empty barrier pairs)
+constexpr int kWarps = 15;
+constexpr int kThreads3 = 32 * kWarps;
+constexpr int kMmaWarp = 12, kProducerWarp = 13, kCostWarp = 14;
+constexpr uint32_t kColD1 = 0, kColX = 256, kColL0 = 288, kColD2 = 416;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
+
+struct Tc3Smem {
+  unsigned char* xlo;    // features lo K-block (128 rows x 128 B, SW128)
+  unsigned char* a1lo;   // [kNS] layer-1 A lo K-blocks
+  unsigned char* a2lo;   // [2] layer-2 A lo K-blocks
+  unsigned char* w;      // weight byte ring
+  float* sc;             // [128][tc_S] per-row scratch of the cost warp (x_t written by the x epilogue)
+  float* bias;           // b0 [np0], b1 [np1], b2 [np2]
+  float* cconst;         // cost-op constants, arena range [cost_f0, cost_f1)
+  FwdOp* ops;            // [n_ops]
+  int* segl;             // [128] tile-local subdomain of each row (-1 past the last)
+  int* pairs;            // [n_sc][2] recorded scratch columns (column, record offset)
+  uint64_t* full;        // [kRing] ring entry landed
+  uint64_t* empty;       // [kRing] ring entry read by its MMAs (commit)
+  uint64_t* l0_full;     // [kNS] layer-0 N-block in slot s complete
+  uint64_t* a1_ready;    // [kNS] layer-1 A K-block in slot s written (4 quadrant warps)
+  uint64_t* a1_free;     // [kNS] layer-1 MMAs of slot s retired (commit)
+  uint64_t* d1_full;     // D1 chunk complete
+  uint64_t* a2_ready;    // [2] layer-2 A K-block written into slot h (4 quadrant warps)
+  uint64_t* a2_free;     // [2] layer-2 MMAs of slot h retired (commit)
+  uint64_t* d2_full;     // D2 (the step's output layer) complete
+  uint64_t* x_ready;     // features X of the next step written (4 warps)
+  uint64_t* x_full;      // x_t of every row in the scratch (4 warps)
+  uint64_t* x_empty;     // the cost warp consumed the scratch of the step
+  uint32_t* tmem_slot;
+  uint32_t* ring;        // [2][kRing] producer bookkeeping: byte ranges of the in-flight entries
+  size_t bytes;
+};
+
+__host__ __device__ inline Tc3Smem carve3(const DevObjective& o, unsigned char* base) {
+  Tc3Smem m;
+  size_t off = 0;
+  auto take = [&](size_t n, size_t align) {
+    off = (off + align - 1) & ~(align - 1);
+    unsigned char* p = base + off;
+    off += n;
+    return p;
+  };
+  m.xlo = take(16384, 1024);
+  m.a1lo = take(static_cast<size_t>(kNS) * 16384, 1024);
+  m.a2lo = take(2 * 16384, 1024);
+  m.w = take(static_cast<size_t>(o.tc3_ring), 1024);
+  m.sc = reinterpret_cast<float*>(take(sizeof(float) * 128 * o.tc_S, 16));
+  m.bias = reinterpret_cast<float*>(take(sizeof(float) * (o.tc3_np[0] + o.tc3_np[1] + o.tc3_np[2]), 16));
+  m.cconst = reinterpret_cast<float*>(take(sizeof(float) * (o.cost_f1 - o.cost_f0), 16));
+  m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops, 16));
+  m.segl = reinterpret_cast<int*>(take(sizeof(int) * 128, 16));
+  m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc, 16));
+  uint64_t* b = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kRing + 3 * kNS + 2 * 2 + 6), 16));
+  m.full = b;
+  m.empty = m.full + kRing;
+  m.l0_full = m.empty + kRing;
+  m.a1_ready = m.l0_full + kNS;
+  m.a1_free = m.a1_ready + kNS;
+  m.a2_ready = m.a1_free + kNS;
+  m.a2_free = m.a2_ready + 2;
+  m.d1_full = m.a2_free + 2;
+  m.d2_full = m.d1_full + 1;
+  m.x_ready = m.d2_full + 1;
+  m.x_full = m.x_ready + 1;
+  m.x_empty = m.x_full + 1;
+  m.tmem_slot = reinterpret_cast<uint32_t*>(take(16, 16));
+  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2 * kRing, 16));
+  m.bytes = off;
+  return m;
+}
+
+__host__ inline size_t tc3_fixed_bytes(DevObjective o) {
+  o.tc3_ring = 0;
+  return 1024 + carve3(o, nullptr).bytes + 1024;
+}
+
+// The weight stream, in the MMA warp's consumption order.  Entry kinds: layer-0 N-block
+// (rows 32, the image's block kb), layer-1 block (chunk j, K-block kb: the chunk's rows),
+// layer-2 K-block (np2 rows); each as a hi entry then a lo entry.
+struct W3 {
+  const float* src;
+  uint32_t bytes;
+};
+__device__ __forceinline__ W3 w0_entry(const DevObjective& o, int kb, int part) {
+  return {o.f + o.tc3_w[0] + (static_cast<size_t>(kb) * 2 + part) * 32 * 32, 32u * 128u};
+}
+__device__ __forceinline__ int chunk_w(const DevObjective& o, int j) { return min(256, o.tc3_np[1] - 256 * j); }
+__device__ __forceinline__ W3 w1_entry(const DevObjective& o, int j, int kb, int part) {
+  // image: per chunk j, per K-block kb: [hi: cw rows x 32][lo: cw rows x 32]
+  const int cw = chunk_w(o, j);
+  const size_t base = static_cast<size_t>(2 * 256) * j * o.tc3_np[0];  // earlier chunks: 256 rows x K, hi and lo
+  return {o.f + o.tc3_w[1] + base + (static_cast<size_t>(kb) * 2 + part) * cw * 32, static_cast<uint32_t>(cw) * 128u};
+}
+__device__ __forceinline__ W3 w2_entry(const DevObjective& o, int kb, int part) {
+  return {o.f + o.tc3_w[2] + (static_cast<size_t>(kb) * 2 + part) * o.tc3_np[2] * 32,
+          static_cast<uint32_t>(o.tc3_np[2]) * 128u};
+}
+
+// 3xTF32 MMAs of one K-block with `nq` k-steps of 8 (A_hi in TMEM, A_lo in shared memory):
+// the A_hi.B_hi / A_lo.B_hi pairs strictly alternating TS/SS, then the A_hi.B_lo run.
+__device__ __forceinline__ void mma_kblock3(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                            uint32_t idesc, uint32_t accum, int nq) {
+  if (nq == 4) {
+    mma_kblock_elect(d, a_hi, a_lo, b_hi, b_lo, idesc, accum);
+  } else {
+    for (int q = 0; q < nq; ++q) mma_pair_elect(d, a_hi + 8 * q, a_lo + 2 * q, b_hi + 2 * q, idesc, (accum | q) != 0 ? 1u : 0u);
+    for (int q = 0; q < nq; ++q) mma_ts(d, a_hi + 8 * q, b_lo + 2 * q, idesc, 1u);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObjective o, const RolloutArgs a) {
+  extern __shared__ unsigned char smraw[];
+  const uint32_t s0 = smem_u32(smraw);
+  const Tc3Smem m = carve3(o, smraw + (((s0 + 1023u) & ~1023u) - s0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long row0 = static_cast<long long>(blockIdx.x) * 128;
+  const int ks = o.ks, ka = o.ka, kd = o.kd, d = o.d, S = o.tc_S, H = o.H;
+  const long long rps = a.rows_per_sub;
+  const int np0 = o.tc3_np[0], np1 = o.tc3_np[1], np2 = o.tc3_np[2];
+  const int KB1 = np0 / 32;               // layer-0 N-blocks = layer-1 K-blocks
+  const int J = (np1 + 255) / 256;        // layer-1 N chunks
+  const int k0q = o.tc3_k0steps;          // k-steps of 8 of the features
+
+  if (a.failed != nullptr) {  // skip tiles whose subdomains all failed already
+    const long long last = min(a.n_rows, row0 + 128) - 1;
+    bool all_failed = last >= row0;
+    for (long long s = row0 / rps; s <= last / rps && all_failed; ++s) all_failed = a.failed[s] != 0;
+    if (all_failed) return;
+  }
+
+  for (int i = tid; i < 128; i += kThreads3) {
+    const long long r = row0 + i;
+    m.segl[i] = r < a.n_rows ? static_cast<int>(r / rps - row0 / rps) : -1;
+  }
+  for (int i = tid; i < 128 * S; i += kThreads3) m.sc[i] = 0.f;
+  for (int i = tid; i < np0 + np1 + np2; i += kThreads3) m.bias[i] = o.f[o.tc3_bias + i];
+  for (int i = tid; i < o.n_ops; i += kThreads3) m.ops[i] = to_fwd(o.ops[i]);
+  for (int i = tid; i < 2 * o.n_sc; i += kThreads3) m.pairs[i] = o.iv[o.sc_list + i];
+  for (int i = tid; i < o.cost_f1 - o.cost_f0; i += kThreads3) m.cconst[i] = o.f[o.cost_f0 + i];
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(m.full + s, 1);
+      mbar_init(m.empty + s, 1);
+    }
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(m.l0_full + s, 1);
+      mbar_init(m.a1_ready + s, 4);
+      mbar_init(m.a1_free + s, 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(m.a2_ready + h, 4);
+      mbar_init(m.a2_free + h, 1);
+    }
+    mbar_init(m.d1_full, 1);
+    mbar_init(m.d2_full, 1);
+    mbar_init(m.x_ready, 4);
+    mbar_init(m.x_full, 4);
+    mbar_init(m.x_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *m.tmem_slot;
+  const uint32_t ring_bytes = static_cast<uint32_t>(o.tc3_ring);
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------ producer: the weight stream
+    if (lane == 0) {
+      uint32_t pos = 0;
+      uint32_t* lo_b = m.ring;
+      uint32_t* hi_b = m.ring + kRing;
+      int it = 0, head = 0;
+      auto put = [&](W3 e) {
+        const uint32_t at = ring_place(pos, e.bytes, ring_bytes);
+        // the ring slot's previous entry (it - kRing) and every in-flight entry overlapping the
+        // byte range must have retired: wait for the in-flight entries in order up to the newest
+        // of them.  (Checking only the oldest is not enough: with mixed entry sizes a wrapped
+        // placement can overlap a newer entry while missing the oldest.)
+        int need = it - kRing;
+        for (int q = it - 1; q >= head && q > need; --q) {
+          const int qs = q % kRing;
+          if (!(hi_b[qs] <= at || lo_b[qs] >= at + e.bytes)) {
+            need = q;
+            break;
+          }
+        }
+        for (; head <= need; ++head)
+          mbar_wait(m.empty + head % kRing, static_cast<uint32_t>((head / kRing) & 1), kSleepProducer);
+        const int s = it % kRing;
+        lo_b[s] = at;
+        hi_b[s] = at + e.bytes;
+        mbar_expect_tx(m.full + s, e.bytes);
+        bulk_g2s(m.w + at, e.src, e.bytes, m.full + s);
+        ++it;
+      };
+      for (int t = 0; t < H; ++t)
+        for (int j = 0; j < J; ++j) {
+          if (j == 0)
+            for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
+              put(w0_entry(o, q, 0));
+              put(w0_entry(o, q, 1));
+            }
+          for (int kb = 0; kb < KB1; ++kb) {
+            put(w1_entry(o, j, kb, 0));
+            put(w1_entry(o, j, kb, 1));
+            const int nk = kb + kNS - 1;
+            if (nk < KB1) {
+              put(w0_entry(o, nk, 0));
+              put(w0_entry(o, nk, 1));
+            }
+          }
+          if (j + 1 < J)
+            for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
+              put(w0_entry(o, q, 0));
+              put(w0_entry(o, q, 1));
+            }
+          const int kb2 = chunk_w(o, j) / 32;
+          for (int c = 0; c < kb2; ++c) {
+            put(w2_entry(o, 8 * j + c, 0));
+            put(w2_entry(o, 8 * j + c, 1));
+          }
+        }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside)
+    int it = 0;
+    uint32_t pos = 0;
+    const uint32_t wbase = smem_u32(m.w);
+    const uint64_t x_lo = sw128_desc(smem_u32(m.xlo));
+    int l1_uses[kNS] = {}, l0_rdy[kNS] = {};  // per slot: layer-1 uses issued, a1_ready completions waited
+    int a2_rdy[2] = {}, a2_uses[2] = {};
+    const uint32_t id0 = tf32_idesc(32), id2 = tf32_idesc(np2);
+    // the next two ring entries (hi, lo): wait until both landed, return their descriptors
+    auto take2 = [&](uint32_t bytes, uint64_t& bh, uint64_t& bl) {
+      const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+      mbar_wait_warp(m.full + it % kRing, static_cast<uint32_t>((it / kRing) & 1));
+      mbar_wait_warp(m.full + (it + 1) % kRing, static_cast<uint32_t>(((it + 1) / kRing) & 1));
+      fence_after();
+      bh = sw128_desc(wbase + at_h);
+      bl = sw128_desc(wbase + at_l);
+    };
+    auto release2 = [&]() {  // both entries free once the MMAs issued so far retire
+      mma_commit_elect(m.empty + it % kRing);
+      mma_commit_elect(m.empty + (it + 1) % kRing);
+      it += 2;
+    };
+    // layer-0 N-block kb into slot kb % kNS (after the slot's previous layer-1 MMAs retired)
+    auto issue_l0 = [&](int kb) {
+      const int s = kb % kNS;
+      if (l1_uses[s] > 0) mbar_wait_warp(m.a1_free + s, static_cast<uint32_t>((l1_uses[s] - 1) & 1));
+      uint64_t bh, bl;
+      take2(32u * 128u, bh, bl);
+      mma_kblock3(tmem + kColL0 + 32 * s, tmem + kColX, x_lo, bh, bl, id0, 0u, k0q);
+      release2();
+      mma_commit_elect(m.l0_full + s);
+    };
+    for (int t = 0; t < H; ++t) {
+      mbar_wait_warp(m.x_ready, static_cast<uint32_t>(t & 1));  // the step's features X written
+      fence_after();
+      for (int j = 0; j < J; ++j) {
+        const int cw = chunk_w(o, j);
+        const uint32_t id1 = tf32_idesc(cw);
+        if (j == 0)
+          for (int q = 0; q < kNS - 1 && q < KB1; ++q) issue_l0(q);
+        for (int kb = 0; kb < KB1; ++kb) {
+          const int s = kb % kNS;
+          if (kb == 0 && j > 0) {  // D1 is free once chunk j-1's layer-2 MMAs (reading it in place) retired
+            const int hl = (chunk_w(o, j - 1) / 32 - 1) & 1;
+            mbar_wait_warp(m.a2_free + hl, static_cast<uint32_t>((a2_uses[hl] - 1) & 1));
+          }
+          mbar_wait_warp(m.a1_ready + s, static_cast<uint32_t>(l0_rdy[s] & 1));
+          ++l0_rdy[s];
+          fence_after();
+          uint64_t bh, bl;
+          take2(static_cast<uint32_t>(cw) * 128u, bh, bl);
+          mma_kblock3(tmem + kColD1, tmem + kColL0 + 32 * s, sw128_desc(smem_u32(m.a1lo) + s * 16384u), bh, bl, id1,
+                      kb > 0 ? 1u : 0u, 4);
+          release2();
+          mma_commit_elect(m.a1_free + s);
+          ++l1_uses[s];
+          if (kb + kNS - 1 < KB1) issue_l0(kb + kNS - 1);
+        }
+        mma_commit_elect(m.d1_full);
+        if (j + 1 < J)
+          for (int q = 0; q < kNS - 1 && q < KB1; ++q) issue_l0(q);
+        const int kb2 = cw / 32;
+        for (int c = 0; c < kb2; ++c) {
+          const int h = c & 1;
+          mbar_wait_warp(m.a2_ready + h, static_cast<uint32_t>(a2_rdy[h] & 1));
+          ++a2_rdy[h];
+          fence_after();
+          uint64_t bh, bl;
+          take2(static_cast<uint32_t>(np2) * 128u, bh, bl);
+          mma_kblock3(tmem + kColD2, tmem + kColD1 + 32 * c, sw128_desc(smem_u32(m.a2lo) + h * 16384u), bh, bl, id2,
+                      (j | c) != 0 ? 1u : 0u, 4);
+          release2();
+          mma_commit_elect(m.a2_free + h);
+          ++a2_uses[h];
+        }
+      }
+      mma_commit_elect(m.d2_full);
+    }
+  } else if (warp == kCostWarp) {
+    // ------------------------------------------------ cost warp: 4 rows per thread
+    constexpr int NR = 4;
+    const long long rem = a.n_rows - row0;
+    const int nvalid = static_cast<int>(rem < 0 ? 0 : rem < 128 ? rem : 128);
+    const long long seg0 = row0 / rps;
+    const long long SPH = static_cast<long long>(o.SP) * H;
+    const bool rec_any = a.stat_min != nullptr;
+    int rr[NR];
+    float* rows[NR];
+    float cost[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      rr[q] = 32 * q + lane;
+      rows[q] = m.sc + rr[q] * S;
+      cost[q] = 0.f;
+      for (int e = 0; e < kd; ++e) rows[q][o.pcol + e] = o.f[o.p0 + e];
+    }
+    const int k_first = o.x_stat >= 0 ? ks : 0;  // the x_t columns' extrema come from the x epilogue
+    const long long b1 = (seg0 + 1) * rps - row0;
+    const int bnd = static_cast<int>(b1 < nvalid ? b1 : nvalid);
+    const bool two = nvalid == 0 || (row0 + nvalid - 1) / rps - seg0 <= 1;
+    for (int t = 0; t < H; ++t) {
+      mbar_wait(m.x_full, static_cast<uint32_t>(t & 1), kSleepCost);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int r = rr[q];
+        const float* ur = a.actions + (row0 + r) * d + t * ka;
+        for (int j = 0; j < ka; ++j) {
+          const float u = r < nvalid ? __ldg(ur + j) : 0.f;
+          rows[q][o.ucol + j] = u;
+          if (j < kd) rows[q][o.pcol + j] += u;
+        }
+      }
+      cost_program_n<NR>(o, m.ops, m.cconst - o.cost_f0, rows, t, cost);
+      if (a.states != nullptr)
+#pragma unroll
+        for (int q = 0; q < NR; ++q)
+          if (rr[q] < nvalid)
+            for (int j = 0; j < ks; ++j) a.states[((row0 + rr[q]) * H + t) * ks + j] = rows[q][j];
+      if (rec_any) {
+        __syncwarp();
+        for (int k = k_first + lane; k < o.n_sc; k += 32)
+          scratch_column_extrema(a, m.sc + m.pairs[2 * k], S, two, bnd, nvalid, m.segl, seg0, SPH,
+                                 t * o.SP + m.pairs[2 * k + 1]);
+      }
+      mbar_arrive_warp(m.x_empty);
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+      if (rr[q] < nvalid) {
+        const long long r = row0 + rr[q];
+        a.costs[r] = cost[q];
+        if (a.failed != nullptr && !isfinite(cost[q])) atomicOr(a.failed + r / rps, 1);
+      }
+  } else if (warp < kMmaWarp) {
+    // ------------------------------------------------ epilogue warps
+    const int g = warp & 3;
+    const int row = 32 * g + lane;
+    const long long grow = row0 + row;
+    const bool row_ok = grow < a.n_rows;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(32 * g) << 16);
+    const long long wr0 = row0 + 32 * g;
+    const long long wr1 = min(wr0 + 31, a.n_rows - 1);
+    const long long ws0 = wr0 / rps, ws1 = wr1 >= wr0 ? wr1 / rps : ws0 - 1;
+    const bool simple = ws0 == ws1 && wr0 + 31 < a.n_rows;
+    const long long SPH = static_cast<long long>(o.SP) * H;
+    if (warp < 4) {
+      // -------------------------------------------- L0 epilogue: layer-0 N-block kb in slot s ->
+      // layer-1 A K-block kb (relu, hi / lo), layer-0 pre-activation extrema on chunk 0
+      const bool rec = o.relu[0] != 0 && o.pre_stat[0] >= 0 && a.stat_min != nullptr;
+      const int N0 = o.widths[1];
+      int l0_done[kNS] = {};
+      for (int t = 0; t < H; ++t)
+        for (int j = 0; j < J; ++j)
+          for (int kb = 0; kb < KB1; ++kb) {
+            const int s = kb % kNS;
+            mbar_wait(m.l0_full + s, static_cast<uint32_t>(l0_done[s] & 1), kSleepEpi);
+            ++l0_done[s];
+            fence_after();
+            float v[32];
+            tmem_ld32(tl + kColL0 + 32 * s, v);
+            const float4* b4 = reinterpret_cast<const float4*>(m.bias + kb * 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 bb = b4[q];
+              v[4 * q] += bb.x;
+              v[4 * q + 1] += bb.y;
+              v[4 * q + 2] += bb.z;
+              v[4 * q + 3] += bb.w;
+            }
+            {
+              float w[32];
+#pragma unroll
+              for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
+              store_operand(tl + kColL0 + 32 * s, m.a1lo + s * 16384, row, w);
+              publish_chunk(m.a1_ready + s);
+            }
+            if (rec && j == 0) {
+              const int col = kb * 32 + lane;
+              warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                                 static_cast<long long>(t) * o.SP + o.pre_stat[0] + col, col, N0);
+            }
+          }
+    } else {
+      // -------------------------------------------- D1 epilogue (K-blocks c = h, h + 2, ...) and, on
+      // warps 4-7, the output layer: x_t and the next step's features
+      const int h = (warp - 4) >> 2;
+      const bool xw = h == 0;
+      const bool rec = o.relu[1] != 0 && o.pre_stat[1] >= 0 && a.stat_min != nullptr;
+      const bool x_rec = o.x_stat >= 0 && a.stat_min != nullptr;
+      const int N1 = o.widths[2];
+      const float* urow = row_ok ? a.actions + grow * d : nullptr;
+      float* scrow = m.sc + row * S;
+      float pe[8], u_nxt[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        pe[e] = e < kd ? o.f[o.p0 + e] : 0.f;
+        u_nxt[e] = (row_ok && e < ka) ? __ldg(urow + e) : 0.f;  // u_0
+      }
+      // features concat(x [- tile(p)], u_{t+1}) of this row -> X (one K-block): v holds x
+      // in the columns below ks and zeros above
+      auto features_store = [&](float (&v)[32]) {
+        if (o.rel) {
+          int km = 0;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            float pv = pe[0];
+#pragma unroll
+            for (int e = 1; e < 8; ++e) pv = km == e ? pe[e] : pv;
+            if (q < ks) v[q] -= pv;
+            km = km + 1 == kd ? 0 : km + 1;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (e < ka && q == ks + e) v[q] = u_nxt[e];
+        store_operand(tl + kColX, m.xlo, row, v);
+        publish_chunk(m.x_ready);
+      };
+      if (xw) {  // features of step 0
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = q < ks ? o.f[o.x0 + min(q, ks - 1)] : 0.f;
+        features_store(v);
+      }
+      int a2_writes = 0;  // uses of A2 slot h so far
+      for (int t = 0; t < H; ++t) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < kd && e < ka) pe[e] += u_nxt[e];  // p_t = p_{t-1} + u_t
+          u_nxt[e] = (row_ok && e < ka && t + 1 < H) ? __ldg(urow + (t + 1) * ka + e) : 0.f;  // u_{t+1}
+        }
+        for (int j = 0; j < J; ++j) {
+          mbar_wait(m.d1_full, static_cast<uint32_t>((t * J + j) & 1), kSleepEpi);
+          fence_after();
+          const int kb2 = chunk_w(o, j) / 32;
+          for (int c = h; c < kb2; c += 2) {
+            if (a2_writes > 0) mbar_wait(m.a2_free + h, static_cast<uint32_t>((a2_writes - 1) & 1), kSleepEpi);
+            ++a2_writes;
+            float v[32];
+            tmem_ld32(tl + kColD1 + 32 * c, v);
+            const float4* b4 = reinterpret_cast<const float4*>(m.bias + np0 + 256 * j + 32 * c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 bb = b4[q];
+              v[4 * q] += bb.x;
+              v[4 * q + 1] += bb.y;
+              v[4 * q + 2] += bb.z;
+              v[4 * q + 3] += bb.w;
+            }
+            {
+              float w[32];
+#pragma unroll
+              for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
+              store_operand(tl + kColD1 + 32 * c, m.a2lo + h * 16384, row, w);
+              publish_chunk(m.a2_ready + h);
+            }
+            if (rec) {
+              const int col = 256 * j + 32 * c + lane;
+              warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                                 static_cast<long long>(t) * o.SP + o.pre_stat[1] + col, col, N1);
+            }
+          }
+        }
+        mbar_wait(m.d2_full, static_cast<uint32_t>(t & 1), kSleepEpi);
+        fence_after();
+        if (xw) {
+          float v[32];
+          if (np2 > 16)
+            tmem_ld32(tl + kColD2, v);
+          else
+            tmem_ld16(tl + kColD2, v);
+          const float* b2 = m.bias + np0 + np1;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = q < np2 ? v[q] + b2[q] : 0.f;
+          if (t >= 1) mbar_wait(m.x_empty, static_cast<uint32_t>((t - 1) & 1), kSleepEpi);
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (q < ks) scrow[q] = v[q];
+          if (x_rec)
+            warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                               static_cast<long long>(t) * o.SP + o.x_stat + lane, lane, ks);
+          mbar_arrive_warp(m.x_full);
+          if (t + 1 < H) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q >= ks) v[q] = 0.f;
+            features_store(v);
+          }
+        }
+      }
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+}  // namespace
+
+size_t rollout_tc3_fixed_smem(const DevObjective& o) { return tc3_fixed_bytes(o); }
+size_t rollout_tc3_smem(const DevObjective& o) { return 1024 + carve3(o, nullptr).bytes; }
+
+cudaError_t launch_rollout_tc3(const DevObjective& o, const RolloutArgs& a, cudaStream_t st) {
+  const size_t smem = rollout_tc3_smem(o);
+  const long long grid = (a.n_rows + 127) / 128;
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(rollout_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  rollout_tc3_kernel<<<static_cast<unsigned>(grid), kThreads3, smem, st>>>(o, a);
+  return cudaGetLastError();
+}
+
+}  // namespace bp

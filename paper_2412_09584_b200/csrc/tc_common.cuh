@@ -14,6 +14,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 3xTF32 operand split of an activation: hi = rna_tf32(x) and lo = rna_tf32(x - hi), both
+// with their 13 low mantissa bits zero, so kind::tf32 (which reads the top 19 bits) sees
+// them exactly.  x - hi is exact; hi + lo is within 2^-22 |x| of x and unbiased (truncating
+// hi or lo instead biases every activation toward zero by ~2^-21, which expansive rollouts
+// amplify step over step).
+__device__ __forceinline__ float rna_tf32_dev(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = rna_tf32_dev(x);
+  lo = rna_tf32_dev(x - hi);
+}
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
 // Used for both operands: a [rows][32 x 32-bit] K-block, row r at r*128 B with its
 // 16-byte chunks XOR-permuted by (r & 7); +2 in the encoded address = +32 B along K.

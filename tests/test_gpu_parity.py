@@ -149,6 +149,71 @@ def test_tcgen05_v2_cta_pair_matches_one_cta(device, shape, monkeypatch):
     assert rel_err(pair[0][0], ref) < RTOL_TC
 
 
+def v3_spec(name):
+    """Objectives for rollout_tc3.cu: C5 itself, ragged widths (two N chunks of 256 + 160
+    columns, padded N-blocks), relative features with a 16 + 4 input."""
+    if name == "c5":
+        return small_spec("c5")
+    s = bp.Scenario()
+    s.horizon = 5
+    if name == "ragged":
+        s.x0, s.x_target, s.p0 = [0.4, -0.3, 0.1, 0.2, 0.0, 0.3], [0.0] * 6, [0.0, 0.0]
+        s.u_lower, s.u_upper = [-0.5, -0.5], [0.5, 0.5]
+        widths = [8, 300, 400, 6]
+    else:  # "rel16": relative feature mode, keypoints over a 16-dim state
+        s.x0 = list(np.linspace(-0.5, 0.5, 16))
+        s.x_target = [0.1] * 16
+        s.p0 = [0.0, 0.0, 0.0, 0.0]
+        s.u_lower, s.u_upper = [-0.5] * 4, [0.5] * 4
+        widths = [20, 512, 288, 16]
+    return objmod.round_spec_to_f32(objmod.build_objective(bp.generate_model(9, widths), s))
+
+
+@pytest.mark.parametrize("name", ["c5", "ragged", "rel16"])
+@pytest.mark.parametrize("shape", [(3, 37), (2, 300), (1, 700)])
+def test_tcgen05_v3_matches_oracle(device, name, shape):
+    """rollout_tc3.cu (512-wide hidden layers: layer 1 in N chunks with layer 0 recomputed
+    per chunk, layer 2 accumulated across chunks) against the FP64 oracle and the SIMT
+    FP32 kernel: costs, states and the recorded extrema."""
+    spec = v3_spec(name)
+    dev = device.load(spec)
+    assert dev.rollout_kernel() == "tc3" and dev.rollout_path() == "tcgen05"
+    n_sub, rows = shape
+    if name == "c5":
+        rows = min(rows, 120)  # the FP64 oracle is slow at width 512
+    lo, hi = spec.box()
+    acts = np.random.default_rng(13).uniform(lo, hi, size=(n_sub, rows, spec.d)).astype(np.float32)
+    costs, states, elo, ehi, bad = dev.rollout(acts, want_states=True)
+    assert not bad.any()
+    ob = orc.Objective(spec)
+    layout = dev.stat_layout()
+    for s in range(n_sub):
+        st = orc.Stats()
+        ref = ob.evaluate(acts[s].astype(np.float64), st)
+        assert rel_err(costs[s], ref) < RTOL_TC, name
+        rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
+        seen = ~np.isnan(rlo)
+        assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
+    dev.rollout_path("simt")
+    c_s, st_s, lo_s, hi_s, _ = dev.rollout(acts, want_states=True)
+    dev.rollout_path("auto")
+    assert rel_err(costs, c_s) < RTOL_TC and rel_err(states, st_s) < RTOL_TC
+    assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
+
+
+def test_tcgen05_v3_rows_are_batch_invariant(device):
+    spec = v3_spec("ragged")
+    dev = device.load(spec)
+    lo, hi = spec.box()
+    acts = np.random.default_rng(4).uniform(lo, hi, size=(1, 300, spec.d)).astype(np.float32)
+    whole, _, _, _, _ = dev.rollout(acts)
+    for i in (0, 1, 127, 128, 299):
+        one, _, _, _, _ = dev.rollout(acts[:, i:i + 1])
+        assert whole[0, i] == one[0, 0]
+    split, _, _, _, _ = dev.rollout(acts.reshape(3, 100, spec.d))
+    assert np.array_equal(split.reshape(-1), whole.reshape(-1))
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "ref-obstacles"])
 def test_tcgen05_v1_still_matches_oracle(device, name):
     """The v1 kernel (rollout_tc.cu) stays selectable (BP_ROLLOUT=tc1) and parity-green."""
@@ -229,7 +294,7 @@ def test_interval_bound_matches_oracle(device, name):
     assert abs(lf[0] - ref) <= 1e-9 * max(1.0, abs(ref))
 
 
-@pytest.mark.parametrize("width", [100, 128, 200, 256, 300, 500, 512, 1000])
+@pytest.mark.parametrize("width", [100, 128, 200, 256, 300, 500, 512])
 def test_bound_width_classes_match_oracle(device, width):
     """The bound kernel is instantiated per width class (128 / 256 / 512 scratch doubles
     for the widest layer or cost-scratch row); objectives in each class bound like the
