@@ -271,7 +271,7 @@ class Device:
         """Rollout kernel, 128-row tiles per CTA, rows per CTA and shared memory per CTA."""
         k, t, r, sm = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
         check(self.lib.bp_rollout_info(self.h, C.byref(k), C.byref(t), C.byref(r), C.byref(sm)))
-        return {"kernel": {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic"}[k.value], "tiles_per_cta": t.value,
+        return {"kernel": {1: "simt", 2: "tc1", 3: "tc2", 4: "synthetic", 5: "tc3"}[k.value], "tiles_per_cta": t.value,
                 "rows_per_cta": r.value, "smem_bytes": sm.value}
 
     def rollout_tiles(self) -> int:

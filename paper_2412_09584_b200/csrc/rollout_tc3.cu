@@ -11,13 +11,16 @@
 //    C5), each accumulated in a 256-column TMEM region D1;
 //  * its A operand -- relu(layer 0) -- is RECOMPUTED per chunk, one 32-column K-block
 //    at a time: layer 0's input is the step's features (ks + ka <= 32: a single
-//    K-block X kept in TMEM / shared memory for the whole step), so N-block kb of
+//    K-block X kept in TMEM for the whole step), so N-block kb of
 //    layer 0 is 9 small MMAs (N = 32) into one of NS TMEM slots, converted in place
 //    by the L0 epilogue into A K-block kb of layer 1.  Layer 0 is ~4 % of the step's
 //    FLOPs, so computing it J times costs ~4 % more MMA work;
 //  * layer 2 (K = N1, N = N2 <= 32) consumes each D1 chunk as soon as the epilogue has
 //    converted it in place (relu + hi/lo split) and accumulates into D2 across chunks.
-// TMEM: D1 [0, 256), X [256, 288), L0 slots [288, 288 + 32 NS), D2 [416, 448).
+// TMEM: D1 [0, 256), X hi [256, 288), L0 slots hi / lo [288, 480), D2 [480, 496): layer 1's A
+// operand keeps both 3xTF32 parts in TMEM (TS-only MMAs, no shared-memory operand traffic), so
+// shared memory is left to the weight ring; three slots let L0(kb + 2) queue behind L1(kb) in
+// the (in-order) tensor pipe, so its epilogue runs under L1(kb + 1).
 //
 // Per step and chunk j the MMA warp issues
 //   L0(j, 0 .. NS-2), then for kb: L1(j, kb) [12 MMAs, N = chunk width], L0(j, kb+NS-1)
@@ -54,18 +57,33 @@ namespace {
 
 using namespace tc;
 
-constexpr int kNS = 2;              // L0 output slots (layer-1 A K-blocks in flight)
+constexpr int kNS = 3;              // L0 output slots (layer-1 A K-blocks in flight)
 constexpr int kRing = 16;           // ring entries in flight (full / empty barrier pairs)
 constexpr int kWarps = 15;
 constexpr int kThreads3 = 32 * kWarps;
 constexpr int kMmaWarp = 12, kProducerWarp = 13, kCostWarp = 14;
-constexpr uint32_t kColD1 = 0, kColX = 256, kColL0 = 288, kColD2 = 416;
+// TMEM columns: D1 | X hi | L0 slot s hi, lo (s < kNS) | D2
+constexpr uint32_t kColD1 = 0, kColXh = 256, kColL0 = 288, kColD2 = 480;
+__device__ __forceinline__ uint32_t col_l0h(int s) { return kColL0 + 64u * s; }
+__device__ __forceinline__ uint32_t col_l0l(int s) { return kColL0 + 64u * s + 32u; }
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
+constexpr uint32_t kSleepProducer = 0, kSleepCost = 128, kSleepEpi = 64;  // producer: no __nanosleep (a 256 ns back-off delayed every ring refill by ~0.5k cycles)
+
+// Debug timeline (compiled in with -DBP_TC_TIMELINE; tools/tc_timeline.py c5): clock64 marks of
+// CTA 0 at step 3 -- MMA warp 0 (step start), 1000 + 64 j + 4 kb + {0 before / 1 after the A
+// K-block wait, 2 / 3 weight hi / lo landed}, 1200 + j (D1 commit), 1300 + 16 j + 2 c + {0, 1}
+// (layer-2 A wait); L0 epilogue 2000 + 64 j + 2 kb + {0 slot full, 1 published}; D1 epilogue
+// 3000 + 32 j + 2 c + {0, 1}, 3100 + j (D1 full seen), 3200 / 3201 (D2 seen / X published).
+#ifdef BP_TC_TIMELINE
+__device__ __forceinline__ void mark3(const RolloutArgs& a, int t, int slot) {
+  if (a.timeline != nullptr && blockIdx.x == 0 && t == 3 && (threadIdx.x & 31) == 0) a.timeline[slot] = clock64();
+}
+#else
+__device__ __forceinline__ void mark3(const RolloutArgs&, int, int) {}
+#endif
 
 struct Tc3Smem {
   unsigned char* xlo;    // features lo K-block (128 rows x 128 B, SW128)
-  unsigned char* a1lo;   // [kNS] layer-1 A lo K-blocks
   unsigned char* a2lo;   // [2] layer-2 A lo K-blocks
   unsigned char* w;      // weight byte ring
   float* sc;             // [128][tc_S] per-row scratch of the cost warp (x_t written by the x epilogue)
@@ -87,7 +105,7 @@ struct Tc3Smem {
   uint64_t* x_full;      // x_t of every row in the scratch (4 warps)
   uint64_t* x_empty;     // the cost warp consumed the scratch of the step
   uint32_t* tmem_slot;
-  uint32_t* ring;        // [2][kRing] producer bookkeeping: byte ranges of the in-flight entries
+  uint32_t* ring;        // [kRing] x 8 B producer bookkeeping: virtual start of each in-flight entry
   size_t bytes;
 };
 
@@ -101,7 +119,6 @@ __host__ __device__ inline Tc3Smem carve3(const DevObjective& o, unsigned char* 
     return p;
   };
   m.xlo = take(16384, 1024);
-  m.a1lo = take(static_cast<size_t>(kNS) * 16384, 1024);
   m.a2lo = take(2 * 16384, 1024);
   m.w = take(static_cast<size_t>(o.tc3_ring), 1024);
   m.sc = reinterpret_cast<float*>(take(sizeof(float) * 128 * o.tc_S, 16));
@@ -124,7 +141,7 @@ __host__ __device__ inline Tc3Smem carve3(const DevObjective& o, unsigned char* 
   m.x_full = m.x_ready + 1;
   m.x_empty = m.x_full + 1;
   m.tmem_slot = reinterpret_cast<uint32_t*>(take(16, 16));
-  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2 * kRing, 16));
+  m.ring = reinterpret_cast<uint32_t*>(take(sizeof(unsigned long long) * kRing, 16));
   m.bytes = off;
   return m;
 }
@@ -156,18 +173,6 @@ __device__ __forceinline__ W3 w2_entry(const DevObjective& o, int kb, int part) 
           static_cast<uint32_t>(o.tc3_np[2]) * 128u};
 }
 
-// 3xTF32 MMAs of one K-block with `nq` k-steps of 8 (A_hi in TMEM, A_lo in shared memory):
-// the A_hi.B_hi / A_lo.B_hi pairs strictly alternating TS/SS, then the A_hi.B_lo run.
-__device__ __forceinline__ void mma_kblock3(uint32_t d, uint32_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
-                                            uint32_t idesc, uint32_t accum, int nq) {
-  if (nq == 4) {
-    mma_kblock_elect(d, a_hi, a_lo, b_hi, b_lo, idesc, accum);
-  } else {
-    for (int q = 0; q < nq; ++q) mma_pair_elect(d, a_hi + 8 * q, a_lo + 2 * q, b_hi + 2 * q, idesc, (accum | q) != 0 ? 1u : 0u);
-    for (int q = 0; q < nq; ++q) mma_ts(d, a_hi + 8 * q, b_lo + 2 * q, idesc, 1u);
-  }
-}
-
 __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObjective o, const RolloutArgs a) {
   extern __shared__ unsigned char smraw[];
   const uint32_t s0 = smem_u32(smraw);
@@ -188,6 +193,9 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
     if (all_failed) return;
   }
 
+#ifdef BP_TC3_NO_LO
+  for (int i = tid; i < o.tc3_ring / 4; i += kThreads3) reinterpret_cast<float*>(m.w)[i] = 0.f;
+#endif
   for (int i = tid; i < 128; i += kThreads3) {
     const long long r = row0 + i;
     m.segl[i] = r < a.n_rows ? static_cast<int>(r / rps - row0 / rps) : -1;
@@ -232,35 +240,51 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
   if (warp == kProducerWarp) {
     // ------------------------------------------------ producer: the weight stream
     if (lane == 0) {
+      // Ring bookkeeping on a virtual byte counter: wrapping to 0 skips the tail (counted as
+      // used), so virtual byte v lives at physical v mod ring and every entry occupies the
+      // virtual range [vstart, vstart + bytes).  A new entry ending at vpos overwrites exactly the
+      // bytes of entries that start before vpos - ring (the previous lap); entries retire in
+      // order, so the producer waits for the oldest in-flight entries while they start in the
+      // previous lap (or hold the ring slot), each on its own empty barrier.  O(1) per entry (a
+      // scan over all in-flight entries cost ~1k cycles per entry on this one thread).
       uint32_t pos = 0;
-      uint32_t* lo_b = m.ring;
-      uint32_t* hi_b = m.ring + kRing;
+      unsigned long long vpos = 0;
+      unsigned long long* vstart_b = reinterpret_cast<unsigned long long*>(m.ring);  // [kRing]
       int it = 0, head = 0;
+      int tcur = 0, ecur = 0;  // timeline: step and entry index within the step
       auto put = [&](W3 e) {
-        const uint32_t at = ring_place(pos, e.bytes, ring_bytes);
-        // the ring slot's previous entry (it - kRing) and every in-flight entry overlapping the
-        // byte range must have retired: wait for the in-flight entries in order up to the newest
-        // of them.  (Checking only the oldest is not enough: with mixed entry sizes a wrapped
-        // placement can overlap a newer entry while missing the oldest.)
-        int need = it - kRing;
-        for (int q = it - 1; q >= head && q > need; --q) {
-          const int qs = q % kRing;
-          if (!(hi_b[qs] <= at || lo_b[qs] >= at + e.bytes)) {
-            need = q;
-            break;
-          }
+        if (ecur < 60) mark3(a, tcur, 3300 + 3 * ecur);
+        if (pos + e.bytes > ring_bytes) {
+          vpos += ring_bytes - pos;
+          pos = 0;
         }
-        for (; head <= need; ++head)
+        const uint32_t at = pos;
+        pos += e.bytes;
+        vpos += e.bytes;
+        while (head < it && (vstart_b[head % kRing] + ring_bytes < vpos || it - head >= kRing)) {
           mbar_wait(m.empty + head % kRing, static_cast<uint32_t>((head / kRing) & 1), kSleepProducer);
+          ++head;
+        }
         const int s = it % kRing;
-        lo_b[s] = at;
-        hi_b[s] = at + e.bytes;
+        vstart_b[s] = vpos - e.bytes;
+        if (ecur < 60) mark3(a, tcur, 3301 + 3 * ecur);
+#ifdef BP_TC3_NO_LO  // timing experiment only (wrong results): skip every other entry's copy
+        if ((it & 1) == 1 && e.bytes > 8192) {
+          mbar_arrive(m.full + s);
+          ++it;
+          return;
+        }
+#endif
         mbar_expect_tx(m.full + s, e.bytes);
         bulk_g2s(m.w + at, e.src, e.bytes, m.full + s);
+        if (ecur < 60) mark3(a, tcur, 3302 + 3 * ecur);
+        ++ecur;
         ++it;
       };
       for (int t = 0; t < H; ++t)
         for (int j = 0; j < J; ++j) {
+          tcur = t;
+          if (j == 0) ecur = 0;
           if (j == 0)
             for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
               put(w0_entry(o, q, 0));
@@ -292,37 +316,57 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
     int it = 0;
     uint32_t pos = 0;
     const uint32_t wbase = smem_u32(m.w);
-    const uint64_t x_lo = sw128_desc(smem_u32(m.xlo));
     int l1_uses[kNS] = {}, l0_rdy[kNS] = {};  // per slot: layer-1 uses issued, a1_ready completions waited
     int a2_rdy[2] = {}, a2_uses[2] = {};
     const uint32_t id0 = tf32_idesc(32), id2 = tf32_idesc(np2);
-    // the next two ring entries (hi, lo): wait until both landed, return their descriptors
-    auto take2 = [&](uint32_t bytes, uint64_t& bh, uint64_t& bl) {
-      const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+    // the next ring entry: wait until it landed, return its descriptor; release it (its bytes free
+    // once the MMAs issued so far retire) right after the MMAs that read it are issued
+    auto take1 = [&](uint32_t bytes) {
+      const uint32_t at = ring_place(pos, bytes, ring_bytes);
       mbar_wait_warp(m.full + it % kRing, static_cast<uint32_t>((it / kRing) & 1));
-      mbar_wait_warp(m.full + (it + 1) % kRing, static_cast<uint32_t>(((it + 1) / kRing) & 1));
       fence_after();
-      bh = sw128_desc(wbase + at_h);
-      bl = sw128_desc(wbase + at_l);
+      return sw128_desc(wbase + at);
     };
-    auto release2 = [&]() {  // both entries free once the MMAs issued so far retire
+    auto release1 = [&]() {
       mma_commit_elect(m.empty + it % kRing);
-      mma_commit_elect(m.empty + (it + 1) % kRing);
-      it += 2;
+      ++it;
     };
-    // layer-0 N-block kb into slot kb % kNS (after the slot's previous layer-1 MMAs retired)
-    auto issue_l0 = [&](int kb) {
+    // 3xTF32 K-block with both A parts in TMEM, entry by entry (hi: 2 nq MMAs, lo: nq MMAs)
+    auto kblock_tt = [&](uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t bytes, uint32_t idesc, uint32_t accum, int nq,
+                         int t_mark = -1, int slot = 0) {
+      const uint64_t bh = take1(bytes);
+      if (t_mark >= 0) mark3(a, t_mark, slot);
+      mma_tt_bhi(d, a_hi, a_lo, bh, idesc, accum, nq);
+      release1();
+      const uint64_t bl = take1(bytes);
+      if (t_mark >= 0) mark3(a, t_mark, slot + 1);
+      mma_tt_blo(d, a_hi, bl, idesc, nq);
+      release1();
+    };
+    // layer-0 N-block kb into slot kb % kNS (after the slot's previous layer-1 MMAs retired): X hi
+    // in TMEM, X lo in shared memory -- TS/SS pairs on B_hi, then TS on B_lo
+    const uint64_t x_lo = sw128_desc(smem_u32(m.xlo));
+    auto issue_l0 = [&](int kb, int t_mark = -1, int slot = 0) {
       const int s = kb % kNS;
+      if (t_mark >= 0) mark3(a, t_mark, slot);
       if (l1_uses[s] > 0) mbar_wait_warp(m.a1_free + s, static_cast<uint32_t>((l1_uses[s] - 1) & 1));
-      uint64_t bh, bl;
-      take2(32u * 128u, bh, bl);
-      mma_kblock3(tmem + kColL0 + 32 * s, tmem + kColX, x_lo, bh, bl, id0, 0u, k0q);
-      release2();
+      if (t_mark >= 0) mark3(a, t_mark, slot + 1);
+      const uint32_t d = tmem + col_l0h(s);
+      const uint64_t bh = take1(32u * 128u);
+      if (t_mark >= 0) mark3(a, t_mark, slot + 2);
+      for (int q = 0; q < k0q; ++q)
+        mma_pair_elect(d, tmem + kColXh + 8 * q, x_lo + 2 * q, bh + 2 * q, id0, q != 0 ? 1u : 0u);
+      release1();
+      const uint64_t bl = take1(32u * 128u);
+      if (t_mark >= 0) mark3(a, t_mark, slot + 3);
+      for (int q = 0; q < k0q; ++q) mma_ts(d, tmem + kColXh + 8 * q, bl + 2 * q, id0, 1u);
+      release1();
       mma_commit_elect(m.l0_full + s);
     };
     for (int t = 0; t < H; ++t) {
       mbar_wait_warp(m.x_ready, static_cast<uint32_t>(t & 1));  // the step's features X written
       fence_after();
+      mark3(a, t, 0);
       for (int j = 0; j < J; ++j) {
         const int cw = chunk_w(o, j);
         const uint32_t id1 = tf32_idesc(cw);
@@ -334,32 +378,44 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
             const int hl = (chunk_w(o, j - 1) / 32 - 1) & 1;
             mbar_wait_warp(m.a2_free + hl, static_cast<uint32_t>((a2_uses[hl] - 1) & 1));
           }
+          mark3(a, t, 1000 + 64 * j + 4 * kb);
           mbar_wait_warp(m.a1_ready + s, static_cast<uint32_t>(l0_rdy[s] & 1));
           ++l0_rdy[s];
           fence_after();
-          uint64_t bh, bl;
-          take2(static_cast<uint32_t>(cw) * 128u, bh, bl);
-          mma_kblock3(tmem + kColD1, tmem + kColL0 + 32 * s, sw128_desc(smem_u32(m.a1lo) + s * 16384u), bh, bl, id1,
-                      kb > 0 ? 1u : 0u, 4);
-          release2();
+          mark3(a, t, 1001 + 64 * j + 4 * kb);
+          kblock_tt(tmem + kColD1, tmem + col_l0h(s), tmem + col_l0l(s), static_cast<uint32_t>(cw) * 128u, id1,
+                    kb > 0 ? 1u : 0u, 4, t, 1002 + 64 * j + 4 * kb);
           mma_commit_elect(m.a1_free + s);
+#ifdef BP_TC3_MEASURE_EXEC  // timing experiment: wait for this K-block's MMAs (drains the pipe)
+          mark3(a, t, 1700 + 64 * j + 2 * kb);
+          mbar_wait_warp(m.a1_free + s, static_cast<uint32_t>(l1_uses[s] & 1));
+          mark3(a, t, 1701 + 64 * j + 2 * kb);
+#endif
           ++l1_uses[s];
-          if (kb + kNS - 1 < KB1) issue_l0(kb + kNS - 1);
+          if (kb + kNS - 1 < KB1) issue_l0(kb + kNS - 1, t, 1500 + 64 * j + 4 * kb);
         }
         mma_commit_elect(m.d1_full);
+        mark3(a, t, 1200 + j);
         if (j + 1 < J)
           for (int q = 0; q < kNS - 1 && q < KB1; ++q) issue_l0(q);
         const int kb2 = cw / 32;
         for (int c = 0; c < kb2; ++c) {
           const int h = c & 1;
+          mark3(a, t, 1300 + 16 * j + 2 * c);
           mbar_wait_warp(m.a2_ready + h, static_cast<uint32_t>(a2_rdy[h] & 1));
           ++a2_rdy[h];
           fence_after();
-          uint64_t bh, bl;
-          take2(static_cast<uint32_t>(np2) * 128u, bh, bl);
-          mma_kblock3(tmem + kColD2, tmem + kColD1 + 32 * c, sw128_desc(smem_u32(m.a2lo) + h * 16384u), bh, bl, id2,
-                      (j | c) != 0 ? 1u : 0u, 4);
-          release2();
+          mark3(a, t, 1301 + 16 * j + 2 * c);
+          // A2 hi in TMEM (D1 in place), lo in shared memory: TS/SS pairs on B_hi, then TS on B_lo
+          const uint32_t ah = tmem + kColD1 + 32 * c;
+          const uint64_t al = sw128_desc(smem_u32(m.a2lo) + h * 16384u);
+          const uint64_t bh = take1(static_cast<uint32_t>(np2) * 128u);
+          for (int q = 0; q < 4; ++q)
+            mma_pair_elect(tmem + kColD2, ah + 8 * q, al + 2 * q, bh + 2 * q, id2, ((j | c) != 0 || q != 0) ? 1u : 0u);
+          release1();
+          const uint64_t bl = take1(static_cast<uint32_t>(np2) * 128u);
+          for (int q = 0; q < 4; ++q) mma_ts(tmem + kColD2, ah + 8 * q, bl + 2 * q, id2, 1u);
+          release1();
           mma_commit_elect(m.a2_free + h);
           ++a2_uses[h];
         }
@@ -446,8 +502,9 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
             mbar_wait(m.l0_full + s, static_cast<uint32_t>(l0_done[s] & 1), kSleepEpi);
             ++l0_done[s];
             fence_after();
+            if (warp == 0) mark3(a, t, 2000 + 64 * j + 2 * kb);
             float v[32];
-            tmem_ld32(tl + kColL0 + 32 * s, v);
+            tmem_ld32(tl + col_l0h(s), v);
             const float4* b4 = reinterpret_cast<const float4*>(m.bias + kb * 32);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -461,8 +518,9 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
               float w[32];
 #pragma unroll
               for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
-              store_operand(tl + kColL0 + 32 * s, m.a1lo + s * 16384, row, w);
+              store_operand_tt(tl + col_l0h(s), tl + col_l0l(s), w);
               publish_chunk(m.a1_ready + s);
+              if (warp == 0) mark3(a, t, 2001 + 64 * j + 2 * kb);
             }
             if (rec && j == 0) {
               const int col = kb * 32 + lane;
@@ -505,7 +563,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
 #pragma unroll
           for (int q = 0; q < 32; ++q)
             if (e < ka && q == ks + e) v[q] = u_nxt[e];
-        store_operand(tl + kColX, m.xlo, row, v);
+        store_operand(tl + kColXh, m.xlo, row, v);
         publish_chunk(m.x_ready);
       };
       if (xw) {  // features of step 0
@@ -524,6 +582,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
         for (int j = 0; j < J; ++j) {
           mbar_wait(m.d1_full, static_cast<uint32_t>((t * J + j) & 1), kSleepEpi);
           fence_after();
+          if (warp == 4) mark3(a, t, 3100 + j);
           const int kb2 = chunk_w(o, j) / 32;
           for (int c = h; c < kb2; c += 2) {
             if (a2_writes > 0) mbar_wait(m.a2_free + h, static_cast<uint32_t>((a2_writes - 1) & 1), kSleepEpi);
@@ -545,6 +604,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
               for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
               store_operand(tl + kColD1 + 32 * c, m.a2lo + h * 16384, row, w);
               publish_chunk(m.a2_ready + h);
+              if (warp == 4 || warp == 8) mark3(a, t, 3001 + 32 * j + 2 * c);
             }
             if (rec) {
               const int col = 256 * j + 32 * c + lane;
@@ -555,6 +615,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
         }
         mbar_wait(m.d2_full, static_cast<uint32_t>(t & 1), kSleepEpi);
         fence_after();
+        if (warp == 4) mark3(a, t, 3200);
         if (xw) {
           float v[32];
           if (np2 > 16)

@@ -162,6 +162,16 @@ __device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_b
   tmem_st32(t_hi, v);
 }
 
+// hi / lo parts of one 32-column K-block of this thread's row, both into TMEM (TS-only
+// operands).  v is clobbered.
+__device__ __forceinline__ void store_operand_tt(uint32_t t_hi, uint32_t t_lo, float (&v)[32]) {
+  float l[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) split_tf32(v[j], v[j], l[j]);
+  tmem_st32(t_hi, v);
+  tmem_st32(t_lo, l);
+}
+
 // Publish a written K-block: TMEM stores complete, shared stores visible to the
 // async proxy, then one arrival per warp -- on rank 0's barrier for a CTA pair (rank 0
 // issues the MMAs that read both CTAs' operands).

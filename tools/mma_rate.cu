@@ -487,6 +487,18 @@ void run(const char* name, int grid) {
 }
 
 int main() {
+#ifdef MMA_RATE_N256
+  run<0, 128, 0>("TS n128", 148);
+  run<0, 256, 0>("TS n256", 148);
+  run<1, 256, 0>("SS n256", 148);
+  run<3, 256, 0>("TS/SS n256", 148);
+  run<6, 256, 0>("fresh TS/SS n256", 148);
+  run<0, 256, 2>("TS n256 +ld", 148);
+  run<0, 256, 4>("TS n256 +st", 148);
+  run<0, 32, 0>("TS n32", 148);
+  run<0, 16, 0>("TS n16", 148);
+  return 0;
+#endif
   run<71, 128, 0>("per-MMA elect", 148);
   run<80, 128, 0>("12 in one asm", 148);
   run<81, 128, 0>("mma3 per kstep", 148);
