@@ -46,6 +46,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "rollout_common.cuh"
 #include "tc_common.cuh"
@@ -93,10 +94,10 @@ struct Tc3Smem {
   int* segl;             // [128] tile-local subdomain of each row (-1 past the last)
   int* pairs;            // [n_sc][2] recorded scratch columns (column, record offset)
   uint64_t* full;        // [kRing] ring entry landed
+  uint64_t* peer_full;   // [kRing] CTA pair, rank 0: the peer's half of the entry landed (relayed)
   uint64_t* empty;       // [kRing] ring entry read by its MMAs (commit)
   uint64_t* l0_full;     // [kNS] layer-0 N-block in slot s complete
   uint64_t* a1_ready;    // [kNS] layer-1 A K-block in slot s written (4 quadrant warps)
-  uint64_t* a1_free;     // [kNS] layer-1 MMAs of slot s retired (commit)
   uint64_t* d1_full;     // D1 chunk complete
   uint64_t* a2_ready;    // [2] layer-2 A K-block written into slot h (4 quadrant warps)
   uint64_t* a2_free;     // [2] layer-2 MMAs of slot h retired (commit)
@@ -127,13 +128,13 @@ __host__ __device__ inline Tc3Smem carve3(const DevObjective& o, unsigned char* 
   m.ops = reinterpret_cast<FwdOp*>(take(sizeof(FwdOp) * o.n_ops, 16));
   m.segl = reinterpret_cast<int*>(take(sizeof(int) * 128, 16));
   m.pairs = reinterpret_cast<int*>(take(sizeof(int) * 2 * o.n_sc, 16));
-  uint64_t* b = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (2 * kRing + 3 * kNS + 2 * 2 + 6), 16));
+  uint64_t* b = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (3 * kRing + 2 * kNS + 2 * 2 + 6), 16));
   m.full = b;
-  m.empty = m.full + kRing;
+  m.peer_full = m.full + kRing;
+  m.empty = m.peer_full + kRing;
   m.l0_full = m.empty + kRing;
   m.a1_ready = m.l0_full + kNS;
-  m.a1_free = m.a1_ready + kNS;
-  m.a2_ready = m.a1_free + kNS;
+  m.a2_ready = m.a1_ready + kNS;
   m.a2_free = m.a2_ready + 2;
   m.d1_full = m.a2_free + 2;
   m.d2_full = m.d1_full + 1;
@@ -158,21 +159,39 @@ struct W3 {
   const float* src;
   uint32_t bytes;
 };
-__device__ __forceinline__ W3 w0_entry(const DevObjective& o, int kb, int part) {
-  return {o.f + o.tc3_w[0] + (static_cast<size_t>(kb) * 2 + part) * 32 * 32, 32u * 128u};
+// CTA pair (half = 1): each CTA streams rows [rank R/2, (rank + 1) R/2) of every block (the
+// cta_group::2 B operand: N/2 rows in each CTA's shared memory at the same offset).
+__device__ __forceinline__ W3 half_of(const float* part_base, int rows, int half, uint32_t rank) {
+  const int r = rows >> half;
+  return {part_base + static_cast<size_t>(rank) * r * 32, static_cast<uint32_t>(r) * 128u};
+}
+__device__ __forceinline__ W3 w0_entry(const DevObjective& o, int kb, int part, int half = 0, uint32_t rank = 0) {
+  return half_of(o.f + o.tc3_w[0] + (static_cast<size_t>(kb) * 2 + part) * 32 * 32, 32, half, rank);
 }
 __device__ __forceinline__ int chunk_w(const DevObjective& o, int j) { return min(256, o.tc3_np[1] - 256 * j); }
-__device__ __forceinline__ W3 w1_entry(const DevObjective& o, int j, int kb, int part) {
+__device__ __forceinline__ W3 w1_entry(const DevObjective& o, int j, int kb, int part, int half = 0, uint32_t rank = 0) {
   // image: per chunk j, per K-block kb: [hi: cw rows x 32][lo: cw rows x 32]
   const int cw = chunk_w(o, j);
   const size_t base = static_cast<size_t>(2 * 256) * j * o.tc3_np[0];  // earlier chunks: 256 rows x K, hi and lo
-  return {o.f + o.tc3_w[1] + base + (static_cast<size_t>(kb) * 2 + part) * cw * 32, static_cast<uint32_t>(cw) * 128u};
+  return half_of(o.f + o.tc3_w[1] + base + (static_cast<size_t>(kb) * 2 + part) * cw * 32, cw, half, rank);
 }
-__device__ __forceinline__ W3 w2_entry(const DevObjective& o, int kb, int part) {
-  return {o.f + o.tc3_w[2] + (static_cast<size_t>(kb) * 2 + part) * o.tc3_np[2] * 32,
-          static_cast<uint32_t>(o.tc3_np[2]) * 128u};
+__device__ __forceinline__ W3 w2_entry(const DevObjective& o, int kb, int part, int half = 0, uint32_t rank = 0) {
+  return half_of(o.f + o.tc3_w[2] + (static_cast<size_t>(kb) * 2 + part) * o.tc3_np[2] * 32, o.tc3_np[2], half, rank);
 }
 
+// Weight-stream groups of one step (the producer's sequence, counted by the pair's relay).
+__device__ __forceinline__ int groups_per_step(const DevObjective& o, int KB1, int J) {
+  int n = 0;
+  for (int j = 0; j < J; ++j) {
+    if (j == 0) n += min(kNS - 1, KB1);
+    n += KB1;
+    if (j + 1 < J) n += min(kNS - 1, KB1);
+    n += chunk_w(o, j) / 32;
+  }
+  return n;
+}
+
+template <bool PAIR>  // PAIR: cluster of two CTAs (two 128-row tiles), rank 0 issues cta_group::2 MMAs (M = 256)
 __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObjective o, const RolloutArgs a) {
   extern __shared__ unsigned char smraw[];
   const uint32_t s0 = smem_u32(smraw);
@@ -185,17 +204,17 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
   const int KB1 = np0 / 32;               // layer-0 N-blocks = layer-1 K-blocks
   const int J = (np1 + 255) / 256;        // layer-1 N chunks
   const int k0q = o.tc3_k0steps;          // k-steps of 8 of the features
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  constexpr int kHalf = PAIR ? 1 : 0;     // each CTA of a pair streams half of every weight block's rows
 
-  if (a.failed != nullptr) {  // skip tiles whose subdomains all failed already
-    const long long last = min(a.n_rows, row0 + 128) - 1;
-    bool all_failed = last >= row0;
-    for (long long s = row0 / rps; s <= last / rps && all_failed; ++s) all_failed = a.failed[s] != 0;
+  if (a.failed != nullptr) {  // skip tiles (pairs) whose subdomains all failed already
+    const long long g0 = PAIR ? row0 - static_cast<long long>(rank) * 128 : row0;
+    const long long last = min(a.n_rows, g0 + (PAIR ? 256 : 128)) - 1;
+    bool all_failed = last >= g0;
+    for (long long s = g0 / rps; s <= last / rps && all_failed; ++s) all_failed = a.failed[s] != 0;
     if (all_failed) return;
   }
 
-#ifdef BP_TC3_NO_LO
-  for (int i = tid; i < o.tc3_ring / 4; i += kThreads3) reinterpret_cast<float*>(m.w)[i] = 0.f;
-#endif
   for (int i = tid; i < 128; i += kThreads3) {
     const long long r = row0 + i;
     m.segl[i] = r < a.n_rows ? static_cast<int>(r / rps - row0 / rps) : -1;
@@ -208,219 +227,273 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
   if (tid == 0) {
     for (int s = 0; s < kRing; ++s) {
       mbar_init(m.full + s, 1);
+      mbar_init(m.peer_full + s, 1);
       mbar_init(m.empty + s, 1);
     }
+    // operand-ready barriers count the quadrant warps of both CTAs of a pair (rank 0's MMA warp waits)
+    constexpr uint32_t kQ = PAIR ? 8 : 4;
     for (int s = 0; s < kNS; ++s) {
       mbar_init(m.l0_full + s, 1);
-      mbar_init(m.a1_ready + s, 4);
-      mbar_init(m.a1_free + s, 1);
+      mbar_init(m.a1_ready + s, kQ);
     }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(m.a2_ready + h, 4);
+      mbar_init(m.a2_ready + h, kQ);
       mbar_init(m.a2_free + h, 1);
     }
     mbar_init(m.d1_full, 1);
     mbar_init(m.d2_full, 1);
-    mbar_init(m.x_ready, 4);
+    mbar_init(m.x_ready, kQ);
     mbar_init(m.x_full, 4);
     mbar_init(m.x_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(m.tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
   fence_after();
   const uint32_t tmem = *m.tmem_slot;
   const uint32_t ring_bytes = static_cast<uint32_t>(o.tc3_ring);
 
+  // The weight stream is cut into GROUPS, one per MMA-warp step, each with one full / empty barrier
+  // pair: a layer-1 K-block (W1 hi, lo) together with the layer-0 N-block issued after it (W0 hi,
+  // lo), a layer-0 prologue, a layer-2 K-block.  One wait and one commit per group keep the MMA
+  // warp's bookkeeping between its bursts short (per-entry barriers cost ~1k cycles per K-block).
   if (warp == kProducerWarp) {
     // ------------------------------------------------ producer: the weight stream
     if (lane == 0) {
       // Ring bookkeeping on a virtual byte counter: wrapping to 0 skips the tail (counted as
-      // used), so virtual byte v lives at physical v mod ring and every entry occupies the
-      // virtual range [vstart, vstart + bytes).  A new entry ending at vpos overwrites exactly the
-      // bytes of entries that start before vpos - ring (the previous lap); entries retire in
-      // order, so the producer waits for the oldest in-flight entries while they start in the
-      // previous lap (or hold the ring slot), each on its own empty barrier.  O(1) per entry (a
-      // scan over all in-flight entries cost ~1k cycles per entry on this one thread).
+      // used), so virtual byte v lives at physical v mod ring and a group occupies the virtual
+      // range [vstart, vpos).  A new group ending at vpos overwrites exactly the bytes of groups
+      // that start before vpos - ring (the previous lap); groups retire in order, so the producer
+      // waits for the oldest in-flight groups while they start in the previous lap (or hold the
+      // barrier slot).  O(1) per group.
       uint32_t pos = 0;
       unsigned long long vpos = 0;
       unsigned long long* vstart_b = reinterpret_cast<unsigned long long*>(m.ring);  // [kRing]
-      int it = 0, head = 0;
-      int tcur = 0, ecur = 0;  // timeline: step and entry index within the step
-      auto put = [&](W3 e) {
-        if (ecur < 60) mark3(a, tcur, 3300 + 3 * ecur);
-        if (pos + e.bytes > ring_bytes) {
-          vpos += ring_bytes - pos;
-          pos = 0;
+      int g = 0, head = 0;
+      int tcur = 0, gcur = 0;  // timeline: step and group index within the step
+      W3 ent[4];
+      uint32_t at[4];
+      auto put_group = [&](int n) {
+        if (gcur < 60) mark3(a, tcur, 3300 + 3 * gcur);
+        unsigned long long vs = 0;  // virtual start of the group's first entry
+        uint32_t bytes = 0;
+        for (int i = 0; i < n; ++i) {
+          if (pos + ent[i].bytes > ring_bytes) {
+            vpos += ring_bytes - pos;
+            pos = 0;
+          }
+          if (i == 0) vs = vpos;
+          at[i] = pos;
+          pos += ent[i].bytes;
+          vpos += ent[i].bytes;
+          bytes += ent[i].bytes;
         }
-        const uint32_t at = pos;
-        pos += e.bytes;
-        vpos += e.bytes;
-        while (head < it && (vstart_b[head % kRing] + ring_bytes < vpos || it - head >= kRing)) {
+        while (head < g && (vstart_b[head % kRing] + ring_bytes < vpos || g - head >= kRing)) {
           mbar_wait(m.empty + head % kRing, static_cast<uint32_t>((head / kRing) & 1), kSleepProducer);
           ++head;
         }
-        const int s = it % kRing;
-        vstart_b[s] = vpos - e.bytes;
-        if (ecur < 60) mark3(a, tcur, 3301 + 3 * ecur);
-#ifdef BP_TC3_NO_LO  // timing experiment only (wrong results): skip every other entry's copy
-        if ((it & 1) == 1 && e.bytes > 8192) {
-          mbar_arrive(m.full + s);
-          ++it;
-          return;
-        }
-#endif
-        mbar_expect_tx(m.full + s, e.bytes);
-        bulk_g2s(m.w + at, e.src, e.bytes, m.full + s);
-        if (ecur < 60) mark3(a, tcur, 3302 + 3 * ecur);
-        ++ecur;
-        ++it;
+        const int sl = g % kRing;
+        vstart_b[sl] = vs;
+        if (gcur < 60) mark3(a, tcur, 3301 + 3 * gcur);
+        mbar_expect_tx(m.full + sl, bytes);
+        for (int i = 0; i < n; ++i) bulk_g2s(m.w + at[i], ent[i].src, ent[i].bytes, m.full + sl);
+        if (gcur < 60) mark3(a, tcur, 3302 + 3 * gcur);
+        ++gcur;
+        ++g;
       };
       for (int t = 0; t < H; ++t)
         for (int j = 0; j < J; ++j) {
           tcur = t;
-          if (j == 0) ecur = 0;
+          if (j == 0) gcur = 0;
           if (j == 0)
             for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
-              put(w0_entry(o, q, 0));
-              put(w0_entry(o, q, 1));
+              ent[0] = w0_entry(o, q, 0, kHalf, rank);
+              ent[1] = w0_entry(o, q, 1, kHalf, rank);
+              put_group(2);
             }
           for (int kb = 0; kb < KB1; ++kb) {
-            put(w1_entry(o, j, kb, 0));
-            put(w1_entry(o, j, kb, 1));
+            ent[0] = w1_entry(o, j, kb, 0, kHalf, rank);
+            ent[1] = w1_entry(o, j, kb, 1, kHalf, rank);
             const int nk = kb + kNS - 1;
             if (nk < KB1) {
-              put(w0_entry(o, nk, 0));
-              put(w0_entry(o, nk, 1));
+              ent[2] = w0_entry(o, nk, 0, kHalf, rank);
+              ent[3] = w0_entry(o, nk, 1, kHalf, rank);
             }
+            put_group(nk < KB1 ? 4 : 2);
           }
           if (j + 1 < J)
             for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
-              put(w0_entry(o, q, 0));
-              put(w0_entry(o, q, 1));
+              ent[0] = w0_entry(o, q, 0, kHalf, rank);
+              ent[1] = w0_entry(o, q, 1, kHalf, rank);
+              put_group(2);
             }
           const int kb2 = chunk_w(o, j) / 32;
           for (int c = 0; c < kb2; ++c) {
-            put(w2_entry(o, 8 * j + c, 0));
-            put(w2_entry(o, 8 * j + c, 1));
+            ent[0] = w2_entry(o, 8 * j + c, 0, kHalf, rank);
+            ent[1] = w2_entry(o, 8 * j + c, 1, kHalf, rank);
+            put_group(2);
           }
         }
     }
+  } else if (warp == kMmaWarp && PAIR && rank == 1) {
+    // ------------------------------------------------ CTA pair, rank 1: relay "my half of group g
+    // landed" to rank 0, which issues the MMAs over both halves
+    const int n_g = H * groups_per_step(o, KB1, J);
+    for (int gi = 0; gi < n_g; ++gi) {
+      mbar_wait_warp(m.full + gi % kRing, static_cast<uint32_t>((gi / kRing) & 1));
+      if (lane == 0) mbar_arrive_cta(m.peer_full + gi % kRing, 0);
+      __syncwarp();
+    }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside)
-    int it = 0;
+    // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside); a
+    // CTA pair's rank 0 issues cta_group::2 MMAs over both CTAs' rows and both halves of B
+    int g = 0;
     uint32_t pos = 0;
     const uint32_t wbase = smem_u32(m.w);
-    int l1_uses[kNS] = {}, l0_rdy[kNS] = {};  // per slot: layer-1 uses issued, a1_ready completions waited
-    int a2_rdy[2] = {}, a2_uses[2] = {};
-    const uint32_t id0 = tf32_idesc(32), id2 = tf32_idesc(np2);
-    // the next ring entry: wait until it landed, return its descriptor; release it (its bytes free
-    // once the MMAs issued so far retire) right after the MMAs that read it are issued
-    auto take1 = [&](uint32_t bytes) {
-      const uint32_t at = ring_place(pos, bytes, ring_bytes);
-      mbar_wait_warp(m.full + it % kRing, static_cast<uint32_t>((it / kRing) & 1));
+    int slot_grp[kNS];  // per L0 slot: the group whose commit follows the slot's last layer-1 use (-1 none)
+    for (int q = 0; q < kNS; ++q) slot_grp[q] = -1;
+    int l0_rdy[kNS] = {};  // per slot: a1_ready completions waited
+    int a2_rdy[2] = {};
+    int a2_last = -1;  // group committed after the last layer-2 K-block (D1 is free once it retired)
+    auto idesc = [&](int n) { return PAIR ? tf32_idesc_mn(256, n) : tf32_idesc(n); };
+    const uint32_t id0 = idesc(32), id2 = idesc(np2);
+    // commits arrive in both CTAs of a pair; operand-ready barriers collect both CTAs' warps
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR)
+        commit_pair_elect(bar);
+      else
+        mma_commit_elect(bar);
+    };
+    auto wait_ready = [&](uint64_t* bar, uint32_t parity) {
+      if constexpr (PAIR)
+        mbar_wait_cluster(bar, parity);
+      else
+        mbar_wait_warp(bar, parity);
+    };
+    auto wait_group_retired = [&](int gi) {  // the MMAs issued before group gi's commit retired
+      if (gi >= 0) mbar_wait_warp(m.empty + gi % kRing, static_cast<uint32_t>((gi / kRing) & 1));
+    };
+    // the next group of n entries of `rows` rows each (this CTA's half for a pair): wait until it
+    // (and the peer's half) landed; descriptors in b[]; released by a commit after its MMAs
+    uint64_t b[4];
+    auto take_group = [&](int n, const uint32_t* rows) {
+      for (int i = 0; i < n; ++i) b[i] = sw128_desc(wbase + ring_place(pos, (rows[i] >> kHalf) * 128u, ring_bytes));
+      mbar_wait_warp(m.full + g % kRing, static_cast<uint32_t>((g / kRing) & 1));
+      if constexpr (PAIR) mbar_wait_cluster(m.peer_full + g % kRing, static_cast<uint32_t>((g / kRing) & 1));
       fence_after();
-      return sw128_desc(wbase + at);
     };
-    auto release1 = [&]() {
-      mma_commit_elect(m.empty + it % kRing);
-      ++it;
+    auto release_group = [&]() {
+      commit(m.empty + g % kRing);
+      ++g;
     };
-    // 3xTF32 K-block with both A parts in TMEM, entry by entry (hi: 2 nq MMAs, lo: nq MMAs)
-    auto kblock_tt = [&](uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t bytes, uint32_t idesc, uint32_t accum, int nq,
-                         int t_mark = -1, int slot = 0) {
-      const uint64_t bh = take1(bytes);
-      if (t_mark >= 0) mark3(a, t_mark, slot);
-      mma_tt_bhi(d, a_hi, a_lo, bh, idesc, accum, nq);
-      release1();
-      const uint64_t bl = take1(bytes);
-      if (t_mark >= 0) mark3(a, t_mark, slot + 1);
-      mma_tt_blo(d, a_hi, bl, idesc, nq);
-      release1();
+    auto tt_bhi = [&](uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint32_t id, uint32_t acc, int nq) {
+      if constexpr (PAIR)
+        mma_tt_bhi2(d, ah, al, bh, id, acc, nq);
+      else
+        mma_tt_bhi(d, ah, al, bh, id, acc, nq);
     };
-    // layer-0 N-block kb into slot kb % kNS (after the slot's previous layer-1 MMAs retired): X hi
-    // in TMEM, X lo in shared memory -- TS/SS pairs on B_hi, then TS on B_lo
+    auto tt_blo = [&](uint32_t d, uint32_t ah, uint64_t bl, uint32_t id, int nq) {
+      if constexpr (PAIR)
+        mma_tt_blo2(d, ah, bl, id, nq);
+      else
+        mma_tt_blo(d, ah, bl, id, nq);
+    };
+    // A hi in TMEM, A lo in shared memory: TS/SS pairs on B_hi, then TS on B_lo
+    auto ts_pair = [&](uint32_t d, uint32_t ah, uint64_t al, uint64_t bh, uint32_t id, uint32_t acc) {
+      if constexpr (PAIR)
+        mma_pair2_elect(d, ah, al, bh, id, acc);
+      else
+        mma_pair_elect(d, ah, al, bh, id, acc);
+    };
+    auto ts_one = [&](uint32_t d, uint32_t ah, uint64_t bl, uint32_t id) {
+      if constexpr (PAIR)
+        mma_ts2(d, ah, bl, id, 1u);
+      else
+        mma_ts(d, ah, bl, id, 1u);
+    };
+    // layer-0 N-block kb into slot kb % kNS with the W0 descriptors bh / bl (after the slot's
+    // previous layer-1 MMAs retired)
     const uint64_t x_lo = sw128_desc(smem_u32(m.xlo));
-    auto issue_l0 = [&](int kb, int t_mark = -1, int slot = 0) {
+    auto l0_mmas = [&](int kb, uint64_t bh, uint64_t bl) {
       const int s = kb % kNS;
-      if (t_mark >= 0) mark3(a, t_mark, slot);
-      if (l1_uses[s] > 0) mbar_wait_warp(m.a1_free + s, static_cast<uint32_t>((l1_uses[s] - 1) & 1));
-      if (t_mark >= 0) mark3(a, t_mark, slot + 1);
+      wait_group_retired(slot_grp[s]);
       const uint32_t d = tmem + col_l0h(s);
-      const uint64_t bh = take1(32u * 128u);
-      if (t_mark >= 0) mark3(a, t_mark, slot + 2);
-      for (int q = 0; q < k0q; ++q)
-        mma_pair_elect(d, tmem + kColXh + 8 * q, x_lo + 2 * q, bh + 2 * q, id0, q != 0 ? 1u : 0u);
-      release1();
-      const uint64_t bl = take1(32u * 128u);
-      if (t_mark >= 0) mark3(a, t_mark, slot + 3);
-      for (int q = 0; q < k0q; ++q) mma_ts(d, tmem + kColXh + 8 * q, bl + 2 * q, id0, 1u);
-      release1();
-      mma_commit_elect(m.l0_full + s);
+      for (int q = 0; q < k0q; ++q) ts_pair(d, tmem + kColXh + 8 * q, x_lo + 2 * q, bh + 2 * q, id0, q != 0 ? 1u : 0u);
+      for (int q = 0; q < k0q; ++q) ts_one(d, tmem + kColXh + 8 * q, bl + 2 * q, id0);
+      commit(m.l0_full + s);
+    };
+    const uint32_t rows_w0[2] = {32u, 32u};
+    const uint32_t rows_w2[2] = {static_cast<uint32_t>(np2), static_cast<uint32_t>(np2)};
+    auto l0_prologue = [&]() {
+      for (int q = 0; q < kNS - 1 && q < KB1; ++q) {
+        take_group(2, rows_w0);
+        l0_mmas(q, b[0], b[1]);
+        release_group();
+      }
     };
     for (int t = 0; t < H; ++t) {
-      mbar_wait_warp(m.x_ready, static_cast<uint32_t>(t & 1));  // the step's features X written
+      wait_ready(m.x_ready, static_cast<uint32_t>(t & 1));  // the step's features X written
       fence_after();
       mark3(a, t, 0);
       for (int j = 0; j < J; ++j) {
         const int cw = chunk_w(o, j);
-        const uint32_t id1 = tf32_idesc(cw);
-        if (j == 0)
-          for (int q = 0; q < kNS - 1 && q < KB1; ++q) issue_l0(q);
+        const uint32_t id1 = idesc(cw);
+        const uint32_t rows_g[4] = {static_cast<uint32_t>(cw), static_cast<uint32_t>(cw), 32u, 32u};
+        if (j == 0) l0_prologue();
         for (int kb = 0; kb < KB1; ++kb) {
           const int s = kb % kNS;
-          if (kb == 0 && j > 0) {  // D1 is free once chunk j-1's layer-2 MMAs (reading it in place) retired
-            const int hl = (chunk_w(o, j - 1) / 32 - 1) & 1;
-            mbar_wait_warp(m.a2_free + hl, static_cast<uint32_t>((a2_uses[hl] - 1) & 1));
-          }
+          const int nk = kb + kNS - 1;
+          if (kb == 0 && j > 0) wait_group_retired(a2_last);  // chunk j-1's layer-2 MMAs read D1 in place
           mark3(a, t, 1000 + 64 * j + 4 * kb);
-          mbar_wait_warp(m.a1_ready + s, static_cast<uint32_t>(l0_rdy[s] & 1));
+          wait_ready(m.a1_ready + s, static_cast<uint32_t>(l0_rdy[s] & 1));
           ++l0_rdy[s];
           fence_after();
           mark3(a, t, 1001 + 64 * j + 4 * kb);
-          kblock_tt(tmem + kColD1, tmem + col_l0h(s), tmem + col_l0l(s), static_cast<uint32_t>(cw) * 128u, id1,
-                    kb > 0 ? 1u : 0u, 4, t, 1002 + 64 * j + 4 * kb);
-          mma_commit_elect(m.a1_free + s);
-#ifdef BP_TC3_MEASURE_EXEC  // timing experiment: wait for this K-block's MMAs (drains the pipe)
-          mark3(a, t, 1700 + 64 * j + 2 * kb);
-          mbar_wait_warp(m.a1_free + s, static_cast<uint32_t>(l1_uses[s] & 1));
-          mark3(a, t, 1701 + 64 * j + 2 * kb);
-#endif
-          ++l1_uses[s];
-          if (kb + kNS - 1 < KB1) issue_l0(kb + kNS - 1, t, 1500 + 64 * j + 4 * kb);
+          take_group(nk < KB1 ? 4 : 2, rows_g);
+          mark3(a, t, 1002 + 64 * j + 4 * kb);
+          tt_bhi(tmem + kColD1, tmem + col_l0h(s), tmem + col_l0l(s), b[0], id1, kb > 0 ? 1u : 0u, 4);
+          tt_blo(tmem + kColD1, tmem + col_l0h(s), b[1], id1, 4);
+          if (nk < KB1) l0_mmas(nk, b[2], b[3]);
+          slot_grp[s] = g;  // this group's commit follows L1(kb), the last use of slot s
+          release_group();
+          mark3(a, t, 1003 + 64 * j + 4 * kb);
         }
-        mma_commit_elect(m.d1_full);
+        commit(m.d1_full);
         mark3(a, t, 1200 + j);
-        if (j + 1 < J)
-          for (int q = 0; q < kNS - 1 && q < KB1; ++q) issue_l0(q);
+        if (j + 1 < J) l0_prologue();
         const int kb2 = cw / 32;
         for (int c = 0; c < kb2; ++c) {
           const int h = c & 1;
           mark3(a, t, 1300 + 16 * j + 2 * c);
-          mbar_wait_warp(m.a2_ready + h, static_cast<uint32_t>(a2_rdy[h] & 1));
+          wait_ready(m.a2_ready + h, static_cast<uint32_t>(a2_rdy[h] & 1));
           ++a2_rdy[h];
           fence_after();
           mark3(a, t, 1301 + 16 * j + 2 * c);
-          // A2 hi in TMEM (D1 in place), lo in shared memory: TS/SS pairs on B_hi, then TS on B_lo
+          // A2 hi in TMEM (D1 in place), lo in shared memory
           const uint32_t ah = tmem + kColD1 + 32 * c;
           const uint64_t al = sw128_desc(smem_u32(m.a2lo) + h * 16384u);
-          const uint64_t bh = take1(static_cast<uint32_t>(np2) * 128u);
+          take_group(2, rows_w2);
           for (int q = 0; q < 4; ++q)
-            mma_pair_elect(tmem + kColD2, ah + 8 * q, al + 2 * q, bh + 2 * q, id2, ((j | c) != 0 || q != 0) ? 1u : 0u);
-          release1();
-          const uint64_t bl = take1(static_cast<uint32_t>(np2) * 128u);
-          for (int q = 0; q < 4; ++q) mma_ts(tmem + kColD2, ah + 8 * q, bl + 2 * q, id2, 1u);
-          release1();
-          mma_commit_elect(m.a2_free + h);
-          ++a2_uses[h];
+            ts_pair(tmem + kColD2, ah + 8 * q, al + 2 * q, b[0] + 2 * q, id2, ((j | c) != 0 || q != 0) ? 1u : 0u);
+          for (int q = 0; q < 4; ++q) ts_one(tmem + kColD2, ah + 8 * q, b[1] + 2 * q, id2);
+          commit(m.a2_free + h);
+          a2_last = g;
+          release_group();
         }
       }
-      mma_commit_elect(m.d2_full);
+      commit(m.d2_full);
     }
   } else if (warp == kCostWarp) {
     // ------------------------------------------------ cost warp: 4 rows per thread
@@ -519,7 +592,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
 #pragma unroll
               for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
               store_operand_tt(tl + col_l0h(s), tl + col_l0l(s), w);
-              publish_chunk(m.a1_ready + s);
+              publish_chunk(m.a1_ready + s, PAIR);
               if (warp == 0) mark3(a, t, 2001 + 64 * j + 2 * kb);
             }
             if (rec && j == 0) {
@@ -564,7 +637,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
           for (int q = 0; q < 32; ++q)
             if (e < ka && q == ks + e) v[q] = u_nxt[e];
         store_operand(tl + kColXh, m.xlo, row, v);
-        publish_chunk(m.x_ready);
+        publish_chunk(m.x_ready, PAIR);
       };
       if (xw) {  // features of step 0
         float v[32];
@@ -603,7 +676,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
 #pragma unroll
               for (int q = 0; q < 32; ++q) w[q] = fmaxf(v[q], 0.f);
               store_operand(tl + kColD1 + 32 * c, m.a2lo + h * 16384, row, w);
-              publish_chunk(m.a2_ready + h);
+              publish_chunk(m.a2_ready + h, PAIR);
               if (warp == 4 || warp == 8) mark3(a, t, 3001 + 32 * j + 2 * c);
             }
             if (rec) {
@@ -646,9 +719,13 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
 
   fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM
   if (warp == 0) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -661,10 +738,36 @@ cudaError_t launch_rollout_tc3(const DevObjective& o, const RolloutArgs& a, cuda
   const size_t smem = rollout_tc3_smem(o);
   const long long grid = (a.n_rows + 127) / 128;
   if (grid <= 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(rollout_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // One CTA per tile by default; BP_TC3_PAIR=1 runs CTA pairs (clusters of two, cta_group::2:
+  // each CTA streams half of every weight block -- the same results bit for bit).  Measured on
+  // C5: pair 160 vs one CTA 165 TFLOP/s -- the pair's cross-CTA operand publishes wait for the
+  // epilogue's extrema atomics still in flight (as in rollout_tc2.cu's pair).
+  const char* env = std::getenv("BP_TC3_PAIR");
+  const bool pair = env != nullptr && env[0] == '1';
+  if (!pair) {
+    cudaError_t e = cudaFuncSetAttribute(rollout_tc3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    rollout_tc3_kernel<false><<<static_cast<unsigned>(grid), kThreads3, smem, st>>>(o, a);
+    return cudaGetLastError();
+  }
+  cudaError_t e = cudaFuncSetAttribute(rollout_tc3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  rollout_tc3_kernel<<<static_cast<unsigned>(grid), kThreads3, smem, st>>>(o, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((grid + 1) & ~1LL));
+  cfg.blockDim = dim3(kThreads3);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, rollout_tc3_kernel<true>, o, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

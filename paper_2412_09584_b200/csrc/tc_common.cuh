@@ -232,6 +232,29 @@ __device__ __forceinline__ void mma_tt_blo(uint32_t d, uint32_t a_hi, uint64_t b
         "r"(a_hi + 8 * q), "l"(b_lo + 2 * q), "r"(idesc));
 }
 
+// The same two halves for a CTA pair (cta_group::2, idesc with M = 256): issued by rank 0.
+__device__ __forceinline__ void mma_tt_bhi2(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi, uint32_t idesc,
+                                            uint32_t accum, int nq) {
+  for (int q = 0; q < nq; ++q)
+    asm volatile(
+        "{\n\t.reg .pred p, e, one;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 one, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %5, one;\n\t}\n" ::"r"(d),
+        "r"(a_hi + 8 * q), "r"(a_lo + 8 * q), "l"(b_hi + 2 * q), "r"((accum | q) != 0 ? 1u : 0u), "r"(idesc));
+}
+__device__ __forceinline__ void mma_tt_blo2(uint32_t d, uint32_t a_hi, uint64_t b_lo, uint32_t idesc, int nq) {
+  for (int q = 0; q < nq; ++q)
+    asm volatile(
+        "{\n\t.reg .pred e, one;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "setp.eq.b32 one, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, one;\n\t}\n" ::"r"(d),
+        "r"(a_hi + 8 * q), "l"(b_lo + 2 * q), "r"(idesc));
+}
+
 // ---- CTA pair (cta_group::2; tools/cta2_probe.cu checks the operand split): M = 256
 // rows across the two CTAs of a cluster (128 in each CTA's TMEM / shared memory), B's N
 // rows split between the CTAs' shared memory at the same offset (N/2 each), D = each

@@ -201,6 +201,24 @@ def test_tcgen05_v3_matches_oracle(device, name, shape):
     assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
 
 
+@pytest.mark.parametrize("name", ["c5", "ragged"])
+@pytest.mark.parametrize("shape", [(3, 37), (1, 300), (3, 130)])
+def test_tcgen05_v3_cta_pair_matches_one_cta(device, name, shape, monkeypatch):
+    """rollout_tc3.cu's CTA-pair form (BP_TC3_PAIR=1: clusters of two, cta_group::2 MMAs with
+    M = 256, each CTA streaming half of every weight block) computes the same rollouts as one
+    CTA per tile bit for bit; odd tile counts leave the last pair's second CTA empty."""
+    spec = v3_spec(name)
+    lo, hi = spec.box()
+    n_sub, rows = shape
+    acts = np.random.default_rng(6).uniform(lo, hi, size=(n_sub, rows, spec.d)).astype(np.float32)
+    dev = device.load(spec)
+    one = dev.rollout(acts, want_states=True)
+    monkeypatch.setenv("BP_TC3_PAIR", "1")
+    pair = dev.rollout(acts, want_states=True)
+    for x, y in zip(one, pair):
+        assert np.array_equal(x, y)
+
+
 def test_tcgen05_v3_rows_are_batch_invariant(device):
     spec = v3_spec("ragged")
     dev = device.load(spec)
