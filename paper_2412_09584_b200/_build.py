@@ -47,6 +47,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+CONSUMER_SRC = os.path.join(os.path.dirname(HERE), "tests", "native", "capi_consumer.cpp")
+CONSUMER = os.path.join(os.path.dirname(HERE), "tests", "native", "_capi_consumer")
+
+
+def build_consumer(force: bool = False) -> str:
+    """The compiled C++ consumer of the C-ABI (tests/native/capi_consumer.cpp), linked against the
+    in-tree libbabplan_cuda.so with an rpath to it."""
+    lib = build()
+    if force or _mtime(CONSUMER) < max(_mtime(CONSUMER_SRC), _mtime(lib), _mtime(os.path.join(os.path.dirname(HERE),
+                                                                                                 "include", "babplan_cuda.h"))):
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(os.path.dirname(HERE), "include"), CONSUMER_SRC,
+               "-L", OUT_DIR, "-lbabplan_cuda", f"-Wl,-rpath,{OUT_DIR}", "-o", CONSUMER]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return CONSUMER
+
+
 def build_variant(name: str, defines: list) -> str:
     """Dev helper: the library compiled with extra -D flags into _lib/variant_<name>.so
     (load it with BP_LIB_PATH); the product library is untouched."""

@@ -9,6 +9,7 @@
 // every rank of a multi-GPU run replays them on the same exchanged heads, so
 // decisions are identical on every rank).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1580,7 +1581,23 @@ struct Planner {
   // BP_STEP_PROFILE: host wall time per phase of step(), printed per iteration (dev aid)
   std::chrono::steady_clock::time_point ph_t;
   std::string ph_line;
+  // NVTX ranges per planner phase (nsys / ncu --nvtx): pick_out, split, search+bound+merge,
+  // gather, prune -- opened and closed at the same boundaries as the BP_STEP_PROFILE marks
+  bool nv_open = false;
+  void nvtx_phase(const char* done) {
+    const char* next = nullptr;
+    if (done == nullptr) next = "bab.pick_out";
+    else if (std::strcmp(done, "pick") == 0) next = "bab.split";
+    else if (std::strcmp(done, "split") == 0) next = "bab.search+bound+merge";
+    else if (std::strcmp(done, "merge+bound") == 0) next = "bab.gather";
+    else if (std::strcmp(done, "gather") == 0) next = "bab.prune";
+    else if (std::strcmp(done, "prune") != 0) return;  // nested marks (setup, search): no range change
+    if (nv_open) nvtxRangePop();
+    nv_open = next != nullptr;
+    if (nv_open) nvtxRangePushA(next);
+  }
   void phase(const char* name) {
+    nvtx_phase(name);
     static const bool on = std::getenv("BP_STEP_PROFILE") != nullptr;
     if (!on) return;
     const auto now = std::chrono::steady_clock::now();

@@ -30,14 +30,17 @@ pytestmark = pytest.mark.gpu
 
 # (config, rows per subdomain): the FP64 oracle bounds the sample size at width 256 / 512
 ROWS = {"c1": 96, "c2": 64, "c3": 24, "c4": 48, "c5": 16}
-# stated bars (max relative error over the sample), per config and kernel family; the
-# measured numbers are in DESIGN.md 5 and gpurun_out/he_init_errors.json
+# stated bars (max relative error over the sample), per config and kernel family: about twice
+# the measured maximum (DESIGN.md 5 lists max and p99 per config and path).  The tensor-core
+# paths sit 10-80x above FP32 here: the tensor pipe accumulates each 8-deep k-step into the FP32
+# accumulator with truncation, a bias of ~2^-24 |D| per MMA that a contractive (Glorot) network
+# forgets (<= 1e-5 there) and an expansive He-init rollout amplifies step over step.
 BAR = {
-    ("c1", "simt"): 1e-5, ("c1", "tcgen05"): 5e-5,
-    ("c2", "simt"): 5e-5, ("c2", "tcgen05"): 2e-4,
-    ("c3", "simt"): 2e-4, ("c3", "tcgen05"): 5e-4,
-    ("c4", "simt"): 5e-5, ("c4", "tcgen05"): 2e-4,
-    ("c5", "simt"): 5e-5, ("c5", "tcgen05"): 2e-4,
+    ("c1", "simt"): 2e-5, ("c1", "tcgen05"): 5e-5,
+    ("c2", "simt"): 2e-5, ("c2", "tcgen05"): 2.5e-4,
+    ("c3", "simt"): 2e-5, ("c3", "tcgen05"): 7e-4,
+    ("c4", "simt"): 2e-5, ("c4", "tcgen05"): 4e-4,
+    ("c5", "simt"): 2e-5, ("c5", "tcgen05"): 1.2e-3,
 }
 _RESULTS = {}
 
