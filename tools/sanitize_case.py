@@ -26,6 +26,7 @@ for name, path in cases:
     acts = rng.uniform(lo, hi, size=(2, 130, spec.d)).astype(np.float32)
     dev.rollout(acts, want_states=True)
     print(name, path, dev.rollout_kernel(), flush=True)
+dev.rollout_path("auto")
 os.environ["BP_TC2_PAIR"] = "1"
 dev.load(small_spec("c3"))
 dev.rollout(rng.uniform(-1, 1, size=(1, 300, small_spec("c3").d)).astype(np.float32))
