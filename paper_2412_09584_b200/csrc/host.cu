@@ -20,6 +20,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <set>
 #include <unordered_map>
 #include <memory>
 #include <numeric>
@@ -1330,62 +1331,90 @@ namespace {
 
 // pick_out (bab.cpp:85-153) over pool metadata; returns pool indices in pick order.
 std::vector<int> pick_indices(const bp_pool_meta* recs, int total, int n, double eta, double temperature, bp_rng& rng) {
+  // pick_out (bab.cpp:85-153), bit-exact: the greedy round(eta n) lowest (uf, index), then n - n1
+  // softmax picks over the rest in (uf, index) order with w = exp(-((lf - lo) / (hi - lo)) / T),
+  // (lo, hi) over the remaining finite lf, u = uniform() * (sequential sum of w) and the first record
+  // whose sequential prefix sum exceeds u.  The same arithmetic, organised for large pools:
+  //  * (lo, hi) from a sorted multiset of the remaining finite lf (O(log N) per pick);
+  //  * the weights are recomputed only when (lo, hi) moved (on host threads when the pool is
+  //    large: each w_i is the same std::exp expression), the prefix sums from the removed position
+  //    onward (the running sum in the reference's order), the selection by binary search on them.
   n = std::min(n, total);
   if (n <= 0) return {};
-  std::vector<int> order(static_cast<size_t>(total));
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int a, int b) {
-    return recs[a].uf != recs[b].uf ? recs[a].uf < recs[b].uf : a < b;
-  });
+  std::vector<std::pair<double, int>> key(static_cast<size_t>(total));  // (uf, index): the reference's order
+  for (int i = 0; i < total; ++i) key[static_cast<size_t>(i)] = {recs[i].uf, i};
+  std::sort(key.begin(), key.end());
   const int n1 = std::clamp(static_cast<int>(std::llround(eta * n)), 0, n);
-  std::vector<int> chosen(order.begin(), order.begin() + n1);
-  std::vector<int> rem(order.begin() + n1, order.end());
+  std::vector<int> chosen(static_cast<size_t>(n1));
+  for (int i = 0; i < n1; ++i) chosen[static_cast<size_t>(i)] = key[static_cast<size_t>(i)].second;
+  std::vector<int> rem(static_cast<size_t>(total - n1));
+  for (size_t i = 0; i < rem.size(); ++i) rem[i] = key[static_cast<size_t>(n1) + i].second;
+  if (n == n1) return chosen;
   const double temp = std::max(temperature, 1e-12);
-  // The weights depend on a record's lf and on (lo, hi) over the remaining records only,
-  // so they are recomputed (exp per record) only when a pick moved lo or hi; the sum is
-  // re-accumulated in pool order every pick, exactly as the reference does.
-  std::vector<double> w;
+  // (lo, hi) over the remaining finite lf: the finite lf sorted once, two cursors skipping removed ones
+  std::vector<std::pair<double, int>> by_lf;  // (lf, rem position)
+  by_lf.reserve(rem.size());
+  for (size_t i = 0; i < rem.size(); ++i)
+    if (std::isfinite(recs[rem[i]].lf)) by_lf.push_back({recs[rem[i]].lf, static_cast<int>(i)});
+  std::sort(by_lf.begin(), by_lf.end());
+  size_t lo_c = 0, hi_c = by_lf.size();  // remaining finite records are within [lo_c, hi_c)
+  // removed records stay in place with weight 0: adding +0.0 leaves every running sum bit for bit
+  // as the reference's sum over the remaining records, and a removed position can never be the
+  // first prefix above u (its prefix equals its predecessor's)
+  const size_t m = rem.size();
+  std::vector<double> w(m), pre(m);
+  std::vector<char> alive(m, 1);
+  size_t last_alive = m - 1;
   double w_lo = std::numeric_limits<double>::quiet_NaN(), w_hi = w_lo;
-  bool w_deg = false;
+  bool w_deg = false, have_w = false;
+  size_t dirty = 0;  // prefix sums valid below this position
   for (int need = n - n1; need > 0; --need) {
-    double lo = std::numeric_limits<double>::infinity(), hi = -lo;
-    for (int idx : rem) {
-      const double lf = recs[idx].lf;
-      if (std::isfinite(lf)) {
-        lo = std::min(lo, lf);
-        hi = std::max(hi, lf);
-      }
-    }
+    while (lo_c < hi_c && !alive[static_cast<size_t>(by_lf[lo_c].second)]) ++lo_c;
+    while (hi_c > lo_c && !alive[static_cast<size_t>(by_lf[hi_c - 1].second)]) --hi_c;
+    const double lo = lo_c < hi_c ? by_lf[lo_c].first : std::numeric_limits<double>::infinity();
+    const double hi = lo_c < hi_c ? by_lf[hi_c - 1].first : -std::numeric_limits<double>::infinity();
     const bool degenerate = !(hi > lo);
-    if (w.empty() || degenerate != w_deg || (!degenerate && (lo != w_lo || hi != w_hi))) {  // w, rem kept in step
-      w.assign(rem.size(), 0.0);
-      for (size_t i = 0; i < rem.size(); ++i) {
-        double scaled = 0.5;
-        if (!degenerate) {
-          const double lf = recs[rem[i]].lf;
-          scaled = std::isfinite(lf) ? (lf - lo) / (hi - lo) : (lf < 0.0 ? 0.0 : 1.0);
+    if (!have_w || degenerate != w_deg || (!degenerate && (lo != w_lo || hi != w_hi))) {
+      auto fill = [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+          if (!alive[i]) {
+            w[i] = 0.0;
+            continue;
+          }
+          double scaled = 0.5;
+          if (!degenerate) {
+            const double lf = recs[rem[i]].lf;
+            scaled = std::isfinite(lf) ? (lf - lo) / (hi - lo) : (lf < 0.0 ? 0.0 : 1.0);
+          }
+          w[i] = degenerate ? 1.0 : std::exp(-scaled / temp);
         }
-        w[i] = degenerate ? 1.0 : std::exp(-scaled / temp);
+      };
+      const int nt = m >= 32768 ? std::min(host_threads(), 16) : 1;
+      if (nt <= 1) {
+        fill(0, m);
+      } else {
+        std::vector<std::thread> th;
+        for (int q = 0; q < nt; ++q) th.emplace_back(fill, m * q / nt, m * (q + 1) / nt);
+        for (auto& x : th) x.join();
       }
       w_lo = lo;
       w_hi = hi;
       w_deg = degenerate;
+      have_w = true;
+      dirty = 0;
     }
-    double sum = 0.0;
-    for (size_t i = 0; i < rem.size(); ++i) sum += w[i];
-    const double u = rng.uniform() * sum;
-    double acc = 0.0;
-    size_t sel = rem.size() - 1;
-    for (size_t i = 0; i < rem.size(); ++i) {
-      acc += w[i];
-      if (u < acc) {
-        sel = i;
-        break;
-      }
-    }
-    chosen.push_back(rem[sel]);
-    rem.erase(rem.begin() + static_cast<std::ptrdiff_t>(sel));
-    w.erase(w.begin() + static_cast<std::ptrdiff_t>(sel));  // the other records' weights stand unless lo / hi move
+    double acc = dirty == 0 ? 0.0 : pre[dirty - 1];
+    for (size_t i = dirty; i < m; ++i) pre[i] = acc = acc + w[i];
+    const double u = rng.uniform() * pre[m - 1];
+    // first position with u < pre[i]; none: the last remaining record (the reference's fallback)
+    size_t sel = static_cast<size_t>(std::upper_bound(pre.begin(), pre.end(), u) - pre.begin());
+    if (sel >= m) sel = last_alive;
+    const int idx = rem[sel];
+    chosen.push_back(idx);
+    alive[sel] = 0;
+    w[sel] = 0.0;  // the other records' weights stand unless lo / hi move
+    while (last_alive > 0 && !alive[last_alive]) --last_alive;
+    dirty = sel;
   }
   return chosen;
 }

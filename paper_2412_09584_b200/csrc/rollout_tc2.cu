@@ -82,7 +82,13 @@ __device__ __forceinline__ void put2(const RolloutArgs&, int, int, long long) {}
 #endif
 constexpr int kSlots = 8;  // weight blocks in flight at most (mbarrier pairs)
 // __nanosleep backoff (ns) of the long waits: producer / cost warp / epilogue
-constexpr uint32_t kSleepProducer = 256, kSleepCost = 128, kSleepEpi = 64;
+#ifndef BP_TC2_SLEEP_PRODUCER
+#define BP_TC2_SLEEP_PRODUCER 256
+#endif
+#ifndef BP_TC2_SLEEP_EPI
+#define BP_TC2_SLEEP_EPI 64
+#endif
+constexpr uint32_t kSleepProducer = BP_TC2_SLEEP_PRODUCER, kSleepCost = 128, kSleepEpi = BP_TC2_SLEEP_EPI;
 
 // A_lo K-block slots per tile: two at width 256 (the rest of shared memory goes to the
 // weight ring, which then holds two K-blocks' weights), four for a CTA pair (its weight

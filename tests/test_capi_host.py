@@ -176,6 +176,22 @@ def test_pick_out_bit_exact_on_large_pools():
             assert product_pick(meta, n, eta, T, 7 + trial) == orc.pick_out(meta, n, eta, T, orc.Rng(7 + trial))
 
 
+def test_pick_out_bit_exact_on_multi_gpu_sized_pools():
+    """Pools above the threaded weight recompute (>= 32768 records: each w_i computed on a host
+    thread, the running sums kept in the reference's order with removed records at weight 0),
+    with tied uf / lf values and +-inf bounds, and picks that drain the low end (lo moves)."""
+    rng = np.random.default_rng(21)
+    n_pool = 40000
+    lf = np.round(rng.normal(size=n_pool) * 8, 1)  # many ties
+    lf[rng.random(n_pool) < 0.02] = -math.inf
+    lf[rng.random(n_pool) < 0.01] = math.inf
+    uf = np.round(lf + rng.exponential(size=n_pool), 1)
+    uf[~np.isfinite(uf)] = math.inf
+    meta = [(float(lf[i]), float(uf[i]), i, -0.1 * i) for i in range(n_pool)]
+    for n, eta, T in ((1024, 0.75, 0.05), (300, 0.0, 1e-3)):
+        assert product_pick(meta, n, eta, T, 3) == orc.pick_out(meta, n, eta, T, orc.Rng(3))
+
+
 def test_workloads_rng_is_the_reference_stream_without_the_cuda_library():
     """workloads.Rng (pure Python mt19937_64 + Box-Muller) draws the reference Rng stream bit for
     bit (rng.hpp:12-35, rng.cpp:20-35; std::mt19937_64 10000th-output KAT), so the bench's
