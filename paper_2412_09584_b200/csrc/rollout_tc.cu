@@ -194,11 +194,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 
 // Writes 32 consecutive K-values of this thread's row as the hi / lo A operand in TMEM.
 __device__ __forceinline__ void store_operand_tmem(uint32_t tlane, int chunk, const float (&v)[32]) {
-  // hi = rna_tf32(v), lo = rna_tf32(v - hi) (split_tf32): unbiased, within 2^-22 |v|.
-  float h[32], l[32];
+  // hi = v (the tensor core truncates it), lo = rna_tf32(v - trunc(v)): unbiased, within 2^-21 |v|.
+  tmem_st32(tlane + kColAhi + 32 * chunk, v);
+  float l[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) split_tf32(v[j], h[j], l[j]);
-  tmem_st32(tlane + kColAhi + 32 * chunk, h);
+  for (int j = 0; j < 32; ++j) l[j] = rna_tf32(v[j] - __uint_as_float(__float_as_uint(v[j]) & 0xffffe000u));
   tmem_st32(tlane + kColAlo + 32 * chunk, l);
 }
 

@@ -615,10 +615,8 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
         for (int e = 0; e < 8; ++e) {
           const int j = u0 + e;
           if (e < ka && j >= 0 && j < 32) {
-            float uh, ul;
-            split_tf32(u_nxt[e], uh, ul);
-            tmem_st1(t_hi + j, uh);
-            line[(((j >> 2) ^ (row & 7)) << 2) + (j & 3)] = ul;
+            tmem_st1(t_hi + j, u_nxt[e]);
+            line[(((j >> 2) ^ (row & 7)) << 2) + (j & 3)] = lo_tf32(u_nxt[e]);
           }
         }
       }

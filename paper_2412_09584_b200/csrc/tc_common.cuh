@@ -16,15 +16,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 // 3xTF32 operand split of an activation: hi = rna_tf32(x) and lo = rna_tf32(x - hi), both
 // with their 13 low mantissa bits zero, so kind::tf32 (which reads the top 19 bits) sees
-// them exactly.  x - hi is exact; hi + lo is within 2^-22 |x| of x and unbiased (truncating
-// hi or lo instead biases every activation toward zero by ~2^-21, which expansive rollouts
-// amplify step over step).
+// them exactly.  x - hi is exact; hi + lo is within 2^-22 |x| of x and unbiased (a truncated
+// lo instead biases every activation toward zero by ~2^-21, which expansive rollouts amplify
+// step over step).
 __device__ __forceinline__ float rna_tf32_dev(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = rna_tf32_dev(x);
   lo = rna_tf32_dev(x - hi);
+}
+// Cheaper epilogue form: hi is stored as x itself (kind::tf32 truncates it to its top 19 bits),
+// lo = rna_tf32(x - trunc_tf32(x)) -- exact difference, rounded to nearest: within 2^-21 |x| of x
+// and unbiased (only a truncated lo would bias the operand toward zero).
+__device__ __forceinline__ float lo_tf32(float x) {
+  return rna_tf32_dev(x - __uint_as_float(__float_as_uint(x) & 0xffffe000u));
 }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.

@@ -145,30 +145,24 @@ __device__ __forceinline__ void warp_chunk_extrema(const RolloutArgs& a, const f
   }
 }
 
-// hi / lo parts of one 32-column K-block of this thread's row (split_tf32): lo into the
-// row's 128-byte line of the SW128 K-block in shared memory (four values at a time, so no
-// second 32-register array is live), then hi in place into TMEM.  v is clobbered.
+// hi / lo parts of one 32-column K-block of this thread's row: lo = lo_tf32(x) into the row's
+// 128-byte line of the SW128 K-block in shared memory (four values at a time), then x itself as
+// hi into TMEM (the tensor core truncates it).
 __device__ __forceinline__ void store_operand(uint32_t t_hi, unsigned char* lo_blk, int row, float (&v)[32]) {
   float4* line = reinterpret_cast<float4*>(lo_blk + row * 128);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float l[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) l[e] = rna_tf32_dev(v[4 * q + e] - rna_tf32_dev(v[4 * q + e]));
-    line[q ^ (row & 7)] = make_float4(l[0], l[1], l[2], l[3]);
-  }
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = rna_tf32_dev(v[j]);
+  for (int q = 0; q < 8; ++q)
+    line[q ^ (row & 7)] = make_float4(lo_tf32(v[4 * q]), lo_tf32(v[4 * q + 1]), lo_tf32(v[4 * q + 2]), lo_tf32(v[4 * q + 3]));
   tmem_st32(t_hi, v);
 }
 
 // hi / lo parts of one 32-column K-block of this thread's row, both into TMEM (TS-only
-// operands).  v is clobbered.
+// operands): hi = x (truncated by the tensor core), lo = lo_tf32(x).
 __device__ __forceinline__ void store_operand_tt(uint32_t t_hi, uint32_t t_lo, float (&v)[32]) {
+  tmem_st32(t_hi, v);
   float l[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) split_tf32(v[j], v[j], l[j]);
-  tmem_st32(t_hi, v);
+  for (int j = 0; j < 32; ++j) l[j] = lo_tf32(v[j]);
   tmem_st32(t_lo, l);
 }
 
