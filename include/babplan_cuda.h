@@ -286,6 +286,17 @@ bp_status bp_result_free(bp_result* r);
 bp_status bp_timing(bp_ctx* ctx, double* rollout_ms, int64_t* rollout_launches, double* bound_ms,
                     double* search_ms, int64_t* launches);
 
+/* Plan log (decision replay; test aid): with logging on, every plan records, per searched child in
+ * the order the planner created it (root first; one rank), its iteration, box, search report (uf,
+ * best, top list ascending, samples, ok) and lower bound -- the inputs the reference plan()
+ * (bab.cpp:266-415) takes from batch_search and the bounder, so its own pick_out / split / merge /
+ * prune can be replayed on them and compared (tests/test_gpu_plan_replay.py).  get fills arrays of
+ * n_children (boxes, best: n_children x d; top values / actions concatenated in child order). */
+bp_status bp_set_plan_log(bp_ctx* ctx, int enable);
+bp_status bp_plan_log_size(bp_ctx* ctx, int* n_children, int* total_top);
+bp_status bp_plan_log_get(bp_ctx* ctx, int* iter, double* lo, double* hi, double* lf, double* uf, double* best,
+                          int* n_top, double* top_val, double* top_act, int64_t* samples, int* ok);
+
 /* Boxes searched since the previous call, and how many of them failed (a non-finite
  * rollout value: SearchReport.ok = false, search.cpp:273-278; their rows are skipped by
  * the rollout and they are bounded by interval propagation). */

@@ -1701,6 +1701,11 @@ void merge_report(SubdomainRecord& rec, SearchReport&& rep, int top_capacity) { 
   }
 }
 
+namespace {
+thread_local const PlanReplay* g_replay = nullptr;
+}  // namespace
+void set_plan_replay(const PlanReplay* replay) { g_replay = replay; }
+
 PlanResult plan(std::shared_ptr<const Objective> objective, const BoxDomain& root, const PlannerConfig& cfg,
                 std::shared_ptr<const Bounder> bounder, const Vec* warm_start) {  // bab.cpp:266-415
   if (!objective) throw std::invalid_argument("plan: null objective");
@@ -1745,14 +1750,15 @@ PlanResult plan(std::shared_ptr<const Objective> objective, const BoxDomain& roo
     SearcherConfig scfg = cfg.search;
     scfg.seed = mix_seed(cfg.seed, 0);
     const std::vector<const Vec*> warms{warm_start};
-    std::vector<SearchReport> reports = batch_search(*objective, {root}, scfg, &warms);
+    std::vector<SearchReport> reports =
+        g_replay ? std::vector<SearchReport>{g_replay->report(0, 0, root)} : batch_search(*objective, {root}, scfg, &warms);
     SearchReport& rep = reports[0];
     if (!rep.ok) throw std::runtime_error("plan: root search failed: " + rep.error);
     SubdomainRecord rec;
     rec.box = root;
     rec.id = 0;
     rec.log_vol = 0.0;
-    rec.lf = bounder->lower(root, &rep);
+    rec.lf = g_replay ? g_replay->lf(0, 0) : bounder->lower(root, &rep);
     merge_report(rec, std::move(reports[0]), cfg.search.top_capacity);
     result.uf = rec.uf;
     result.best = rec.best;
@@ -1792,14 +1798,22 @@ PlanResult plan(std::shared_ptr<const Objective> objective, const BoxDomain& roo
       }
       SearcherConfig scfg = cfg.search;
       scfg.seed = mix_seed(cfg.seed, static_cast<std::uint64_t>(iter) + 1);
-      std::vector<SearchReport> reports = batch_search(*objective, boxes, scfg, &warms);
-      // The reference bounds children serially (bab.cpp:392-403); the
-      // bounds are independent, so the oracle fans them out like batch_search.
+      std::vector<SearchReport> reports;
       std::vector<double> lfs(children.size());
-      parallel_chunks(static_cast<std::int64_t>(children.size()), [&](std::int64_t b, std::int64_t e) {
-        for (std::int64_t i = b; i < e; ++i)
-          lfs[static_cast<size_t>(i)] = bounder->lower(children[static_cast<size_t>(i)].box, &reports[static_cast<size_t>(i)]);
-      });
+      if (g_replay) {
+        for (size_t i = 0; i < children.size(); ++i) {
+          reports.push_back(g_replay->report(iter, static_cast<int>(i), children[i].box));
+          lfs[i] = g_replay->lf(iter, static_cast<int>(i));
+        }
+      } else {
+        reports = batch_search(*objective, boxes, scfg, &warms);
+        // The reference bounds children serially (bab.cpp:392-403); the
+        // bounds are independent, so the oracle fans them out like batch_search.
+        parallel_chunks(static_cast<std::int64_t>(children.size()), [&](std::int64_t b, std::int64_t e) {
+          for (std::int64_t i = b; i < e; ++i)
+            lfs[static_cast<size_t>(i)] = bounder->lower(children[static_cast<size_t>(i)].box, &reports[static_cast<size_t>(i)]);
+        });
+      }
       for (size_t i = 0; i < children.size(); ++i) {
         SubdomainRecord& c = children[i];
         result.samples += reports[i].samples;

@@ -284,6 +284,15 @@ struct SearchHooks {
                      const SearchReport& so_far, const std::vector<TopSample>& top)> after;
 };
 void set_search_hooks(const SearchHooks* hooks);  // thread-local; null = none
+
+// Test hook (not in the reference): plan() takes each child's search report and lower bound from
+// `report` / `lf` (iteration, index of the child in the iteration's order, its box) instead of
+// running batch_search and the bounder -- the plan-level decision replay against the device planner.
+struct PlanReplay {
+  std::function<SearchReport(int iter, int index, const BoxDomain& box)> report;
+  std::function<double(int iter, int index)> lf;
+};
+void set_plan_replay(const PlanReplay* replay);  // thread-local; null = none
 std::vector<SearchReport> batch_search(const Objective& f, const std::vector<BoxDomain>& boxes,
                                        const SearcherConfig& cfg,
                                        const std::vector<const Vec*>* warm_starts = nullptr);

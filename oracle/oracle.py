@@ -387,12 +387,40 @@ class Objective:
                                  C.byref(h)))
         return Reports(h, self, lo, hi)
 
+    def plan_replay(self, cfg: dict, log: dict) -> dict:
+        """plan() (bab.cpp:266-415) taking every child's search report and bound from a device plan
+        log (Device.plan_log()) instead of searching and bounding: the decisions (pick_out, split,
+        merge_report, prune, the incumbent and the trace) are the oracle's own.  Adds box_mismatch
+        (children whose box differs from the device's) and order_mismatch to the plan dict."""
+        packed = PackedConfig(cfg, "babnd")
+        n = len(log["lf"])
+        n_top = np.ascontiguousarray(log["n_top"], dtype=np.int32)
+        off = np.zeros(n, dtype=np.int32)
+        if n > 1:
+            off[1:] = np.cumsum(n_top)[:-1]
+        arrs = {k: np.ascontiguousarray(log[k], dtype=np.float64) for k in ("lo", "hi", "lf", "uf", "best", "top_val", "top_act")}
+        it = np.ascontiguousarray(log["iter"], dtype=np.int32)
+        samples = np.ascontiguousarray(log["samples"], dtype=np.int64)
+        ok = np.ascontiguousarray(log["ok"], dtype=np.int32)
+        bm, om = C.c_int(), C.c_int()
+        h = vp()
+        ck(lib().or_plan_replay(self.h, packed.ref(), C.c_int(n), it.ctypes.data_as(ip), *[arrs[k].ctypes.data_as(dp) for k in ("lo", "hi", "lf", "uf", "best")],
+                                n_top.ctypes.data_as(ip), off.ctypes.data_as(ip), arrs["top_val"].ctypes.data_as(dp),
+                                arrs["top_act"].ctypes.data_as(dp), samples.ctypes.data_as(C.POINTER(C.c_int64)),
+                                ok.ctypes.data_as(ip), C.byref(bm), C.byref(om), C.byref(h)))
+        res = self._plan_result(h)
+        res["box_mismatch"], res["order_mismatch"] = bm.value, om.value
+        return res
+
     def plan(self, cfg: dict, warm=None, method: str = "babnd") -> dict:
         packed = PackedConfig(cfg, method)
         w = _d(warm)
         h = vp()
         ck(lib().or_plan(self.h, packed.ref(), w.ctypes.data_as(dp) if w is not None else None,
                          1 if method == "babnd" else 0, C.byref(h)))
+        return self._plan_result(h)
+
+    def _plan_result(self, h) -> dict:
         try:
             uf, mlf = C.c_double(), C.c_double()
             cert, iters = C.c_int(), C.c_int()

@@ -729,6 +729,68 @@ int or_plan(void* h, const bp_planner_config* cfg, const double* warm, int metho
     *out = ph;
   });
 }
+// plan() replaying the device planner's per-child search reports and bounds (PlanReplay): child c
+// (in the order plan() creates them, root first) takes iteration it[c], box lo/hi (checked against
+// the oracle's own split: a mismatch is counted), lf, uf, best, its top list (n_top, values,
+// actions, ascending) and samples.  Returns the plan; *box_mismatch counts boxes that differed,
+// *order_mismatch requests that did not match the log's (iteration, index) sequence.
+int or_plan_replay(void* h, const bp_planner_config* cfg, int n_log, const int* it, const double* lo, const double* hi,
+                   const double* lf, const double* uf, const double* best, const int* n_top, const int* top_off,
+                   const double* top_val, const double* top_act, const int64_t* samples, const int* ok, int* box_mismatch,
+                   int* order_mismatch, void** out) {
+  return guard([&] {
+    const int d = O->obj->dim();
+    int cursor = 0, iter_base = 0, cur_iter = 0;
+    *box_mismatch = 0;
+    *order_mismatch = 0;
+    PlanReplay rp;
+    rp.report = [&](int iter, int index, const BoxDomain& box) {
+      if (iter != cur_iter) {
+        iter_base = cursor;
+        cur_iter = iter;
+      }
+      const int c = iter_base + index;
+      if (c >= n_log || it[c] != iter) {
+        ++*order_mismatch;
+        throw std::runtime_error("plan replay: the oracle asked for a child the device did not search");
+      }
+      cursor = std::max(cursor, c + 1);
+      for (int j = 0; j < d; ++j)
+        if (box.lower()[static_cast<size_t>(j)] != lo[static_cast<size_t>(c) * d + j] ||
+            box.upper()[static_cast<size_t>(j)] != hi[static_cast<size_t>(c) * d + j]) {
+          ++*box_mismatch;
+          break;
+        }
+      SearchReport r;
+      r.ok = ok[c] != 0;
+      if (!r.ok) {
+        r.error = "evaluate: non-finite objective value (malformed weights?)";
+        return r;
+      }
+      r.uf = uf[c];
+      r.best = vec_of(best + static_cast<size_t>(c) * d, d);
+      r.samples = samples[c];
+      for (int k = 0; k < n_top[c]; ++k) {
+        const size_t o = static_cast<size_t>(top_off[c]) + k;
+        r.top.push_back({top_val[o], vec_of(top_act + o * d, d)});
+      }
+      return r;
+    };
+    rp.lf = [&](int iter, int index) { return lf[(iter == cur_iter ? iter_base : cursor) + index]; };
+    auto* ph = new PlanHandle();
+    set_plan_replay(&rp);
+    try {
+      ph->r = plan(O->obj, O->box, planner_cfg(*cfg), nullptr, nullptr);
+    } catch (...) {
+      set_plan_replay(nullptr);
+      delete ph;
+      throw;
+    }
+    set_plan_replay(nullptr);
+    *out = ph;
+  });
+}
+
 void or_plan_free(void* p) { delete static_cast<PlanHandle*>(p); }
 int or_plan_summary(void* p, double* uf, double* min_lf, int* certified, int64_t* samples, int* iterations,
                     char* stop, int cap, double* best) {

@@ -92,7 +92,7 @@ class PoolMeta(C.Structure):
 EXPORTS = [
     "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_alltoall", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds", "bp_gradient",
     "bp_load_objective", "bp_load_synthetic",
-    "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_search_update", "bp_search_counters", "bp_report_summary", "bp_report_top",
+    "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_search_update", "bp_search_counters", "bp_set_plan_log", "bp_plan_log_size", "bp_plan_log_get", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
     "bp_planner_finish", "bp_planner_destroy", "bp_result_summary", "bp_result_best",
     "bp_result_trace", "bp_result_free", "bp_timing", "bp_rng_new", "bp_rng_free",
@@ -155,6 +155,9 @@ def load() -> C.CDLL:
             "bp_result_trace": (C.c_int, [vp, C.POINTER(TraceRow), C.c_int]),
             "bp_result_free": (C.c_int, [vp]),
             "bp_search_counters": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+            "bp_set_plan_log": (C.c_int, [vp, C.c_int]),
+            "bp_plan_log_size": (C.c_int, [vp, _ip, _ip]),
+            "bp_plan_log_get": (C.c_int, [vp, _ip, _dp, _dp, _dp, _dp, _dp, _ip, _dp, _dp, C.POINTER(C.c_int64), _ip]),
             "bp_timing": (C.c_int, [vp, _dp, C.POINTER(C.c_int64), _dp, _dp, C.POINTER(C.c_int64)]),
             "bp_rng_new": (C.c_int, [C.c_uint64, C.POINTER(vp)]),
             "bp_rng_free": (C.c_int, [vp]),

@@ -294,6 +294,25 @@ class Device:
                 "launches": l.value}
 
 
+    def plan_log(self, enable: Optional[bool] = None) -> Optional[dict]:
+        """Decision-replay log of the plans run on this device (bp_set_plan_log): enable / disable
+        with a bool; with no argument, the log of the last plan as arrays in child order."""
+        if enable is not None:
+            check(self.lib.bp_set_plan_log(self.h, 1 if enable else 0))
+            return None
+        n, tot = C.c_int(), C.c_int()
+        check(self.lib.bp_plan_log_size(self.h, C.byref(n), C.byref(tot)))
+        n, tot, d = n.value, tot.value, self.spec.d
+        out = {"iter": np.zeros(n, np.int32), "lo": np.zeros((n, d)), "hi": np.zeros((n, d)), "lf": np.zeros(n),
+               "uf": np.zeros(n), "best": np.zeros((n, d)), "n_top": np.zeros(n, np.int32),
+               "top_val": np.zeros(max(tot, 1)), "top_act": np.zeros((max(tot, 1), d)),
+               "samples": np.zeros(n, np.int64), "ok": np.zeros(n, np.int32)}
+        check(self.lib.bp_plan_log_get(self.h, _capi.iptr(out["iter"]), _capi.dptr(out["lo"]), _capi.dptr(out["hi"]),
+                                       _capi.dptr(out["lf"]), _capi.dptr(out["uf"]), _capi.dptr(out["best"]),
+                                       _capi.iptr(out["n_top"]), _capi.dptr(out["top_val"]), _capi.dptr(out["top_act"]),
+                                       out["samples"].ctypes.data_as(C.POINTER(C.c_int64)), _capi.iptr(out["ok"])))
+        return out
+
     def search_counters(self) -> dict:
         """Boxes searched and boxes whose search failed (non-finite rollout) since the previous call."""
         b, f = C.c_int64(), C.c_int64()

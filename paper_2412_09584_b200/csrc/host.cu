@@ -847,6 +847,16 @@ struct bp_ctx {
   int reserve_boxes = 0;
   std::vector<int> h_failed;
   int64_t boxes_searched = 0, boxes_failed = 0;  // bp_search_counters
+  // plan log (bp_set_plan_log): per searched child of a plan, in the order the planner created it --
+  // the decision-replay test feeds these reports and bounds to the oracle's plan()
+  struct LogChild {
+    int iter;
+    std::vector<double> lo, hi;
+    double lf;
+    Report rep;
+  };
+  bool plan_log_on = false;
+  std::vector<LogChild> plan_log;
   std::vector<Report> reports;
   // sharding: rank / world and the allgather hook (host buffers)
   int rank = 0, world = 1;
@@ -1699,6 +1709,16 @@ struct Planner {
     phase("setup");
     search_run(c, a, scfg);
     phase("search");
+    std::vector<Report> log_reps;
+    std::vector<double> log_lo, log_hi;
+    if (c->plan_log_on) {  // the children's search reports and boxes, before the merge
+      search_harvest(c, a, scfg, &log_reps);
+      log_lo.resize(static_cast<size_t>(n) * d);
+      log_hi.resize(static_cast<size_t>(n) * d);
+      ck(cudaMemcpyAsync(log_lo.data(), S.lo_d, log_lo.size() * 8, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaMemcpyAsync(log_hi.data(), S.hi_d, log_hi.size() * 8, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+    }
     const size_t nb = static_cast<size_t>(std::max(n, c->reserve_boxes));  // no reallocation while ramping up
     int* ds = d_slots.get(nb);
     ck(memcpy_counted(ds, slots.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st), "H2D");
@@ -1720,6 +1740,14 @@ struct Planner {
     }
     c->search_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count();
     c->harvest_roll_events();
+    if (c->plan_log_on)
+      for (int i = 0; i < n; ++i)
+        c->plan_log.push_back({iter,
+                               std::vector<double>(log_lo.begin() + static_cast<std::ptrdiff_t>(i) * d,
+                                                   log_lo.begin() + static_cast<std::ptrdiff_t>(i + 1) * d),
+                               std::vector<double>(log_hi.begin() + static_cast<std::ptrdiff_t>(i) * d,
+                                                   log_hi.begin() + static_cast<std::ptrdiff_t>(i + 1) * d),
+                               o.lf[static_cast<size_t>(i)], log_reps[static_cast<size_t>(i)]});
     return o;
   }
 
@@ -1737,6 +1765,7 @@ struct Planner {
         t0(std::chrono::steady_clock::now()), slab(ctx, ctx->comp.d, std::max(config.search.top_capacity, 1)),
         pick_rng(mix_seed(config.seed, 1)) {
     if (cfg.batch <= 0) fail(BP_INVALID_ARGUMENT, "plan: batch must be positive");
+    c->plan_log.clear();
     const int W = world();
     // at most 2 * batch children per step, ceil(2 * batch / W) of them on this rank
     c->reserve_boxes = std::max(c->reserve_boxes, (2 * cfg.batch + W - 1) / W);
@@ -2583,6 +2612,50 @@ bp_status bp_result_trace(const bp_result* r, bp_trace_row* rows, int cap) {
 bp_status bp_result_free(bp_result* r) {
   delete r;
   return BP_OK;
+}
+
+bp_status bp_set_plan_log(bp_ctx* ctx, int enable) {
+  return guard([&] {
+    check_ctx(ctx);
+    ctx->plan_log_on = enable != 0;
+    ctx->plan_log.clear();
+  });
+}
+
+bp_status bp_plan_log_size(bp_ctx* ctx, int* n_children, int* total_top) {
+  return guard([&] {
+    check_ctx(ctx);
+    int tot = 0;
+    for (const auto& e : ctx->plan_log) tot += static_cast<int>(e.rep.top_val.size());
+    if (n_children) *n_children = static_cast<int>(ctx->plan_log.size());
+    if (total_top) *total_top = tot;
+  });
+}
+
+bp_status bp_plan_log_get(bp_ctx* ctx, int* iter, double* lo, double* hi, double* lf, double* uf, double* best, int* n_top,
+                          double* top_val, double* top_act, int64_t* samples, int* ok) {
+  return guard([&] {
+    check_ctx(ctx);
+    const int d = ctx->comp.d;
+    size_t off = 0;
+    for (size_t c = 0; c < ctx->plan_log.size(); ++c) {
+      const auto& e = ctx->plan_log[c];
+      iter[c] = e.iter;
+      std::copy(e.lo.begin(), e.lo.end(), lo + c * d);
+      std::copy(e.hi.begin(), e.hi.end(), hi + c * d);
+      lf[c] = e.lf;
+      uf[c] = e.rep.ok ? e.rep.uf : INFINITY;
+      for (int j = 0; j < d; ++j) best[c * d + j] = e.rep.ok && !e.rep.best.empty() ? e.rep.best[static_cast<size_t>(j)] : 0.0;
+      n_top[c] = static_cast<int>(e.rep.top_val.size());
+      for (size_t k = 0; k < e.rep.top_val.size(); ++k) {
+        top_val[off + k] = e.rep.top_val[k];
+        for (int j = 0; j < d; ++j) top_act[(off + k) * d + j] = e.rep.top_act[k * d + static_cast<size_t>(j)];
+      }
+      off += e.rep.top_val.size();
+      samples[c] = e.rep.ok ? e.rep.samples : 0;
+      ok[c] = e.rep.ok ? 1 : 0;
+    }
+  });
 }
 
 bp_status bp_search_counters(bp_ctx* ctx, int64_t* boxes, int64_t* failed) {
