@@ -19,6 +19,7 @@ struct DevOp {
   int c0, c1;    // scratch columns of src0 / src1 (c1 = -1 without a second argument)
   int stat;      // offset of its recorded extrema within one step's record, -1 if not recorded
   int stop;      // RELU op anchored as the last-ReLU stop at step H
+  int folded;    // LINEAR on x_t computed by the v2 rollout's output-layer MMA (extra N columns)
   // float arena offsets (forward)
   int w, b, tgt, wt, ctr;
   // double arena offsets (bound)
@@ -64,6 +65,10 @@ struct DevObjective {
   // weight ring bytes.  The tc_w images of layers wider than 128 hold per K-block two N halves
   // [kb][half][hi|lo][rows x 32] (half 0 = 128 rows); narrower layers are the v1 layout.
   int tc2, tc2_rw, tc2_ring;  // tc2_rw: TMEM region width (128 or 256 columns)
+  // v2 output-layer folding: the cost program's LINEAR ops on x_t become extra output columns
+  // ks .. ks + fold_n - 1 of the last layer's MMA (W_op W_L, W_op b_L + b_op); int arena
+  // fold_list: the scratch column of each extra output column
+  int fold_n, fold_list;
   int tc2_pair;               // width 256 as a CTA pair (cta_group::2): every layer 256 wide or <= 128 in 32s
   // tcgen05 v3 (rollout_tc3.cu): three layers [K0 <= 32, N0 <= 512, N1 <= 512, N2 <= 32], relu after
   // the hidden two; layer 1 in N chunks of <= 256 with layer 0 recomputed per chunk

@@ -448,6 +448,7 @@ Compiled compile(const bp_objective_desc& d) {
     p.weight_by_step = s.weight_by_step;
     p.stat = -1;
     p.stop = 0;
+    p.folded = 0;
     int dim = s.dim;
     switch (s.kind) {
       case BP_OP_LINEAR:
@@ -741,6 +742,77 @@ Compiled compile(const bp_objective_desc& d) {
           break;
         }
         o.tc2 = 0;
+      }
+    }
+    // v2 output-layer folding: every cost-program LINEAR on x_t (C4's L1 goal [I; -I] and its
+    // state-bound [e0; -e0]) becomes extra N columns of the last layer's MMA -- W_op W_L and
+    // W_op b_L + b_op, formed in FP64 and rounded once -- so the cost warps read those values from
+    // the scratch instead of computing them row by row.  Only for the v2 kernel (v1 keeps the
+    // plain image; SIMT and the bound kernels read the ops as given).
+    o.fold_n = 0;
+    o.fold_list = 0;
+    if (ok2 && !net && o.tc == 0 && o.tc2 != 0 && o.tc2_pair == 0 && std::getenv("BP_NO_FOLD") == nullptr) {
+      const int l = d.n_layers - 1, K = d.widths[l], N = d.widths[l + 1];
+      std::vector<int> fold_ops;
+      int fold_n = 0;
+      for (int i = 0; i < d.n_ops; ++i)
+        if (d.ops[i].kind == BP_OP_LINEAR && d.ops[i].src0 == BP_VAL_X) {
+          fold_ops.push_back(i);
+          fold_n += o.ops[i].dim;
+        }
+      const int np2 = std::max(16, r16(N + fold_n));
+      if (fold_n > 0 && np2 <= std::min(o.tc2_rw, 256)) {
+        // extended output layer: rows [0, N) = W_L, then per folded op its rows of W_op W_L
+        std::vector<double> Wx(static_cast<size_t>(N + fold_n) * K), bx(static_cast<size_t>(N + fold_n));
+        for (int n = 0; n < N; ++n) {
+          for (int k = 0; k < K; ++k) Wx[static_cast<size_t>(n) * K + k] = d.W[l][static_cast<size_t>(n) * K + k];
+          bx[static_cast<size_t>(n)] = d.b[l][n];
+        }
+        std::vector<int> fcols;
+        int row = N;
+        for (int i : fold_ops) {
+          const bp_cost_op& op = d.ops[i];
+          for (int r = 0; r < o.ops[i].dim; ++r, ++row) {
+            for (int k = 0; k < K; ++k) {
+              double acc = 0.0;
+              for (int j = 0; j < N; ++j)
+                acc += op.W[static_cast<size_t>(r) * N + j] * d.W[l][static_cast<size_t>(j) * K + k];
+              Wx[static_cast<size_t>(row) * K + k] = acc;
+            }
+            double bb = op.b[r];
+            for (int j = 0; j < N; ++j) bb += op.W[static_cast<size_t>(r) * N + j] * d.b[l][j];
+            bx[static_cast<size_t>(row)] = bb;
+            fcols.push_back(o.ops[i].col + r);
+          }
+          o.ops[i].folded = 1;
+        }
+        const int NX = N + fold_n, kb = (K + 31) / 32;
+        std::vector<double> img(static_cast<size_t>(kb) * 2 * np2 * 32, 0.0);
+        for (int b = 0; b < kb; ++b)
+          for (int n = 0; n < np2; ++n) {
+            const int half = np2 > 128 && n >= 128 ? 1 : 0;
+            const int rows = np2 > 128 ? (half ? np2 - 128 : 128) : np2;
+            const int nr = n - 128 * half;
+            const size_t blk = static_cast<size_t>(b) * 2 * np2 * 32 + (half ? 2 * 128 * 32 : 0);
+            for (int cc = 0; cc < 32; ++cc) {
+              const int k = b * 32 + cc;
+              const float w = (n < NX && k < K) ? static_cast<float>(Wx[static_cast<size_t>(n) * K + k]) : 0.f;
+              const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
+              const size_t pos = static_cast<size_t>(nr) * 32 + (((cc >> 2) ^ (nr & 7)) << 2) + (cc & 3);
+              img[blk + pos] = hi;
+              img[blk + static_cast<size_t>(rows) * 32 + pos] = lo;
+            }
+          }
+        o.tc_w[l] = push_f(c.fa, img.data(), img.size());
+        std::vector<double> bp(static_cast<size_t>(np2), 0.0);
+        for (int n = 0; n < NX; ++n) bp[static_cast<size_t>(n)] = static_cast<double>(static_cast<float>(bx[static_cast<size_t>(n)]));
+        o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
+        o.tc_npad[l] = np2;
+        o.tc_npadmax = std::max(o.tc_npadmax, np2);
+        o.fold_n = fold_n;
+        while (c.ia.size() % 4) c.ia.push_back(0);
+        o.fold_list = static_cast<int>(c.ia.size());
+        c.ia.insert(c.ia.end(), fcols.begin(), fcols.end());
       }
     }
     // tcgen05 v3 (rollout_tc3.cu): [K0 <= 32, N0, N1 <= 512, N2 <= 32] with relu after the two

@@ -242,6 +242,11 @@ __device__ __forceinline__ void cost_program_n(const DevObjective& o, const OpT*
         }
         break;
       }
+      case 7: {  // a LINEAR on x_t folded into the output layer's MMA (rollout_tc2.cu): its values are in the scratch
+#pragma unroll
+        for (int q = 0; q < NR; ++q) v[q] = row[q][oc];
+        break;
+      }
       default: {  // SLICE
         const int b0 = c0 + op.begin;
 #pragma unroll 4

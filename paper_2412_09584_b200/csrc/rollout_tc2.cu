@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
     const int l = i / RW, j = i % RW;
     m.bias[i] = j < o.tc_npad[l] ? o.f[o.tc_bias[l] + j] : 0.f;
   }
-  for (int i = tid; i < o.n_ops; i += C::kThreads) m.ops[i] = to_fwd(o.ops[i]);
+  for (int i = tid; i < o.n_ops; i += C::kThreads) {
+    m.ops[i] = to_fwd(o.ops[i]);
+    if (o.ops[i].folded) m.ops[i].kind = 7;  // values come from the output layer's extra columns
+  }
   for (int i = tid; i < 2 * o.n_sc; i += C::kThreads) m.pairs[i] = o.iv[o.sc_list + i];
   for (int i = tid; i < o.cost_f1 - o.cost_f0; i += C::kThreads) m.cconst[i] = o.f[o.cost_f0 + i];
   if (tid == 0) {
@@ -690,7 +693,8 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
           // output layer: x_t -> the cost warps' scratch; features of step t+1 -> A in place
           const int nf = t + 1 < H ? o.tc_kb[0] : 0;
           const int ncx = max(nch, nf);
-          if (h * 32 < ks && t >= 1) mbar_wait(m.x_empty + ti, static_cast<uint32_t>((t - 1) & 1), kSleepEpi);
+          const int kx = ks + o.fold_n;  // x_t, then the folded cost-op columns (host.cu)
+          if (h * 32 < kx && t >= 1) mbar_wait(m.x_empty + ti, static_cast<uint32_t>((t - 1) & 1), kSleepEpi);
           for (int c = h; c < ncx; c += WPQ) {
             float v[32];
             if (c < nch) {
@@ -710,6 +714,14 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (c * 32 + j < ks) scrow[c * 32 + j] = v[j];
+              if (c * 32 + 32 > ks && c * 32 < kx) {
+                const int* fc = o.iv + o.fold_list - ks;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const int k = c * 32 + j;
+                  if (k >= ks && k < kx) scrow[__ldg(fc + k)] = v[j];
+                }
+              }
               if (x_rec && c * 32 < ks)  // x_t extrema here; the cost warp skips the x columns
                 warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
                                    static_cast<long long>(t) * o.SP + o.x_stat + c * 32 + lane, c * 32 + lane, ks);

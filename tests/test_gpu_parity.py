@@ -477,3 +477,54 @@ def test_tcgen05_and_simt_rollouts_agree(device, name):
         ref = ob.evaluate(acts[s].astype(np.float64))
         assert rel_err(c_tc[s], ref) < RTOL_TC and rel_err(c_simt[s], ref) < RTOL
     assert rel_err(lo_tc, lo_s) < RTOL_TC and rel_err(hi_tc, hi_s) < RTOL_TC
+
+
+def fold_spec(name):
+    """Objectives whose cost program reads x_t through LINEAR ops (folded into the v2 output
+    layer's MMA, host.cu): C4, and a 160-wide model whose 70 folded columns plus x_t span
+    three 32-column chunks, with a folded op feeding a SUM, a SLICE and a RELU."""
+    if name == "c4":
+        return workloads.c4(glorot=True).spec
+    from paper_2412_09584_b200.objective import Op, X, op_id
+    from paper_2412_09584_b200._capi import BP_OP_LINEAR, BP_OP_RELU, BP_OP_SLICE, BP_OP_SUM
+    r = np.random.default_rng(3)
+    W1 = (r.standard_normal((70, 12)) / 4).astype(np.float32)
+    W2 = (r.standard_normal((12, 12)) / 4).astype(np.float32)
+    ops = [Op(BP_OP_LINEAR, X, dim=70, W=W1, b=r.standard_normal(70).astype(np.float32)),
+           Op(BP_OP_RELU, op_id(0)),
+           Op(BP_OP_LINEAR, op_id(1), dim=1, W=np.ones((1, 70)), b=np.zeros(1), is_term=True),
+           Op(BP_OP_LINEAR, X, dim=12, W=W2, b=np.zeros(12)),
+           Op(BP_OP_SLICE, op_id(3), begin=2, dim=5),
+           Op(BP_OP_SUM, op_id(4), src1=op_id(4)),
+           Op(BP_OP_RELU, op_id(5)),
+           Op(BP_OP_LINEAR, op_id(6), dim=1, W=np.ones((1, 5)), b=np.zeros(1), is_term=True)]
+    return workloads._spec([14, 160, 160, 12], 12, 2, 7, ops, glorot=True)
+
+
+@pytest.mark.parametrize("name", ["c4", "wide"])
+def test_v2_folded_cost_linears_match_oracle_and_unfolded(device, name, monkeypatch):
+    """Cost-program LINEARs on x_t computed as extra N columns of the v2 output layer's MMA
+    (W_op W_L, W_op b_L + b_op): the same costs and extrema as the oracle and as the
+    unfolded kernel (BP_NO_FOLD=1) within the 3xTF32 tolerance."""
+    spec = fold_spec(name)
+    lo, hi = spec.box()
+    acts = np.random.default_rng(12).uniform(lo, hi, size=(2, 300, spec.d)).astype(np.float32)
+    dev = device.load(spec)
+    assert dev.rollout_kernel() == "tc2"
+    costs, states, elo, ehi, bad = dev.rollout(acts, want_states=True)
+    assert not bad.any()
+    monkeypatch.setenv("BP_NO_FOLD", "1")
+    dev2 = bp.Device(0).load(spec)
+    assert dev2.rollout_kernel() == "tc2"
+    c2, s2, lo2, hi2, _ = dev2.rollout(acts, want_states=True)
+    assert rel_err(costs, c2) < RTOL_TC and rel_err(states, s2) < RTOL_TC
+    assert rel_err(elo, lo2) < RTOL_TC and rel_err(ehi, hi2) < RTOL_TC
+    ob = orc.Objective(spec)
+    layout = dev.stat_layout()
+    for s in range(2):
+        st = orc.Stats()
+        ref = ob.evaluate(acts[s].astype(np.float64), st)
+        assert rel_err(costs[s], ref) < RTOL_TC, name
+        rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
+        seen = ~np.isnan(rlo)
+        assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
