@@ -137,6 +137,28 @@ float rna_tf32_host(float x) {  // cvt.rna.tf32.f32: round the 13 dropped mantis
   std::memcpy(&r, &b, 4);
   return r;
 }
+
+// tcgen05 weight image of one layer (W row-major [N][K]): per 32-wide K-block, [hi: npad rows x 32]
+// then [lo: npad rows x 32], 128-byte rows with the SW128 K-major swizzle (16-byte chunk q of row n at
+// q ^ (n & 7)); hi = rna_tf32(w), lo = rna_tf32(w - hi), rows >= N and columns >= K zero.  One block
+// of npad rows is the B operand of a single N = npad MMA (npad <= 256).
+std::vector<double> tc_image(const double* W, int N, int K, int npad) {
+  const int kb = (K + 31) / 32;
+  std::vector<double> img(static_cast<size_t>(kb) * 2 * npad * 32, 0.0);
+  for (int b = 0; b < kb; ++b) {
+    const size_t blk = static_cast<size_t>(b) * 2 * npad * 32;
+    for (int n = 0; n < npad; ++n)
+      for (int cc = 0; cc < 32; ++cc) {
+        const int k = b * 32 + cc;
+        const float w = (n < N && k < K) ? static_cast<float>(W[static_cast<size_t>(n) * K + k]) : 0.f;
+        const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
+        const size_t pos = static_cast<size_t>(n) * 32 + (((cc >> 2) ^ (n & 7)) << 2) + (cc & 3);
+        img[blk + pos] = hi;
+        img[blk + static_cast<size_t>(npad) * 32 + pos] = lo;
+      }
+  }
+  return img;
+}
 int r8(int x) { return (x + 7) & ~7; }
 
 // Grow-only device buffer.
@@ -681,24 +703,7 @@ Compiled compile(const bp_objective_desc& d) {
         o.tc_npad[l] = npad;
         o.tc_kb[l] = kb;
         o.tc_ksteps[l] = (K + 7) / 8;
-        // per K-block: N halves of <= 128 rows, each [hi rows x 32][lo rows x 32], 128B-swizzled rows
-        std::vector<double> img(static_cast<size_t>(kb) * 2 * npad * 32, 0.0);
-        for (int b = 0; b < kb; ++b)
-          for (int n = 0; n < npad; ++n) {
-            const int half = npad > 128 && n >= 128 ? 1 : 0;
-            const int rows = npad > 128 ? (half ? npad - 128 : 128) : npad;
-            const int nr = n - 128 * half;
-            const size_t blk = static_cast<size_t>(b) * 2 * npad * 32 + (half ? 2 * 128 * 32 : 0);
-            for (int cc = 0; cc < 32; ++cc) {
-              const int k = b * 32 + cc;
-              const float w = (n < N && k < K) ? static_cast<float>(d.W[l][static_cast<size_t>(n) * K + k]) : 0.f;
-              const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
-              const size_t pos = static_cast<size_t>(nr) * 32 + (((cc >> 2) ^ (nr & 7)) << 2) + (cc & 3);
-              img[blk + pos] = hi;
-              img[blk + static_cast<size_t>(rows) * 32 + pos] = lo;
-            }
-          }
-        o.tc_w[l] = push_f(c.fa, img.data(), img.size());
+        o.tc_w[l] = push_f(c.fa, tc_image(d.W[l], N, K, npad).data(), static_cast<size_t>(kb) * 2 * npad * 32);
         std::vector<double> bp(static_cast<size_t>(npad), 0.0);
         for (int n = 0; n < N; ++n) bp[static_cast<size_t>(n)] = d.b[l][n];
         o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
@@ -709,8 +714,8 @@ Compiled compile(const bp_objective_desc& d) {
       }
       // two ping-pong tiles when the widths allow it and both tiles' scratch rows fit,
       // else one tile; the weight ring takes the rest (>= three 128-row blocks)
-      // the MMA warp holds a K-block's weight blocks at once (hi, lo per N half: four 16 KB
-      // blocks at width 256), and the producer needs one more in flight
+      // the MMA warp holds a K-block's weight blocks at once (hi, lo, placed contiguously: 64 KB at
+      // width 256); one more block in flight keeps the producer ahead
       const size_t min_ring_narrow = 3 * 128 * 128, min_ring_wide = 5 * 128 * 128;
       const bool narrow = npadmax <= 128 && kbmax <= 4;
       const int plans[3][2] = {{2, 128}, {1, 128}, {1, 256}};
@@ -787,23 +792,7 @@ Compiled compile(const bp_objective_desc& d) {
           o.ops[i].folded = 1;
         }
         const int NX = N + fold_n, kb = (K + 31) / 32;
-        std::vector<double> img(static_cast<size_t>(kb) * 2 * np2 * 32, 0.0);
-        for (int b = 0; b < kb; ++b)
-          for (int n = 0; n < np2; ++n) {
-            const int half = np2 > 128 && n >= 128 ? 1 : 0;
-            const int rows = np2 > 128 ? (half ? np2 - 128 : 128) : np2;
-            const int nr = n - 128 * half;
-            const size_t blk = static_cast<size_t>(b) * 2 * np2 * 32 + (half ? 2 * 128 * 32 : 0);
-            for (int cc = 0; cc < 32; ++cc) {
-              const int k = b * 32 + cc;
-              const float w = (n < NX && k < K) ? static_cast<float>(Wx[static_cast<size_t>(n) * K + k]) : 0.f;
-              const float hi = rna_tf32_host(w), lo = rna_tf32_host(w - hi);
-              const size_t pos = static_cast<size_t>(nr) * 32 + (((cc >> 2) ^ (nr & 7)) << 2) + (cc & 3);
-              img[blk + pos] = hi;
-              img[blk + static_cast<size_t>(rows) * 32 + pos] = lo;
-            }
-          }
-        o.tc_w[l] = push_f(c.fa, img.data(), img.size());
+        o.tc_w[l] = push_f(c.fa, tc_image(Wx.data(), NX, K, np2).data(), static_cast<size_t>(kb) * 2 * np2 * 32);
         std::vector<double> bp(static_cast<size_t>(np2), 0.0);
         for (int n = 0; n < NX; ++n) bp[static_cast<size_t>(n)] = static_cast<double>(static_cast<float>(bx[static_cast<size_t>(n)]));
         o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());

@@ -13,19 +13,20 @@
 //      RW = 128 (widths <= 128): TWO tiles per CTA ping-pong -- the MMAs of one
 //           tile run while the epilogue of the other drains, so the tensor pipe
 //           no longer idles through every epilogue (v1's serial chain);
-//      RW = 256 (widths <= 256, C3): one tile, layers issued as N=128 halves.
+//      RW = 256 (widths <= 256, C3): one tile, one N = 256 MMA per k-step.
 //  * Sample extrema of the recorded pre-activations are reduced in the epilogue
 //    registers by a transposing warp butterfly (lane j ends with column j over
 //    the warp's 32 rows) and go straight to the global record with one atomic
 //    pair per column and warp -- no staging buffer, no extrema warps.
-//  * Weight blocks stream as separate hi and lo entries ([rows][128 B] each).  The MMA
-//    warp walks K-blocks outermost (N halves inside): it waits for all of a K-block's
-//    weight blocks, then issues the K-block's 12 (24 at width 256) MMAs in one burst
-//    from one elected asm per N half, and commits one barrier per K-block (a_free) that
-//    frees both its ring bytes and its A_lo slot.  A_lo keeps only ALO K-block slots
-//    (2 at width 256: K-block c waits until K-block c-2's MMAs retired), which leaves
-//    the weight ring room for two K-blocks' weights (C3: 162.9 -> 178 TFLOP/s; the
-//    timeline shows the 64 KB weight stream per K-block now pacing the 24-MMA bursts).
+//  * Weight blocks stream as separate hi and lo entries ([npad rows][128 B] each, placed
+//    next to each other in the ring).  The MMA warp walks K-blocks: it waits for a
+//    K-block's two blocks, issues its 12 MMAs (N = npad, up to 256) in one burst from one
+//    elected asm, and commits one barrier per K-block (a_free) that frees both its ring
+//    bytes and its A_lo slot.  A_lo keeps only ALO K-block slots (2 at width 256: K-block
+//    c waits until K-block c-2's MMAs retired), which leaves the weight ring room for two
+//    K-blocks' weights.  C3: 162.9 (N = 128 halves, per-block bursts) -> 178 (K-block
+//    bursts) -> 193 TFLOP/s (N = 256: the SS MMAs read each A_lo k-step once instead of
+//    once per half -- the MMA phases are bound by shared-memory reads).
 //
 // Precision (as v1): 3xTF32, D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, hi read as the top
 // 19 bits of the FP32 value, lo = x - trunc(x) exact; ~2^-21 relative per product.  The
@@ -173,9 +174,6 @@ __host__ inline size_t tc2_fixed_bytes(DevObjective o) {
   return 1024 + carve2(o, nullptr).bytes + 1024;  // base alignment + ring alignment slack
 }
 
-// Number of N halves of layer l (<= 128 columns per MMA) and the rows of half h.
-__device__ __forceinline__ int n_halves(int npad) { return npad > 128 ? 2 : 1; }
-__device__ __forceinline__ int half_rows(int npad, int h) { return npad > 128 ? (h == 0 ? 128 : npad - 128) : npad; }
 
 template <int NT, int RW_, int EPI_, int CW_, bool PAIR>
 __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
@@ -259,8 +257,11 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
     // completion's parity recorded when the block was placed.
     if (lane == 0) {
       uint32_t pos = 0;
-      uint32_t* lo_b = m.ring;  // byte ranges of the in-flight blocks, oldest first
-      uint32_t* hi_b = m.ring + kSlots;
+      // virtual byte counter: advances by every block and by the tail a wrap skips, so block j
+      // sits at virtual [vs_j, vs_j + bytes) and a new block ending at virtual ve overwrites
+      // exactly the in-flight blocks with vs_j < ve - ring (a prefix of them, oldest first)
+      uint32_t vpos = 0;
+      uint32_t* vs_b = m.ring;  // virtual start of the in-flight blocks
       uint32_t* fr_b = m.ring + 2 * kSlots;  // a_free barrier index << 1 | parity of the completion
       uint32_t ppar = 0;  // bit i*KBMAX+kb: parity of a_free[i][kb]'s next completion
       int it = 0, head = 0;
@@ -270,34 +271,34 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
       for (int t = 0; t < H; ++t)
         for (int l = 0; l < L; ++l)
           for (int i = kLock ? NT - 1 : 0; i < NT; ++i) {
-            const int npad = o.tc_npad[l], nh = n_halves(npad);
+            const int npad = o.tc_npad[l];
             for (int kb = 0; kb < o.tc_kb[l]; ++kb) {  // K-block outer: its A_lo slot is freed after it
               const int bit = i * KBMAX + kb;
-              for (int h = 0; h < (PAIR ? 1 : nh); ++h) {
-                // one N half per block; a CTA of a pair streams its half of the N rows
-                // (256 wide: image half `rank`; <= 128 wide: rows [rank n/2, (rank+1) n/2))
-                const int nr = PAIR ? (npad > 128 ? 128 : npad / 2) : half_rows(npad, h);
+              {
+                // one block per part (hi, lo) holding all npad rows: the B operand of one N = npad
+                // MMA per k-step; a CTA of a pair streams its half, rows [rank npad/2, (rank+1) npad/2)
+                const int nr = PAIR ? npad / 2 : npad;
                 const float* kbase = o.f + o.tc_w[l] + static_cast<size_t>(kb) * 2 * npad * 32;
                 const uint32_t bytes = static_cast<uint32_t>(nr) * 128u;
+                // the K-block's hi and lo blocks are placed contiguously (one wrap decision for
+                // both), so a ring of two blocks' bytes never deadlocks on the pair the MMA waits for
+                if (pos + 2u * bytes > ring_bytes) vpos += ring_bytes - pos;  // the tail the wrap skips
+                const uint32_t at0 = ring_place(pos, 2u * bytes, ring_bytes);
                 for (int part = 0; part < 2; ++part, ++it) {
-                  const float* src = !PAIR ? kbase + (h ? 2 * 128 * 32 : 0) + part * nr * 32
-                                     : npad > 128 ? kbase + (rank ? 2 * 128 * 32 : 0) + part * nr * 32
-                                                  : kbase + part * npad * 32 + rank * nr * 32;
-                  const uint32_t at = ring_place(pos, bytes, ring_bytes);
-                  // free the oldest blocks while they block the slot or the byte range.  (The
-                  // release barriers are per K-block and shared between layers, so blocks are
-                  // released strictly in order from the head; this stream's block sizes never
-                  // let a wrapped placement overlap a newer block without the oldest --
-                  // rollout_tc3.cu, with mixed sizes, has per-entry barriers instead.)
+                  const float* src = kbase + part * npad * 32 + (PAIR ? rank * nr * 32 : 0);
+                  const uint32_t at = at0 + static_cast<uint32_t>(part) * bytes;
+                  const uint32_t vs = vpos;
+                  vpos += bytes;
+                  // free the oldest blocks while they hold the barrier slot or the byte range
+                  // (blocks are released strictly in order: per-K-block barriers shared between layers)
                   while (head < it) {
                     const int hs = head % kSlots;
-                    if (it - head < kSlots && (hi_b[hs] <= at || lo_b[hs] >= at + bytes)) break;
+                    if (it - head < kSlots && static_cast<int32_t>(vs_b[hs] - (vpos - ring_bytes)) >= 0) break;
                     mbar_wait(m.a_free + (fr_b[hs] >> 1), fr_b[hs] & 1u, kSleepProducer);
                     ++head;
                   }
                   const int s = it % kSlots;
-                  lo_b[s] = at;
-                  hi_b[s] = at + bytes;
+                  vs_b[s] = vs;
                   fr_b[s] = (static_cast<uint32_t>(bit) << 1) | ((ppar >> bit) & 1u);
                   mbar_expect_tx(m.full + s, bytes);
                   bulk_g2s(m.w + at, src, bytes, m.full + s);
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
           const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(kb % ALO) * 16384u);
           const int nq = min(4, ksteps - kb * 4);
           const uint32_t a0 = areg + 32 * kb;
-          const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+          const uint32_t at_h = ring_place(pos, 2u * bytes, ring_bytes), at_l = at_h + bytes;  // hi, lo contiguous
           const long long w0 = tl_clock();
           for (int b = 0; b < 2; ++b) {
             mbar_wait_warp(m.full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
         const uint32_t bytes = static_cast<uint32_t>(npad) * 128u;
         for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
           const int nq = min(4, ksteps - kb * 4);
-          const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
+          const uint32_t at_h = ring_place(pos, 2u * bytes, ring_bytes), at_l = at_h + bytes;  // hi, lo contiguous
           bool weights = false;
           for (int i = 0; i < NT; ++i) {
             const int bit = i * KBMAX + kb;
@@ -435,12 +436,12 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
     for (int t = 0; t < H; ++t)
       for (int l = 0; l < L; ++l, ++li)
         for (int i = 0; i < NT; ++i) {
-          const int npad = o.tc_npad[l], nh = n_halves(npad), ksteps = o.tc_ksteps[l];
+          const int npad = o.tc_npad[l], ksteps = o.tc_ksteps[l];
           const uint32_t dreg = tmem + static_cast<uint32_t>(i * 2 * RW + (li & 1) * RW);
           const uint32_t areg = tmem + static_cast<uint32_t>(i * 2 * RW + ((li + 1) & 1) * RW);
+          const uint32_t idesc = tf32_idesc(npad);  // one N = npad MMA per k-step (up to 256)
+          const uint32_t bytes = static_cast<uint32_t>(npad) * 128u;
           long long wfull = 0, awt = 0;  // timeline: cycles waiting for weight blocks / A K-blocks
-          // K-block outer, N half inner: K-block kb's A_lo slot is free for the epilogue's
-          // next K-block in that slot once both halves' MMAs have read it
           for (int kb = 0; kb < o.tc_kb[l]; ++kb) {
             const int bit = i * KBMAX + kb;
             if (kb == 0) mark2(a, t, 100 + 20 * l + 10 * i);
@@ -453,35 +454,29 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
             const uint64_t alo_d = sw128_desc(abase + static_cast<uint32_t>(i * ALO + kb % ALO) * 16384u);
             const int nq = min(4, ksteps - kb * 4);
             const uint32_t a0 = areg + 32 * kb;
-            // every weight block of the K-block (hi, lo per N half: consecutive ring entries)
-            // first, then all its MMAs back to back: one burst per K-block keeps the tensor
-            // pipe fed (the waits and commits between bursts are the issuer's overhead)
-            const int nblk = 2 * nh;
+            // the K-block's hi and lo weight blocks (consecutive ring entries), then all its MMAs
+            // back to back: one burst per K-block keeps the tensor pipe fed (the waits and
+            // commits between bursts are the issuer's overhead)
             if (l == 1 && i == 0) mark2(a, t, 600 + 2 * kb);
-            for (int h = 0; h < nh; ++h) {
-              // this half's hi and lo blocks (the other half's keep landing under this burst)
-              const uint32_t bytes = static_cast<uint32_t>(half_rows(npad, h)) * 128u;
-              const uint32_t at_h = ring_place(pos, bytes, ring_bytes), at_l = ring_place(pos, bytes, ring_bytes);
-              const int b0 = it + 2 * h;
+            {
+              const uint32_t at_h = ring_place(pos, 2u * bytes, ring_bytes), at_l = at_h + bytes;  // hi, lo contiguous
               const long long w0 = tl_clock();
-              mbar_wait_warp(m.full + b0 % kSlots, static_cast<uint32_t>((b0 / kSlots) & 1));
-              mbar_wait_warp(m.full + (b0 + 1) % kSlots, static_cast<uint32_t>(((b0 + 1) / kSlots) & 1));
+              mbar_wait_warp(m.full + it % kSlots, static_cast<uint32_t>((it / kSlots) & 1));
+              mbar_wait_warp(m.full + (it + 1) % kSlots, static_cast<uint32_t>(((it + 1) / kSlots) & 1));
               wfull += tl_clock() - w0;
-              const uint32_t idesc = tf32_idesc(half_rows(npad, h));
-              const uint32_t dcol = dreg + static_cast<uint32_t>(h * 128);
               const uint64_t bh = sw128_desc(wbase + at_h), bl = sw128_desc(wbase + at_l);
               if (nq == 4) {
-                mma_kblock_elect(dcol, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
+                mma_kblock_elect(dreg, a0, alo_d, bh, bl, idesc, kb != 0 ? 1u : 0u);
               } else {
                 // hi block: A_hi.B_hi and A_lo.B_hi as strictly alternating TS/SS pairs
                 for (int q = 0; q < nq; ++q)
-                  mma_pair_elect(dcol, a0 + 8 * q, alo_d + 2 * q, bh + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
+                  mma_pair_elect(dreg, a0 + 8 * q, alo_d + 2 * q, bh + 2 * q, idesc, (kb | q) != 0 ? 1u : 0u);
                 // lo block: A_hi.B_lo
-                for (int q = 0; q < nq; ++q) mma_ts(dcol, a0 + 8 * q, bl + 2 * q, idesc, 1u);
+                for (int q = 0; q < nq; ++q) mma_ts(dreg, a0 + 8 * q, bl + 2 * q, idesc, 1u);
               }
             }
             if (l == 1 && i == 0) mark2(a, t, 601 + 2 * kb);
-            it += nblk;  // the blocks are free once these MMAs retire: the a_free commit below
+            it += 2;  // the blocks are free once these MMAs retire: the a_free commit below
             mma_commit_elect(m.a_free + bit);
           }
           mma_commit_elect(m.d_full + 2 * i + (li & 1));  // accumulator region complete

@@ -17,3 +17,11 @@ def device():
     import paper_2412_09584_b200 as bp
 
     return bp.Device(0)
+
+
+@pytest.fixture(autouse=True)
+def _rollout_path_reset(request):
+    """A failing test that forced a rollout kernel must not leave it forced for the next."""
+    yield
+    if "device" in request.fixturenames:
+        request.getfixturevalue("device").rollout_path("auto")
