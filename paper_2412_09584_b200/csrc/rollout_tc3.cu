@@ -68,7 +68,13 @@ constexpr uint32_t kColD1 = 0, kColXh = 256, kColL0 = 288, kColD2 = 480;
 __device__ __forceinline__ uint32_t col_l0h(int s) { return kColL0 + 64u * s; }
 __device__ __forceinline__ uint32_t col_l0l(int s) { return kColL0 + 64u * s + 32u; }
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kSleepProducer = 0, kSleepCost = 128, kSleepEpi = 64;  // producer: no __nanosleep (a 256 ns back-off delayed every ring refill by ~0.5k cycles)
+#ifndef BP_TC3_SLEEP_EPI
+#define BP_TC3_SLEEP_EPI 64
+#endif
+#ifndef BP_TC3_SLEEP_COST
+#define BP_TC3_SLEEP_COST 128
+#endif
+constexpr uint32_t kSleepProducer = 0, kSleepCost = BP_TC3_SLEEP_COST, kSleepEpi = BP_TC3_SLEEP_EPI;  // producer: no __nanosleep (a 256 ns back-off delayed every ring refill by ~0.5k cycles)
 
 // Debug timeline (compiled in with -DBP_TC_TIMELINE; tools/tc_timeline.py c5): clock64 marks of
 // CTA 0 at step 3 -- MMA warp 0 (step start), 1000 + 64 j + 4 kb + {0 before / 1 after the A
@@ -307,6 +313,14 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
         const int sl = g % kRing;
         vstart_b[sl] = vs;
         if (gcur < 60) mark3(a, tcur, 3301 + 3 * gcur);
+#ifdef BP_TC3_WEIGHTS_ONCE  // timing-only experiment: no weight traffic after step 0 (wrong results)
+        if (tcur > 0) {
+          mbar_arrive(m.full + sl);
+          ++gcur;
+          ++g;
+          return;
+        }
+#endif
         mbar_expect_tx(m.full + sl, bytes);
         for (int i = 0; i < n; ++i) bulk_g2s(m.w + at[i], ent[i].src, ent[i].bytes, m.full + sl);
         if (gcur < 60) mark3(a, tcur, 3302 + 3 * gcur);
