@@ -185,6 +185,19 @@ typedef int (*bp_alltoallv_fn)(void* user, const void* send, const int64_t* send
 bp_status bp_set_alltoall(bp_ctx* ctx, bp_alltoallv_fn a2a);
 bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, void* user);
 
+/* Device-direct exchange over NCCL (NVLink / NVSwitch), replacing both hooks above: no host
+ * callback, and the child records go from the splitting rank's device pack buffer straight
+ * into the searching rank's device receive buffer (one grouped ncclSend / ncclRecv per
+ * iteration); the heads and status words are all-gathered through small device staging
+ * buffers.  Rank 0 makes the 128-byte id with bp_nccl_unique_id, the caller broadcasts it
+ * (e.g. torch.distributed), and every rank calls bp_set_nccl collectively.  libnccl.so.2 is
+ * dlopen'ed (the process's copy when one is loaded).  bp_nccl_selftest checks an all-gather
+ * and an all-to-all-v of `bytes`-sized segments across the ranks: *ok = 1 when every segment
+ * arrived in rank order. */
+bp_status bp_nccl_unique_id(unsigned char id[128]);
+bp_status bp_set_nccl(bp_ctx* ctx, int rank, int world, const unsigned char id[128]);
+bp_status bp_nccl_selftest(bp_ctx* ctx, int64_t bytes, int* ok);
+
 /* Launch the context's work on an external stream (NULL = its own stream),
  * e.g. torch.cuda.current_stream(), so caller-side CUDA events time it. */
 bp_status bp_set_stream(bp_ctx* ctx, void* cuda_stream);

@@ -90,7 +90,7 @@ class PoolMeta(C.Structure):
 
 # Every symbol the header declares (tests check the library exports them all).
 EXPORTS = [
-    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_alltoall", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds", "bp_gradient",
+    "bp_init", "bp_destroy", "bp_get_last_error", "bp_set_exchange", "bp_set_alltoall", "bp_nccl_unique_id", "bp_set_nccl", "bp_nccl_selftest", "bp_set_stream", "bp_set_rollout_path", "bp_rollout_info", "bp_io_bytes", "bp_node_bounds", "bp_gradient",
     "bp_load_objective", "bp_load_synthetic",
     "bp_stat_layout", "bp_rollout", "bp_batch_search", "bp_search_update", "bp_search_counters", "bp_set_plan_log", "bp_plan_log_size", "bp_plan_log_get", "bp_report_summary", "bp_report_top",
     "bp_report_stats", "bp_batch_bound", "bp_bound_boxes", "bp_plan", "bp_planner_create", "bp_planner_step",
@@ -126,6 +126,9 @@ def load() -> C.CDLL:
             "bp_get_last_error": (C.c_size_t, [C.c_char_p, C.c_size_t]),
             "bp_set_exchange": (C.c_int, [vp, C.c_int, C.c_int, EXCHANGE_FN, vp]),
             "bp_set_alltoall": (C.c_int, [vp, ALLTOALL_FN]),
+            "bp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+            "bp_set_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+            "bp_nccl_selftest": (C.c_int, [vp, C.c_int64, C.POINTER(C.c_int)]),
             "bp_set_stream": (C.c_int, [vp, vp]),
             "bp_set_rollout_path": (C.c_int, [vp, C.c_int, _ip]),
             "bp_rollout_info": (C.c_int, [vp, _ip, _ip, _ip, C.POINTER(C.c_int64)]),

@@ -9,6 +9,8 @@
 // every rank of a multi-GPU run replays them on the same exchanged heads, so
 // decisions are identical on every rank).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: libnccl is dlopen'ed at bp_set_nccl
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
@@ -871,6 +873,105 @@ struct Report {  // SearchReport (search.hpp:53-63) as the planner consumes it
 
 }  // namespace
 
+// Device-direct exchange over NCCL (bp_set_nccl).  libnccl.so.2 is dlopen'ed, so the library
+// has no link-time NCCL dependency and shares the process's copy when one is loaded (torch's).
+struct NcclLink {
+  void* dl = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) err_str = nullptr;
+  cudaStream_t* stream = nullptr;  // the context's current stream
+  unsigned char* d_send = nullptr;
+  unsigned char* d_recv = nullptr;
+  size_t cap_send = 0, cap_recv = 0;
+
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess) fail(BP_NCCL, std::string("nccl: ") + what + ": " + (err_str ? err_str(r) : "error"));
+  }
+  static NcclLink* open_lib() {
+    std::unique_ptr<NcclLink> L(new NcclLink());
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      L->dl = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (L->dl) break;
+    }
+    if (!L->dl) fail(BP_NCCL, "nccl: libnccl.so.2 not found");
+    auto sym = [&](const char* n) {
+      void* f = dlsym(L->dl, n);
+      if (!f) fail(BP_NCCL, std::string("nccl: missing symbol ") + n);
+      return f;
+    };
+    L->get_id = reinterpret_cast<decltype(L->get_id)>(sym("ncclGetUniqueId"));
+    L->init = reinterpret_cast<decltype(L->init)>(sym("ncclCommInitRank"));
+    L->destroy = reinterpret_cast<decltype(L->destroy)>(sym("ncclCommDestroy"));
+    L->allgather = reinterpret_cast<decltype(L->allgather)>(sym("ncclAllGather"));
+    L->send = reinterpret_cast<decltype(L->send)>(sym("ncclSend"));
+    L->recv = reinterpret_cast<decltype(L->recv)>(sym("ncclRecv"));
+    L->group_start = reinterpret_cast<decltype(L->group_start)>(sym("ncclGroupStart"));
+    L->group_end = reinterpret_cast<decltype(L->group_end)>(sym("ncclGroupEnd"));
+    L->err_str = reinterpret_cast<decltype(L->err_str)>(sym("ncclGetErrorString"));
+    return L.release();
+  }
+  ~NcclLink() {
+    if (comm && destroy) destroy(comm);
+    if (d_send) cudaFree(d_send);
+    if (d_recv) cudaFree(d_recv);
+    // the library handle stays open: other users (torch) may share it
+  }
+  unsigned char* buf(unsigned char*& p, size_t& cap, size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      if (cudaMalloc(reinterpret_cast<void**>(&p), n) != cudaSuccess) fail(BP_CUDA, "nccl: staging buffer");
+      cap = n;
+    }
+    return p;
+  }
+  // all-gather of device buffers: world * bytes land in recv in rank order
+  void allgather_dev(const void* send, void* recv, size_t bytes) const {
+    check(allgather(send, recv, bytes, ncclUint8, comm, *stream), "all-gather");
+  }
+  // all-to-all-v of device buffers: send segments in rank order (send_bytes[r] to rank r),
+  // receive segments in rank order (recv_bytes[r] from rank r); one NCCL group
+  void alltoallv_dev(const unsigned char* send, const int64_t* send_bytes, unsigned char* recv,
+                     const int64_t* recv_bytes) const {
+    check(group_start(), "group start");
+    size_t so = 0, ro = 0;
+    for (int r = 0; r < world; ++r) {
+      const size_t sb = static_cast<size_t>(send_bytes[r]), rb = static_cast<size_t>(recv_bytes[r]);
+      if (sb > 0) check(this->send(send + so, sb, ncclUint8, r, comm, *stream), "send");
+      if (rb > 0) check(this->recv(recv + ro, rb, ncclUint8, r, comm, *stream), "recv");
+      so += sb;
+      ro += rb;
+    }
+    check(group_end(), "group end");
+  }
+};
+
+// bp_exchange_fn over NCCL for the planner's host-side all-gathers (heads, status words):
+// staged through device buffers on the context's stream
+int nccl_allgather_host(void* user, const void* send, size_t bytes, void* recv) {
+  try {
+    NcclLink* L = static_cast<NcclLink*>(user);
+    unsigned char* ds = L->buf(L->d_send, L->cap_send, std::max<size_t>(bytes, 1));
+    unsigned char* dr = L->buf(L->d_recv, L->cap_recv, std::max<size_t>(bytes * L->world, 1));
+    if (cudaMemcpyAsync(ds, send, bytes, cudaMemcpyHostToDevice, *L->stream) != cudaSuccess) return 1;
+    L->allgather_dev(ds, dr, bytes);
+    if (cudaMemcpyAsync(recv, dr, bytes * L->world, cudaMemcpyDeviceToHost, *L->stream) != cudaSuccess) return 1;
+    return cudaStreamSynchronize(*L->stream) == cudaSuccess ? 0 : 1;
+  } catch (...) {
+    return 1;
+  }
+}
+
 struct bp_ctx {
   int device = 0;
   int sms = 148;
@@ -924,6 +1025,7 @@ struct bp_ctx {
   bp_exchange_fn exchange = nullptr;
   bp_alltoallv_fn alltoallv = nullptr;
   void* exchange_user = nullptr;
+  std::unique_ptr<NcclLink> nccl;  // bp_set_nccl: device-direct exchange (replaces the hooks)
   // scratch for bp_rollout
   DBuf<float> r_actions, r_costs, r_states;
   DBuf<long long> timeline;
@@ -948,6 +1050,7 @@ struct bp_ctx {
   }
 
   ~bp_ctx() {
+    nccl.reset();  // before the streams go
     for (unsigned char* p : slab_spare) cudaFree(p);
     for (auto& e : roll_events) {
       cudaEventDestroy(e.first);
@@ -2035,6 +2138,20 @@ struct Planner {
       }
     size_t r_total = 0;
     for (int r = 0; r < W; ++r) r_total += static_cast<size_t>(rbts[static_cast<size_t>(r)]);
+    if (c->nccl) {  // device-direct: the split's pack buffer goes out as is, records land in d_recv
+      unsigned char* dr = d_recv.get(std::max<size_t>(r_total, 1));
+      c->nccl->alltoallv_dev(d_pack.p, sb.data(), dr, rbts.data());
+      local([&] {
+        const int n_in = static_cast<int>(r_total / rb);
+        std::vector<double> keys(static_cast<size_t>(n_in));
+        if (n_in > 0)  // each record's first word: the child's index in the iteration
+          ck(cudaMemcpy2DAsync(keys.data(), sizeof(double), dr, rb, sizeof(double), static_cast<size_t>(n_in),
+                               cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        unpack_children_dev(dr, keys, li_of, slots);
+      });
+      return;
+    }
     unsigned char* send = h_pack.get(std::max<size_t>(static_cast<size_t>(n_pack) * rb, 1));
     local([&] {  // a failure here is carried to the heads all-gather; the all-to-all still runs
       if (n_pack > 0) {
@@ -2054,18 +2171,27 @@ struct Planner {
     const size_t rb = bp::pool_record_bytes(d, K);
     const int n_in = static_cast<int>(r_total / rb);
     if (n_in == 0) return;
+    std::vector<double> keys(static_cast<size_t>(n_in));
+    for (int q = 0; q < n_in; ++q) std::memcpy(&keys[static_cast<size_t>(q)], recv.data() + static_cast<size_t>(q) * rb, sizeof(double));
+    unsigned char* dr = d_recv.get(r_total);
+    ck(memcpy_counted(dr, recv.data(), r_total, cudaMemcpyHostToDevice, st), "H2D");
+    unpack_children_dev(dr, keys, li_of, slots);
+  }
+  // received child records (device, one per key) into their local search slots
+  void unpack_children_dev(unsigned char* dr, const std::vector<double>& keys, const std::vector<int>& li_of,
+                           const std::vector<int>& slots) {
+    cudaStream_t st = c->stream;
+    const int n_in = static_cast<int>(keys.size());
+    if (n_in == 0) return;
     std::vector<int> dst(static_cast<size_t>(n_in)), slot(static_cast<size_t>(n_in));
     for (int q = 0; q < n_in; ++q) {
-      double key;
-      std::memcpy(&key, recv.data() + static_cast<size_t>(q) * rb, sizeof(double));
+      const double key = keys[static_cast<size_t>(q)];
       const int64_t k = static_cast<int64_t>(key);
       if (k < 0 || k >= static_cast<int64_t>(li_of.size()) || li_of[static_cast<size_t>(k)] < 0)
         fail(BP_NCCL, "exchange: child record for another rank");
       dst[static_cast<size_t>(q)] = li_of[static_cast<size_t>(k)];
       slot[static_cast<size_t>(q)] = slots[static_cast<size_t>(li_of[static_cast<size_t>(k)])];
     }
-    unsigned char* dr = d_recv.get(r_total);
-    ck(memcpy_counted(dr, recv.data(), r_total, cudaMemcpyHostToDevice, st), "H2D");
     int* dd = d_unpack_dst.get(static_cast<size_t>(n_in));
     int* ds = d_unpack_slot.get(static_cast<size_t>(n_in));
     ck(memcpy_counted(dd, dst.data(), static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, st), "H2D");
@@ -2273,10 +2399,83 @@ bp_status bp_set_exchange(bp_ctx* ctx, int rank, int world, bp_exchange_fn fn, v
     check_ctx(ctx);
     if (world < 1 || rank < 0 || rank >= world) fail(BP_INVALID_ARGUMENT, "bp_set_exchange: bad rank / world");
     if (world > 1 && fn == nullptr) fail(BP_INVALID_ARGUMENT, "bp_set_exchange: null exchange for world > 1");
+    ctx->nccl.reset();  // host hooks replace a device-direct link
     ctx->rank = rank;
     ctx->world = world;
     ctx->exchange = fn;
     ctx->exchange_user = user;
+  });
+}
+
+bp_status bp_nccl_unique_id(unsigned char* id) {
+  return guard([&] {
+    if (id == nullptr) fail(BP_INVALID_ARGUMENT, "bp_nccl_unique_id: null id");
+    std::unique_ptr<NcclLink> L(NcclLink::open_lib());
+    ncclUniqueId u;
+    L->check(L->get_id(&u), "get unique id");
+    std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+bp_status bp_set_nccl(bp_ctx* ctx, int rank, int world, const unsigned char* id) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (world < 1 || rank < 0 || rank >= world) fail(BP_INVALID_ARGUMENT, "bp_set_nccl: bad rank / world");
+    if (id == nullptr) fail(BP_INVALID_ARGUMENT, "bp_set_nccl: null id");
+    ctx->use();
+    std::unique_ptr<NcclLink> L(NcclLink::open_lib());
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    L->check(L->init(&L->comm, world, u, rank), "communicator init");  // collective over the ranks
+    L->rank = rank;
+    L->world = world;
+    L->stream = &ctx->stream;
+    ctx->nccl = std::move(L);
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->exchange = nccl_allgather_host;  // heads and status words: staged all-gathers
+    ctx->exchange_user = ctx->nccl.get();
+    ctx->alltoallv = nullptr;  // child records go device to device (ship_children)
+  });
+}
+
+bp_status bp_nccl_selftest(bp_ctx* ctx, int64_t bytes, int* ok) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!ctx->nccl) fail(BP_INVALID_ARGUMENT, "bp_nccl_selftest: no NCCL link (bp_set_nccl)");
+    if (bytes < 1) fail(BP_INVALID_ARGUMENT, "bp_nccl_selftest: bytes < 1");
+    ctx->use();
+    NcclLink& L = *ctx->nccl;
+    const int W = L.world, R = L.rank;
+    const size_t n = static_cast<size_t>(bytes);
+    auto pat = [](int from, int to, size_t i) { return static_cast<unsigned char>((from * 131 + to * 31 + i * 7) & 0xff); };
+    bool good = true;
+    // all-gather through the host-staged hook the planner uses
+    std::vector<unsigned char> mine(n), all(n * W);
+    for (size_t i = 0; i < n; ++i) mine[i] = pat(R, R, i);
+    if (nccl_allgather_host(&L, mine.data(), n, all.data()) != 0) fail(BP_NCCL, "selftest: all-gather");
+    for (int r = 0; r < W; ++r)
+      for (size_t i = 0; i < n; ++i) good = good && all[static_cast<size_t>(r) * n + i] == pat(r, r, i);
+    // all-to-all-v device to device: rank R sends (r + 1) * n bytes to rank r
+    std::vector<int64_t> sb(static_cast<size_t>(W)), rb(static_cast<size_t>(W));
+    size_t st = 0, rt = 0;
+    for (int r = 0; r < W; ++r) {
+      sb[static_cast<size_t>(r)] = static_cast<int64_t>((r + 1) * n);
+      rb[static_cast<size_t>(r)] = static_cast<int64_t>((R + 1) * n);
+      st += (r + 1) * n;
+      rt += (R + 1) * n;
+    }
+    std::vector<unsigned char> hs(st), hr(rt);
+    for (int r = 0, o = 0; r < W; ++r)
+      for (size_t i = 0; i < (r + 1) * n; ++i) hs[static_cast<size_t>(o++)] = pat(R, r, i);
+    DBuf<unsigned char> ds, dr;
+    ck(cudaMemcpyAsync(ds.get(st), hs.data(), st, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    L.alltoallv_dev(ds.p, sb.data(), dr.get(rt), rb.data());
+    ck(cudaMemcpyAsync(hr.data(), dr.p, rt, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    for (int r = 0; r < W; ++r)
+      for (size_t i = 0; i < (R + 1) * n; ++i) good = good && hr[static_cast<size_t>(r) * (R + 1) * n + i] == pat(r, R, i);
+    if (ok) *ok = good ? 1 : 0;
   });
 }
 

@@ -10,8 +10,9 @@ the children's heads are all-gathered (bp_set_exchange / bp_set_alltoall in
 include/babplan_cuda.h).  Each child's sampler stream is keyed by its global
 index, so the whole run is independent of the number of GPUs.
 
-The exchange goes over NCCL (NVLink 5 / NVSwitch) when the process group is
-NCCL, or gloo for the CPU / same-GPU tests.
+With an NCCL process group the library runs the exchange itself (NcclLink:
+its own communicator, device-direct child records); with gloo (the CPU and
+same-GPU tests) the torch.distributed hooks (Exchange) carry it.
 """
 from __future__ import annotations
 
@@ -86,12 +87,58 @@ def shard_of(child: int, world: int) -> int:
     return child % world
 
 
-def attach(dev, group=None) -> Optional[Exchange]:
-    """Shard dev's planner over the default (or given) process group."""
+class NcclLink:
+    """Device-direct exchange (bp_set_nccl): the library's own NCCL communicator over NVLink /
+    NVSwitch.  Child records go from the splitting GPU's pack buffer to the searching GPU in one
+    grouped send / receive per iteration, with no Python callback and no host staging; the
+    heads and status words (64 B per child) are all-gathered through small device buffers.
+    torch.distributed only carries the 128-byte communicator id from rank 0."""
+
+    def __init__(self, dev, rank: int, world: int, uid: bytes):
+        self.rank, self.world = rank, world
+        _capi.check(dev.lib.bp_set_nccl(dev.h, rank, world, uid))
+        self.dev = dev
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _capi.check(_capi.load().bp_nccl_unique_id(buf))
+        return buf.raw
+
+    def selftest(self, nbytes: int = 4096) -> bool:
+        """All-gather and all-to-all-v of nbytes-sized segments across the ranks, checked."""
+        ok = C.c_int(0)
+        _capi.check(self.dev.lib.bp_nccl_selftest(self.dev.h, int(nbytes), C.byref(ok)))
+        return ok.value == 1
+
+
+def nccl_single(dev) -> NcclLink:
+    """A one-rank device-direct link (tests: the NCCL path on one GPU)."""
+    return NcclLink(dev, 0, 1, NcclLink.unique_id())
+
+
+def attach(dev, group=None, direct: Optional[bool] = None):
+    """Shard dev's planner over the default (or given) process group: device-direct NCCL
+    (NcclLink) when the group's backend is NCCL (BP_EXCHANGE=host keeps the staged hooks),
+    else the torch.distributed hooks (Exchange; gloo in the CPU tests)."""
+    import os
+
+    import torch
     import torch.distributed as dist
 
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return None
+    if direct is None:
+        direct = dist.get_backend(group) == "nccl" and os.environ.get("BP_EXCHANGE", "nccl") != "host"
+    if direct:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = NcclLink.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast(t, src=src, group=group)
+        link = NcclLink(dev, rank, world, bytes(t.cpu().tolist()))
+        dev._exchange = link
+        return link
     ex = Exchange(group)
     _capi.check(dev.lib.bp_set_exchange(dev.h, ex.rank, ex.world, ex.c_fn, None))
     _capi.check(dev.lib.bp_set_alltoall(dev.h, ex.c_a2a))
