@@ -425,16 +425,28 @@ def test_reference_smoke_plan_reaches_target():
 
 
 def test_plan_matches_or_beats_cpu_reference_objective(device):
-    """Same or better best objective than the CPU planner at equal iteration count (C1)."""
+    """Best objective against the CPU planner (the oracle's bab.cpp restatement) at equal
+    iteration count and batch on C1, over 8 seeds.  The samplers differ (Philox on the device,
+    mt19937_64 + Box-Muller in the reference), so single runs differ by the seed-to-seed spread
+    (~3 % here); the bar is on the median over the seeds: no worse than the CPU's by 1 %, and the
+    device's best run no worse than the CPU's best by 1 %.  Both sides are deterministic per seed."""
     wl = workloads.c1()
-    cfg = wl.planner_config()
-    cfg["termination"]["max_iterations"] = 6
     dev = device.load(wl.spec)
-    gpu = dev.plan(cfg)
-    cpu = orc.Objective(wl.spec).plan(cfg)
-    assert gpu["iterations"] == cpu["iterations"] == 6
-    assert gpu["objective"] <= cpu["objective"] * 1.05 + 1e-3
-    assert gpu["trace"]["pool_size"][0] == 1
+    ob = orc.Objective(wl.spec)
+    gpu, cpu = [], []
+    for seed in range(2, 10):
+        cfg = wl.planner_config()
+        cfg["termination"]["max_iterations"] = 6
+        cfg["seed"] = seed
+        g = dev.plan(cfg)
+        c = ob.plan(cfg)
+        assert g["iterations"] == c["iterations"] == 6
+        assert g["trace"]["pool_size"][0] == 1
+        gpu.append(g["objective"])
+        cpu.append(c["objective"])
+    gpu, cpu = np.array(gpu), np.array(cpu)
+    assert np.median(gpu) <= np.median(cpu) * 1.01, (gpu, cpu)
+    assert gpu.min() <= cpu.min() * 1.01, (gpu, cpu)
 
 
 def test_plan_sample_only_method(device):
@@ -456,8 +468,11 @@ def test_nonfinite_rollouts_fail_the_box_not_the_batch(device):
     cfg = from_json('{"search": {"samples_per_iter": 32, "iterations": 2}}')
     rep = dev.batch_search(np.stack([lo, lo]), np.stack([hi, hi]), None, cfg, seed=1)
     assert not rep["ok"].any()
-    lf = dev.batch_bound(2)  # interval fallback
+    lf = dev.batch_bound(2)  # no valid samples: the bound falls back to intervals (bab.cpp)
+    ref = orc.Objective(big).lower_bound(lo, hi, "early-stop-empirical", None)
     assert lf.shape == (2,)
+    for v in lf:
+        assert v == ref or abs(v - ref) <= 1e-9 * max(1.0, abs(ref)), (lf, ref)
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "ref-obstacles", "ref-linear"])
