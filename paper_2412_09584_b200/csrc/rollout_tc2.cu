@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
     rollout_tc2_kernel(const DevObjective o, const RolloutArgs a) {
   using C = Tc2<NT, RW_, EPI_, CW_, PAIR>;
   constexpr int RW = C::RW, KBMAX = C::KBMAX, ALO = C::ALO, WPQ = C::WPQ, CW = C::CW, NR = C::NR;
+  constexpr bool kRedux = RW == 128;  // redux.sync column extrema (tc_epilogue.cuh): faster at width 128 only
   constexpr uint32_t kTmemCols = 2 * NT * RW;  // a power of two >= 32
   extern __shared__ unsigned char smraw[];
   const uint32_t s0 = smem_u32(smraw);
@@ -679,7 +680,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
             }
             if (rec) {
               const int col = c * 32 + lane;
-              warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+              warp_chunk_extrema<kRedux>(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
                                  static_cast<long long>(t) * o.SP + stat + col, col, N);
             }
           }
@@ -718,7 +719,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
                 }
               }
               if (x_rec && c * 32 < ks)  // x_t extrema here; the cost warp skips the x columns
-                warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
+                warp_chunk_extrema<kRedux>(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
                                    static_cast<long long>(t) * o.SP + o.x_stat + c * 32 + lane, c * 32 + lane, ks);
             } else {
 #pragma unroll
