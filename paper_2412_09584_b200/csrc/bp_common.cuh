@@ -62,14 +62,19 @@ struct DevObjective {
   int tc_w[kMaxLayers], tc_bias[kMaxLayers], tc_npad[kMaxLayers], tc_kb[kMaxLayers], tc_ksteps[kMaxLayers];
   int tc_kbmax, tc_npadmax, tc_S, tc_cols, tc_xs;
   // tcgen05 v2 (rollout_tc2.cu): tiles per CTA (2: widths <= 128, 1: widths <= 256; 0 ineligible) and the
-  // weight ring bytes.  The tc_w images of layers wider than 128 hold per K-block two N halves
-  // [kb][half][hi|lo][rows x 32] (half 0 = 128 rows); narrower layers are the v1 layout.
+  // weight ring bytes.  The tc_w images hold per K-block [hi: npad rows][lo: npad rows] x 32 (the B operand
+  // of one N = npad MMA), each image starting on a 128-byte row of the arena.
   int tc2, tc2_rw, tc2_ring;  // tc2_rw: TMEM region width (128 or 256 columns)
   // v2 output-layer folding: the cost program's LINEAR ops on x_t become extra output columns
   // ks .. ks + fold_n - 1 of the last layer's MMA (W_op W_L, W_op b_L + b_op); int arena
   // fold_list: the scratch column of each extra output column
   int fold_n, fold_list;
   int tc2_pair;               // width 256 as a CTA pair (cta_group::2): every layer 256 wide or <= 128 in 32s
+  // CTA pair: TMA tensor maps over the float arena as [rows][32] fp32 rows (one map per distinct box
+  // height npad / 2; bp_load_objective encodes them): each CTA's half-block load completes on rank 0's
+  // barrier (cp.async.bulk.tensor .cta_group::2), so rank 0 needs no relay of the peer's arrivals
+  int tmap_idx[kMaxLayers];
+  const void* tmaps;          // device array of CUtensorMap (64-byte aligned), null when not encoded
   // tcgen05 v3 (rollout_tc3.cu): three layers [K0 <= 32, N0 <= 512, N1 <= 512, N2 <= 32], relu after
   // the hidden two; layer 1 in N chunks of <= 256 with layer 0 recomputed per chunk
   int tc3;                   // eligible

@@ -8,6 +8,8 @@
 // heads (O(pool) bookkeeping; pick_out's softmax needs the reference's exp();
 // every rank of a multi-GPU run replays them on the same exchanged heads, so
 // decisions are identical on every rank).
+#include <cuda.h>  // CUtensorMap types (the encoder is fetched through cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types and prototypes only: libnccl is dlopen'ed at bp_set_nccl
@@ -348,6 +350,11 @@ int push_f(std::vector<float>& a, const double* p, size_t n) {
   const int off = static_cast<int>(a.size());
   for (size_t i = 0; i < n; ++i) a.push_back(static_cast<float>(p[i]));
   return off;
+}
+// an image starting on a 128-byte row of the arena (the TMA tensor maps address the arena in rows of 32)
+int push_f_row(std::vector<float>& a, const double* p, size_t n) {
+  while (a.size() % 32) a.push_back(0.f);
+  return push_f(a, p, n);
 }
 int push_d(std::vector<double>& a, const double* p, size_t n) {
   while (a.size() % 2) a.push_back(0.0);
@@ -705,7 +712,7 @@ Compiled compile(const bp_objective_desc& d) {
         o.tc_npad[l] = npad;
         o.tc_kb[l] = kb;
         o.tc_ksteps[l] = (K + 7) / 8;
-        o.tc_w[l] = push_f(c.fa, tc_image(d.W[l], N, K, npad).data(), static_cast<size_t>(kb) * 2 * npad * 32);
+        o.tc_w[l] = push_f_row(c.fa, tc_image(d.W[l], N, K, npad).data(), static_cast<size_t>(kb) * 2 * npad * 32);
         std::vector<double> bp(static_cast<size_t>(npad), 0.0);
         for (int n = 0; n < N; ++n) bp[static_cast<size_t>(n)] = d.b[l][n];
         o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
@@ -794,7 +801,7 @@ Compiled compile(const bp_objective_desc& d) {
           o.ops[i].folded = 1;
         }
         const int NX = N + fold_n, kb = (K + 31) / 32;
-        o.tc_w[l] = push_f(c.fa, tc_image(Wx.data(), NX, K, np2).data(), static_cast<size_t>(kb) * 2 * np2 * 32);
+        o.tc_w[l] = push_f_row(c.fa, tc_image(Wx.data(), NX, K, np2).data(), static_cast<size_t>(kb) * 2 * np2 * 32);
         std::vector<double> bp(static_cast<size_t>(np2), 0.0);
         for (int n = 0; n < NX; ++n) bp[static_cast<size_t>(n)] = static_cast<double>(static_cast<float>(bx[static_cast<size_t>(n)]));
         o.tc_bias[l] = push_f(c.fa, bp.data(), bp.size());
@@ -980,6 +987,7 @@ struct bp_ctx {
   bool loaded = false;
   Compiled comp;
   DBuf<float> d_fa;
+  DBuf<unsigned char> d_tmaps;  // CUtensorMap array for the v2 CTA pair (encode_tmaps)
   DBuf<double> d_da;
   DBuf<int> d_ia;
   // search state
@@ -1064,6 +1072,7 @@ struct bp_ctx {
   bp::DevObjective dev() {
     bp::DevObjective o = comp.o;
     o.f = d_fa.p;
+    o.tmaps = comp.o.tc2_pair ? d_tmaps.p : nullptr;
     o.dd = d_da.p;
     o.iv = d_ia.p;
     return o;
@@ -2518,17 +2527,55 @@ bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h) {
   return BP_OK;
 }
 
+// TMA tensor maps for the v2 CTA pair: the float arena as a [rows][32] fp32 tensor (128-byte rows,
+// no swizzle: the images are pre-swizzled), one map per distinct per-CTA block height npad / 2.
+// cuTensorMapEncodeTiled comes from the driver through cudaGetDriverEntryPoint (no -lcuda).
+void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (encode == nullptr) fail(BP_CUDA, "cuTensorMapEncodeTiled unavailable");
+  bp::DevObjective& o = cp.o;
+  std::vector<int> heights;
+  for (int l = 0; l < o.L; ++l) {
+    const int h = o.tc_npad[l] / 2;
+    auto it = std::find(heights.begin(), heights.end(), h);
+    o.tmap_idx[l] = static_cast<int>(it - heights.begin());
+    if (it == heights.end()) heights.push_back(h);
+  }
+  std::vector<CUtensorMap> maps(heights.size());
+  const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(cp.fa.size() / 32)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t estr[2] = {1, 1};
+  for (size_t i = 0; i < heights.size(); ++i) {
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(heights[i])};
+    const CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, arena, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(BP_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  unsigned char* dm = ctx->d_tmaps.get(maps.size() * sizeof(CUtensorMap));
+  ck(memcpy_counted(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+}
+
 bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
   return guard([&] {
     check_ctx(ctx);
     if (desc == nullptr) fail(BP_INVALID_ARGUMENT, "null objective");
     Compiled cp = compile(*desc);
+    while (cp.fa.size() % 32) cp.fa.push_back(0.f);  // whole 128-byte rows for the tensor maps
     float* f = ctx->d_fa.get(cp.fa.size());
     double* dd = ctx->d_da.get(cp.da.size());
     int* iv = ctx->d_ia.get(cp.ia.size());
     ck(memcpy_counted(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(memcpy_counted(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(memcpy_counted(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (cp.o.tc2_pair) encode_tmaps(ctx, cp, f);
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->comp = std::move(cp);
     ctx->loaded = true;

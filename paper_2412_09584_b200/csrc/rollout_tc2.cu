@@ -301,8 +301,15 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
                   const int s = it % kSlots;
                   vs_b[s] = vs;
                   fr_b[s] = (static_cast<uint32_t>(bit) << 1) | ((ppar >> bit) & 1u);
-                  mbar_expect_tx(m.full + s, bytes);
-                  bulk_g2s(m.w + at, src, bytes, m.full + s);
+                  if (PAIR && o.tmaps != nullptr) {  // both halves complete on rank 0's barrier
+                    if (rank == 0) mbar_expect_tx(m.full + s, 2u * bytes);
+                    const int row = static_cast<int>((src - o.f) / 32);  // images start on arena rows
+                    tma_rows_to_rank0(m.w + at, static_cast<const unsigned char*>(o.tmaps) + 128 * o.tmap_idx[l], row,
+                                      m.full + s);
+                  } else {
+                    mbar_expect_tx(m.full + s, bytes);
+                    bulk_g2s(m.w + at, src, bytes, m.full + s);
+                  }
                 }
               }
             }
@@ -310,17 +317,20 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
           }
     }
   } else if (warp == C::kMmaWarp && PAIR && rank == 1) {
-    // ------------------------------------------------ CTA pair, rank 1: relay "my half of
-    // the block landed" to rank 0, which issues the MMAs over both halves
-    int it = 0;
-    for (int t = 0; t < H; ++t)
-      for (int l = 0; l < L; ++l)
-        for (int kb = 0; kb < o.tc_kb[l]; ++kb)
-          for (int part = 0; part < 2; ++part, ++it) {
-            mbar_wait(m.full + it % kSlots, static_cast<uint32_t>((it / kSlots) & 1));
-            if (lane == 0) mbar_arrive_cta(m.peer_full + it % kSlots, 0);
-            __syncwarp();
-          }
+    // (with the tensor maps the TMA completes on rank 0's barriers itself: nothing to relay)
+    if (o.tmaps == nullptr) {
+      // ---------------------------------------------- CTA pair, rank 1: relay "my half of
+      // the block landed" to rank 0, which issues the MMAs over both halves
+      int it = 0;
+      for (int t = 0; t < H; ++t)
+        for (int l = 0; l < L; ++l)
+          for (int kb = 0; kb < o.tc_kb[l]; ++kb)
+            for (int part = 0; part < 2; ++part, ++it) {
+              mbar_wait(m.full + it % kSlots, static_cast<uint32_t>((it / kSlots) & 1));
+              if (lane == 0) mbar_arrive_cta(m.peer_full + it % kSlots, 0);
+              __syncwarp();
+            }
+    }
   } else if (warp == C::kMmaWarp && PAIR) {
     // ------------------------------------------------ CTA pair, rank 0: MMA issuer for both
     // CTAs (M = 256: each CTA's 128 rows of A from its TMEM / shared memory, B's N rows
@@ -352,7 +362,8 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
           const long long w0 = tl_clock();
           for (int b = 0; b < 2; ++b) {
             mbar_wait_warp(m.full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
-            mbar_wait_cluster(m.peer_full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
+            if (o.tmaps == nullptr)
+              mbar_wait_cluster(m.peer_full + (it + b) % kSlots, static_cast<uint32_t>(((it + b) / kSlots) & 1));
           }
           wfull += tl_clock() - w0;
           fence_after();

@@ -297,6 +297,16 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
     if (spin > (1ll << 24)) asm volatile("trap;");
   }
 }
+// CTA pair: this CTA's half of a weight block by TMA (2-D tensor map over the float arena as
+// [rows][32] fp32, box [h][32]) into its own shared memory, completing on rank 0's barrier at the
+// same offset (.cta_group::2): rank 0's one expect_tx covers both halves, no relay.
+__device__ __forceinline__ void tma_rows_to_rank0(void* dst, const void* tmap, int row, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 rb;\n\tmapa.shared::cluster.u32 rb, %2, 0;\n\t"
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [rb];\n\t}\n"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(0), "r"(row)
+      : "memory");
+}
 __device__ __forceinline__ void commit_pair_elect(uint64_t* bar) {  // arrive on `bar` in both CTAs
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
