@@ -70,10 +70,11 @@ struct DevObjective {
   // fold_list: the scratch column of each extra output column
   int fold_n, fold_list;
   int tc2_pair;               // width 256 as a CTA pair (cta_group::2): every layer 256 wide or <= 128 in 32s
-  // CTA pair: TMA tensor maps over the float arena as [rows][32] fp32 rows (one map per distinct box
-  // height npad / 2; bp_load_objective encodes them): each CTA's half-block load completes on rank 0's
-  // barrier (cp.async.bulk.tensor .cta_group::2), so rank 0 needs no relay of the peer's arrivals
-  int tmap_idx[kMaxLayers];
+  // CTA pairs (v2, v3): TMA tensor maps over the float arena as [rows][32] fp32 rows, one per distinct
+  // per-CTA block height (bp_load_objective encodes them): each CTA's half-block load completes on
+  // rank 0's barrier (cp.async.bulk.tensor .cta_group::2), so rank 0 needs no relay of the peer's
+  // arrivals
+  int tmap_h[8], n_tmap;      // box height (rows) of each map
   const void* tmaps;          // device array of CUtensorMap (64-byte aligned), null when not encoded
   // tcgen05 v3 (rollout_tc3.cu): three layers [K0 <= 32, N0 <= 512, N1 <= 512, N2 <= 32], relu after
   // the hidden two; layer 1 in N chunks of <= 256 with layer 0 recomputed per chunk
@@ -93,6 +94,13 @@ struct DevObjective {
   const double* dd;
   const int* iv;
 };
+
+// The tensor map (CTA pairs) whose box is `rows` arena rows tall.
+__device__ __forceinline__ const void* tmap_rows(const DevObjective& o, int rows) {
+  int i = 0;
+  while (i + 1 < o.n_tmap && o.tmap_h[i] != rows) ++i;
+  return static_cast<const unsigned char*>(o.tmaps) + 128 * i;
+}
 
 // Device-resident subdomain pool (pool.cu; SubdomainRecord payload, bab.hpp:18-28):
 // per slot the box, the incumbent action and the top-sample list.  The head fields

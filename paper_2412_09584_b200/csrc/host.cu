@@ -845,9 +845,9 @@ Compiled compile(const bp_objective_desc& d) {
       for (int j = 0; j * 256 < np1; ++j)
         for (int kb = 0; kb < np0 / 32; ++kb) block(i1, 1, 256 * j, std::min(256, np1 - 256 * j), 32 * kb);
       for (int kb = 0; kb < np1 / 32; ++kb) block(i2, 2, 0, np2, 32 * kb);
-      o.tc3_w[0] = push_f(c.fa, i0.data(), i0.size());
-      o.tc3_w[1] = push_f(c.fa, i1.data(), i1.size());
-      o.tc3_w[2] = push_f(c.fa, i2.data(), i2.size());
+      o.tc3_w[0] = push_f_row(c.fa, i0.data(), i0.size());
+      o.tc3_w[1] = push_f_row(c.fa, i1.data(), i1.size());
+      o.tc3_w[2] = push_f_row(c.fa, i2.data(), i2.size());
       std::vector<double> bb(static_cast<size_t>(np0 + np1 + np2), 0.0);
       for (int n = 0; n < d.widths[1]; ++n) bb[static_cast<size_t>(n)] = d.b[0][n];
       for (int n = 0; n < d.widths[2]; ++n) bb[static_cast<size_t>(np0 + n)] = d.b[1][n];
@@ -1072,7 +1072,7 @@ struct bp_ctx {
   bp::DevObjective dev() {
     bp::DevObjective o = comp.o;
     o.f = d_fa.p;
-    o.tmaps = comp.o.tc2_pair ? d_tmaps.p : nullptr;
+    o.tmaps = comp.o.n_tmap > 0 ? d_tmaps.p : nullptr;
     o.dd = d_da.p;
     o.iv = d_ia.p;
     return o;
@@ -2541,13 +2541,20 @@ void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
   }();
   if (encode == nullptr) fail(BP_CUDA, "cuTensorMapEncodeTiled unavailable");
   bp::DevObjective& o = cp.o;
-  std::vector<int> heights;
-  for (int l = 0; l < o.L; ++l) {
-    const int h = o.tc_npad[l] / 2;
-    auto it = std::find(heights.begin(), heights.end(), h);
-    o.tmap_idx[l] = static_cast<int>(it - heights.begin());
-    if (it == heights.end()) heights.push_back(h);
+  std::vector<int> heights;  // per-CTA block rows of the pair forms' weight entries
+  auto add = [&](int h) {
+    if (std::find(heights.begin(), heights.end(), h) == heights.end()) heights.push_back(h);
+  };
+  if (o.tc2_pair)
+    for (int l = 0; l < o.L; ++l) add(o.tc_npad[l] / 2);
+  if (o.tc3) {
+    add(16);  // W0 N-blocks of 32 rows
+    for (int j = 0; 256 * j < o.tc3_np[1]; ++j) add(std::min(256, o.tc3_np[1] - 256 * j) / 2);  // W1 chunks
+    add(o.tc3_np[2] / 2);  // W2
   }
+  if (heights.size() > 8) fail(BP_UNSUPPORTED, "tensor maps: too many block heights");
+  o.n_tmap = static_cast<int>(heights.size());
+  for (size_t i = 0; i < heights.size(); ++i) o.tmap_h[i] = heights[i];
   std::vector<CUtensorMap> maps(heights.size());
   const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(cp.fa.size() / 32)};
   const cuuint64_t strides[1] = {128};
@@ -2575,7 +2582,8 @@ bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
     ck(memcpy_counted(f, cp.fa.data(), cp.fa.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(memcpy_counted(dd, cp.da.data(), cp.da.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(memcpy_counted(iv, cp.ia.data(), cp.ia.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (cp.o.tc2_pair) encode_tmaps(ctx, cp, f);
+    cp.o.n_tmap = 0;
+    if (cp.o.tc2_pair || cp.o.tc3) encode_tmaps(ctx, cp, f);
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->comp = std::move(cp);
     ctx->loaded = true;
@@ -2587,6 +2595,7 @@ bp_status bp_load_synthetic(bp_ctx* ctx, int dim) {
   return guard([&] {
     check_ctx(ctx);
     Compiled cp = compile_synthetic(dim);
+    cp.o.n_tmap = 0;
     float* f = ctx->d_fa.get(cp.fa.size());
     double* dd = ctx->d_da.get(cp.da.size());
     int* iv = ctx->d_ia.get(cp.ia.size());

@@ -304,8 +304,7 @@ __global__ void __launch_bounds__(Tc2<NT, RW_, EPI_, CW_, PAIR>::kThreads, 1)
                   if (PAIR && o.tmaps != nullptr) {  // both halves complete on rank 0's barrier
                     if (rank == 0) mbar_expect_tx(m.full + s, 2u * bytes);
                     const int row = static_cast<int>((src - o.f) / 32);  // images start on arena rows
-                    tma_rows_to_rank0(m.w + at, static_cast<const unsigned char*>(o.tmaps) + 128 * o.tmap_idx[l], row,
-                                      m.full + s);
+                    tma_rows_to_rank0(m.w + at, tmap_rows(o, nr), row, m.full + s);
                   } else {
                     mbar_expect_tx(m.full + s, bytes);
                     bulk_g2s(m.w + at, src, bytes, m.full + s);

@@ -321,8 +321,15 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
           return;
         }
 #endif
-        mbar_expect_tx(m.full + sl, bytes);
-        for (int i = 0; i < n; ++i) bulk_g2s(m.w + at[i], ent[i].src, ent[i].bytes, m.full + sl);
+        if (PAIR && o.tmaps != nullptr) {  // both CTAs' halves complete on rank 0's barrier
+          if (rank == 0) mbar_expect_tx(m.full + sl, 2u * bytes);
+          for (int i = 0; i < n; ++i)
+            tma_rows_to_rank0(m.w + at[i], tmap_rows(o, static_cast<int>(ent[i].bytes / 128u)),
+                              static_cast<int>((ent[i].src - o.f) / 32), m.full + sl);
+        } else {
+          mbar_expect_tx(m.full + sl, bytes);
+          for (int i = 0; i < n; ++i) bulk_g2s(m.w + at[i], ent[i].src, ent[i].bytes, m.full + sl);
+        }
         if (gcur < 60) mark3(a, tcur, 3302 + 3 * gcur);
         ++gcur;
         ++g;
@@ -363,8 +370,9 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
     }
   } else if (warp == kMmaWarp && PAIR && rank == 1) {
     // ------------------------------------------------ CTA pair, rank 1: relay "my half of group g
-    // landed" to rank 0, which issues the MMAs over both halves
-    const int n_g = H * groups_per_step(o, KB1, J);
+    // landed" to rank 0, which issues the MMAs over both halves (nothing to relay when the halves
+    // arrive by tensor-map TMA completing on rank 0's barriers)
+    const int n_g = o.tmaps != nullptr ? 0 : H * groups_per_step(o, KB1, J);
     for (int gi = 0; gi < n_g; ++gi) {
       mbar_wait_warp(m.full + gi % kRing, static_cast<uint32_t>((gi / kRing) & 1));
       if (lane == 0) mbar_arrive_cta(m.peer_full + gi % kRing, 0);
@@ -405,7 +413,8 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
     auto take_group = [&](int n, const uint32_t* rows) {
       for (int i = 0; i < n; ++i) b[i] = sw128_desc(wbase + ring_place(pos, (rows[i] >> kHalf) * 128u, ring_bytes));
       mbar_wait_warp(m.full + g % kRing, static_cast<uint32_t>((g / kRing) & 1));
-      if constexpr (PAIR) mbar_wait_cluster(m.peer_full + g % kRing, static_cast<uint32_t>((g / kRing) & 1));
+      if constexpr (PAIR)
+        if (o.tmaps == nullptr) mbar_wait_cluster(m.peer_full + g % kRing, static_cast<uint32_t>((g / kRing) & 1));
       fence_after();
     };
     auto release_group = [&]() {
@@ -754,8 +763,8 @@ cudaError_t launch_rollout_tc3(const DevObjective& o, const RolloutArgs& a, cuda
   if (grid <= 0) return cudaSuccess;
   // One CTA per tile by default; BP_TC3_PAIR=1 runs CTA pairs (clusters of two, cta_group::2:
   // each CTA streams half of every weight block -- the same results bit for bit).  Measured on
-  // C5: pair 160 vs one CTA 165 TFLOP/s -- the pair's cross-CTA operand publishes wait for the
-  // epilogue's extrema atomics still in flight (as in rollout_tc2.cu's pair).
+  // C5: pair 157 vs one CTA 164 TFLOP/s, with or without the relay of the peer's weight halves
+  // (tensor-map TMA completing on rank 0's barriers): the cross-CTA operand hand-offs pace it.
   const char* env = std::getenv("BP_TC3_PAIR");
   const bool pair = env != nullptr && env[0] == '1';
   if (!pair) {
