@@ -425,6 +425,12 @@ def main():
             "config": conf,
             "sample_steps_per_s": sample_steps,
             "failed_boxes": {"timed": cnt["failed"], "searched": cnt["boxes"]},
+            # K7 alone: the boxes bounded per second of bound-kernel device time, and the
+            # device-time shares of the step's kernels
+            "bound": {"subdomains_per_s": ((children if sweep else children / world) / (tm["bound_ms"] / 1e3))
+                                          if tm["bound_ms"] > 0 else None,
+                      "bound_ms_per_step": tm["bound_ms"] / args.steps,
+                      "rollout_ms_per_step": tm["rollout_ms"] / args.steps},
             "roofline": roof,
             "e2e": e2e, "gpu_launches": int(tm["launches"]), "clocks": clk, "cpu_baseline": cpu,
             "best_objective_vs_cpu": objective,
