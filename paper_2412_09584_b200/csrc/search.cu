@@ -45,7 +45,8 @@ __global__ void search_init_kernel(const SearchArgs a) {
       if (a.method == 0 && g > 0) {
         const uint4 r = Philox::gen(make_uint4(0xFFFFFFFFu, static_cast<uint32_t>(g), static_cast<uint32_t>(j), 7u),
                                     key_of(a.seeds[s]));
-        const double u = (static_cast<double>(r.x >> 11) * 2097152.0 + static_cast<double>(r.y >> 11)) * 0x1.0p-53;
+        // 53 random bits (r.x:r.y >> 11), as the reference's (bits >> 11) * 2^-53 (rng.cpp:16)
+        const double u = (static_cast<double>(r.x) * 2097152.0 + static_cast<double>(r.y >> 11)) * 0x1.0p-53;
         m = static_cast<float>(static_cast<double>(lo[j]) + (static_cast<double>(hi[j]) - lo[j]) * u);
       }
       a.mu[(static_cast<size_t>(s) * a.groups + g) * d + j] = m;
