@@ -1,7 +1,7 @@
 """Distribution of the root-box search's best value, device vs CPU oracle, over many seeds (dev helper):
 a systematic gap would point at a sampler difference (the update is bit-exact on identical samples).
 
-usage: python tools/search_seeds.py c2 32 [M] [iters]
+usage: python tools/search_seeds.py c2 32 [M] [iters] [method]
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,6 +13,7 @@ from paper_2412_09584_b200 import workloads
 name, n = sys.argv[1], int(sys.argv[2])
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 256
 iters = int(sys.argv[4]) if len(sys.argv) > 4 else 10
+method = sys.argv[5] if len(sys.argv) > 5 else "cem"
 wl = workloads.ALL[name]()
 lo, hi = wl.spec.box()
 dev = bp.Device(0)
@@ -21,6 +22,7 @@ ob = orc.Objective(wl.spec)
 cfg = wl.planner_config()
 cfg["search"]["samples_per_iter"] = M
 cfg["search"]["iterations"] = iters
+cfg["search"]["method"] = method
 g, c = [], []
 t0 = time.time()
 for seed in range(100, 100 + n):
