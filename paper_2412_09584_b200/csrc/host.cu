@@ -3041,7 +3041,6 @@ bp_status bp_pool_split(bp_ctx* ctx, int n, int d, int K, const double* lo, cons
     for (int i = 0; i < n; ++i)
       if (n_top[i] < 0 || n_top[i] > K) fail(BP_INVALID_ARGUMENT, "pool_split: top list longer than K");
     cudaStream_t st = ctx->stream;
-    const size_t nd = static_cast<size_t>(n) * d, nk = static_cast<size_t>(n) * K;
     DevPool slab(nullptr, d, K);
     for (int i = 0; i < 3 * n; ++i) slab.alloc(st);  // parents 0..n-1, children n..3n-1
     const bp::PoolArgs H = slab.host_args();
