@@ -35,7 +35,7 @@ def test_device_matches_golden(device, name):
     costs, _, _, _, bad = dev.rollout(np.array(g["actions"], dtype=np.float32)[None])
     ref = np.array(g["costs"])
     assert not bad.any()
-    tol = 5e-5 if dev.rollout_path() == "tcgen05" else 1e-5  # 3xTF32 vs FP32 bar
+    tol = 1e-5  # the FP32 bar, on the SIMT and the 3xTF32 tensor-core paths alike
     assert np.max(np.abs(costs[0] - ref) / np.maximum(np.abs(ref), 1.0)) < tol
     lo, hi = spec.box()
     lf = dev.bound_boxes(lo[None], hi[None], "early-stop-interval")[0]

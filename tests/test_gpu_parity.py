@@ -18,9 +18,12 @@ pytestmark = pytest.mark.gpu
 
 RTOL = 1e-5
 # The tcgen05 path computes every Linear layer in 3xTF32 (~2^-21 per product
-# instead of FP32's 2^-24); the north star allows a looser stated tolerance
-# for it: 5e-5 relative.
-RTOL_TC = 5e-5
+# instead of FP32's 2^-24).  Costs meet the FP32 bar (1e-5; measured <= 6e-6);
+# sample extrema and states get the stated looser tensor-core bar, 2.5e-5 (measured
+# <= 1.3e-5: a relative-feature pre-activation x - p cancels), well inside the
+# north star's 5e-5 allowance for the TF32 path.
+RTOL_TC_COST = 1e-5
+RTOL_TC = 2.5e-5
 
 
 def rtol_for(dev):
@@ -79,7 +82,7 @@ def test_rollout_costs_and_extrema_match_oracle(device, name):
         st = orc.Stats()
         ref = ob.evaluate(acts[s].astype(np.float64), st)
         tol = rtol_for(dev)
-        assert rel_err(costs[s], ref) < tol, name
+        assert rel_err(costs[s], ref) < (RTOL_TC_COST if dev.rollout_path() == "tcgen05" else RTOL), name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
         # the device records x_t at every step; the oracle watches it only where
         # a bound reads it (stop steps, quadratic / ReLU arguments)
@@ -115,7 +118,7 @@ def test_tcgen05_v2_matches_oracle(device, name, tiles, shape):
     for s in range(n_sub):
         st = orc.Stats()
         ref = ob.evaluate(acts[s].astype(np.float64), st)
-        assert rel_err(costs[s], ref) < RTOL_TC, name
+        assert rel_err(costs[s], ref) < RTOL_TC_COST, name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
         seen = ~np.isnan(rlo)
         assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
@@ -123,7 +126,7 @@ def test_tcgen05_v2_matches_oracle(device, name, tiles, shape):
     dev.rollout_path("simt")
     c_s, st_s, lo_s, hi_s, _ = dev.rollout(acts, want_states=True)
     dev.rollout_path("auto")
-    assert rel_err(costs, c_s) < RTOL_TC and rel_err(states, st_s) < RTOL_TC
+    assert rel_err(costs, c_s) < RTOL_TC_COST and rel_err(states, st_s) < RTOL_TC
     assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
 
 
@@ -146,7 +149,7 @@ def test_tcgen05_v2_cta_pair_matches_one_cta(device, shape, monkeypatch):
         assert np.array_equal(x, y)
     ob = orc.Objective(spec)
     ref = ob.evaluate(acts[0].astype(np.float64))
-    assert rel_err(pair[0][0], ref) < RTOL_TC
+    assert rel_err(pair[0][0], ref) < RTOL_TC_COST
 
 
 def v3_spec(name):
@@ -190,14 +193,14 @@ def test_tcgen05_v3_matches_oracle(device, name, shape):
     for s in range(n_sub):
         st = orc.Stats()
         ref = ob.evaluate(acts[s].astype(np.float64), st)
-        assert rel_err(costs[s], ref) < RTOL_TC, name
+        assert rel_err(costs[s], ref) < RTOL_TC_COST, name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
         seen = ~np.isnan(rlo)
         assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
     dev.rollout_path("simt")
     c_s, st_s, lo_s, hi_s, _ = dev.rollout(acts, want_states=True)
     dev.rollout_path("auto")
-    assert rel_err(costs, c_s) < RTOL_TC and rel_err(states, st_s) < RTOL_TC
+    assert rel_err(costs, c_s) < RTOL_TC_COST and rel_err(states, st_s) < RTOL_TC
     assert rel_err(elo, lo_s) < RTOL_TC and rel_err(ehi, hi_s) < RTOL_TC
 
 
@@ -246,8 +249,8 @@ def test_tcgen05_v1_still_matches_oracle(device, name):
     ob = orc.Objective(spec)
     for s in range(2):
         ref = ob.evaluate(acts[s].astype(np.float64))
-        assert rel_err(costs[s], ref) < RTOL_TC
-    assert rel_err(costs, c2) < RTOL_TC and rel_err(elo, lo2) < RTOL_TC and rel_err(ehi, hi2) < RTOL_TC
+        assert rel_err(costs[s], ref) < RTOL_TC_COST
+    assert rel_err(costs, c2) < RTOL_TC_COST and rel_err(elo, lo2) < RTOL_TC and rel_err(ehi, hi2) < RTOL_TC
 
 
 def test_rollout_rows_are_batch_invariant(device):
@@ -490,7 +493,7 @@ def test_tcgen05_and_simt_rollouts_agree(device, name):
     ob = orc.Objective(spec)
     for s in range(2):
         ref = ob.evaluate(acts[s].astype(np.float64))
-        assert rel_err(c_tc[s], ref) < RTOL_TC and rel_err(c_simt[s], ref) < RTOL
+        assert rel_err(c_tc[s], ref) < RTOL_TC_COST and rel_err(c_simt[s], ref) < RTOL
     assert rel_err(lo_tc, lo_s) < RTOL_TC and rel_err(hi_tc, hi_s) < RTOL_TC
 
 
@@ -532,14 +535,14 @@ def test_v2_folded_cost_linears_match_oracle_and_unfolded(device, name, monkeypa
     dev2 = bp.Device(0).load(spec)
     assert dev2.rollout_kernel() == "tc2"
     c2, s2, lo2, hi2, _ = dev2.rollout(acts, want_states=True)
-    assert rel_err(costs, c2) < RTOL_TC and rel_err(states, s2) < RTOL_TC
+    assert rel_err(costs, c2) < RTOL_TC_COST and rel_err(states, s2) < RTOL_TC
     assert rel_err(elo, lo2) < RTOL_TC and rel_err(ehi, hi2) < RTOL_TC
     ob = orc.Objective(spec)
     layout = dev.stat_layout()
     for s in range(2):
         st = orc.Stats()
         ref = ob.evaluate(acts[s].astype(np.float64), st)
-        assert rel_err(costs[s], ref) < RTOL_TC, name
+        assert rel_err(costs[s], ref) < RTOL_TC_COST, name
         rlo, rhi = ob.stats_in_layout(st, layout, spec.horizon)
         seen = ~np.isnan(rlo)
         assert rel_err(elo[s][seen], rlo[seen]) < RTOL_TC and rel_err(ehi[s][seen], rhi[seen]) < RTOL_TC, name
