@@ -49,6 +49,9 @@ CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
 # times a fixed slice of each box's search (1 of the 10 CEM iterations: every iteration does the
 # same work) and reports the full-search equivalent (SURVEY 8(d) "time a fixed slice")
 CPU_CEM_SLICE = {"c1": None, "c2": None, "c3": 1, "c4": 1, "c5": 1}
+# ... and 1/f of the samples of that iteration (the search cost is linear in the rows rolled out), so
+# a reference-arm step stays near 20 s of CPU time (--steps 5 --warmup 3 in under three minutes)
+CPU_ROW_FRACTION = {"c1": 1, "c2": 1, "c3": 4, "c4": 1, "c5": 2}
 
 
 def parse():
@@ -131,6 +134,8 @@ def cpu_children_per_s(cfg_name, wl, n_children: int, steps: int = 1, warmup: in
     full_iters = cfg["search"]["iterations"]
     k = CPU_CEM_SLICE[cfg_name] or full_iters
     cfg["search"]["iterations"] = k
+    f = CPU_ROW_FRACTION[cfg_name]
+    cfg["search"]["samples_per_iter"] = wl.samples_per_iter // f
     times = []
     for i in range(warmup + steps):
         t0 = time.perf_counter()
@@ -139,10 +144,12 @@ def cpu_children_per_s(cfg_name, wl, n_children: int, steps: int = 1, warmup: in
         reps.bound_all()
         t2 = time.perf_counter()
         if i >= warmup:
-            times.append((t1 - t0) * full_iters / k + (t2 - t1))
+            times.append((t1 - t0) * f * full_iters / k + (t2 - t1))
     sample = (f"{n_children} pre-split {wl.name} boxes per step: batch_search (CEM M={wl.samples_per_iter}, "
-              + (f"{k} of {full_iters} iterations timed, scaled to the full search" if k != full_iters
-                 else f"{full_iters} iterations") + ") + early-stop-empirical CROWN, FP64 oracle restatement")
+              + (f"{k} of {full_iters} iterations" if k != full_iters else f"{full_iters} iterations")
+              + (f" of M/{f} samples" if f != 1 else "")
+              + (" timed, scaled to the full search" if (k != full_iters or f != 1) else "")
+              + ") + early-stop-empirical CROWN, FP64 oracle restatement")
     return n_children / (sum(times) / len(times)), times, orc.thread_count(), sample
 
 
