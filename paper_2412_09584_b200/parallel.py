@@ -132,13 +132,19 @@ def attach(dev, group=None, direct: Optional[bool] = None):
         direct = dist.get_backend(group) == "nccl" and os.environ.get("BP_EXCHANGE", "nccl") != "host"
     if direct:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        uid = NcclLink.unique_id() if rank == 0 else bytes(128)
+        # rank 0's id (or an empty one when it cannot make one: every rank then takes the staged hooks)
+        try:
+            uid = NcclLink.unique_id() if rank == 0 else bytes(128)
+        except _capi.BabplanError:
+            uid = bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
         src = dist.get_global_rank(group, 0) if group is not None else 0
         dist.broadcast(t, src=src, group=group)
-        link = NcclLink(dev, rank, world, bytes(t.cpu().tolist()))
-        dev._exchange = link
-        return link
+        uid = bytes(t.cpu().tolist())
+        if any(uid):
+            link = NcclLink(dev, rank, world, uid)
+            dev._exchange = link
+            return link
     ex = Exchange(group)
     _capi.check(dev.lib.bp_set_exchange(dev.h, ex.rank, ex.world, ex.c_fn, None))
     _capi.check(dev.lib.bp_set_alltoall(dev.h, ex.c_a2a))
