@@ -403,7 +403,7 @@ def objective_value(model: Model, scenario: Scenario, actions) -> np.ndarray:
     """pymodule.cpp:171-178: objective per row of flattened action sequences.  The device
     evaluates in FP32 (3xTF32 on the tensor-core kernels): the FP64 actions are rounded to FP32
     here, and the result agrees with the reference's FP64 evaluation within the stated bars
-    (1e-5 SIMT, 5e-5 tensor cores, relative to max(|value|, 1))."""
+    (1e-5 relative to max(|value|, 1) on the SIMT and tensor-core kernels)."""
     a = np.asarray(actions, dtype=np.float64)
     if a.ndim == 1:
         a = a.reshape(1, -1)

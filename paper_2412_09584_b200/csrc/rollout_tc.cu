@@ -7,8 +7,8 @@
 // Precision: 3xTF32.  Activations and weights are split into hi = rna_tf32(x)
 // and lo = x - hi (the tensor core reads lo's top 19 bits); D += A_hi.B_hi +
 // A_hi.B_lo + A_lo.B_hi keeps ~2^-21 relative per product (FP32 is 2^-24).
-// Measured against the FP64 oracle: <= 1e-5 relative on the parity cases; the
-// tests state 5e-5 for this path.
+// Measured against the FP64 oracle: <= 6e-6 relative on the parity cases; the
+// tests hold costs to the FP32 bar (1e-5) and extrema / states to 2.5e-5.
 //
 // One CTA = 128 rows (the MMA M), 14 warps, warp-specialized:
 //   warps 0-7   epilogue: warp w owns TMEM lanes 32(w%4).. = rows 32(w%4)..+31
