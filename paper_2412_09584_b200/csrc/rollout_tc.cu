@@ -4,9 +4,11 @@
 // with every Linear layer done by tcgen05.mma (kind::tf32) into a TMEM
 // accumulator.
 //
-// Precision: 3xTF32.  Activations and weights are split into hi = rna_tf32(x)
-// and lo = x - hi (the tensor core reads lo's top 19 bits); D += A_hi.B_hi +
-// A_hi.B_lo + A_lo.B_hi keeps ~2^-21 relative per product (FP32 is 2^-24).
+// Precision: 3xTF32.  Weights are split on the host into hi = rna_tf32(w) and
+// lo = rna_tf32(w - hi); activations into hi = x (the tensor core reads its top 19
+// bits, i.e. truncates) and lo = rna_tf32(x - trunc_tf32(x)) -- an unbiased split;
+// D += A_hi.B_hi + A_hi.B_lo + A_lo.B_hi keeps ~2^-21 relative per product (FP32 is
+// 2^-24).  The pipe's FP32 accumulation truncates (tools/tc_rounding.cu).
 // Measured against the FP64 oracle: <= 6e-6 relative on the parity cases; the
 // tests hold costs to the FP32 bar (1e-5) and extrema / states to 2.5e-5.
 //
