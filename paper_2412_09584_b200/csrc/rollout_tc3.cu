@@ -68,6 +68,9 @@ constexpr uint32_t kColD1 = 0, kColXh = 256, kColL0 = 288, kColD2 = 480;
 __device__ __forceinline__ uint32_t col_l0h(int s) { return kColL0 + 64u * s; }
 __device__ __forceinline__ uint32_t col_l0l(int s) { return kColL0 + 64u * s + 32u; }
 constexpr uint32_t kTmemCols = 512;
+#ifndef BP_TC3_FEATURES_FIRST
+#define BP_TC3_FEATURES_FIRST 1
+#endif
 #ifndef BP_TC3_SLEEP_EPI
 #define BP_TC3_SLEEP_EPI 64
 #endif
@@ -721,6 +724,12 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
           const float* b2 = m.bias + np0 + np1;
 #pragma unroll
           for (int q = 0; q < 32; ++q) v[q] = q < np2 ? v[q] + b2[q] : 0.f;
+          if (BP_TC3_FEATURES_FIRST && t + 1 < H) {  // the next step's layer 0 waits on these first
+            float f[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) f[q] = q < ks ? v[q] : 0.f;
+            features_store(f);
+          }
           if (t >= 1) mbar_wait(m.x_empty, static_cast<uint32_t>((t - 1) & 1), kSleepEpi);
 #pragma unroll
           for (int q = 0; q < 32; ++q)
@@ -729,7 +738,7 @@ __global__ void __launch_bounds__(kThreads3, 1) rollout_tc3_kernel(const DevObje
             warp_chunk_extrema(a, v, simple, ws0, ws1, row_ok, grow, rps, SPH,
                                static_cast<long long>(t) * o.SP + o.x_stat + lane, lane, ks);
           mbar_arrive_warp(m.x_full);
-          if (t + 1 < H) {
+          if (!BP_TC3_FEATURES_FIRST && t + 1 < H) {
 #pragma unroll
             for (int q = 0; q < 32; ++q)
               if (q >= ks) v[q] = 0.f;
