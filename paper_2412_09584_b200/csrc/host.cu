@@ -2529,7 +2529,8 @@ bp_status bp_io_bytes(int64_t* h2d, int64_t* d2h) {
 
 // TMA tensor maps for the v2 CTA pair: the float arena as a [rows][32] fp32 tensor (128-byte rows,
 // no swizzle: the images are pre-swizzled), one map per distinct per-CTA block height npad / 2.
-// cuTensorMapEncodeTiled comes from the driver through cudaGetDriverEntryPoint (no -lcuda).
+// cuTensorMapEncodeTiled comes from the driver through cudaGetDriverEntryPoint (no -lcuda).  Without
+// maps (no encoder, too many heights) n_tmap stays 0 and the pair forms relay the peer's arrivals.
 void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
@@ -2539,7 +2540,7 @@ void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (encode == nullptr) fail(BP_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (encode == nullptr) return;
   bp::DevObjective& o = cp.o;
   std::vector<int> heights;  // per-CTA block rows of the pair forms' weight entries
   auto add = [&](int h) {
@@ -2552,9 +2553,7 @@ void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
     for (int j = 0; 256 * j < o.tc3_np[1]; ++j) add(std::min(256, o.tc3_np[1] - 256 * j) / 2);  // W1 chunks
     add(o.tc3_np[2] / 2);  // W2
   }
-  if (heights.size() > 8) fail(BP_UNSUPPORTED, "tensor maps: too many block heights");
-  o.n_tmap = static_cast<int>(heights.size());
-  for (size_t i = 0; i < heights.size(); ++i) o.tmap_h[i] = heights[i];
+  if (heights.size() > 8) return;
   std::vector<CUtensorMap> maps(heights.size());
   const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(cp.fa.size() / 32)};
   const cuuint64_t strides[1] = {128};
@@ -2564,10 +2563,12 @@ void encode_tmaps(bp_ctx* ctx, Compiled& cp, float* arena) {
     const CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, arena, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(BP_CUDA, "cuTensorMapEncodeTiled failed");
+    if (r != CUDA_SUCCESS) return;
   }
   unsigned char* dm = ctx->d_tmaps.get(maps.size() * sizeof(CUtensorMap));
   ck(memcpy_counted(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  o.n_tmap = static_cast<int>(heights.size());
+  for (size_t i = 0; i < heights.size(); ++i) o.tmap_h[i] = heights[i];
 }
 
 bp_status bp_load_objective(bp_ctx* ctx, const bp_objective_desc* desc) {
