@@ -49,6 +49,7 @@ CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
 # times a fixed slice of each box's search (1 of the 10 CEM iterations: every iteration does the
 # same work) and reports the full-search equivalent (SURVEY 8(d) "time a fixed slice")
 CPU_CEM_SLICE = {"c1": None, "c2": None, "c3": 1, "c4": 1, "c5": 1}
+CROWN_FLOP = {"c1": 0.095e6, "c2": 1.42e6, "c3": 8.91e6, "c4": 3.48e6, "c5": 22.4e6}
 # ... and 1/f of the samples of that iteration (the search cost is linear in the rows rolled out), so
 # a reference-arm step stays near 20 s of CPU time (--steps 5 --warmup 3 in under three minutes)
 CPU_ROW_FRACTION = {"c1": 1, "c2": 1, "c3": 4, "c4": 1, "c5": 2}
@@ -439,6 +440,10 @@ def main():
             # device-time shares of the step's kernels
             "bound": {"subdomains_per_s": ((children if sweep else children / world) / (tm["bound_ms"] / 1e3))
                                           if tm["bound_ms"] > 0 else None,
+                      # CROWN lower-form FLOP per subdomain over all H steps (early stop does less)
+                      "crown_flop_per_subdomain": CROWN_FLOP[args.config],
+                      "fp64_tflops_upper": ((children if sweep else children / world) * CROWN_FLOP[args.config]
+                                            / (tm["bound_ms"] / 1e3) / 1e12) if tm["bound_ms"] > 0 else None,
                       "bound_ms_per_step": tm["bound_ms"] / args.steps,
                       "rollout_ms_per_step": tm["rollout_ms"] / args.steps},
             "roofline": roof,
